@@ -1,0 +1,193 @@
+"""Pin the CPU oracle against the reference's own outputs (golden vectors).
+
+These run without a GPU.  Every comparison is bitwise: the oracle restates
+the reference loops with the same rounding (no FMA contraction, same
+order), so any difference is a restatement bug.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden_problem
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8).tobytes()).hexdigest()
+
+
+SEEDS = range(30)
+
+
+# ---- known-answer tests copied as numbers from the reference's tests -------
+
+
+def test_kat_single_coefficient(oracle):
+    # /root/reference/pkg/tests/test_engine.py:21-41
+    p = dict(atoms=np.array([0], np.uint32), voxels=np.array([0], np.uint32),
+             fibers=np.array([0], np.uint32), values=np.array([2.0]),
+             dict=np.array([1.0, 0.5]), dims=(1, 1, 1, 2, 1), ordering="unsorted")
+    y = np.zeros(2)
+    oracle.dsc(p, np.array([3.0]), y)
+    assert y.tolist() == [6.0, 3.0]
+    w = np.zeros(1)
+    oracle.wc(p, np.array([6.0, 3.0]), w)
+    assert w.tolist() == [15.0]
+
+
+def test_kat_sort_and_runs(oracle):
+    # test_restructure.py:17-23, 34-41, 72-80
+    assert oracle.stable_argsort(np.array([2, 0, 1], np.uint32)).tolist() == [1, 2, 0]
+    perm = oracle.stable_argsort(np.array([1, 0, 1, 0], np.uint32))
+    assert np.array([10.0, 11.0, 12.0, 13.0])[perm].tolist() == [11.0, 13.0, 10.0, 12.0]
+    b, k = oracle.detect_runs(np.array([0, 0, 1, 1, 1, 2], np.uint32))
+    assert b.tolist() == [0, 2, 5, 6] and k.tolist() == [0, 1, 2]
+    b, k = oracle.detect_runs(np.array([], np.uint32))
+    assert b.tolist() == [0] and k.size == 0
+
+
+def test_kat_snap(oracle):
+    # test_engine.py:121-129
+    p = dict(voxels=np.array([0, 0, 1, 1, 4, 4, 4, 5, 5, 7], np.uint32),
+             dims=(1, 8, 2, 1, 10))
+    assert oracle.build_plan(p, "coefficient", True, 2) == ((0, 4), (4, 10))
+
+
+def test_kat_solve_identity(oracle):
+    # test_sbbnnls.py:120-126: 1x1 identity, b=3 -> w=[3] in one step
+    p = dict(atoms=np.array([0], np.uint32), voxels=np.array([0], np.uint32),
+             fibers=np.array([0], np.uint32), values=np.array([1.0]),
+             dict=np.array([1.0]), y=np.array([3.0]), dims=(1, 1, 1, 1, 1),
+             ordering="unsorted")
+    w, tr = oracle.solve(p, w0=np.array([0.0]), max_iters=10)
+    assert tr["termination"] == "grad_tol"
+    assert w.tolist() == [3.0]
+    assert len(tr["records"]) == 1
+
+
+# ---- golden vectors: desk scale ------------------------------------------
+
+
+@pytest.mark.parametrize("seed", SEEDS)
+def test_generator_bitwise(oracle, golden, seed):
+    p = oracle.small_problem(seed)
+    g = golden_problem(golden, seed)
+    assert p["dims"] == g["dims"]
+    for k in ("atoms", "voxels", "fibers", "values", "dict", "y", "w_true"):
+        assert np.array_equal(p[k], g[k]), k
+
+
+@pytest.mark.parametrize("seed", SEEDS)
+def test_kernels_bitwise(oracle, golden, seed):
+    g = golden_problem(golden, seed)
+    pre = f"s{seed}_"
+    nv, nf, nd = g["dims"][1], g["dims"][2], g["dims"][3]
+    for wkey in ("w_in", "w_sparse"):
+        y = np.zeros(nv * nd)
+        sk = oracle.dsc(g, golden[pre + wkey], y)
+        assert np.array_equal(y, golden[pre + "dsc_" + wkey])
+        assert sk == int(golden[pre + "dsc_" + wkey + "_skipped"])
+    w = np.zeros(nf)
+    oracle.wc(g, golden[pre + "y_in"], w)
+    assert np.array_equal(w, golden[pre + "wc_y_in"])
+
+
+@pytest.mark.parametrize("seed", SEEDS)
+def test_restructure_bitwise(oracle, golden, seed):
+    g = golden_problem(golden, seed)
+    pre = f"s{seed}_"
+    nv, nf, nd = g["dims"][1], g["dims"][2], g["dims"][3]
+    for key in ("atom", "voxel", "fiber"):
+        s, perm = oracle.sort_by(g, key)
+        assert np.array_equal(perm, golden[pre + "perm_" + key])
+        b, k = oracle.detect_runs(s[key + "s"])
+        assert np.array_equal(b, golden[pre + "runs_" + key])
+        assert np.array_equal(k, golden[pre + "runkeys_" + key])
+        y = np.zeros(nv * nd)
+        oracle.dsc(s, golden[pre + "w_in"], y)
+        assert np.array_equal(y, golden[pre + "dsc_sorted_" + key])
+        w = np.zeros(nf)
+        oracle.wc(s, golden[pre + "y_in"], w)
+        assert np.array_equal(w, golden[pre + "wc_sorted_" + key])
+        chunks = oracle.build_plan(s, "coefficient", False, 3)
+        w = np.zeros(nf)
+        oracle.wc_chunks(s, golden[pre + "y_in"], w, chunks)
+        assert np.array_equal(w, golden[pre + "wc_priv3_" + key])
+        if key == "voxel":
+            for T in (2, 3, 4, 8):
+                sf = oracle.build_plan(s, "coefficient", True, T)
+                assert np.array_equal(np.array(sf, dtype=np.int64).reshape(-1, 2),
+                                      golden[pre + f"plan_sf_{T}"])
+                vp = oracle.build_plan(s, "voxel", False, T)
+                assert np.array_equal(np.array(vp, dtype=np.int64).reshape(-1, 2),
+                                      golden[pre + f"plan_voxel_{T}"])
+                y = np.zeros(nv * nd)
+                oracle.dsc_chunks(s, golden[pre + "w_in"], y,
+                                  oracle.build_plan(s, "coefficient", False, T), False)
+                assert np.array_equal(y, golden[pre + f"dsc_edge_{T}"])
+    y = np.zeros(nv * nd)
+    oracle.dsc_chunks(g, golden[pre + "w_in"], y,
+                      oracle.build_plan(g, "coefficient", False, 4), False)
+    assert np.array_equal(y, golden[pre + "dsc_full4"])
+
+
+def _solver_problem(golden, name):
+    pre = f"solp_{name}_"
+    return dict(atoms=golden[pre + "atoms"], voxels=golden[pre + "voxels"],
+                fibers=golden[pre + "fibers"], values=golden[pre + "values"],
+                dict=golden[pre + "dict"], y=golden[pre + "y"],
+                dims=tuple(int(x) for x in golden[pre + "dims"]), ordering="unsorted")
+
+
+@pytest.mark.parametrize("threads", [1, 4])
+def test_solver_bitwise(oracle, golden, threads):
+    for name in golden["solver_case_names"]:
+        p = _solver_problem(golden, str(name))
+        w, tr = oracle.solve(p, max_iters=30, grad_tol=0.0, threads=threads)
+        pre = f"sol_{name}_t{threads}_"
+        assert tr["termination"] == str(golden[pre + "termination"])
+        assert np.array_equal(w, golden[pre + "w"]), name
+        rec = tr["records"]
+        assert np.array_equal([r["objective"] for r in rec], golden[pre + "objective"])
+        assert np.array_equal([r["alpha"] for r in rec], golden[pre + "alpha"])
+        assert np.array_equal([r["zeros"] for r in rec], golden[pre + "zeros"])
+        assert np.array_equal([r["dsc_skipped"] for r in rec], golden[pre + "dsc_skipped"])
+        assert tr["final_objective"] == float(golden[pre + "final_objective"])
+
+
+# ---- hashed cases: generator + restructuring + kernels at scale ------------
+
+
+def _check_hashed(oracle, rec, solve=False):
+    dims = tuple(rec["dims"])
+    p = oracle.generate(dims, rec["mean_run_length"], rec["weight_density"],
+                        rec["noise_sigma"], rec["seed"])
+    for k in ("atoms", "voxels", "fibers", "values", "dict", "y", "w_true"):
+        assert sha(p[k]) == rec["sha_" + k], k
+    w = np.zeros(dims[2])
+    oracle.wc(p, p["y"], w)
+    assert sha(w) == rec["sha_wc_y"]
+    y = np.zeros(dims[1] * dims[3])
+    sk = oracle.dsc(p, w, y)
+    assert sha(y) == rec["sha_dsc_wc_y"] and sk == rec["skipped_dsc_wc_y"]
+    for key in ("atom", "voxel", "fiber"):
+        s, perm = oracle.sort_by(p, key)
+        assert sha(perm) == rec["sha_perm_" + key], key
+        b, _ = oracle.detect_runs(s[key + "s"])
+        assert len(b) - 1 == rec["n_runs_" + key]
+        assert sha(b) == rec["sha_runs_" + key]
+    if solve:
+        w, tr = oracle.solve(p, max_iters=rec["solve_iters"], grad_tol=0.0,
+                             threads=rec["solve_threads"])
+        assert sha(w) == rec["sha_solve_w"]
+        assert tr["final_objective"] == rec["solve_final_objective"]
+
+
+def test_hashed_medium(oracle, golden_hashes):
+    _check_hashed(oracle, golden_hashes["medium"], solve=True)
+
+
+@pytest.mark.slow
+def test_hashed_c1(oracle, golden_hashes):
+    _check_hashed(oracle, golden_hashes["c1"], solve=False)
