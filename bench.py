@@ -1,0 +1,372 @@
+"""Benchmark: SBBNNLS iterations/sec on the STN96-shaped problem (C2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one SBBNNLS iteration (2 DSC + 1.5 WC on average, Alg. 1) over
+the whole synthetic problem of BASELINE.json configs[1]: N_theta=96,
+Na=1057, Nv=200k, Nf=500k, Nc=100M (data: the reference generator's
+algorithm, seed 0, noise 0.1).  ``value`` times exactly K iterations with
+the problem resident in HBM (CUDA events, max over ranks); ``e2e`` times a
+public ``solve()`` of K iterations from host numpy arrays (H2D of Phi/D/b,
+device restructuring, the iterations, D2H of w).  The reference arm
+(``--impl reference``) times the CPU oracle port of the reference on a
+bounded sample of the same workload on this host's cores.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (Na, Nv, Nf, Ntheta, Nc)
+    "c2": (1057, 200_000, 500_000, 96, 100_000_000),
+    "c1": (1057, 10_000, 20_000, 96, 5_000_000),
+    "c2s": (1057, 50_000, 125_000, 96, 25_000_000),
+}
+METRIC = "SBBNNLS iters/sec"
+UNIT = "it/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def spmv_bytes(dims, val_bytes=4, idx_bytes=4, vec_bytes=4):
+    """Algorithmic (compulsory) bytes per call, SURVEY.md 8(d)."""
+    na, nv, nf, nt, nc = dims
+    dsc = nc * (2 * idx_bytes + val_bytes) + (nv + 1) * 4 + nf * vec_bytes \
+        + nv * nt * vec_bytes + na * nt * vec_bytes
+    wc = nc * (2 * idx_bytes + val_bytes) + (nv + 1) * 4 + nv * nt * vec_bytes \
+        + nf * vec_bytes + na * nt * vec_bytes
+    return dsc, wc
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: CPU oracle port on a bounded sample
+# ---------------------------------------------------------------------------
+
+
+def sample_dims(dims, target_nc=5_000_000):
+    """Same per-voxel / per-fascicle densities, ~target_nc coefficients."""
+    na, nv, nf, nt, nc = dims
+    f = min(1.0, target_nc / nc)
+    return (na, max(1, int(round(nv * f))), max(1, int(round(nf * f))), nt,
+            max(1, int(round(nc * f))))
+
+
+def cpu_reference(dims, iters_lo=1, iters_hi=5, threads=None):
+    """Per-iteration cost of the oracle port of sbbnnls.solve on a sample,
+    scaled to the full workload (linear in Nc).  (t(k2) - t(k1)) / (k2 - k1)
+    removes the per-solve sorting, as BASELINE.md prescribes."""
+    from oracle import oracle as O
+    threads = threads or os.cpu_count()
+    O.set_threads(threads)
+    sd = sample_dims(dims)
+    p = O.generate(sd, max(1.0, 1.04 * sd[4] / sd[1]), 0.5, 0.1, 0)
+    t0 = time.perf_counter()
+    O.solve(p, max_iters=iters_lo, grad_tol=0.0, threads=threads)
+    t1 = time.perf_counter()
+    O.solve(p, max_iters=iters_hi, grad_tol=0.0, threads=threads)
+    t2 = time.perf_counter()
+    per_iter = ((t2 - t1) - (t1 - t0)) / (iters_hi - iters_lo)
+    scale = sd[4] / dims[4]
+    return {"value": scale / per_iter, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": (f"oracle port of sbbnnls.solve, Nc={sd[4]} (Na={sd[0]} Nv={sd[1]} "
+                       f"Nf={sd[2]} Nt={sd[3]}), (t({iters_hi})-t({iters_lo}))/"
+                       f"{iters_hi - iters_lo} per iteration, scaled by Nc ratio {scale:.4g}"),
+            "sample_seconds_per_iter": per_iter}
+
+
+def run_reference(args, dims):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    threads = os.cpu_count()
+    O.set_threads(threads)
+    sd = sample_dims(dims)
+    p = O.generate(sd, max(1.0, 1.04 * sd[4] / sd[1]), 0.5, 0.1, 0)
+    # each step: one oracle SBBNNLS iteration on the sample; differencing
+    # solves of W and W+K iterations isolates exactly K iterations
+    t0 = time.perf_counter()
+    O.solve(p, max_iters=max(1, args.warmup), grad_tol=0.0, threads=threads)
+    t1 = time.perf_counter()
+    O.solve(p, max_iters=max(1, args.warmup) + args.steps, grad_tol=0.0, threads=threads)
+    t2 = time.perf_counter()
+    per_iter = ((t2 - t1) - (t1 - t0)) / args.steps
+    scale = sd[4] / dims[4]
+    value = scale / per_iter
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(dims, args, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"oracle port (C + numpy, OpenMP) of sbbnnls.solve on "
+                                       f"Nc={sd[4]} of the same density; per-iteration time "
+                                       f"by differencing solves of {max(1, args.warmup)} and "
+                                       f"{max(1, args.warmup) + args.steps} iterations, scaled "
+                                       f"by the Nc ratio {scale:.4g}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(dims, args, world):
+    na, nv, nf, nt, nc = dims
+    return {"workload": f"{args.config.upper()} STN96-shaped synthetic LiFE problem "
+                        f"(BASELINE.json configs[1])" if args.config == "c2" else args.config,
+            "n_atoms": na, "n_voxels": nv, "n_fibers": nf, "n_dirs": nt, "n_coeffs": nc,
+            "mean_run_length": round(1.04 * nc / nv, 3), "noise_sigma": 0.1, "seed": 0,
+            "parallelism": f"voxel-shard x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (Phi alone 1.2 GB vs 126 MB L2)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args, dims):
+    import torch
+
+    import paper_1905_06234_b200 as L
+    from paper_1905_06234_b200 import _native, datagen
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    na, nv, nf, nt, nc = dims
+    cfg = L.GenConfig(dims=L.Dims(*dims), mean_run_length=1.04 * nc / nv,
+                      weight_density=0.5, noise_sigma=0.1, seed=0)
+    t_gen = time.perf_counter()
+    problem = L.generate(cfg)
+    t_gen = time.perf_counter() - t_gen
+    info = {"generate_s": round(t_gen, 2)}
+
+    # ---- device-resident timing of exactly K iterations ---------------------
+    total_iters = args.warmup + args.steps
+    op = L.DeviceOperator(problem.tensor, problem.dictionary)
+    info["restructure_ms"] = round(op.info.sort_ms, 1)
+    info["atom_groups"] = op.info.atom_groups
+    b = torch.from_numpy(problem.y).to(device="cuda", dtype=torch.float32)
+    w = torch.empty(nf, dtype=torch.float32, device="cuda")
+    scfg = L.SolverConfig(max_iters=total_iters, grad_tol=0.0)
+    sess = L.sbbnnls.SolverSession(op, b, w, scfg)
+    sess.iterate(args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _native.launch_count()
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        start.record()
+        sess.iterate(args.steps)
+        stop.record()
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    ms = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    terminated_early = sess.poll() and False
+    res, recs = sess.finish()
+    if res.iterations < total_iters:
+        raise RuntimeError(f"solver stopped after {res.iterations} < {total_iters} iterations "
+                           f"({res.termination}); timed region would contain no-op steps")
+    value = args.steps / (ms * 1e-3)
+    del terminated_early
+
+    # ---- kernel-level timing (DSC / WC) for the roofline -------------------
+    dsc_b, wc_b = spmv_bytes(dims)
+    y = torch.empty(nv * nt, dtype=torch.float32, device="cuda")
+    g = torch.empty(nf, dtype=torch.float32, device="cuda")
+    ymax = torch.zeros(1, dtype=torch.float32, device="cuda")
+    iso = max(5, min(20, args.steps))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(iso)]
+    for _ in range(2):
+        op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absmax=ymax)
+    for e0, e1 in ev:
+        e0.record()
+        op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absmax=ymax)
+        e1.record()
+    torch.cuda.synchronize()
+    t_dsc = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3
+    for _ in range(2):
+        op.wc_f32(y, g, y_absmax=ymax)
+    for e0, e1 in ev:
+        e0.record()
+        op.wc_f32(y, g, y_absmax=ymax)
+        e1.record()
+    torch.cuda.synchronize()
+    t_wc = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3
+    peak, peak_kind = peaks()
+    dsc_gbs, wc_gbs = dsc_b / t_dsc / 1e9, wc_b / t_wc / 1e9
+    if 2 * t_dsc >= 1.5 * t_wc:
+        dom, ach, traffic_key = "dsc", dsc_gbs, "dsc"
+    else:
+        dom, ach, traffic_key = "wc", wc_gbs, "wc"
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(traffic_key)
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the public API from host buffers ---------------
+    e2e = None
+    if not args.no_e2e:
+        t = problem.tensor
+        fresh = L.PhiTensor(atoms=t.atoms, voxels=t.voxels, fibers=t.fibers, values=t.values,
+                            dims=t.dims)
+        p2 = L.Problem(tensor=fresh, dictionary=problem.dictionary, y=problem.y)
+        del op, sess
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        w_host, tr = L.solve(p2, config=L.SolverConfig(max_iters=args.steps, grad_tol=0.0))
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([e2e_s], device="cuda")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        h2d = nc * (4 * 3 + 8) + na * nt * 8 + nv * nt * 8
+        e2e = {"value": args.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": nf * 8 // args.steps,
+               "seconds": round(e2e_s, 3),
+               "what": f"one solve() of {args.steps} iterations from host numpy arrays: "
+                       "H2D of Phi/D/b + device restructuring + iterations + D2H of w "
+                       "(bytes spread over the steps)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_reference(dims)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": workload_config(dims, args, world),
+                "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                             "frac": ach / peak, "traffic": traffic, "kernel": dom,
+                             "peak_source": peak_kind},
+                "spmv": {"dsc_ms": t_dsc * 1e3, "wc_ms": t_wc * 1e3,
+                         "dsc_gbs": dsc_gbs, "wc_gbs": wc_gbs,
+                         "dsc_bytes": dsc_b, "wc_bytes": wc_b,
+                         "dsc_frac": dsc_gbs / peak, "wc_frac": wc_gbs / peak},
+                "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks.summary(),
+                "gpu_launches": int(launches), "info": info}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    dims = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, dims)
+    else:
+        run_ours(args, dims)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+// life_common.cuh -- internal declarations shared by the liblife_b200 sources.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "life_b200.h"
+
+namespace life {
+
+// ---- errors ----------------------------------------------------------------
+int fail(int status, const std::string &msg);  // records msg, returns status
+int ok();                                      // clears msg, returns LIFE_OK
+extern std::atomic<uint64_t> g_launches;
+
+#define LIFE_CUDA(call)                                                        \
+    do {                                                                       \
+        cudaError_t e_ = (call);                                               \
+        if (e_ != cudaSuccess)                                                 \
+            return ::life::fail(e_ == cudaErrorMemoryAllocation                \
+                                    ? LIFE_ERR_OUT_OF_MEMORY                   \
+                                    : LIFE_ERR_CUDA,                           \
+                                std::string(#call) + ": " +                    \
+                                    cudaGetErrorString(e_));                   \
+    } while (0)
+
+#define LIFE_CHECK_LAUNCH()                                                    \
+    do {                                                                       \
+        ::life::g_launches.fetch_add(1, std::memory_order_relaxed);           \
+        cudaError_t e_ = cudaGetLastError();                                   \
+        if (e_ != cudaSuccess)                                                 \
+            return ::life::fail(LIFE_ERR_CUDA, std::string("launch: ") +       \
+                                                   cudaGetErrorString(e_));    \
+    } while (0)
+
+#define LIFE_TRY(expr)                                                         \
+    do {                                                                       \
+        int s_ = (expr);                                                       \
+        if (s_ != LIFE_OK) return s_;                                          \
+    } while (0)
+
+constexpr int kMaxNT = 10;          // n_dirs <= 320 (SPEC: 10..300 directions)
+constexpr int kSpmvThreads = 512;   // 16 warps per CTA, one CTA per SM
+
+// ---- device helpers --------------------------------------------------------
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
+
+// Per-call reduction outputs, fixed-order (deterministic) completion.
+struct ReduceSlots {
+    double *part_d;               // [nwarps] sum of squares partials
+    unsigned long long *part_u;   // [nwarps] counts
+    float *part_f;                // [nwarps] abs-max partials
+    unsigned *counter;            // blocks finished (reset by last block)
+};
+
+// Timing/termination hooks used by the on-device solver (all optional).
+struct CallHooks {
+    const int *done;                     // kernel no-ops when *done != 0
+    unsigned long long *t_begin;         // globaltimer at entry (block 0)
+    unsigned long long *t_accum;         // += (end - begin) ns by last block
+};
+
+}  // namespace life
+
+// ---- the operator handle ---------------------------------------------------
+struct life_phi {
+    life_dims dims{};
+    int na = 0, nv = 0, nf = 0, nt = 0;
+    int64_t nc = 0;
+    int sms = 0;
+    int device = 0;
+
+    // fp32 fast layout: coefficients sorted by (atom group, voxel), stable.
+    bool has_fast = false;
+    int G = 1;            // atom groups (D slices staged in shared memory)
+    int ag = 0;           // atoms per group
+    int slice_floats = 0; // floats per staged slice (16-byte padded)
+    uint32_t *atom = nullptr;   // atom index local to its group
+    uint32_t *fiber = nullptr;
+    float *val = nullptr;
+    uint32_t *gptr = nullptr;   // [G*nv + 1] segment starts
+    int *wpart = nullptr;       // [W + 1] voxel range per persistent warp
+    float *Dg = nullptr;        // [G*slice_floats] fp32 dictionary slices
+    int nblocks = 0, W = 0;
+    size_t smem = 0;
+
+    // fixed-point WC accumulator and its scale inputs
+    unsigned long long *wfix = nullptr;  // [nf] two's-complement int64
+    double vmax = 0.0;                   // max |value|
+    double dmax = 0.0;                   // max ||D_a||_2
+    int64_t fmax_nnz = 0;                // longest fascicle segment
+
+    // fp64 bit-exact layouts (stable voxel sort, stable fiber sort)
+    bool has_exact = false;
+    uint32_t *xv_atom = nullptr, *xv_voxel = nullptr, *xv_fiber = nullptr;
+    double *xv_val = nullptr;
+    uint32_t *xv_ptr = nullptr;     // [nv + 1]
+    int *xv_wpart = nullptr;        // [xW + 1] voxel ranges
+    uint32_t *xf_atom = nullptr, *xf_voxel = nullptr, *xf_fiber = nullptr;
+    double *xf_val = nullptr;
+    uint32_t *xf_ptr = nullptr;     // [nf + 1]
+    int *xf_wpart = nullptr;        // [xW + 1] fiber ranges
+    double *D64 = nullptr;
+    int xW = 0, xblocks = 0;
+
+    // scratch
+    life::ReduceSlots red{};
+    double *part_d2 = nullptr;       // second slot set for finalize kernels
+    unsigned long long *part_u2 = nullptr;
+    unsigned *counter2 = nullptr;
+    float *ybound = nullptr;         // device scalar for standalone WC
+    int red_cap = 0;                 // capacity of partial arrays
+
+    // statistics
+    int64_t n_voxel_runs = 0, n_fiber_runs = 0, max_voxel_run = 0,
+            max_fiber_run = 0;
+    double sort_ms = 0.0;
+    int64_t device_bytes = 0;
+    std::vector<void *> allocs;
+};
+
+namespace life {
+template <typename T>
+int dalloc(life_phi *phi, T **p, size_t n)
+{
+    *p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T));
+    if (e != cudaSuccess)
+        return fail(e == cudaErrorMemoryAllocation ? LIFE_ERR_OUT_OF_MEMORY
+                                                    : LIFE_ERR_CUDA,
+                    std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    phi->allocs.push_back(*p);
+    phi->device_bytes += static_cast<int64_t>(n * sizeof(T));
+    return LIFE_OK;
+}
+
+// Fixed-point exponent for the WC accumulator: every |coefficient term| is
+// at most vmax * dmax * ||y_v||_2 <= vmax * dmax * sqrt(nt) * ymax, a
+// fascicle sums at most fmax_nnz of them; the sum stays below 2^62.
+__host__ __device__ inline int wc_fix_exponent(double vmax, double dmax,
+                                               double nt, double fmax_nnz,
+                                               float ymax)
+{
+    double bound = vmax * dmax * sqrt(nt) * (double)ymax * fmax_nnz;
+    if (!(bound > 0.0)) return 0;
+    int e;
+    frexp(bound, &e);          // bound < 2^e
+    int ex = 62 - e;
+    if (ex > 1000) ex = 1000;
+    if (ex < -1000) ex = -1000;
+    return ex;
+}
+
+// Internal launchers exposed across translation units.
+struct DscOut {
+    unsigned long long *skipped;
+    double *sumsq;
+    float *absmax;
+};
+int launch_absmax(life_phi *phi, const float *x, int64_t n, float *out,
+                  cudaStream_t st);
+int launch_dsc(life_phi *phi, const float *w, float *y, const float *b,
+               uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st);
+int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
+              const float *ymax_dev, uint32_t flags, double *sumsq,
+              const CallHooks &h, cudaStream_t st);
+int prepare_spmv(life_phi *phi);
+}  // namespace life

@@ -1,0 +1,739 @@
+// life_phi.cu -- operator construction (restructuring), argsort, run
+// detection, and the library's error plumbing.
+//
+// Restructuring follows restructure.sort_by / detect_runs
+// (/root/reference/pkg/src/lifespmv/restructure.py:54-92): a STABLE sort of
+// the coefficient list by a key, realised on the device with a LSD radix
+// sort (stable by construction), so the permutation is bit-identical to
+// np.argsort(kind="stable").
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "life_common.cuh"
+
+namespace life {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_last_error;
+
+int fail(int status, const std::string &msg)
+{
+    t_last_error = msg;
+    return status;
+}
+
+int ok()
+{
+    t_last_error.clear();
+    return LIFE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+
+__global__ void k_iota_u32(uint32_t *out, int64_t n)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void k_widen_u32_i64(const uint32_t *in, int64_t *out, int64_t n)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = static_cast<int64_t>(in[i]);
+}
+
+// first position k with idx[k] >= bound, per dimension (atomicMin)
+__global__ void k_check_range(const uint32_t *a, const uint32_t *v,
+                              const uint32_t *f, int64_t n, uint32_t na,
+                              uint32_t nv, uint32_t nf,
+                              unsigned long long *first_bad)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (a[i] >= na) atomicMin(&first_bad[0], (unsigned long long)i);
+        if (v[i] >= nv) atomicMin(&first_bad[1], (unsigned long long)i);
+        if (f[i] >= nf) atomicMin(&first_bad[2], (unsigned long long)i);
+    }
+}
+
+// composite key: (atom group) * nv + voxel
+__global__ void k_group_voxel_key(const uint32_t *a, const uint32_t *v,
+                                  int64_t n, uint32_t ag, uint32_t nv,
+                                  uint32_t *key)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        key[i] = (a[i] / ag) * nv + v[i];
+}
+
+__global__ void k_gather_fast(const uint32_t *perm, int64_t n,
+                              const uint32_t *a, const uint32_t *f,
+                              const double *val, uint32_t ag, uint32_t *a_out,
+                              uint32_t *f_out, float *val_out)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = perm[i];
+        const uint32_t at = a[p];
+        a_out[i] = at % ag;
+        f_out[i] = f[p];
+        val_out[i] = static_cast<float>(val[p]);
+    }
+}
+
+__global__ void k_gather_exact(const uint32_t *perm, int64_t n,
+                               const uint32_t *a, const uint32_t *v,
+                               const uint32_t *f, const double *val,
+                               uint32_t *a_out, uint32_t *v_out,
+                               uint32_t *f_out, double *val_out)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = perm[i];
+        a_out[i] = a[p];
+        v_out[i] = v[p];
+        f_out[i] = f[p];
+        val_out[i] = val[p];
+    }
+}
+
+__global__ void k_gather_coo(const int64_t *perm, int64_t n, const uint32_t *a,
+                             const uint32_t *v, const uint32_t *f,
+                             const double *val, uint32_t *a_out,
+                             uint32_t *v_out, uint32_t *f_out, double *val_out)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = perm[i];
+        if (a_out) a_out[i] = a[p];
+        if (v_out) v_out[i] = v[p];
+        if (f_out) f_out[i] = f[p];
+        if (val_out) val_out[i] = val[p];
+    }
+}
+
+// ptr[s] = lower_bound(sorted_keys, s) for s in [0, nseg]
+__global__ void k_segment_starts(const uint32_t *keys, int64_t n, int64_t nseg,
+                                 uint32_t *ptr)
+{
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= nseg;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)keys[mid] < s) lo = mid + 1; else hi = mid;
+        }
+        ptr[s] = static_cast<uint32_t>(lo);
+    }
+}
+
+__global__ void k_absmax_f64(const double *x, int64_t n, unsigned long long *out)
+{
+    double m = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = fmax(m, fabs(x[i]));
+    // nonnegative doubles order like their bit patterns
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_run_flags(const uint32_t *keys, int64_t n, uint8_t *flags,
+                            int *unsorted)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool head = (i == 0) || keys[i] != keys[i - 1];
+        flags[i] = head ? 1 : 0;
+        if (i > 0 && keys[i] < keys[i - 1]) *unsorted = 1;
+    }
+}
+
+__global__ void k_set_i64(int64_t *p, int64_t v) { *p = v; }
+
+static int grid_for(int64_t n, int threads = 256)
+{
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 65535 * 8) b = 65535 * 8;
+    return static_cast<int>(b);
+}
+
+// ---------------------------------------------------------------------------
+// stable radix sort of (u32 key, u32 original index)
+// ---------------------------------------------------------------------------
+static int bits_for(uint64_t max_key)
+{
+    int b = 0;
+    while (b < 32 && (max_key >> b) != 0) ++b;
+    return b < 1 ? 1 : b;
+}
+
+// keys_in is not modified; perm_out[i] = original index of i-th sorted item;
+// keys_out (optional) receives the sorted keys.
+static int stable_sort_u32(const uint32_t *keys_in, int64_t n, uint64_t max_key,
+                           uint32_t *perm_out, uint32_t *keys_out,
+                           cudaStream_t st)
+{
+    if (n == 0) return LIFE_OK;
+    uint32_t *iota = nullptr, *kout = keys_out;
+    LIFE_CUDA(cudaMallocAsync(&iota, n * sizeof(uint32_t), st));
+    bool own_kout = false;
+    if (!kout) {
+        LIFE_CUDA(cudaMallocAsync(&kout, n * sizeof(uint32_t), st));
+        own_kout = true;
+    }
+    k_iota_u32<<<grid_for(n), 256, 0, st>>>(iota, n);
+    LIFE_CHECK_LAUNCH();
+    size_t temp = 0;
+    const int end_bit = bits_for(max_key);
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys_in, kout, iota,
+                                              perm_out, n, 0, end_bit, st));
+    void *d_temp = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&d_temp, temp, st));
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(d_temp, temp, keys_in, kout, iota,
+                                              perm_out, n, 0, end_bit, st));
+    g_launches.fetch_add(4, std::memory_order_relaxed);
+    LIFE_CUDA(cudaFreeAsync(d_temp, st));
+    LIFE_CUDA(cudaFreeAsync(iota, st));
+    if (own_kout) LIFE_CUDA(cudaFreeAsync(kout, st));
+    return LIFE_OK;
+}
+
+// Split [0, nseg) into `parts` contiguous ranges of near-equal cost where
+// cost(s) = count(s) + lambda; counts given by a host prefix array
+// `start[s]` (start[nseg] = total).  Mirrors the balancing intent of
+// engine.build_plan's coefficient split snapped to run boundaries
+// (engine.py:113-184): ranges never cut a segment.
+static std::vector<int> balance_ranges(const std::vector<int64_t> &start,
+                                       int64_t nseg, int parts, double lambda)
+{
+    std::vector<int> out(parts + 1, 0);
+    const double total = (double)start[nseg] + lambda * (double)nseg;
+    int64_t s = 0;
+    for (int i = 1; i < parts; ++i) {
+        const double target = total * (double)i / (double)parts;
+        while (s < nseg && ((double)start[s] + lambda * (double)s) < target) ++s;
+        out[i] = static_cast<int>(s);
+    }
+    out[parts] = static_cast<int>(nseg);
+    for (int i = 1; i <= parts; ++i)
+        if (out[i] < out[i - 1]) out[i] = out[i - 1];
+    return out;
+}
+
+}  // namespace life
+
+using namespace life;
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int life_abi_version(void) { return LIFE_B200_ABI_VERSION; }
+
+const char *life_last_error(void) { return t_last_error.c_str(); }
+
+uint64_t life_launch_count(void) { return g_launches.load(); }
+
+const char *life_status_string(int status)
+{
+    switch (status) {
+    case LIFE_OK: return "ok";
+    case LIFE_ERR_CONFIG_INVALID: return "ConfigInvalid";
+    case LIFE_ERR_DIMENSION_MISMATCH: return "DimensionMismatch";
+    case LIFE_ERR_PLAN_TENSOR_MISMATCH: return "PlanTensorMismatch";
+    case LIFE_ERR_STRATEGY_REQUIRES_SORTED: return "StrategyRequiresSorted";
+    case LIFE_ERR_DEGENERATE_STEP: return "DegenerateStep";
+    case LIFE_ERR_INDEX_OUT_OF_RANGE: return "IndexOutOfRange";
+    case LIFE_ERR_ARITHMETIC_OVERFLOW: return "ArithmeticOverflow";
+    case LIFE_ERR_NOT_SORTED: return "NotSorted";
+    case LIFE_ERR_NON_FINITE: return "NonFiniteValue";
+    case LIFE_ERR_CUDA: return "CudaError";
+    case LIFE_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+    case LIFE_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+    case LIFE_ERR_NCCL: return "NcclError";
+    default: return "unknown";
+    }
+}
+
+int life_stable_argsort_u32(const uint32_t *keys_dev, int64_t n,
+                            int64_t *perm_dev, void *stream)
+{
+    if (n < 0 || (n > 0 && (!keys_dev || !perm_dev)))
+        return fail(LIFE_ERR_INVALID_ARGUMENT, "null array");
+    if (n > 0xFFFFFFFFll)
+        return fail(LIFE_ERR_CONFIG_INVALID, "n exceeds 2^32-1");
+    if (n == 0) return ok();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t *perm32 = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&perm32, n * sizeof(uint32_t), st));
+    LIFE_TRY(stable_sort_u32(keys_dev, n, 0xFFFFFFFFull, perm32, nullptr, st));
+    k_widen_u32_i64<<<grid_for(n), 256, 0, st>>>(perm32, perm_dev, n);
+    LIFE_CHECK_LAUNCH();
+    LIFE_CUDA(cudaFreeAsync(perm32, st));
+    return ok();
+}
+
+int life_detect_runs_u32(const uint32_t *keys_dev, int64_t n,
+                         int64_t *boundaries_dev, uint32_t *run_keys_dev,
+                         int64_t *n_runs_out, void *stream)
+{
+    if (!boundaries_dev || !n_runs_out || (n > 0 && (!keys_dev || !run_keys_dev)))
+        return fail(LIFE_ERR_INVALID_ARGUMENT, "null array");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        k_set_i64<<<1, 1, 0, st>>>(boundaries_dev, 0);
+        LIFE_CHECK_LAUNCH();
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        *n_runs_out = 0;
+        return ok();
+    }
+    uint8_t *flags = nullptr;
+    int *unsorted = nullptr;
+    int64_t *nsel = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&flags, n, st));
+    LIFE_CUDA(cudaMallocAsync(&unsorted, sizeof(int), st));
+    LIFE_CUDA(cudaMallocAsync(&nsel, 2 * sizeof(int64_t), st));
+    LIFE_CUDA(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
+    k_run_flags<<<grid_for(n), 256, 0, st>>>(keys_dev, n, flags, unsorted);
+    LIFE_CHECK_LAUNCH();
+    cub::CountingInputIterator<int64_t> pos(0);
+    size_t t1 = 0, t2 = 0;
+    LIFE_CUDA(cub::DeviceSelect::Flagged(nullptr, t1, pos, flags, boundaries_dev,
+                                         nsel, n, st));
+    LIFE_CUDA(cub::DeviceSelect::Flagged(nullptr, t2, keys_dev, flags,
+                                         run_keys_dev, nsel + 1, n, st));
+    void *temp = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&temp, std::max(t1, t2), st));
+    LIFE_CUDA(cub::DeviceSelect::Flagged(temp, t1, pos, flags, boundaries_dev,
+                                         nsel, n, st));
+    LIFE_CUDA(cub::DeviceSelect::Flagged(temp, t2, keys_dev, flags,
+                                         run_keys_dev, nsel + 1, n, st));
+    g_launches.fetch_add(4, std::memory_order_relaxed);
+    int64_t h_nsel[2] = {0, 0};
+    int h_unsorted = 0;
+    LIFE_CUDA(cudaMemcpyAsync(h_nsel, nsel, sizeof(h_nsel), cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaMemcpyAsync(&h_unsorted, unsorted, sizeof(int),
+                              cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    k_set_i64<<<1, 1, 0, st>>>(boundaries_dev + h_nsel[0], n);
+    LIFE_CHECK_LAUNCH();
+    LIFE_CUDA(cudaFreeAsync(temp, st));
+    LIFE_CUDA(cudaFreeAsync(flags, st));
+    LIFE_CUDA(cudaFreeAsync(unsorted, st));
+    LIFE_CUDA(cudaFreeAsync(nsel, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    if (h_unsorted) return fail(LIFE_ERR_NOT_SORTED, "key array is not sorted");
+    *n_runs_out = h_nsel[0];
+    return ok();
+}
+
+int life_gather_coo(const int64_t *perm_dev, int64_t n, const uint32_t *atoms,
+                    const uint32_t *voxels, const uint32_t *fibers,
+                    const double *values, uint32_t *atoms_out,
+                    uint32_t *voxels_out, uint32_t *fibers_out,
+                    double *values_out, void *stream)
+{
+    if (n == 0) return ok();
+    if (!perm_dev) return fail(LIFE_ERR_INVALID_ARGUMENT, "null perm");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_gather_coo<<<grid_for(n), 256, 0, st>>>(perm_dev, n, atoms, voxels, fibers,
+                                              values, atoms_out, voxels_out,
+                                              fibers_out, values_out);
+    LIFE_CHECK_LAUNCH();
+    return ok();
+}
+
+// ---------------------------------------------------------------------------
+// operator construction
+// ---------------------------------------------------------------------------
+static int build_exact(life_phi *phi, const uint32_t *a, const uint32_t *v,
+                       const uint32_t *f, const double *val, const double *dict,
+                       cudaStream_t st, std::vector<int64_t> &fiber_start)
+{
+    const int64_t n = phi->nc;
+    uint32_t *perm = nullptr, *skeys = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&perm, std::max<int64_t>(n, 1) * sizeof(uint32_t), st));
+    LIFE_CUDA(cudaMallocAsync(&skeys, std::max<int64_t>(n, 1) * sizeof(uint32_t), st));
+    const int exact_threads = 256;
+    phi->xblocks = phi->sms * 4;
+    phi->xW = phi->xblocks * (exact_threads / 32);
+
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool by_voxel = pass == 0;
+        const uint32_t *key = by_voxel ? v : f;
+        const int64_t nseg = by_voxel ? phi->nv : phi->nf;
+        uint32_t **ao = by_voxel ? &phi->xv_atom : &phi->xf_atom;
+        uint32_t **vo = by_voxel ? &phi->xv_voxel : &phi->xf_voxel;
+        uint32_t **fo = by_voxel ? &phi->xv_fiber : &phi->xf_fiber;
+        double **valo = by_voxel ? &phi->xv_val : &phi->xf_val;
+        uint32_t **ptro = by_voxel ? &phi->xv_ptr : &phi->xf_ptr;
+        int **wpo = by_voxel ? &phi->xv_wpart : &phi->xf_wpart;
+        LIFE_TRY(dalloc(phi, ao, n));
+        LIFE_TRY(dalloc(phi, vo, n));
+        LIFE_TRY(dalloc(phi, fo, n));
+        LIFE_TRY(dalloc(phi, valo, n));
+        LIFE_TRY(dalloc(phi, ptro, nseg + 1));
+        LIFE_TRY(stable_sort_u32(key, n, (uint64_t)nseg, perm, skeys, st));
+        if (n > 0) {
+            k_gather_exact<<<grid_for(n), 256, 0, st>>>(perm, n, a, v, f, val, *ao,
+                                                        *vo, *fo, *valo);
+            LIFE_CHECK_LAUNCH();
+        }
+        k_segment_starts<<<grid_for(nseg + 1), 256, 0, st>>>(skeys, n, nseg, *ptro);
+        LIFE_CHECK_LAUNCH();
+        std::vector<uint32_t> hptr(nseg + 1);
+        LIFE_CUDA(cudaMemcpyAsync(hptr.data(), *ptro, (nseg + 1) * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        std::vector<int64_t> start(nseg + 1);
+        for (int64_t s = 0; s <= nseg; ++s) start[s] = hptr[s];
+        std::vector<int> parts = balance_ranges(start, nseg, phi->xW, 2.0);
+        LIFE_TRY(dalloc(phi, wpo, phi->xW + 1));
+        LIFE_CUDA(cudaMemcpyAsync(*wpo, parts.data(), (phi->xW + 1) * sizeof(int),
+                                  cudaMemcpyHostToDevice, st));
+        int64_t runs = 0, mx = 0;
+        for (int64_t s = 0; s < nseg; ++s) {
+            const int64_t len = start[s + 1] - start[s];
+            if (len) ++runs;
+            mx = std::max(mx, len);
+        }
+        if (by_voxel) {
+            phi->n_voxel_runs = runs;
+            phi->max_voxel_run = mx;
+        } else {
+            phi->n_fiber_runs = runs;
+            phi->max_fiber_run = mx;
+            fiber_start = start;
+        }
+        LIFE_CUDA(cudaStreamSynchronize(st));
+    }
+    LIFE_TRY(dalloc(phi, &phi->D64, (size_t)phi->na * phi->nt));
+    LIFE_CUDA(cudaMemcpyAsync(phi->D64, dict, (size_t)phi->na * phi->nt * sizeof(double),
+                              cudaMemcpyDeviceToDevice, st));
+    LIFE_CUDA(cudaFreeAsync(perm, st));
+    LIFE_CUDA(cudaFreeAsync(skeys, st));
+    phi->has_exact = true;
+    return LIFE_OK;
+}
+
+static int build_fast(life_phi *phi, const uint32_t *a, const uint32_t *v,
+                      const uint32_t *f, const double *val,
+                      const std::vector<double> &hdict, cudaStream_t st)
+{
+    const int64_t n = phi->nc;
+    int optin = 0;
+    LIFE_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                     phi->device));
+    const int64_t budget = (int64_t)optin - 4096;  // static smem + slack
+    const int64_t row_bytes = (int64_t)phi->nt * 4;
+    int64_t ag = budget / row_bytes;
+    if (ag < 1) return fail(LIFE_ERR_CONFIG_INVALID, "n_dirs too large for one shared-memory row");
+    int G = 1;
+    if (ag >= phi->na) {
+        ag = phi->na;
+    } else {
+        G = (int)((phi->na + ag - 1) / ag);
+        ag = (phi->na + G - 1) / G;  // equalize the groups
+    }
+    if ((int64_t)G * phi->nv >= 0xFFFFFFFFll)
+        return fail(LIFE_ERR_CONFIG_INVALID, "atom groups x voxels exceed u32 keys");
+    phi->G = G;
+    phi->ag = (int)ag;
+    phi->slice_floats = (int)(((ag * phi->nt) + 3) / 4 * 4);
+    phi->smem = (size_t)phi->slice_floats * sizeof(float);
+
+    // persistent grid: one 512-thread CTA per SM (the slice fills shared memory)
+    int bps = 1;
+    phi->nblocks = phi->sms * bps;
+    phi->W = phi->nblocks * (kSpmvThreads / 32);
+
+    // sort by (group, voxel), stable
+    uint32_t *key = nullptr, *skeys = nullptr, *perm = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&key, std::max<int64_t>(n, 1) * sizeof(uint32_t), st));
+    LIFE_CUDA(cudaMallocAsync(&skeys, std::max<int64_t>(n, 1) * sizeof(uint32_t), st));
+    LIFE_CUDA(cudaMallocAsync(&perm, std::max<int64_t>(n, 1) * sizeof(uint32_t), st));
+    const int64_t nseg = (int64_t)G * phi->nv;
+    if (n > 0) {
+        k_group_voxel_key<<<grid_for(n), 256, 0, st>>>(a, v, n, (uint32_t)ag,
+                                                       (uint32_t)phi->nv, key);
+        LIFE_CHECK_LAUNCH();
+    }
+    LIFE_TRY(stable_sort_u32(key, n, (uint64_t)nseg, perm, skeys, st));
+    LIFE_TRY(dalloc(phi, &phi->atom, n));
+    LIFE_TRY(dalloc(phi, &phi->fiber, n));
+    LIFE_TRY(dalloc(phi, &phi->val, n));
+    LIFE_TRY(dalloc(phi, &phi->gptr, nseg + 1));
+    if (n > 0) {
+        k_gather_fast<<<grid_for(n), 256, 0, st>>>(perm, n, a, f, val, (uint32_t)ag,
+                                                   phi->atom, phi->fiber, phi->val);
+        LIFE_CHECK_LAUNCH();
+    }
+    k_segment_starts<<<grid_for(nseg + 1), 256, 0, st>>>(skeys, n, nseg, phi->gptr);
+    LIFE_CHECK_LAUNCH();
+    std::vector<uint32_t> hptr(nseg + 1);
+    LIFE_CUDA(cudaMemcpyAsync(hptr.data(), phi->gptr, (nseg + 1) * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    // per-voxel totals over groups -> warp partition
+    std::vector<int64_t> start(phi->nv + 1, 0);
+    int64_t runs = 0, mx = 0;
+    for (int64_t vv = 0; vv < phi->nv; ++vv) {
+        int64_t tot = 0;
+        for (int g = 0; g < G; ++g)
+            tot += (int64_t)hptr[(int64_t)g * phi->nv + vv + 1] - hptr[(int64_t)g * phi->nv + vv];
+        start[vv + 1] = start[vv] + tot;
+        if (tot) ++runs;
+        mx = std::max(mx, tot);
+    }
+    phi->n_voxel_runs = runs;
+    phi->max_voxel_run = mx;
+    std::vector<int> parts = balance_ranges(start, phi->nv, phi->W, 2.0);
+    LIFE_TRY(dalloc(phi, &phi->wpart, phi->W + 1));
+    LIFE_CUDA(cudaMemcpyAsync(phi->wpart, parts.data(), (phi->W + 1) * sizeof(int),
+                              cudaMemcpyHostToDevice, st));
+    // fp32 dictionary slices, each 16-byte aligned
+    std::vector<float> hD((size_t)G * phi->slice_floats, 0.f);
+    for (int64_t at = 0; at < phi->na; ++at) {
+        const int64_t g = at / ag, al = at % ag;
+        for (int t = 0; t < phi->nt; ++t)
+            hD[(size_t)g * phi->slice_floats + al * phi->nt + t] =
+                static_cast<float>(hdict[(size_t)at * phi->nt + t]);
+    }
+    LIFE_TRY(dalloc(phi, &phi->Dg, hD.size()));
+    LIFE_CUDA(cudaMemcpyAsync(phi->Dg, hD.data(), hD.size() * sizeof(float),
+                              cudaMemcpyHostToDevice, st));
+    LIFE_TRY(dalloc(phi, &phi->wfix, phi->nf));
+    LIFE_CUDA(cudaMemsetAsync(phi->wfix, 0, (size_t)phi->nf * sizeof(unsigned long long), st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    LIFE_CUDA(cudaFreeAsync(key, st));
+    LIFE_CUDA(cudaFreeAsync(skeys, st));
+    LIFE_CUDA(cudaFreeAsync(perm, st));
+    phi->has_fast = true;
+    return LIFE_OK;
+}
+
+__global__ void k_fiber_hist(const uint32_t *f, int64_t n, unsigned *count)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&count[f[i]], 1u);
+}
+
+__global__ void k_max_u32(const unsigned *x, int64_t n, unsigned *mx, unsigned *nz)
+{
+    unsigned m = 0, c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        m = max(m, x[i]);
+        c += x[i] ? 1u : 0u;
+    }
+    atomicMax(mx, m);
+    atomicAdd(nz, c);
+}
+
+static int create_impl(const life_dims *dims, const uint32_t *atoms,
+                       const uint32_t *voxels, const uint32_t *fibers,
+                       const double *values, const double *dict, uint32_t flags,
+                       cudaStream_t st, life_phi **out, int64_t *bad_position)
+{
+    if (!dims || !out) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (dims->n_atoms <= 0 || dims->n_voxels <= 0 || dims->n_fibers <= 0 ||
+        dims->n_dirs <= 0 || dims->n_coeffs < 0)
+        return fail(LIFE_ERR_CONFIG_INVALID, "dimensions must be positive");
+    if (dims->n_atoms > 0x7FFFFFFF || dims->n_voxels > 0x7FFFFFFF ||
+        dims->n_fibers > 0x7FFFFFFF || dims->n_coeffs > 0xFFFFFFFEll)
+        return fail(LIFE_ERR_CONFIG_INVALID, "dimension exceeds the 32-bit index space");
+    if (dims->n_dirs > 32 * kMaxNT)
+        return fail(LIFE_ERR_CONFIG_INVALID, "n_dirs > 320 unsupported");
+    if (dims->n_voxels * dims->n_dirs > 0xFFFFFFFFll * 4)
+        return fail(LIFE_ERR_ARITHMETIC_OVERFLOW, "signal length too large");
+    const int64_t n = dims->n_coeffs;
+    if (n > 0 && (!atoms || !voxels || !fibers || !values))
+        return fail(LIFE_ERR_INVALID_ARGUMENT, "null coefficient array");
+    if (!dict) return fail(LIFE_ERR_INVALID_ARGUMENT, "null dictionary");
+
+    auto t0 = std::chrono::steady_clock::now();
+    life_phi *phi = new life_phi();
+    phi->dims = *dims;
+    phi->na = (int)dims->n_atoms;
+    phi->nv = (int)dims->n_voxels;
+    phi->nf = (int)dims->n_fibers;
+    phi->nt = (int)dims->n_dirs;
+    phi->nc = n;
+    LIFE_CUDA(cudaGetDevice(&phi->device));
+    LIFE_CUDA(cudaDeviceGetAttribute(&phi->sms, cudaDevAttrMultiProcessorCount, phi->device));
+
+    struct Guard {
+        life_phi **slot;
+        life_phi *p;
+        std::vector<void *> tmp;
+        cudaStream_t st;
+        ~Guard()
+        {
+            for (void *q : tmp) cudaFree(q);
+            if (p) life_phi_destroy(p);
+        }
+    } guard{out, phi, {}, st};
+
+    const bool host = flags & LIFE_PHI_HOST_INPUT;
+    const uint32_t *a = atoms, *v = voxels, *f = fibers;
+    const double *val = values, *D = dict;
+    const size_t dlen = (size_t)phi->na * phi->nt;
+    if (host) {
+        uint32_t *da, *dv, *df;
+        double *dval, *dD;
+        const size_t nn = std::max<int64_t>(n, 1);
+        LIFE_CUDA(cudaMalloc(&da, nn * 4)); guard.tmp.push_back(da);
+        LIFE_CUDA(cudaMalloc(&dv, nn * 4)); guard.tmp.push_back(dv);
+        LIFE_CUDA(cudaMalloc(&df, nn * 4)); guard.tmp.push_back(df);
+        LIFE_CUDA(cudaMalloc(&dval, nn * 8)); guard.tmp.push_back(dval);
+        LIFE_CUDA(cudaMalloc(&dD, dlen * 8)); guard.tmp.push_back(dD);
+        if (n > 0) {
+            LIFE_CUDA(cudaMemcpyAsync(da, atoms, n * 4, cudaMemcpyHostToDevice, st));
+            LIFE_CUDA(cudaMemcpyAsync(dv, voxels, n * 4, cudaMemcpyHostToDevice, st));
+            LIFE_CUDA(cudaMemcpyAsync(df, fibers, n * 4, cudaMemcpyHostToDevice, st));
+            LIFE_CUDA(cudaMemcpyAsync(dval, values, n * 8, cudaMemcpyHostToDevice, st));
+        }
+        LIFE_CUDA(cudaMemcpyAsync(dD, dict, dlen * 8, cudaMemcpyHostToDevice, st));
+        a = da; v = dv; f = df; val = dval; D = dD;
+    }
+
+    // index range check (validate(), tensor.py:232-286; first bad position)
+    {
+        unsigned long long *bad = nullptr;
+        LIFE_CUDA(cudaMalloc(&bad, 3 * sizeof(unsigned long long)));
+        guard.tmp.push_back(bad);
+        LIFE_CUDA(cudaMemsetAsync(bad, 0xFF, 3 * sizeof(unsigned long long), st));
+        if (n > 0) {
+            k_check_range<<<grid_for(n), 256, 0, st>>>(a, v, f, n, phi->na, phi->nv,
+                                                       phi->nf, bad);
+            LIFE_CHECK_LAUNCH();
+        }
+        unsigned long long hb[3];
+        LIFE_CUDA(cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        static const char *names[3] = {"atom", "voxel", "fiber"};
+        for (int i = 0; i < 3; ++i)
+            if (hb[i] != ~0ull) {
+                if (bad_position) *bad_position = (int64_t)hb[i];
+                return fail(LIFE_ERR_INDEX_OUT_OF_RANGE,
+                            std::string(names[i]) + " index out of range at position " +
+                                std::to_string(hb[i]));
+            }
+    }
+
+    // host copy of the dictionary (small): fp32 slices and row norms
+    std::vector<double> hdict(dlen);
+    LIFE_CUDA(cudaMemcpyAsync(hdict.data(), D, dlen * 8, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    double dmax = 0.0;
+    for (int64_t at = 0; at < phi->na; ++at) {
+        double s = 0.0;
+        for (int t = 0; t < phi->nt; ++t) s += hdict[at * phi->nt + t] * hdict[at * phi->nt + t];
+        dmax = std::max(dmax, std::sqrt(s));
+    }
+    phi->dmax = dmax * (1.0 + 1e-6);
+    {
+        unsigned long long *vm = nullptr;
+        unsigned *cnt = nullptr, *mx = nullptr;
+        LIFE_CUDA(cudaMalloc(&vm, 8)); guard.tmp.push_back(vm);
+        LIFE_CUDA(cudaMalloc(&cnt, (size_t)phi->nf * 4)); guard.tmp.push_back(cnt);
+        LIFE_CUDA(cudaMalloc(&mx, 8)); guard.tmp.push_back(mx);
+        LIFE_CUDA(cudaMemsetAsync(vm, 0, 8, st));
+        LIFE_CUDA(cudaMemsetAsync(cnt, 0, (size_t)phi->nf * 4, st));
+        LIFE_CUDA(cudaMemsetAsync(mx, 0, 8, st));
+        if (n > 0) {
+            k_absmax_f64<<<std::min(grid_for(n), phi->sms * 8), 256, 0, st>>>(val, n, vm);
+            LIFE_CHECK_LAUNCH();
+            k_fiber_hist<<<grid_for(n), 256, 0, st>>>(f, n, cnt);
+            LIFE_CHECK_LAUNCH();
+        }
+        k_max_u32<<<std::min(grid_for(phi->nf), phi->sms * 8), 256, 0, st>>>(cnt, phi->nf, mx, mx + 1);
+        LIFE_CHECK_LAUNCH();
+        unsigned long long hvm;
+        unsigned hmx[2];
+        LIFE_CUDA(cudaMemcpyAsync(&hvm, vm, 8, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaMemcpyAsync(hmx, mx, 8, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        double dv;
+        std::memcpy(&dv, &hvm, 8);
+        phi->vmax = dv * (1.0 + 1e-6);
+        phi->fmax_nnz = std::max<int64_t>(hmx[0], 1);
+        phi->max_fiber_run = hmx[0];
+        phi->n_fiber_runs = hmx[1];
+    }
+
+    if (!(flags & LIFE_PHI_NO_FAST_F32))
+        LIFE_TRY(build_fast(phi, a, v, f, val, hdict, st));
+    std::vector<int64_t> fiber_start;
+    if (flags & LIFE_PHI_EXACT_F64)
+        LIFE_TRY(build_exact(phi, a, v, f, val, D, st, fiber_start));
+
+    // reduction scratch
+    phi->red_cap = std::max(std::max(phi->W, phi->xW), phi->sms * 8) + 1;
+    LIFE_TRY(dalloc(phi, &phi->red.part_d, phi->red_cap));
+    LIFE_TRY(dalloc(phi, &phi->red.part_u, phi->red_cap));
+    LIFE_TRY(dalloc(phi, &phi->red.part_f, phi->red_cap));
+    LIFE_TRY(dalloc(phi, &phi->red.counter, 4));
+    LIFE_TRY(dalloc(phi, &phi->part_d2, phi->red_cap));
+    LIFE_TRY(dalloc(phi, &phi->part_u2, phi->red_cap));
+    LIFE_TRY(dalloc(phi, &phi->counter2, 4));
+    LIFE_TRY(dalloc(phi, &phi->ybound, 4));
+    LIFE_CUDA(cudaMemsetAsync(phi->red.counter, 0, 16, st));
+    LIFE_CUDA(cudaMemsetAsync(phi->counter2, 0, 16, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    phi->sort_ms = std::chrono::duration<double, std::milli>(
+                       std::chrono::steady_clock::now() - t0).count();
+    guard.p = nullptr;
+    *out = phi;
+    return ok();
+}
+
+int life_phi_create(const life_dims *dims, const uint32_t *atoms,
+                    const uint32_t *voxels, const uint32_t *fibers,
+                    const double *values, const double *dict, uint32_t flags,
+                    void *stream, life_phi **out, int64_t *bad_position)
+{
+    return create_impl(dims, atoms, voxels, fibers, values, dict, flags,
+                       static_cast<cudaStream_t>(stream), out, bad_position);
+}
+
+int life_phi_destroy(life_phi *phi)
+{
+    if (!phi) return ok();
+    cudaDeviceSynchronize();
+    for (void *p : phi->allocs) cudaFree(p);
+    delete phi;
+    return ok();
+}
+
+int life_phi_get_info(const life_phi *phi, life_phi_info *info)
+{
+    if (!phi || !info) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
+    info->dims = phi->dims;
+    info->atom_groups = phi->G;
+    info->atoms_per_group = phi->ag;
+    info->n_warps = phi->W;
+    info->has_exact = phi->has_exact ? 1 : 0;
+    info->n_voxel_runs = phi->n_voxel_runs;
+    info->n_fiber_runs = phi->n_fiber_runs;
+    info->max_fiber_run = phi->max_fiber_run;
+    info->max_voxel_run = phi->max_voxel_run;
+    info->device_bytes = phi->device_bytes;
+    info->sort_ms = phi->sort_ms;
+    return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,237 @@
+"""Device-resident operator: a life_phi handle plus its call wrappers.
+
+``DeviceOperator`` owns the restructured copies of Phi and D in HBM
+(C-ABI ``life_phi_create``).  ``dsc``/``wc`` run one product through the
+C ABI on either host arrays (numpy: copied in and out) or CUDA tensors
+(used in place).  Two precisions:
+
+* ``"fp32"`` -- the fast path (fp32 values, FFMA, fixed-point WC
+  accumulation); within ~1e-7 relative of the reference.
+* ``"fp64"`` -- the bit-exact path: same rounding and per-output order as
+  the reference loops (_kernels.py:14-68), equal to
+  ``dsc_sequential``/``wc_sequential`` bit for bit.
+"""
+
+import ctypes
+import weakref
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigInvalid, DimensionMismatch
+from .tensor import OffsetPhiTensor
+
+_DEFAULT_PRECISION = ["fp32"]
+
+
+def set_default_precision(precision):
+    if precision not in ("fp32", "fp64"):
+        raise ConfigInvalid(f"precision must be 'fp32' or 'fp64', got {precision!r}")
+    _DEFAULT_PRECISION[0] = precision
+
+
+def default_precision():
+    return _DEFAULT_PRECISION[0]
+
+
+def _phi(tensor):
+    return tensor.tensor if isinstance(tensor, OffsetPhiTensor) else tensor
+
+
+def _u32_cuda(torch, arr):
+    a = np.ascontiguousarray(arr, dtype=np.uint32)
+    return torch.from_numpy(a.view(np.int32)).to("cuda")
+
+
+class DeviceOperator:
+    """The operator M = Phi x_1 D resident on the current CUDA device."""
+
+    def __init__(self, tensor, dictionary, exact=False, fast=True, stream=None):
+        torch = N.require_cuda()
+        phi = _phi(tensor)
+        d = phi.dims
+        if dictionary.data.shape[0] != d.dict_len:
+            raise DimensionMismatch("dictionary length != n_atoms * n_dirs")
+        self.dims = d
+        self.exact = bool(exact)
+        self.fast = bool(fast)
+        nc = d.n_coeffs
+        a = _u32_cuda(torch, phi.atoms) if nc else None
+        v = _u32_cuda(torch, phi.voxels) if nc else None
+        f = _u32_cuda(torch, phi.fibers) if nc else None
+        val = torch.from_numpy(np.ascontiguousarray(phi.values)).to("cuda") if nc else None
+        dic = torch.from_numpy(np.ascontiguousarray(dictionary.data)).to("cuda")
+        self._create(d, a, v, f, val, dic, stream)
+
+    @classmethod
+    def from_device(cls, dims, atoms, voxels, fibers, values, dictionary,
+                    exact=False, fast=True, stream=None):
+        """Build from CUDA tensors (u32 indices viewed as int32, f64 values)."""
+        self = cls.__new__(cls)
+        N.require_cuda()
+        self.dims, self.exact, self.fast = dims, bool(exact), bool(fast)
+        self._create(dims, atoms, voxels, fibers, values, dictionary, stream)
+        return self
+
+    def _create(self, d, a, v, f, val, dic, stream):
+        flags = (N.PHI_EXACT_F64 if self.exact else 0) | (0 if self.fast else N.PHI_NO_FAST_F32)
+        dims = N.Dims(d.n_atoms, d.n_voxels, d.n_fibers, d.n_dirs, d.n_coeffs)
+        handle = ctypes.c_void_p()
+        bad = ctypes.c_int64(-1)
+        ptr = (lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None)
+        st = N.stream_ptr(stream)
+        rc = N.lib().life_phi_create(ctypes.byref(dims), ptr(a), ptr(v), ptr(f), ptr(val),
+                                     ptr(dic), flags, st, ctypes.byref(handle),
+                                     ctypes.byref(bad))
+        N.check(rc, bad.value)
+        self._handle = handle
+        self._finalizer = weakref.finalize(self, N.lib().life_phi_destroy, handle)
+        info = N.PhiInfo()
+        N.check(N.lib().life_phi_get_info(handle, ctypes.byref(info)))
+        self.info = info
+
+    @property
+    def handle(self):
+        return self._handle
+
+    def close(self):
+        self._finalizer()
+
+    # ---- products on device tensors -------------------------------------
+    def dsc_f32(self, w, y, b=None, flags=0, skipped=None, sumsq=None, absmax=None,
+                stream=None):
+        out = N.SpmvOut(_p(skipped), _p(sumsq), _p(absmax))
+        N.check(N.lib().life_dsc_f32(self._handle, _p(w), _p(y), _p(b), flags,
+                                     ctypes.byref(out), N.stream_ptr(stream)))
+
+    def wc_f32(self, y, w, w_ref=None, y_absmax=None, flags=0, sumsq=None, stream=None):
+        out = N.SpmvOut(None, _p(sumsq), None)
+        N.check(N.lib().life_wc_f32(self._handle, _p(y), _p(w), _p(w_ref), _p(y_absmax),
+                                    flags, ctypes.byref(out), N.stream_ptr(stream)))
+
+    def dsc_f64(self, w, y, flags=0, skipped=None, stream=None):
+        N.check(N.lib().life_dsc_f64(self._handle, _p(w), _p(y), flags, _p(skipped),
+                                     N.stream_ptr(stream)))
+
+    def wc_f64(self, y, w, stream=None):
+        N.check(N.lib().life_wc_f64(self._handle, _p(y), _p(w), N.stream_ptr(stream)))
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def operator_for(tensor, dictionary, exact=False):
+    """Cached DeviceOperator for (tensor, dictionary); rebuilt when the exact
+    layout is requested but missing."""
+    phi = _phi(tensor)
+    cache = phi.__dict__.setdefault("_device_cache", {})
+    entry = cache.get("op")
+    if entry is not None:
+        op, dic = entry
+        if dic is dictionary and (op.exact or not exact):
+            return op
+        op.close()
+    op = DeviceOperator(phi, dictionary, exact=exact, fast=True)
+    cache["op"] = (op, dictionary)
+    return op
+
+
+# ---- reference-shaped products (accumulate into caller buffers) ------------
+
+
+def _as_device(torch, x, dtype):
+    if isinstance(x, torch.Tensor):
+        if not x.is_cuda:
+            return x.to(device="cuda", dtype=dtype).contiguous()
+        return x.to(dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(
+        device="cuda", dtype=dtype)
+
+
+def _accumulate_into(torch, dst, add):
+    """dst += add, keeping dst's own storage and dtype."""
+    if isinstance(dst, torch.Tensor):
+        dst.add_(add.to(device=dst.device, dtype=dst.dtype))
+    else:
+        dst += add.double().cpu().numpy()
+
+
+def dsc_accumulate(tensor, dictionary, w, y_out, skip_zero=True, precision=None):
+    """y_out += M w; returns (skipped, gpu_seconds)."""
+    torch = N.require_cuda()
+    precision = precision or default_precision()
+    op = operator_for(tensor, dictionary, exact=(precision == "fp64"))
+    d = op.dims
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    skipped = torch.zeros(1, dtype=torch.int64, device="cuda")
+    flags = N.SKIP_ZERO if skip_zero else 0
+    if precision == "fp64":
+        wd = _as_device(torch, w, torch.float64)
+        if isinstance(y_out, torch.Tensor) and y_out.is_cuda and y_out.dtype == torch.float64 \
+                and y_out.is_contiguous():
+            yd = y_out
+        else:
+            yd = _as_device(torch, y_out, torch.float64)
+        start.record()
+        op.dsc_f64(wd, yd, flags, skipped)
+        stop.record()
+        if yd is not y_out:
+            if isinstance(y_out, torch.Tensor):
+                y_out.copy_(yd)
+            else:
+                y_out[...] = yd.cpu().numpy()
+    else:
+        wd = _as_device(torch, w, torch.float32)
+        if isinstance(y_out, torch.Tensor) and y_out.is_cuda and y_out.dtype == torch.float32 \
+                and y_out.is_contiguous():
+            start.record()
+            op.dsc_f32(wd, y_out, None, flags | N.ACCUMULATE, skipped)
+            stop.record()
+        else:
+            yd = torch.empty(d.signal_len, dtype=torch.float32, device="cuda")
+            start.record()
+            op.dsc_f32(wd, yd, None, flags, skipped)
+            stop.record()
+            _accumulate_into(torch, y_out, yd)
+    torch.cuda.synchronize()
+    return int(skipped.item()), start.elapsed_time(stop) * 1e-3
+
+
+def wc_accumulate(tensor, dictionary, y, w_out, precision=None):
+    """w_out += M^T y; returns gpu_seconds."""
+    torch = N.require_cuda()
+    precision = precision or default_precision()
+    op = operator_for(tensor, dictionary, exact=(precision == "fp64"))
+    d = op.dims
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if precision == "fp64":
+        yd = _as_device(torch, y, torch.float64)
+        if isinstance(w_out, torch.Tensor) and w_out.is_cuda and w_out.dtype == torch.float64 \
+                and w_out.is_contiguous():
+            wd = w_out
+        else:
+            wd = _as_device(torch, w_out, torch.float64)
+        start.record()
+        op.wc_f64(yd, wd)
+        stop.record()
+        if wd is not w_out:
+            if isinstance(w_out, torch.Tensor):
+                w_out.copy_(wd)
+            else:
+                w_out[...] = wd.cpu().numpy()
+    else:
+        yd = _as_device(torch, y, torch.float32)
+        if isinstance(w_out, torch.Tensor) and w_out.is_cuda and w_out.dtype == torch.float32 \
+                and w_out.is_contiguous():
+            start.record()
+            op.wc_f32(yd, w_out, flags=N.ACCUMULATE)
+            stop.record()
+        else:
+            wd = torch.empty(d.n_fibers, dtype=torch.float32, device="cuda")
+            start.record()
+            op.wc_f32(yd, wd)
+            stop.record()
+            _accumulate_into(torch, w_out, wd)
+    torch.cuda.synchronize()
+    return start.elapsed_time(stop) * 1e-3
