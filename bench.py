@@ -214,6 +214,8 @@ def run_ours(args, dims):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
+    from paper_1905_06234_b200 import device as _dev
+    _dev.set_layout(args.layout)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -230,6 +232,7 @@ def run_ours(args, dims):
     op = L.DeviceOperator(problem.tensor, problem.dictionary)
     info["restructure_ms"] = round(op.info.sort_ms, 1)
     info["atom_groups"] = op.info.atom_groups
+    info["kernels"] = op.kind
     b = torch.from_numpy(problem.y).to(device="cuda", dtype=torch.float32)
     w = torch.empty(nf, dtype=torch.float32, device="cuda")
     scfg = L.SolverConfig(max_iters=total_iters, grad_tol=0.0)
@@ -358,6 +361,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--layout", default="auto", choices=["auto", "sparse", "dense"])
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -20,6 +20,8 @@ c_void_p, c_double = ctypes.c_void_p, ctypes.c_double
 PHI_HOST_INPUT = 0x1
 PHI_EXACT_F64 = 0x2
 PHI_NO_FAST_F32 = 0x4
+PHI_FORCE_SPARSE = 0x8
+PHI_FORCE_DENSE = 0x10
 ACCUMULATE = 0x01
 SKIP_ZERO = 0x02
 SUBTRACT_B = 0x04

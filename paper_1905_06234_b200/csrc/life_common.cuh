@@ -96,6 +96,17 @@ struct life_phi {
     int nblocks = 0, W = 0;
     size_t smem = 0;
 
+    // dense tile layout (register-tiled kernels, life_dense.cu): coefficients
+    // sorted by (voxel tile of 16, atom chunk of 64, duplicate rank, cell)
+    bool has_dense = false;
+    uint32_t *d_cr = nullptr;     // rank << 10 | (atom%64)*16 + voxel%16
+    uint32_t *d_fiber = nullptr;
+    float *d_val = nullptr;
+    uint32_t *d_tptr = nullptr;   // [n_tiles*n_chunks + 1]
+    float *d_D = nullptr;         // [n_chunks][64][nt_pad] zero padded
+    int n_tiles = 0, n_chunks = 0, nt_pad = 0, d_blocks = 0, d_W = 0;
+    size_t d_smem = 0;
+
     // fixed-point WC accumulator and its scale inputs
     unsigned long long *wfix = nullptr;  // [nf] two's-complement int64
     double vmax = 0.0;                   // max |value|
@@ -164,6 +175,16 @@ __host__ __device__ inline int wc_fix_exponent(double vmax, double dmax,
     return ex;
 }
 
+// Raise (never lower) a kernel's dynamic shared-memory limit.  The attribute
+// caps every later launch of that function, so lowering it for a small
+// operator would break a larger operator still in use.
+int ensure_smem_ptr(const void *func, size_t bytes);
+template <typename F>
+int ensure_smem(F *func, size_t bytes)
+{
+    return ensure_smem_ptr(reinterpret_cast<const void *>(func), bytes);
+}
+
 // Internal launchers exposed across translation units.
 struct DscOut {
     unsigned long long *skipped;
@@ -178,4 +199,6 @@ int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
               const float *ymax_dev, uint32_t flags, double *sumsq,
               const CallHooks &h, cudaStream_t st);
 int prepare_spmv(life_phi *phi);
+int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
+                const double *val, const std::vector<double> &hdict, cudaStream_t st);
 }  // namespace life

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "life_common.cuh"
 
@@ -30,6 +31,21 @@ int fail(int status, const std::string &msg)
 int ok()
 {
     t_last_error.clear();
+    return LIFE_OK;
+}
+
+int ensure_smem_ptr(const void *func, size_t bytes)
+{
+    static std::mutex mu;
+    static std::unordered_map<const void *, size_t> have;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t &cur = have[func];
+    if (bytes <= cur || bytes <= 48 * 1024) return LIFE_OK;
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bytes);
+    if (e != cudaSuccess)
+        return fail(LIFE_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    cur = bytes;
     return LIFE_OK;
 }
 
@@ -513,8 +529,6 @@ static int build_fast(life_phi *phi, const uint32_t *a, const uint32_t *v,
     LIFE_TRY(dalloc(phi, &phi->Dg, hD.size()));
     LIFE_CUDA(cudaMemcpyAsync(phi->Dg, hD.data(), hD.size() * sizeof(float),
                               cudaMemcpyHostToDevice, st));
-    LIFE_TRY(dalloc(phi, &phi->wfix, phi->nf));
-    LIFE_CUDA(cudaMemsetAsync(phi->wfix, 0, (size_t)phi->nf * sizeof(unsigned long long), st));
     LIFE_CUDA(cudaStreamSynchronize(st));
     LIFE_CUDA(cudaFreeAsync(key, st));
     LIFE_CUDA(cudaFreeAsync(skeys, st));
@@ -675,14 +689,45 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         phi->n_fiber_runs = hmx[1];
     }
 
-    if (!(flags & LIFE_PHI_NO_FAST_F32))
-        LIFE_TRY(build_fast(phi, a, v, f, val, hdict, st));
+    if (!(flags & LIFE_PHI_NO_FAST_F32)) {
+        // Layout choice: register-tiled dense kernels when voxels
+        // carry >= 1/8 of all atoms on average, sparse segment kernels
+        // otherwise; flags can force either.
+        int64_t occupied = 0;
+        {
+            unsigned *cnt = nullptr, *mx = nullptr;
+            LIFE_CUDA(cudaMalloc(&cnt, (size_t)phi->nv * 4)); guard.tmp.push_back(cnt);
+            LIFE_CUDA(cudaMalloc(&mx, 8)); guard.tmp.push_back(mx);
+            LIFE_CUDA(cudaMemsetAsync(cnt, 0, (size_t)phi->nv * 4, st));
+            LIFE_CUDA(cudaMemsetAsync(mx, 0, 8, st));
+            if (n > 0) {
+                k_fiber_hist<<<grid_for(n), 256, 0, st>>>(v, n, cnt);
+                LIFE_CHECK_LAUNCH();
+            }
+            k_max_u32<<<std::min(grid_for(phi->nv), phi->sms * 8), 256, 0, st>>>(cnt, phi->nv, mx, mx + 1);
+            LIFE_CHECK_LAUNCH();
+            unsigned hm[2];
+            LIFE_CUDA(cudaMemcpyAsync(hm, mx, 8, cudaMemcpyDeviceToHost, st));
+            LIFE_CUDA(cudaStreamSynchronize(st));
+            occupied = hm[1];
+            phi->n_voxel_runs = hm[1];
+            phi->max_voxel_run = hm[0];
+        }
+        bool dense = (n * 8 >= occupied * (int64_t)phi->na) && n > 0;
+        if (flags & LIFE_PHI_FORCE_SPARSE) dense = false;
+        if (flags & LIFE_PHI_FORCE_DENSE) dense = n > 0;
+        if (dense) LIFE_TRY(build_dense(phi, a, v, f, val, hdict, st));
+        if (!phi->has_dense) LIFE_TRY(build_fast(phi, a, v, f, val, hdict, st));
+    }
     std::vector<int64_t> fiber_start;
     if (flags & LIFE_PHI_EXACT_F64)
         LIFE_TRY(build_exact(phi, a, v, f, val, D, st, fiber_start));
 
     // reduction scratch
-    phi->red_cap = std::max(std::max(phi->W, phi->xW), phi->sms * 8) + 1;
+    // fixed-point WC accumulator (both fp32 kernel families)
+    LIFE_TRY(dalloc(phi, &phi->wfix, phi->nf));
+    LIFE_CUDA(cudaMemsetAsync(phi->wfix, 0, (size_t)phi->nf * sizeof(unsigned long long), st));
+    phi->red_cap = std::max(std::max(std::max(phi->W, phi->xW), phi->d_W), phi->sms * 8) + 1;
     LIFE_TRY(dalloc(phi, &phi->red.part_d, phi->red_cap));
     LIFE_TRY(dalloc(phi, &phi->red.part_u, phi->red_cap));
     LIFE_TRY(dalloc(phi, &phi->red.part_f, phi->red_cap));
@@ -723,7 +768,7 @@ int life_phi_get_info(const life_phi *phi, life_phi_info *info)
 {
     if (!phi || !info) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
     info->dims = phi->dims;
-    info->atom_groups = phi->G;
+    info->atom_groups = phi->has_dense ? 0 : phi->G;
     info->atoms_per_group = phi->ag;
     info->n_warps = phi->W;
     info->has_exact = phi->has_exact ? 1 : 0;

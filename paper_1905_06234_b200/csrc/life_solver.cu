@@ -367,7 +367,7 @@ extern "C" int life_sbb_create(life_phi *phi, const void *b_dev, void *w_dev,
     const bool exact = cfg->exact_f64 != 0;
     if (exact && !phi->has_exact)
         return fail(LIFE_ERR_CONFIG_INVALID, "exact_f64 needs an operator built with LIFE_PHI_EXACT_F64");
-    if (!exact && !phi->has_fast)
+    if (!exact && !phi->has_fast && !phi->has_dense)
         return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t ny = (int64_t)phi->nv * phi->nt;
@@ -448,11 +448,18 @@ extern "C" int life_sbb_create(life_phi *phi, const void *b_dev, void *w_dev,
         if (cfg->use_graph) {
             // capture one odd+even iteration pair; replays are parity-correct
             // because pairs always start at an odd iteration index
-            LIFE_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            // (captured on a private stream: the legacy default stream cannot
+            // be captured; the graph is launched on the caller's stream)
+            cudaStream_t cs = nullptr;
+            LIFE_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            S.st = cs;
+            LIFE_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
             const uint64_t before = g_launches.load();
             int rc = iter_fast(S, (const float *)b_dev, (float *)w_dev, 0);
             if (rc == LIFE_OK) rc = iter_fast(S, (const float *)b_dev, (float *)w_dev, 1);
-            cudaError_t ce = cudaStreamEndCapture(st, &x->graph);
+            cudaError_t ce = cudaStreamEndCapture(cs, &x->graph);
+            cudaStreamDestroy(cs);
+            S.st = st;
             x->graph_kernels = g_launches.load() - before;
             g_launches.fetch_sub(x->graph_kernels);  // counted when replayed
             if (rc != LIFE_OK) return rc;

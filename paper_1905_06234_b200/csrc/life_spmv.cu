@@ -628,13 +628,7 @@ static int launch_dsc_t(life_phi *phi, const float *w, float *y, const float *b,
                         uint32_t flags, const DscOut &o, const CallHooks &h,
                         cudaStream_t st)
 {
-    static size_t attr_smem = 0;
-    if (phi->smem > attr_smem) {
-        LIFE_CUDA(cudaFuncSetAttribute(k_dsc_f32<NT, FULL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)phi->smem));
-        attr_smem = phi->smem;
-    }
+    LIFE_TRY(ensure_smem(k_dsc_f32<NT, FULL>, phi->smem));
     FastArgs A{phi->atom, phi->fiber, phi->val, phi->gptr, phi->wpart, phi->Dg,
                phi->nv, phi->nt, phi->G, phi->ag, phi->na, phi->slice_floats};
     k_dsc_f32<NT, FULL><<<phi->nblocks, kSpmvThreads, phi->smem, st>>>(
@@ -647,13 +641,7 @@ template <int NT, bool FULL>
 static int launch_wc_t(life_phi *phi, const float *y, const WcFix &fx,
                        const CallHooks &h, cudaStream_t st)
 {
-    static size_t attr_smem = 0;
-    if (phi->smem > attr_smem) {
-        LIFE_CUDA(cudaFuncSetAttribute(k_wc_f32<NT, FULL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)phi->smem));
-        attr_smem = phi->smem;
-    }
+    LIFE_TRY(ensure_smem(k_wc_f32<NT, FULL>, phi->smem));
     FastArgs A{phi->atom, phi->fiber, phi->val, phi->gptr, phi->wpart, phi->Dg,
                phi->nv, phi->nt, phi->G, phi->ag, phi->na, phi->slice_floats};
     k_wc_f32<NT, FULL><<<phi->nblocks, kSpmvThreads, phi->smem, st>>>(A, y, fx, h);
@@ -676,16 +664,37 @@ static int launch_wc_t(life_phi *phi, const float *y, const WcFix &fx,
     default: return fail(LIFE_ERR_CONFIG_INVALID, "unsupported n_dirs");     \
     }
 
+int launch_dsc_dense(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
+                     const DscOut &o, const CallHooks &h, cudaStream_t st);
+int launch_wc_dense(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+                    cudaStream_t st);
+int prepare_dense(life_phi *phi);
+
+static int launch_dsc_sparse(life_phi *phi, const float *w, float *y, const float *b,
+                             uint32_t flags, const DscOut &o, const CallHooks &h,
+                             cudaStream_t st)
+{
+    LIFE_NT_DISPATCH(launch_dsc_t, phi, w, y, b, flags, o, h, st);
+}
+
 int launch_dsc(life_phi *phi, const float *w, float *y, const float *b,
                uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st)
 {
-    LIFE_NT_DISPATCH(launch_dsc_t, phi, w, y, b, flags, o, h, st);
+    if (phi->has_dense) return launch_dsc_dense(phi, w, y, b, flags, o, h, st);
+    return launch_dsc_sparse(phi, w, y, b, flags, o, h, st);
+}
+
+static int launch_wc_sparse(life_phi *phi, const float *y, const WcFix &fx,
+                            const CallHooks &h, cudaStream_t st)
+{
+    LIFE_NT_DISPATCH(launch_wc_t, phi, y, fx, h, st);
 }
 
 int launch_wc_main(life_phi *phi, const float *y, const WcFix &fx,
                    const CallHooks &h, cudaStream_t st)
 {
-    LIFE_NT_DISPATCH(launch_wc_t, phi, y, fx, h, st);
+    if (phi->has_dense) return launch_wc_dense(phi, y, fx.ymax, h, st);
+    return launch_wc_sparse(phi, y, fx, h, st);
 }
 
 int launch_absmax(life_phi *phi, const float *x, int64_t n, float *out,
@@ -701,14 +710,18 @@ int launch_absmax(life_phi *phi, const float *x, int64_t n, float *out,
 template <int NT, bool FULL>
 static int prepare_t(life_phi *phi)
 {
-    LIFE_CUDA(cudaFuncSetAttribute(k_dsc_f32<NT, FULL>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)phi->smem));
-    LIFE_CUDA(cudaFuncSetAttribute(k_wc_f32<NT, FULL>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)phi->smem));
+    LIFE_TRY(ensure_smem(k_dsc_f32<NT, FULL>, phi->smem));
+    LIFE_TRY(ensure_smem(k_wc_f32<NT, FULL>, phi->smem));
     return LIFE_OK;
 }
 
-int prepare_spmv(life_phi *phi) { LIFE_NT_DISPATCH(prepare_t, phi); }
+static int prepare_sparse(life_phi *phi) { LIFE_NT_DISPATCH(prepare_t, phi); }
+
+int prepare_spmv(life_phi *phi)
+{
+    if (phi->has_dense) return prepare_dense(phi);
+    return prepare_sparse(phi);
+}
 
 int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
               const float *ymax_dev, uint32_t flags, double *sumsq,
@@ -738,7 +751,8 @@ int life_dsc_f32(life_phi *phi, const float *w, float *y, const float *b,
                  uint32_t flags, const life_spmv_out *out, void *stream)
 {
     if (!phi || !w || !y) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
-    if (!phi->has_fast) return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
+    if (!phi->has_fast && !phi->has_dense)
+        return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     if ((flags & LIFE_SUBTRACT_B) && !b) return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_SUBTRACT_B needs b");
     DscOut o{nullptr, nullptr, nullptr};
     if (out) o = DscOut{out->skipped, out->sumsq, out->absmax};
@@ -752,7 +766,8 @@ int life_wc_f32(life_phi *phi, const float *y, float *w, const float *w_ref,
                 const life_spmv_out *out, void *stream)
 {
     if (!phi || !w || !y) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
-    if (!phi->has_fast) return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
+    if (!phi->has_fast && !phi->has_dense)
+        return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     if ((flags & LIFE_PROJECT_GRAD) && !w_ref)
         return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_PROJECT_GRAD needs w_ref");
     CallHooks h{nullptr, nullptr, nullptr};

@@ -13,6 +13,7 @@ C ABI on either host arrays (numpy: copied in and out) or CUDA tensors
 """
 
 import ctypes
+import warnings
 import weakref
 
 import numpy as np
@@ -22,6 +23,23 @@ from .errors import ConfigInvalid, DimensionMismatch
 from .tensor import OffsetPhiTensor
 
 _DEFAULT_PRECISION = ["fp32"]
+# Frozen (read-only) numpy arrays are only ever copied to the device.
+warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+
+
+_LAYOUT = ["auto"]
+
+
+def set_layout(name):
+    """fp32 kernel family for operators built from now on: "auto" (density
+    heuristic), "sparse" (voxel-segment kernels) or "dense" (register-tiled)."""
+    if name not in ("auto", "sparse", "dense"):
+        raise ConfigInvalid(f"layout must be auto/sparse/dense, got {name!r}")
+    _LAYOUT[0] = name
+
+
+def layout():
+    return _LAYOUT[0]
 
 
 def set_default_precision(precision):
@@ -75,6 +93,7 @@ class DeviceOperator:
 
     def _create(self, d, a, v, f, val, dic, stream):
         flags = (N.PHI_EXACT_F64 if self.exact else 0) | (0 if self.fast else N.PHI_NO_FAST_F32)
+        flags |= {"auto": 0, "sparse": N.PHI_FORCE_SPARSE, "dense": N.PHI_FORCE_DENSE}[_LAYOUT[0]]
         dims = N.Dims(d.n_atoms, d.n_voxels, d.n_fibers, d.n_dirs, d.n_coeffs)
         handle = ctypes.c_void_p()
         bad = ctypes.c_int64(-1)
@@ -89,6 +108,11 @@ class DeviceOperator:
         info = N.PhiInfo()
         N.check(N.lib().life_phi_get_info(handle, ctypes.byref(info)))
         self.info = info
+
+    @property
+    def kind(self):
+        """"dense" or "sparse": the fp32 kernel family this operator uses."""
+        return "sparse" if self.info.atom_groups > 0 else "dense"
 
     @property
     def handle(self):
