@@ -105,6 +105,8 @@ struct life_phi {
     uint32_t *d_tptr = nullptr;   // [n_tiles*n_chunks + 1]
     float *d_D = nullptr;         // [n_chunks][64][nt_pad] zero padded
     int n_tiles = 0, n_chunks = 0, nt_pad = 0, d_blocks = 0, d_W = 0;
+    int d_kind = 0;       // 1: register-tiled v1 (life_dense.cu), 2: warp-specialized (life_ws.cu)
+    int d_tv = 0;         // voxels per tile
     size_t d_smem = 0;
 
     // fixed-point WC accumulator and its scale inputs

@@ -481,24 +481,26 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
 // ---------------------------------------------------------------------------
 // layout construction
 // ---------------------------------------------------------------------------
-__global__ void k_dense_key1(const uint32_t *a, const uint32_t *v, int64_t n, int nch,
-                             unsigned long long *key, uint32_t *iota)
+__global__ void k_dense_key1(const uint32_t *a, const uint32_t *v, int64_t n, int nch, int tv,
+                             int cell_bits, unsigned long long *key, uint32_t *iota)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t at = a[i], vx = v[i];
-        const unsigned long long tc = (unsigned long long)(vx / kTV) * nch + at / kCA;
-        const uint32_t cell = (at % kCA) * kTV + vx % kTV;
-        key[i] = (tc << 10) | cell;
+        const unsigned long long tc = (unsigned long long)(vx / tv) * nch + at / kCA;
+        const uint32_t cell = (at % kCA) * tv + vx % tv;
+        key[i] = (tc << cell_bits) | cell;
         iota[i] = (uint32_t)i;
     }
 }
 
-// rank = position within the run of equal keys; key2 = tc<<32 | rank<<10 | cell
-__global__ void k_dense_key2(const unsigned long long *sk, int64_t n, unsigned long long *key2,
-                             unsigned *max_rank)
+// rank = position within the run of equal keys;
+// key2 = tc<<32 | rank<<cell_bits | cell
+__global__ void k_dense_key2(const unsigned long long *sk, int64_t n, int cell_bits,
+                             unsigned long long *key2, unsigned *max_rank)
 {
     unsigned mr = 0;
+    const unsigned long long cmask = (1ull << cell_bits) - 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long k = sk[i];
@@ -509,7 +511,7 @@ __global__ void k_dense_key2(const unsigned long long *sk, int64_t n, unsigned l
         }
         const unsigned long long rank = (unsigned long long)(i - lo);
         mr = max(mr, rank > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)rank);
-        key2[i] = ((k >> 10) << 32) | (rank << 10) | (k & 1023ull);
+        key2[i] = ((k >> cell_bits) << 32) | (rank << cell_bits) | (k & cmask);
     }
     atomicMax(max_rank, mr);
 }
@@ -563,14 +565,28 @@ static int pad_dirs(int nt)
     return p;
 }
 
+size_t ws_smem_bytes(int nt_pad);
+
 int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
                 const double *val, const std::vector<double> &hdict, cudaStream_t st)
 {
     const int64_t n = phi->nc;
-    const int nt_pad = pad_dirs(phi->nt);
-    if (!dense_supported_dpl(nt_pad) || n == 0) return LIFE_OK;  // sparse kernels only
+    // warp-specialized kernels (life_ws.cu) for n_dirs <= 96, the v1
+    // register-tiled kernels above for n_dirs <= 160, else sparse only
+    int kind = 2, tv = 32, cell_bits = 11;
+    int nt_pad = (phi->nt + 31) / 32 * 32;
+    if (nt_pad > 96) {
+        kind = 1;
+        tv = kTV;
+        cell_bits = 10;
+        nt_pad = pad_dirs(phi->nt);
+        if (!dense_supported_dpl(nt_pad)) return LIFE_OK;
+    }
+    if (n == 0) return LIFE_OK;
+    phi->d_kind = kind;
+    phi->d_tv = tv;
     phi->nt_pad = nt_pad;
-    phi->n_tiles = (phi->nv + kTV - 1) / kTV;
+    phi->n_tiles = (phi->nv + tv - 1) / tv;
     phi->n_chunks = (phi->na + kCA - 1) / kCA;
     const int64_t ntc = (int64_t)phi->n_tiles * phi->n_chunks;
     if (ntc >= (1ll << 31)) return LIFE_OK;
@@ -583,26 +599,26 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     LIFE_CUDA(cudaMallocAsync(&perm1, n * 4, st));
     LIFE_CUDA(cudaMallocAsync(&mr, 4, st));
     LIFE_CUDA(cudaMemsetAsync(mr, 0, 4, st));
-    k_dense_key1<<<gridn(n), 256, 0, st>>>(a, v, n, phi->n_chunks, k1, iota);
+    k_dense_key1<<<gridn(n), 256, 0, st>>>(a, v, n, phi->n_chunks, tv, cell_bits, k1, iota);
     LIFE_CHECK_LAUNCH();
     int bits_tc = 1;
     while (bits_tc < 40 && (ntc >> bits_tc) != 0) ++bits_tc;
     size_t tb = 0;
-    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, sk1, iota, perm1, n, 0, 10 + bits_tc, st));
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, sk1, iota, perm1, n, 0, cell_bits + bits_tc, st));
     void *temp = nullptr;
     LIFE_CUDA(cudaMallocAsync(&temp, tb, st));
-    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, k1, sk1, iota, perm1, n, 0, 10 + bits_tc, st));
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, k1, sk1, iota, perm1, n, 0, cell_bits + bits_tc, st));
     LIFE_CUDA(cudaFreeAsync(temp, st));
     g_launches.fetch_add(4, std::memory_order_relaxed);
     LIFE_CUDA(cudaFreeAsync(k1, st));
     LIFE_CUDA(cudaFreeAsync(iota, st));
     LIFE_CUDA(cudaMallocAsync(&k2, n * 8, st));
-    k_dense_key2<<<gridn(n), 256, 0, st>>>(sk1, n, k2, mr);
+    k_dense_key2<<<gridn(n), 256, 0, st>>>(sk1, n, cell_bits, k2, mr);
     LIFE_CHECK_LAUNCH();
     unsigned hmr = 0;
     LIFE_CUDA(cudaMemcpyAsync(&hmr, mr, 4, cudaMemcpyDeviceToHost, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
-    if (hmr >= (1u << 21)) {
+    if (hmr >= (1u << (32 - cell_bits))) {
         cudaFreeAsync(sk1, st); cudaFreeAsync(perm1, st); cudaFreeAsync(k2, st); cudaFreeAsync(mr, st);
         return LIFE_OK;  // pathological duplicate counts: stay sparse
     }
@@ -637,12 +653,17 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     LIFE_TRY(dalloc(phi, &phi->d_D, hD.size()));
     LIFE_CUDA(cudaMemcpyAsync(phi->d_D, hD.data(), hD.size() * 4, cudaMemcpyHostToDevice, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
-    phi->d_smem = ((size_t)2 * kCA * nt_pad + (size_t)kDenseWarps * kCells) * sizeof(float);
-    int bps = 0;
-    // residency: 2 CTAs per SM when shared memory allows
-    bps = (2 * (phi->d_smem + 1024) <= 227 * 1024) ? 2 : 1;
-    phi->d_blocks = phi->sms * bps;
-    phi->d_W = phi->d_blocks * kDenseWarps;
+    if (kind == 2) {
+        phi->d_smem = ws_smem_bytes(nt_pad);
+        phi->d_blocks = phi->sms;
+        phi->d_W = phi->d_blocks * 12;
+    } else {
+        phi->d_smem = ((size_t)2 * kCA * nt_pad + (size_t)kDenseWarps * kCells) * sizeof(float);
+        // residency: 2 CTAs per SM when shared memory allows
+        const int bps = (2 * (phi->d_smem + 1024) <= 227 * 1024) ? 2 : 1;
+        phi->d_blocks = phi->sms * bps;
+        phi->d_W = phi->d_blocks * kDenseWarps;
+    }
     phi->has_dense = true;
     return LIFE_OK;
 }
@@ -697,18 +718,44 @@ static int dense_prepare_t(life_phi *phi)
     default: return fail(LIFE_ERR_CONFIG_INVALID, "dense layout: unsupported n_dirs"); \
     }
 
+int launch_dsc_ws(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
+                  const DscOut &o, const CallHooks &h, cudaStream_t st);
+int launch_wc_ws(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+                 cudaStream_t st);
+int prepare_ws(life_phi *phi);
+
+static int dense_v1_dsc(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
+                        const DscOut &o, const CallHooks &h, cudaStream_t st)
+{
+    LIFE_DPL_DISPATCH(dense_dsc_t, phi, w, y, b, flags, o, h, st);
+}
+
+static int dense_v1_wc(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+                       cudaStream_t st)
+{
+    LIFE_DPL_DISPATCH(dense_wc_t, phi, y, ymax, h, st);
+}
+
+static int dense_v1_prepare(life_phi *phi) { LIFE_DPL_DISPATCH(dense_prepare_t, phi); }
+
 int launch_dsc_dense(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
                      const DscOut &o, const CallHooks &h, cudaStream_t st)
 {
-    LIFE_DPL_DISPATCH(dense_dsc_t, phi, w, y, b, flags, o, h, st);
+    if (phi->d_kind == 2) return launch_dsc_ws(phi, w, y, b, flags, o, h, st);
+    return dense_v1_dsc(phi, w, y, b, flags, o, h, st);
 }
 
 int launch_wc_dense(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
                     cudaStream_t st)
 {
-    LIFE_DPL_DISPATCH(dense_wc_t, phi, y, ymax, h, st);
+    if (phi->d_kind == 2) return launch_wc_ws(phi, y, ymax, h, st);
+    return dense_v1_wc(phi, y, ymax, h, st);
 }
 
-int prepare_dense(life_phi *phi) { LIFE_DPL_DISPATCH(dense_prepare_t, phi); }
+int prepare_dense(life_phi *phi)
+{
+    if (phi->d_kind == 2) return prepare_ws(phi);
+    return dense_v1_prepare(phi);
+}
 
 }  // namespace life

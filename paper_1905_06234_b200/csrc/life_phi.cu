@@ -579,6 +579,20 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
     if (!dict) return fail(LIFE_ERR_INVALID_ARGUMENT, "null dictionary");
 
     auto t0 = std::chrono::steady_clock::now();
+    {   // keep freed stream-ordered allocations mapped for reuse (restructuring
+        // temporaries are GBs at C2; re-mapping them each create costs seconds)
+        static bool pool_set = false;
+        if (!pool_set) {
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess &&
+                cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            pool_set = true;
+        }
+    }
     life_phi *phi = new life_phi();
     phi->dims = *dims;
     phi->na = (int)dims->n_atoms;

@@ -1,0 +1,698 @@
+// life_ws.cu -- warp-specialized dense DSC / WC (the C2 hot path).
+//
+// Same contraction as life_dense.cu (Y_tile += C_tile . D_chunk for DSC,
+// Z_tile = Y_tile . D_chunk^T then value*Z[cell] -> fascicles for WC), but
+// split between two roles inside one persistent CTA per SM:
+//
+//   4 producer warps  stream the sorted coefficient segment of the next
+//                     (voxel tile, atom chunk) step, gather w[f], and build
+//                     the 64 x 32 coefficient tile C in shared memory (DSC);
+//                     or scatter value * Z[cell] into the fixed-point fascicle
+//                     sums with RED.ADD (WC).  Producer warp 0 also issues
+//                     the TMA bulk copy of the next dictionary chunk.
+//   8 consumer warps  do only register-tiled FFMA2 work: each lane owns
+//                     8 voxels x 12 directions (96 fp32 accumulators), so a
+//                     dictionary value feeds 8 FMAs and a coefficient 12.
+//
+// Steps are double buffered (C/Z tiles and dictionary chunks) and handed
+// over with mbarriers (full/empty), so coefficient latency hides behind the
+// consumers' FMA stream.  Each LDS.128 costs four shared-memory wavefronts on
+// sm_100 (measured, tools/ubench); the 8x12 lane tile needs 5 of them per 96
+// FMAs per lane, keeping shared memory (80 wavefronts per 96-cycle FMA step
+// per SM) below the FP32 pipe.
+#include <algorithm>
+
+#include "life_common.cuh"
+
+namespace life {
+
+constexpr int kWsCons = 8;
+constexpr int kWsProd = 4;
+constexpr int kWsWarps = kWsCons + kWsProd;
+constexpr int kWsThreads = kWsWarps * 32;
+constexpr int kWsTV = 32;                  // voxels per consumer tile
+constexpr int kWsCA = 64;                  // atoms per chunk
+constexpr int kWsCells = kWsTV * kWsCA;    // 2048
+constexpr int kWsCellBits = 11;
+
+struct WsArgs {
+    const uint32_t *cr;
+    const uint32_t *fiber;
+    const float *val;
+    const uint32_t *tptr;
+    const float *D;
+    int nv, nt, nt_pad, nch, n_tiles, na;
+};
+
+__device__ __forceinline__ unsigned long long wpk(float a, float b)
+{
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void wupk(unsigned long long r, float &a, float &b)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ void wfma2(unsigned long long &d, unsigned long long a,
+                                      unsigned long long b)
+{
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+
+__device__ __forceinline__ unsigned smaddr(const void *p)
+{
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t *b, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smaddr(b)), "r"(count));
+}
+__device__ __forceinline__ void bar_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smaddr(b)) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(uint64_t *b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smaddr(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t *b, unsigned parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WSW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WSW_%=;\n}" ::"r"(smaddr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_chunk(float *dst, const float *src, unsigned bytes, uint64_t *b)
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    bar_arrive_tx(b, bytes);
+    const char *s = reinterpret_cast<const char *>(src);
+    char *d = reinterpret_cast<char *>(dst);
+    for (unsigned off = 0; off < bytes; off += 32768u) {
+        const unsigned sz = min(32768u, bytes - off);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smaddr(d + off)),
+            "l"(s + off), "r"(sz), "r"(smaddr(b))
+            : "memory");
+    }
+}
+
+template <typename T, typename Op>
+__device__ T ws_reduce(const T *part, int n, T init, Op op)
+{
+    __shared__ T s[32];
+    T acc = init;
+    for (int i = threadIdx.x; i < n; i += kWsThreads) acc = op(acc, __ldcg(part + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = op(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    T r = init;
+    if (threadIdx.x < 32) {
+        r = threadIdx.x < kWsWarps ? s[threadIdx.x] : init;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r = op(r, __shfl_xor_sync(0xffffffffu, r, o));
+        if (threadIdx.x == 0) s[0] = r;
+    }
+    __syncthreads();
+    r = s[0];
+    __syncthreads();
+    return r;
+}
+struct WAdd {
+    template <typename T>
+    __device__ T operator()(T a, T b) const { return a + b; }
+};
+struct WMax {
+    __device__ float operator()(float a, float b) const { return fmaxf(a, b); }
+};
+
+__device__ __forceinline__ bool ws_last_block(unsigned *counter)
+{
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
+// ---- producer: coefficient tile build (DSC) ---------------------------------
+// A producer warp builds two consumer tiles per step.  Their segments are
+// walked as one sequence of groups (4 rounds x 32 coefficients); a 4-deep
+// software pipeline keeps stream loads three groups ahead and w-gathers one
+// group ahead of the group being applied, and the next step's segments are
+// prefetched into L2 (cp.async.bulk.prefetch) a whole step in advance.
+struct BGroup {
+    uint32_t cr[4], f[4];
+    float v[4], wv[4];
+    bool ok[4];
+    int t;
+};
+
+struct Segs {
+    uint32_t p0[2], p1[2];
+    int ng0, ng;
+};
+
+__device__ __forceinline__ void seg_init(Segs &S, const WsArgs &A, int ct, int c, int p)
+{
+    S.ng = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int wt = ct * kWsCons + p * 2 + q;
+        if (wt < A.n_tiles) {
+            const uint32_t *tp = A.tptr + (size_t)wt * A.nch + c;
+            S.p0[q] = tp[0];
+            S.p1[q] = tp[1];
+        } else {
+            S.p0[q] = S.p1[q] = 0;
+        }
+    }
+    S.ng0 = (int)((S.p1[0] - S.p0[0] + 127) / 128);
+    S.ng = S.ng0 + (int)((S.p1[1] - S.p0[1] + 127) / 128);
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *ptr, uint32_t bytes)
+{
+    if (bytes == 0) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_range(const WsArgs &A, uint32_t p0, uint32_t p1)
+{
+    if (p1 <= p0) return;
+    const uint32_t a0 = p0 & ~3u, a1 = (p1 + 3u) & ~3u;  // 16-byte aligned u32/f32 ranges
+    const uint32_t bytes = (a1 - a0) * 4u;
+    prefetch_l2(A.cr + a0, bytes);
+    prefetch_l2(A.fiber + a0, bytes);
+    prefetch_l2(A.val + a0, bytes);
+}
+
+__device__ __forceinline__ void bg_load(BGroup &G, const WsArgs &A, const Segs &S, int g, int lane)
+{
+    int t = 0;
+    uint32_t base = 0, p1 = 0;
+    if (g < S.ng0) {
+        base = S.p0[0] + (uint32_t)g * 128u;
+        p1 = S.p1[0];
+    } else if (g < S.ng) {
+        t = 1;
+        base = S.p0[1] + (uint32_t)(g - S.ng0) * 128u;
+        p1 = S.p1[1];
+    }
+    G.t = t;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t k = base + 32 * r + lane;
+        G.ok[r] = k < p1;
+        G.cr[r] = G.ok[r] ? ld_stream(A.cr + k) : 0u;
+        G.f[r] = G.ok[r] ? ld_stream(A.fiber + k) : 0u;
+        G.v[r] = G.ok[r] ? ld_stream(A.val + k) : 0.f;
+    }
+}
+
+__device__ __forceinline__ void bg_gather(BGroup &G, const float *__restrict__ w)
+{
+#pragma unroll
+    for (int r = 0; r < 4; ++r) G.wv[r] = G.ok[r] ? __ldg(w + G.f[r]) : 0.f;
+}
+
+__device__ __forceinline__ unsigned bg_apply(const BGroup &G, float *C0, float *C1)
+{
+    float *C = G.t ? C1 : C0;
+    unsigned zeros = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const bool ok = G.ok[r];
+        const float s = __fmul_rn(G.wv[r], G.v[r]);
+        zeros += __popc(__ballot_sync(0xffffffffu, ok && s == 0.f));
+        const uint32_t rank = G.cr[r] >> kWsCellBits, cell = G.cr[r] & (kWsCells - 1);
+        const uint32_t rmin = __reduce_min_sync(0xffffffffu, ok ? rank : 0xFFFFFFFFu);
+        if (rmin == 0xFFFFFFFFu) continue;
+        const uint32_t rmax = __reduce_max_sync(0xffffffffu, ok ? rank : 0u);
+        if (rmin == rmax) {
+            if (ok) {
+                if (rmin == 0) C[cell] = s;
+                else C[cell] += s;
+            }
+        } else {
+            for (uint32_t rr = rmin; rr <= rmax; ++rr) {
+                if (ok && rank == rr) {
+                    if (rr == 0) C[cell] = s;
+                    else C[cell] += s;
+                }
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+    }
+    return zeros;
+}
+
+__device__ __forceinline__ unsigned build_step(float *C0, float *C1, const WsArgs &A,
+                                               const float *__restrict__ w, const Segs &S,
+                                               int lane)
+{
+    float4 *Z0 = reinterpret_cast<float4 *>(C0);
+    float4 *Z1 = reinterpret_cast<float4 *>(C1);
+#pragma unroll 4
+    for (int i = 0; i < kWsCells / 4 / 32; ++i) {
+        Z0[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        Z1[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+    unsigned zeros = 0;
+    if (S.ng == 0) return 0;
+    BGroup G0, G1, G2, G3;
+    bg_load(G0, A, S, 0, lane);
+    bg_load(G1, A, S, 1, lane);
+    bg_load(G2, A, S, 2, lane);
+    bg_gather(G0, w);
+    for (int g = 0; g < S.ng; ++g) {
+        bg_load(G3, A, S, g + 3, lane);
+        bg_gather(G1, w);
+        zeros += bg_apply(G0, C0, C1);
+        G0 = G1;
+        G1 = G2;
+        G2 = G3;
+    }
+    return zeros;
+}
+
+// next (ct, c) step of this CTA, or ct >= n_ct when none
+__device__ __forceinline__ void next_step(int &ct, int &c, int nch)
+{
+    if (++c == nch) {
+        c = 0;
+        ct += gridDim.x;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// DSC
+// ---------------------------------------------------------------------------
+template <int DPL>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    k_dsc_ws(const WsArgs A, const float *__restrict__ w, float *__restrict__ y,
+             const float *__restrict__ b, const uint32_t flags, const ReduceSlots red,
+             const DscOut out, const CallHooks hooks)
+{
+    extern __shared__ __align__(128) float sm[];
+    __shared__ __align__(8) uint64_t full[2], empty[2];
+    if (hooks.done && *hooks.done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
+    const int chunk_floats = kWsCA * A.nt_pad;
+    const unsigned chunk_bytes = (unsigned)chunk_floats * 4u;
+    float *Dbuf = sm;
+    float *Cbuf = sm + 2 * chunk_floats;
+    const int n_ct = (A.n_tiles + kWsCons - 1) / kWsCons;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            bar_init(&full[s], kWsProd + 1);
+            bar_init(&empty[s], kWsCons);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    double sq = 0.0;
+    float amax = 0.f;
+    unsigned long long skipped = 0;
+
+    if (warp < kWsCons) {
+        // ===== consumers: register-tiled FFMA2 =====
+        const int vg = lane >> 3, dg = lane & 7;
+        const bool accumulate = flags & LIFE_ACCUMULATE;
+        const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
+        int k = 0;
+        for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
+            const int wt = ct * kWsCons + warp;
+            const bool tile_ok = wt < A.n_tiles;
+            unsigned long long acc[8][DPL / 2];
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+#pragma unroll
+                for (int j = 0; j < DPL / 2; ++j) acc[v][j] = 0ull;
+            for (int c = 0; c < A.nch; ++c, ++k) {
+                const int s = k & 1;
+                bar_wait(&full[s], (k >> 1) & 1);
+                if (tile_ok) {
+                    const float *C = Cbuf + (s * kWsCons + warp) * kWsCells + vg * 8;
+                    const float *D = Dbuf + s * chunk_floats + dg * DPL;
+                    const int na_c = min(kWsCA, A.na - c * kWsCA);
+#pragma unroll 2
+                    for (int a = 0; a < na_c; ++a) {
+                        const float4 c0 = *reinterpret_cast<const float4 *>(C + a * kWsTV);
+                        const float4 c1 = *reinterpret_cast<const float4 *>(C + a * kWsTV + 4);
+                        unsigned long long dp[DPL / 2];
+                        const float4 *d4 = reinterpret_cast<const float4 *>(D + a * A.nt_pad);
+#pragma unroll
+                        for (int i = 0; i < DPL / 4; ++i) {
+                            const float4 t = d4[i];
+                            dp[2 * i] = wpk(t.x, t.y);
+                            dp[2 * i + 1] = wpk(t.z, t.w);
+                        }
+                        const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+                        for (int v = 0; v < 8; ++v) {
+                            const unsigned long long cp = wpk(cv[v], cv[v]);
+#pragma unroll
+                            for (int j = 0; j < DPL / 2; ++j) wfma2(acc[v][j], dp[j], cp);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) bar_arrive(&empty[s]);
+            }
+            if (tile_ok) {
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const int voxel = wt * kWsTV + vg * 8 + v;
+                    if (voxel >= A.nv) continue;
+                    const size_t yo = (size_t)voxel * A.nt;
+#pragma unroll
+                    for (int j = 0; j < DPL / 2; ++j) {
+                        float o[2];
+                        wupk(acc[v][j], o[0], o[1]);
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int t = dg * DPL + 2 * j + e;
+                            if (t < A.nt) {
+                                float r = o[e];
+                                if (accumulate) r += y[yo + t];
+                                if (subtract) r -= b[yo + t];
+                                y[yo + t] = r;
+                                sq += (double)r * (double)r;
+                                amax = fmaxf(amax, fabsf(r));
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    } else {
+        // ===== producers: TMA for D, coefficient tiles =====
+        const int p = warp - kWsCons;
+        int k = 0;
+        for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
+            for (int c = 0; c < A.nch; ++c, ++k) {
+                const int s = k & 1;
+                Segs S;
+                seg_init(S, A, ct, c, p);
+                {   // warm L2 with the next step's coefficient segments
+                    int nct = ct, nc = c;
+                    next_step(nct, nc, A.nch);
+                    if (nct < n_ct && lane < 2) {
+                        Segs Sn;
+                        seg_init(Sn, A, nct, nc, p);
+                        prefetch_range(A, lane ? Sn.p0[1] : Sn.p0[0], lane ? Sn.p1[1] : Sn.p1[0]);
+                    }
+                }
+                if (k >= 2) bar_wait(&empty[s], ((k - 2) >> 1) & 1);
+                if (p == 0 && lane == 0)
+                    tma_chunk(Dbuf + s * chunk_floats, A.D + (size_t)c * chunk_floats,
+                              chunk_bytes, &full[s]);
+                skipped += build_step(Cbuf + (s * kWsCons + 2 * p) * kWsCells,
+                                      Cbuf + (s * kWsCons + 2 * p + 1) * kWsCells, A, w, S, lane);
+                __syncwarp();
+                if (lane == 0) bar_arrive(&full[s]);
+            }
+        }
+    }
+
+    // ---- fixed-order completion --------------------------------------------
+    const int gw = blockIdx.x * kWsWarps + warp;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    if (lane == 0) {
+        red.part_d[gw] = sq;
+        red.part_u[gw] = skipped;
+        red.part_f[gw] = amax;
+    }
+    if (ws_last_block(red.counter)) {
+        const int W = gridDim.x * kWsWarps;
+        const double tsq = ws_reduce<double>(red.part_d, W, 0.0, WAdd{});
+        const unsigned long long tsk = ws_reduce<unsigned long long>(red.part_u, W, 0ull, WAdd{});
+        const float tmax = ws_reduce<float>(red.part_f, W, 0.f, WMax{});
+        if (threadIdx.x == 0) {
+            if (out.sumsq) *out.sumsq = tsq;
+            if (out.skipped) *out.skipped = tsk;
+            if (out.absmax) *out.absmax = tmax;
+            *red.counter = 0;
+            if (hooks.t_accum && hooks.t_begin) *hooks.t_accum += globaltimer() - *hooks.t_begin;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// WC
+// ---------------------------------------------------------------------------
+struct WsFix {
+    unsigned long long *wfix;
+    const float *ymax;
+    double vmax, dmax, fmax_nnz;
+};
+
+template <int DPL>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    k_wc_ws(const WsArgs A, const float *__restrict__ y, const WsFix fx, const CallHooks hooks)
+{
+    extern __shared__ __align__(128) float sm[];
+    __shared__ __align__(8) uint64_t dfull[2], dempty[2], zfull[2], zempty[2];
+    if (hooks.done && *hooks.done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
+    const int chunk_floats = kWsCA * A.nt_pad;
+    const unsigned chunk_bytes = (unsigned)chunk_floats * 4u;
+    float *Dbuf = sm;
+    float *Zbuf = sm + 2 * chunk_floats;
+    const int n_ct = (A.n_tiles + kWsCons - 1) / kWsCons;
+    const int my_ct = (int)blockIdx.x < n_ct ? (n_ct - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int total = my_ct * A.nch;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            bar_init(&dfull[s], 1);
+            bar_init(&dempty[s], kWsCons);
+            bar_init(&zfull[s], kWsCons);
+            bar_init(&zempty[s], kWsProd);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp < kWsCons) {
+        // ===== consumers: Z = Y . D^T =====
+        const int vg = lane >> 3, dg = lane & 7;
+        const int b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
+        int k = 0;
+        for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
+            const int wt = ct * kWsCons + warp;
+            const bool tile_ok = wt < A.n_tiles;
+            unsigned long long yp[8][DPL / 2];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                const int voxel = wt * kWsTV + vg * 8 + v;
+                const bool ok = tile_ok && voxel < A.nv;
+                const size_t yo = (size_t)(ok ? voxel : 0) * A.nt;
+#pragma unroll
+                for (int j = 0; j < DPL / 2; ++j) {
+                    const int t = dg * DPL + 2 * j;
+                    const float e0 = (ok && t < A.nt) ? y[yo + t] : 0.f;
+                    const float e1 = (ok && t + 1 < A.nt) ? y[yo + t + 1] : 0.f;
+                    yp[v][j] = wpk(e0, e1);
+                }
+            }
+            for (int c = 0; c < A.nch; ++c, ++k) {
+                const int s = k & 1;
+                bar_wait(&dfull[s], (k >> 1) & 1);
+                if (k >= 2) bar_wait(&zempty[s], ((k - 2) >> 1) & 1);
+                if (tile_ok) {
+                    float *Z = Zbuf + (s * kWsCons + warp) * kWsCells;
+                    const float *D = Dbuf + s * chunk_floats + dg * DPL;
+                    const int na_c = min(kWsCA, A.na - c * kWsCA);
+                    for (int a0 = 0; a0 < na_c; a0 += 2) {
+                        unsigned long long pp[2][8];
+#pragma unroll
+                        for (int aa = 0; aa < 2; ++aa) {
+                            const float4 *d4 = reinterpret_cast<const float4 *>(D + (a0 + aa) * A.nt_pad);
+                            unsigned long long dp[DPL / 2];
+#pragma unroll
+                            for (int i = 0; i < DPL / 4; ++i) {
+                                const float4 t = d4[i];
+                                dp[2 * i] = wpk(t.x, t.y);
+                                dp[2 * i + 1] = wpk(t.z, t.w);
+                            }
+#pragma unroll
+                            for (int v = 0; v < 8; ++v) {
+                                pp[aa][v] = 0ull;
+#pragma unroll
+                                for (int j = 0; j < DPL / 2; ++j) wfma2(pp[aa][v], yp[v][j], dp[j]);
+                            }
+                        }
+                        float q[16];
+#pragma unroll
+                        for (int aa = 0; aa < 2; ++aa)
+#pragma unroll
+                            for (int v = 0; v < 8; ++v) {
+                                float lo, hi;
+                                wupk(pp[aa][v], lo, hi);
+                                q[aa * 8 + v] = lo + hi;
+                            }
+                        // butterfly over the 8 direction lanes of this voxel group
+#pragma unroll
+                        for (int m = 4, h = 8; m >= 1; m >>= 1, h >>= 1) {
+                            const bool up = (lane & m) != 0;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                if (i < h) {
+                                    const float send = up ? q[i] : q[i + h];
+                                    const float keep = up ? q[i + h] : q[i];
+                                    q[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                                }
+                            }
+                        }
+                        *reinterpret_cast<float2 *>(Z + (a0 + b2) * kWsTV + vg * 8 + 4 * b1 + 2 * b0) =
+                            make_float2(q[0], q[1]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    bar_arrive(&dempty[s]);
+                    bar_arrive(&zfull[s]);
+                }
+            }
+        }
+    } else {
+        // ===== producers: D chunks via TMA; scatter value * Z[cell] =====
+        const int p = warp - kWsCons;
+        const int ex = wc_fix_exponent(fx.vmax, fx.dmax, (double)A.nt, fx.fmax_nnz, *fx.ymax);
+        const double scale = ldexp(1.0, ex);
+        if (p == 0 && lane == 0 && total > 0)
+            tma_chunk(Dbuf, A.D, chunk_bytes, &dfull[0]);
+        int k = 0;
+        for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
+            for (int c = 0; c < A.nch; ++c, ++k) {
+                const int s = k & 1;
+                if (p == 0 && lane == 0 && k + 1 < total) {
+                    const int s1 = (k + 1) & 1;
+                    if (k + 1 >= 2) bar_wait(&dempty[s1], ((k - 1) >> 1) & 1);
+                    const int c1 = (c + 1) % A.nch;
+                    tma_chunk(Dbuf + s1 * chunk_floats, A.D + (size_t)c1 * chunk_floats,
+                              chunk_bytes, &dfull[s1]);
+                }
+                __syncwarp();
+                Segs S;
+                seg_init(S, A, ct, c, p);
+                {
+                    int nct = ct, nc = c;
+                    next_step(nct, nc, A.nch);
+                    if (nct < n_ct && lane < 2) {
+                        Segs Sn;
+                        seg_init(Sn, A, nct, nc, p);
+                        prefetch_range(A, lane ? Sn.p0[1] : Sn.p0[0], lane ? Sn.p1[1] : Sn.p1[0]);
+                    }
+                }
+                BGroup G0, G1, G2;
+                bg_load(G0, A, S, 0, lane);
+                bg_load(G1, A, S, 1, lane);
+                bar_wait(&zfull[s], (k >> 1) & 1);
+                const float *Z0 = Zbuf + (s * kWsCons + 2 * p) * kWsCells;
+                const float *Z1 = Z0 + kWsCells;
+                for (int g = 0; g < S.ng; ++g) {
+                    bg_load(G2, A, S, g + 2, lane);
+                    const float *Z = G0.t ? Z1 : Z0;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (G0.ok[r]) {
+                            const float z = Z[G0.cr[r] & (kWsCells - 1)] * G0.v[r];
+                            const long long qv = __double2ll_rn((double)z * scale);
+                            atomicAdd(fx.wfix + G0.f[r], static_cast<unsigned long long>(qv));
+                        }
+                    }
+                    G0 = G1;
+                    G1 = G2;
+                }
+                __syncwarp();
+                if (lane == 0) bar_arrive(&zempty[s]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+template <int DPL>
+static int ws_dsc_t(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
+                    const DscOut &o, const CallHooks &h, cudaStream_t st)
+{
+    LIFE_TRY(ensure_smem(k_dsc_ws<DPL>, phi->d_smem));
+    WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_D,
+             phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
+    k_dsc_ws<DPL><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, w, y, b, flags, phi->red,
+                                                                   o, h);
+    LIFE_CHECK_LAUNCH();
+    return LIFE_OK;
+}
+
+template <int DPL>
+static int ws_wc_t(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+                   cudaStream_t st)
+{
+    LIFE_TRY(ensure_smem(k_wc_ws<DPL>, phi->d_smem));
+    WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_D,
+             phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
+    WsFix fx{phi->wfix, ymax, phi->vmax, phi->dmax, (double)phi->fmax_nnz};
+    k_wc_ws<DPL><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, y, fx, h);
+    LIFE_CHECK_LAUNCH();
+    return LIFE_OK;
+}
+
+template <int DPL>
+static int ws_prepare_t(life_phi *phi)
+{
+    LIFE_TRY(ensure_smem(k_dsc_ws<DPL>, phi->d_smem));
+    LIFE_TRY(ensure_smem(k_wc_ws<DPL>, phi->d_smem));
+    return LIFE_OK;
+}
+
+#define LIFE_WS_DISPATCH(FN, ...)                                              \
+    switch (phi->nt_pad / 8) {                                                 \
+    case 4: return FN<4>(__VA_ARGS__);                                         \
+    case 8: return FN<8>(__VA_ARGS__);                                         \
+    case 12: return FN<12>(__VA_ARGS__);                                       \
+    default: return fail(LIFE_ERR_CONFIG_INVALID, "ws layout: unsupported n_dirs"); \
+    }
+
+int launch_dsc_ws(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
+                  const DscOut &o, const CallHooks &h, cudaStream_t st)
+{
+    LIFE_WS_DISPATCH(ws_dsc_t, phi, w, y, b, flags, o, h, st);
+}
+
+int launch_wc_ws(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+                 cudaStream_t st)
+{
+    LIFE_WS_DISPATCH(ws_wc_t, phi, y, ymax, h, st);
+}
+
+int prepare_ws(life_phi *phi) { LIFE_WS_DISPATCH(ws_prepare_t, phi); }
+
+size_t ws_smem_bytes(int nt_pad)
+{
+    return ((size_t)2 * kWsCA * nt_pad + (size_t)2 * kWsCons * kWsCells) * sizeof(float);
+}
+
+}  // namespace life

@@ -9,6 +9,7 @@ counts and trace fields follow the reference exactly.
 """
 
 import ctypes
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -80,6 +81,7 @@ class SolverTrace:
     total_dsc_calls: int = 0
     total_wc_calls: int = 0
     loop_seconds: float = 0.0
+    setup_seconds: float = 0.0   # operator build (H2D + restructuring) + uploads
 
     @property
     def iterations(self):
@@ -216,6 +218,7 @@ def solve(problem, w0=None, config=None):
     if problem.y is None:
         raise ConfigInvalid("problem has no signal vector to fit")
     torch = N.require_cuda()
+    t_setup = time.perf_counter()
     exact = config.precision == "fp64"
     dtype = torch.float64 if exact else torch.float32
     op = device.operator_for(problem.tensor, problem.dictionary, exact=exact)
@@ -227,13 +230,15 @@ def solve(problem, w0=None, config=None):
         w = torch.from_numpy(np.ascontiguousarray(w0, dtype=np.float64)).to(
             device="cuda", dtype=dtype)
     config._has_w0 = w0 is not None
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
     res, recs = solve_device(op, b, w, config)
     trace = SolverTrace(termination=N.TERM_NAMES.get(res.termination, "max_iters"),
                         initial_objective=res.initial_objective,
                         final_objective=res.final_objective,
                         total_dsc_calls=int(res.total_dsc_calls),
                         total_wc_calls=int(res.total_wc_calls),
-                        loop_seconds=res.loop_seconds)
+                        loop_seconds=res.loop_seconds, setup_seconds=t_setup)
     for i in range(res.iterations):
         r = recs[i]
         trace.records.append(TraceRecord(

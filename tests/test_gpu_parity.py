@@ -304,19 +304,19 @@ def test_single_giant_run_and_long_fascicle(oracle, layout):
     # every coefficient in voxel 0 and fascicle 0 (maximal segments)
     n = 20000
     rng = np.random.default_rng(5)
-    d = L.Dims(50, 3, 4, 96, n)
-    q = dict(atoms=rng.integers(0, 50, n).astype(np.uint32), voxels=np.zeros(n, np.uint32),
+    d = L.Dims(1057, 3, 8, 96, n)
+    q = dict(atoms=rng.integers(0, 1057, n).astype(np.uint32), voxels=np.zeros(n, np.uint32),
              fibers=np.zeros(n, np.uint32), values=rng.random(n) + 0.1,
-             dict=rng.standard_normal(50 * 96), dims=(50, 3, 4, 96, n), ordering="unsorted")
+             dict=rng.standard_normal(1057 * 96), dims=(1057, 3, 8, 96, n), ordering="unsorted")
     t = L.PhiTensor(atoms=q["atoms"], voxels=q["voxels"], fibers=q["fibers"],
                     values=q["values"], dims=d)
     dic = L.Dictionary(data=q["dict"], dims=d)
-    w = np.array([0.7, 0.0, 1.0, 2.0])
+    w = np.array([0.7, 0.0, 1.0, 2.0, 0.0, 0.0, 0.0, 0.0])
     yo = np.zeros(d.signal_len)
     oracle.dsc(q, w, yo)
     assert rel_l2(dsc(t, dic, d, w, "fp32")[0], yo) <= TOL32
     y_in = rng.standard_normal(d.signal_len)
-    wo = np.zeros(4)
+    wo = np.zeros(8)
     oracle.wc(q, y_in, wo)
     assert rel_l2(wc(t, dic, d, y_in, "fp32"), wo) <= TOL32
 
@@ -358,7 +358,8 @@ def test_fp32_repeat_bitwise_and_accumulate(layout):
     # accumulate contract: out += M x
     y3 = y1.clone()
     op.dsc_f32(w, y3, flags=L._native.ACCUMULATE)
-    assert torch.allclose(y3, 2 * y1, rtol=1e-6, atol=1e-6)
+    scale = float(y1.abs().max())
+    assert torch.allclose(y3, 2 * y1, rtol=1e-5, atol=1e-5 * scale)
     # adjointness <M w, y> == <w, M^T y> at scale
     lhs = float(torch.dot(y1.double(), y1.double()))
     rhs = float(torch.dot(w.double(), g1.double()))
