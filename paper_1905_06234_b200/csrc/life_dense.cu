@@ -516,14 +516,30 @@ __global__ void k_dense_key2(const unsigned long long *sk, int64_t n, int cell_b
     atomicMax(max_rank, mr);
 }
 
+// cr = (mixed << 31) | rank << cell_bits | cell.  "mixed" (warp-specialized
+// layout only) marks entries of a 32-entry window, counted from the start of
+// their (tile, chunk) segment, whose ranks differ: only those windows need
+// the ordered per-rank pass when building the coefficient tile.
 __global__ void k_dense_gather(const unsigned long long *sk2, const uint32_t *perm, int64_t n,
-                               const uint32_t *f, const double *val, uint32_t *cr_out,
+                               const uint32_t *f, const double *val, const uint32_t *tptr,
+                               int cell_bits, int mark_mixed, uint32_t *cr_out,
                                uint32_t *f_out, float *val_out)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t p = perm[i];
-        cr_out[i] = (uint32_t)(sk2[i] & 0xFFFFFFFFull);
+        const unsigned long long k = sk2[i];
+        uint32_t cr = (uint32_t)(k & 0xFFFFFFFFull);
+        if (mark_mixed) {
+            const uint32_t tc = (uint32_t)(k >> 32);
+            const int64_t seg0 = tptr[tc], seg1 = tptr[tc + 1];
+            const int64_t w0 = seg0 + ((i - seg0) / 32) * 32;
+            const int64_t w1 = (w0 + 32 < seg1 ? w0 + 32 : seg1) - 1;
+            const uint32_t r0 = (uint32_t)(sk2[w0] & 0xFFFFFFFFull) >> cell_bits;
+            const uint32_t r1 = (uint32_t)(sk2[w1] & 0xFFFFFFFFull) >> cell_bits;
+            if (r0 != r1) cr |= 0x80000000u;
+        }
+        cr_out[i] = cr;
         f_out[i] = f[p];
         val_out[i] = (float)val[p];
     }
@@ -618,7 +634,7 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     unsigned hmr = 0;
     LIFE_CUDA(cudaMemcpyAsync(&hmr, mr, 4, cudaMemcpyDeviceToHost, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
-    if (hmr >= (1u << (32 - cell_bits))) {
+    if (hmr >= (1u << (31 - cell_bits))) {
         cudaFreeAsync(sk1, st); cudaFreeAsync(perm1, st); cudaFreeAsync(k2, st); cudaFreeAsync(mr, st);
         return LIFE_OK;  // pathological duplicate counts: stay sparse
     }
@@ -637,10 +653,11 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     LIFE_TRY(dalloc(phi, &phi->d_fiber, n));
     LIFE_TRY(dalloc(phi, &phi->d_val, n));
     LIFE_TRY(dalloc(phi, &phi->d_tptr, ntc + 1));
-    k_dense_gather<<<gridn(n), 256, 0, st>>>(sk2, perm, n, f, val, phi->d_cr, phi->d_fiber,
-                                             phi->d_val);
-    LIFE_CHECK_LAUNCH();
     k_dense_tptr<<<gridn(ntc + 1), 256, 0, st>>>(sk2, n, ntc, phi->d_tptr);
+    LIFE_CHECK_LAUNCH();
+    k_dense_gather<<<gridn(n), 256, 0, st>>>(sk2, perm, n, f, val, phi->d_tptr, cell_bits,
+                                             kind == 2 ? 1 : 0, phi->d_cr, phi->d_fiber,
+                                             phi->d_val);
     LIFE_CHECK_LAUNCH();
     LIFE_CUDA(cudaFreeAsync(sk2, st));
     LIFE_CUDA(cudaFreeAsync(perm, st));

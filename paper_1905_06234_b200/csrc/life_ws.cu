@@ -227,25 +227,28 @@ __device__ __forceinline__ void bg_gather(BGroup &G, const float *__restrict__ w
     for (int r = 0; r < 4; ++r) G.wv[r] = G.ok[r] ? __ldg(w + G.f[r]) : 0.f;
 }
 
-__device__ __forceinline__ unsigned bg_apply(const BGroup &G, float *C0, float *C1)
+// Apply one group to the tile.  Windows whose entries share one rank touch
+// distinct cells (one STS or LDS+FADD+STS per lane); a window straddling
+// rank levels ("mixed", precomputed bit 31 of cr) is applied rank by rank.
+// Zero products are counted per lane (summed once per kernel).
+__device__ __forceinline__ void bg_apply(const BGroup &G, float *C0, float *C1, unsigned &zeros)
 {
     float *C = G.t ? C1 : C0;
-    unsigned zeros = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const bool ok = G.ok[r];
         const float s = __fmul_rn(G.wv[r], G.v[r]);
-        zeros += __popc(__ballot_sync(0xffffffffu, ok && s == 0.f));
-        const uint32_t rank = G.cr[r] >> kWsCellBits, cell = G.cr[r] & (kWsCells - 1);
-        const uint32_t rmin = __reduce_min_sync(0xffffffffu, ok ? rank : 0xFFFFFFFFu);
-        if (rmin == 0xFFFFFFFFu) continue;
-        const uint32_t rmax = __reduce_max_sync(0xffffffffu, ok ? rank : 0u);
-        if (rmin == rmax) {
+        zeros += (ok && s == 0.f) ? 1u : 0u;
+        const uint32_t cr = G.cr[r];
+        const uint32_t rank = (cr >> kWsCellBits) & 0xFFFFFu, cell = cr & (kWsCells - 1);
+        if (!__any_sync(0xffffffffu, ok && (cr >> 31))) {
             if (ok) {
-                if (rmin == 0) C[cell] = s;
+                if (rank == 0) C[cell] = s;
                 else C[cell] += s;
             }
         } else {
+            const uint32_t rmin = __reduce_min_sync(0xffffffffu, ok ? rank : 0xFFFFFFFFu);
+            const uint32_t rmax = __reduce_max_sync(0xffffffffu, ok ? rank : 0u);
             for (uint32_t rr = rmin; rr <= rmax; ++rr) {
                 if (ok && rank == rr) {
                     if (rr == 0) C[cell] = s;
@@ -256,7 +259,6 @@ __device__ __forceinline__ unsigned bg_apply(const BGroup &G, float *C0, float *
         }
         __syncwarp();
     }
-    return zeros;
 }
 
 __device__ __forceinline__ unsigned build_step(float *C0, float *C1, const WsArgs &A,
@@ -281,7 +283,7 @@ __device__ __forceinline__ unsigned build_step(float *C0, float *C1, const WsArg
     for (int g = 0; g < S.ng; ++g) {
         bg_load(G3, A, S, g + 3, lane);
         bg_gather(G1, w);
-        zeros += bg_apply(G0, C0, C1);
+        bg_apply(G0, C0, C1, zeros);
         G0 = G1;
         G1 = G2;
         G2 = G3;
@@ -338,11 +340,14 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
             const int wt = ct * kWsCons + warp;
             const bool tile_ok = wt < A.n_tiles;
-            unsigned long long acc[8][DPL / 2];
+            // acc[vp][t] = (y[2vp][t], y[2vp+1][t]): pairs across voxels so
+            // the coefficient pair is a native 64-bit operand and the
+            // dictionary value a broadcast scalar (FFMA2 Rd, Rc.F32x2, Rd.F32)
+            unsigned long long acc[4][DPL];
 #pragma unroll
-            for (int v = 0; v < 8; ++v)
+            for (int v = 0; v < 4; ++v)
 #pragma unroll
-                for (int j = 0; j < DPL / 2; ++j) acc[v][j] = 0ull;
+                for (int j = 0; j < DPL; ++j) acc[v][j] = 0ull;
             for (int c = 0; c < A.nch; ++c, ++k) {
                 const int s = k & 1;
                 bar_wait(&full[s], (k >> 1) & 1);
@@ -350,24 +355,23 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     const float *C = Cbuf + (s * kWsCons + warp) * kWsCells + vg * 8;
                     const float *D = Dbuf + s * chunk_floats + dg * DPL;
                     const int na_c = min(kWsCA, A.na - c * kWsCA);
-#pragma unroll 2
-                    for (int a = 0; a < na_c; ++a) {
+#pragma unroll 32
+                    for (int a = 0; a < kWsCA; ++a) {
                         const float4 c0 = *reinterpret_cast<const float4 *>(C + a * kWsTV);
                         const float4 c1 = *reinterpret_cast<const float4 *>(C + a * kWsTV + 4);
-                        unsigned long long dp[DPL / 2];
+                        const unsigned long long cp[4] = {wpk(c0.x, c0.y), wpk(c0.z, c0.w),
+                                                          wpk(c1.x, c1.y), wpk(c1.z, c1.w)};
                         const float4 *d4 = reinterpret_cast<const float4 *>(D + a * A.nt_pad);
 #pragma unroll
                         for (int i = 0; i < DPL / 4; ++i) {
                             const float4 t = d4[i];
-                            dp[2 * i] = wpk(t.x, t.y);
-                            dp[2 * i + 1] = wpk(t.z, t.w);
-                        }
-                        const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+                            const float dv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-                        for (int v = 0; v < 8; ++v) {
-                            const unsigned long long cp = wpk(cv[v], cv[v]);
+                            for (int e = 0; e < 4; ++e) {
+                                const unsigned long long dd = wpk(dv[e], dv[e]);
 #pragma unroll
-                            for (int j = 0; j < DPL / 2; ++j) wfma2(acc[v][j], dp[j], cp);
+                                for (int vp = 0; vp < 4; ++vp) wfma2(acc[vp][4 * i + e], cp[vp], dd);
+                            }
                         }
                     }
                 }
@@ -376,19 +380,19 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             }
             if (tile_ok) {
 #pragma unroll
-                for (int v = 0; v < 8; ++v) {
-                    const int voxel = wt * kWsTV + vg * 8 + v;
-                    if (voxel >= A.nv) continue;
-                    const size_t yo = (size_t)voxel * A.nt;
+                for (int vp = 0; vp < 4; ++vp) {
 #pragma unroll
-                    for (int j = 0; j < DPL / 2; ++j) {
-                        float o[2];
-                        wupk(acc[v][j], o[0], o[1]);
+                    for (int h = 0; h < 2; ++h) {
+                        const int voxel = wt * kWsTV + vg * 8 + 2 * vp + h;
+                        if (voxel >= A.nv) continue;
+                        const size_t yo = (size_t)voxel * A.nt;
 #pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int t = dg * DPL + 2 * j + e;
+                        for (int j = 0; j < DPL; ++j) {
+                            float o[2];
+                            wupk(acc[vp][j], o[0], o[1]);
+                            const int t = dg * DPL + j;
                             if (t < A.nt) {
-                                float r = o[e];
+                                float r = o[h];
                                 if (accumulate) r += y[yo + t];
                                 if (subtract) r -= b[yo + t];
                                 y[yo + t] = r;
@@ -436,6 +440,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     for (int o = 16; o > 0; o >>= 1) {
         sq += __shfl_xor_sync(0xffffffffu, sq, o);
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        skipped += __shfl_xor_sync(0xffffffffu, skipped, o);  // producers count per lane
     }
     if (lane == 0) {
         red.part_d[gw] = sq;
@@ -500,19 +505,26 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
             const int wt = ct * kWsCons + warp;
             const bool tile_ok = wt < A.n_tiles;
-            unsigned long long yp[8][DPL / 2];
+            // yv[vp][t] = (y[2vp][t], y[2vp+1][t]) over this lane's DPL
+            // directions: pairs across voxels, so each dictionary value is a
+            // broadcast scalar operand and partial dots come out as voxel pairs
+            unsigned long long yv[4][DPL];
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-                const int voxel = wt * kWsTV + vg * 8 + v;
-                const bool ok = tile_ok && voxel < A.nv;
-                const size_t yo = (size_t)(ok ? voxel : 0) * A.nt;
+            for (int vp = 0; vp < 4; ++vp) {
+                float e[2][DPL];
 #pragma unroll
-                for (int j = 0; j < DPL / 2; ++j) {
-                    const int t = dg * DPL + 2 * j;
-                    const float e0 = (ok && t < A.nt) ? y[yo + t] : 0.f;
-                    const float e1 = (ok && t + 1 < A.nt) ? y[yo + t + 1] : 0.f;
-                    yp[v][j] = wpk(e0, e1);
+                for (int h = 0; h < 2; ++h) {
+                    const int voxel = wt * kWsTV + vg * 8 + 2 * vp + h;
+                    const bool ok = tile_ok && voxel < A.nv;
+                    const size_t yo = (size_t)(ok ? voxel : 0) * A.nt;
+#pragma unroll
+                    for (int j = 0; j < DPL; ++j) {
+                        const int t = dg * DPL + j;
+                        e[h][j] = (ok && t < A.nt) ? y[yo + t] : 0.f;
+                    }
                 }
+#pragma unroll
+                for (int j = 0; j < DPL; ++j) yv[vp][j] = wpk(e[0][j], e[1][j]);
             }
             for (int c = 0; c < A.nch; ++c, ++k) {
                 const int s = k & 1;
@@ -522,34 +534,32 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     float *Z = Zbuf + (s * kWsCons + warp) * kWsCells;
                     const float *D = Dbuf + s * chunk_floats + dg * DPL;
                     const int na_c = min(kWsCA, A.na - c * kWsCA);
+#pragma unroll 1
                     for (int a0 = 0; a0 < na_c; a0 += 2) {
-                        unsigned long long pp[2][8];
+                        unsigned long long pp[2][4];
 #pragma unroll
                         for (int aa = 0; aa < 2; ++aa) {
                             const float4 *d4 = reinterpret_cast<const float4 *>(D + (a0 + aa) * A.nt_pad);
-                            unsigned long long dp[DPL / 2];
+#pragma unroll
+                            for (int vp = 0; vp < 4; ++vp) pp[aa][vp] = 0ull;
 #pragma unroll
                             for (int i = 0; i < DPL / 4; ++i) {
                                 const float4 t = d4[i];
-                                dp[2 * i] = wpk(t.x, t.y);
-                                dp[2 * i + 1] = wpk(t.z, t.w);
-                            }
+                                const float dv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-                            for (int v = 0; v < 8; ++v) {
-                                pp[aa][v] = 0ull;
+                                for (int e = 0; e < 4; ++e) {
+                                    const unsigned long long dd = wpk(dv[e], dv[e]);
 #pragma unroll
-                                for (int j = 0; j < DPL / 2; ++j) wfma2(pp[aa][v], yp[v][j], dp[j]);
+                                    for (int vp = 0; vp < 4; ++vp) wfma2(pp[aa][vp], yv[vp][4 * i + e], dd);
+                                }
                             }
                         }
                         float q[16];
 #pragma unroll
                         for (int aa = 0; aa < 2; ++aa)
 #pragma unroll
-                            for (int v = 0; v < 8; ++v) {
-                                float lo, hi;
-                                wupk(pp[aa][v], lo, hi);
-                                q[aa * 8 + v] = lo + hi;
-                            }
+                            for (int vp = 0; vp < 4; ++vp)
+                                wupk(pp[aa][vp], q[aa * 8 + 2 * vp], q[aa * 8 + 2 * vp + 1]);
                         // butterfly over the 8 direction lanes of this voxel group
 #pragma unroll
                         for (int m = 4, h = 8; m >= 1; m >>= 1, h >>= 1) {
@@ -579,6 +589,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         const int p = warp - kWsCons;
         const int ex = wc_fix_exponent(fx.vmax, fx.dmax, (double)A.nt, fx.fmax_nnz, *fx.ymax);
         const double scale = ldexp(1.0, ex);
+        // z * 2^ex is exact in fp32 (power-of-two scale) when the exponent
+        // stays in range, so the fixed-point term needs no fp64 arithmetic
+        const bool f32_scale = ex >= -120 && ex <= 120;
+        const float scalef = f32_scale ? ldexpf(1.f, ex) : 1.f;
         if (p == 0 && lane == 0 && total > 0)
             tma_chunk(Dbuf, A.D, chunk_bytes, &dfull[0]);
         int k = 0;
@@ -617,7 +631,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     for (int r = 0; r < 4; ++r) {
                         if (G0.ok[r]) {
                             const float z = Z[G0.cr[r] & (kWsCells - 1)] * G0.v[r];
-                            const long long qv = __double2ll_rn((double)z * scale);
+                            const long long qv = f32_scale ? __float2ll_rn(z * scalef)
+                                                           : __double2ll_rn((double)z * scale);
                             atomicAdd(fx.wfix + G0.f[r], static_cast<unsigned long long>(qv));
                         }
                     }
