@@ -182,6 +182,33 @@ LIFE_API int life_dsc_f64(life_phi *phi, const double *w, double *y, uint32_t fl
                  unsigned long long *skipped_dev, void *stream);
 LIFE_API int life_wc_f64(life_phi *phi, const double *y, double *w, void *stream);
 
+/* ---- multi-GPU ------------------------------------------
+ * Phi is sharded by contiguous voxel ranges, one process per GPU.  DSC is
+ * local; each WC ends with one all-reduce of the length-Nf fixed-point
+ * fascicle sums (int64, so the result is bit-identical on every rank), and
+ * each DSC with one all-reduce of two doubles (sum of squares, skip count).
+ * The library does not link a communication library: the caller supplies an
+ * all-reduce that enqueues on `stream` (the Python layer binds it to
+ * torch.distributed / NCCL over NVLink). */
+typedef enum life_dtype { LIFE_DT_F64 = 0, LIFE_DT_F32 = 1, LIFE_DT_I64 = 2 } life_dtype;
+typedef enum life_redop { LIFE_OP_SUM = 0, LIFE_OP_MAX = 1 } life_redop;
+typedef int (*life_allreduce_fn)(void *buf, int64_t count, int dtype, int op, void *stream,
+                                 void *ctx);
+typedef struct life_comm {
+    life_allreduce_fn allreduce;
+    void *ctx;
+    int32_t rank;
+    int32_t nranks;
+} life_comm;
+
+/* Global bounds for the WC fixed-point scale (every rank must use the same
+ * exponent): max |value| and the longest fascicle over the WHOLE problem,
+ * and max ||D_a||_2.  Defaults are the handle's own (single-GPU) values. */
+LIFE_API int life_phi_set_fix_bounds(life_phi *phi, double vmax, double dmax,
+                                     int64_t fmax_nnz);
+LIFE_API int life_phi_get_fix_bounds(const life_phi *phi, double *vmax, double *dmax,
+                                     int64_t *fmax_nnz);
+
 /* ---- SBBNNLS (sbbnnls.py:34-291) --------------------------------------- */
 
 typedef struct life_solver_config {  /* sbbnnls.SolverConfig, sbbnnls.py:34-62 */
@@ -192,6 +219,7 @@ typedef struct life_solver_config {  /* sbbnnls.SolverConfig, sbbnnls.py:34-62 *
     double grad_tol;
     int32_t poll_every;     /* iterations between host termination polls    */
     int32_t use_graph;      /* capture iterations in a CUDA graph           */
+    const life_comm *comm;  /* NULL: single GPU; else voxel-sharded run     */
 } life_solver_config;
 
 typedef struct life_trace_record {   /* sbbnnls.TraceRecord, sbbnnls.py:65-85 */

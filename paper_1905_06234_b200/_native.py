@@ -45,10 +45,22 @@ class SpmvOut(ctypes.Structure):
     _fields_ = [("skipped", c_void_p), ("sumsq", c_void_p), ("absmax", c_void_p)]
 
 
+# int (*)(void *buf, int64_t count, int dtype, int op, void *stream, void *ctx)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, c_void_p, c_i64, ctypes.c_int, ctypes.c_int,
+                                c_void_p, c_void_p)
+DT_F64, DT_F32, DT_I64 = 0, 1, 2
+OP_SUM, OP_MAX = 0, 1
+
+
+class CommC(ctypes.Structure):
+    _fields_ = [("allreduce", ALLREDUCE_FN), ("ctx", c_void_p), ("rank", c_i32),
+                ("nranks", c_i32)]
+
+
 class SolverConfigC(ctypes.Structure):
     _fields_ = [("max_iters", c_i32), ("skip_zero", c_i32), ("exact_f64", c_i32),
                 ("has_w0", c_i32), ("grad_tol", c_double), ("poll_every", c_i32),
-                ("use_graph", c_i32)]
+                ("use_graph", c_i32), ("comm", ctypes.POINTER(CommC))]
 
 
 class TraceRecordC(ctypes.Structure):
@@ -101,6 +113,10 @@ SIGNATURES = {
     "life_sbb_finish": (ctypes.c_int, [c_void_p, ctypes.POINTER(TraceRecordC),
                                        ctypes.POINTER(SolverResultC), c_void_p]),
     "life_sbb_destroy": (ctypes.c_int, [c_void_p]),
+    "life_phi_set_fix_bounds": (ctypes.c_int, [c_void_p, c_double, c_double, c_i64]),
+    "life_phi_get_fix_bounds": (ctypes.c_int, [c_void_p, ctypes.POINTER(c_double),
+                                               ctypes.POINTER(c_double),
+                                               ctypes.POINTER(c_i64)]),
 }
 
 _lib = None

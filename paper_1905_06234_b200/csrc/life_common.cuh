@@ -160,21 +160,35 @@ int dalloc(life_phi *phi, T **p, size_t n)
     return LIFE_OK;
 }
 
-// Fixed-point exponent for the WC accumulator: every |coefficient term| is
-// at most vmax * dmax * ||y_v||_2 <= vmax * dmax * sqrt(nt) * ymax, a
-// fascicle sums at most fmax_nnz of them; the sum stays below 2^62.
-__host__ __device__ inline int wc_fix_exponent(double vmax, double dmax,
-                                               double nt, double fmax_nnz,
-                                               float ymax)
+// Fixed-point exponent for the WC accumulator: a coefficient term is at most
+// vmax * dmax * ||y_v||_2; a fascicle sums at most fmax_nnz of them, and the
+// total must stay below 2^62.  ||y_v||_2 is bounded either by sqrt(nt)*max|y|
+// (standalone WC) or by sqrt(sum y^2) (solver: one scalar that multi-GPU
+// runs all-reduce, so every rank derives the same exponent).
+struct FixParams {
+    unsigned long long *wfix;  // [nf] two's-complement int64 accumulators
+    const float *ymax;         // device max|y|, or null
+    const double *ysumsq;      // device sum of y^2, or null (takes precedence)
+    double vmax, dmax, fmax_nnz;
+};
+
+__host__ __device__ inline int fix_exponent_from(double vmax, double dmax, double ynorm,
+                                                 double fmax_nnz)
 {
-    double bound = vmax * dmax * sqrt(nt) * (double)ymax * fmax_nnz;
+    const double bound = vmax * dmax * ynorm * fmax_nnz;
     if (!(bound > 0.0)) return 0;
     int e;
-    frexp(bound, &e);          // bound < 2^e
+    frexp(bound, &e);  // bound < 2^e
     int ex = 62 - e;
     if (ex > 1000) ex = 1000;
     if (ex < -1000) ex = -1000;
     return ex;
+}
+
+__device__ inline int fix_exponent(const FixParams &fx, int nt)
+{
+    const double yn = fx.ysumsq ? sqrt(*fx.ysumsq) : sqrt((double)nt) * (double)*fx.ymax;
+    return fix_exponent_from(fx.vmax, fx.dmax, yn, fx.fmax_nnz);
 }
 
 // Raise (never lower) a kernel's dynamic shared-memory limit.  The attribute
@@ -192,14 +206,15 @@ struct DscOut {
     unsigned long long *skipped;
     double *sumsq;
     float *absmax;
+    double *skipped_d;  // the skip count again as a double (packed solver scalars)
 };
 int launch_absmax(life_phi *phi, const float *x, int64_t n, float *out,
                   cudaStream_t st);
 int launch_dsc(life_phi *phi, const float *w, float *y, const float *b,
                uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st);
 int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
-              const float *ymax_dev, uint32_t flags, double *sumsq,
-              const CallHooks &h, cudaStream_t st);
+              const float *ymax_dev, const double *ysumsq_dev, uint32_t flags, double *sumsq,
+              const CallHooks &h, const life_comm *comm, cudaStream_t st);
 int prepare_spmv(life_phi *phi);
 int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
                 const double *val, const std::vector<double> &hdict, cudaStream_t st);

@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
         if (threadIdx.x == 0) {
             if (out.sumsq) *out.sumsq = tsq;
             if (out.skipped) *out.skipped = tsk;
+            if (out.skipped_d) *out.skipped_d = (double)tsk;
             if (out.absmax) *out.absmax = tmax;
             *red.counter = 0;
             if (hooks.t_accum && hooks.t_begin) *hooks.t_accum += globaltimer() - *hooks.t_begin;
@@ -345,11 +346,7 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
 // ---------------------------------------------------------------------------
 // WC: Z_tile = Y_tile . D_chunk^T, then value*Z[cell] -> fixed-point fascicle sums
 // ---------------------------------------------------------------------------
-struct DenseFix {
-    unsigned long long *wfix;
-    const float *ymax;
-    double vmax, dmax, fmax_nnz;
-};
+using DenseFix = FixParams;
 
 template <int DPL>
 __global__ void __launch_bounds__(kDenseThreads, 2)
@@ -369,7 +366,7 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
     const int n_ct = (A.n_tiles + kDenseWarps - 1) / kDenseWarps;
     const int my_tiles = (int)blockIdx.x < n_ct ? (n_ct - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int total = my_tiles * A.nch;
-    const int ex = wc_fix_exponent(fx.vmax, fx.dmax, (double)A.nt, fx.fmax_nnz, *fx.ymax);
+    const int ex = fix_exponent(fx, A.nt);
     const double scale = ldexp(1.0, ex);
     if (threadIdx.x == 0) {
         dmbar_init(&bar[0]);
@@ -702,13 +699,12 @@ static int dense_dsc_t(life_phi *phi, const float *w, float *y, const float *b, 
 }
 
 template <int DPL>
-static int dense_wc_t(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+static int dense_wc_t(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
                       cudaStream_t st)
 {
     LIFE_TRY(ensure_smem(k_wc_dense<DPL>, phi->d_smem));
     DenseArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_D,
                 phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
-    DenseFix fx{phi->wfix, ymax, phi->vmax, phi->dmax, (double)phi->fmax_nnz};
     k_wc_dense<DPL><<<phi->d_blocks, kDenseThreads, phi->d_smem, st>>>(A, y, fx, h);
     LIFE_CHECK_LAUNCH();
     return LIFE_OK;
@@ -737,7 +733,7 @@ static int dense_prepare_t(life_phi *phi)
 
 int launch_dsc_ws(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
                   const DscOut &o, const CallHooks &h, cudaStream_t st);
-int launch_wc_ws(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+int launch_wc_ws(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
                  cudaStream_t st);
 int prepare_ws(life_phi *phi);
 
@@ -747,10 +743,10 @@ static int dense_v1_dsc(life_phi *phi, const float *w, float *y, const float *b,
     LIFE_DPL_DISPATCH(dense_dsc_t, phi, w, y, b, flags, o, h, st);
 }
 
-static int dense_v1_wc(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+static int dense_v1_wc(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
                        cudaStream_t st)
 {
-    LIFE_DPL_DISPATCH(dense_wc_t, phi, y, ymax, h, st);
+    LIFE_DPL_DISPATCH(dense_wc_t, phi, fx, y, h, st);
 }
 
 static int dense_v1_prepare(life_phi *phi) { LIFE_DPL_DISPATCH(dense_prepare_t, phi); }
@@ -762,11 +758,11 @@ int launch_dsc_dense(life_phi *phi, const float *w, float *y, const float *b, ui
     return dense_v1_dsc(phi, w, y, b, flags, o, h, st);
 }
 
-int launch_wc_dense(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+int launch_wc_dense(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
                     cudaStream_t st)
 {
-    if (phi->d_kind == 2) return launch_wc_ws(phi, y, ymax, h, st);
-    return dense_v1_wc(phi, y, ymax, h, st);
+    if (phi->d_kind == 2) return launch_wc_ws(phi, fx, y, h, st);
+    return dense_v1_wc(phi, fx, y, h, st);
 }
 
 int prepare_dense(life_phi *phi)

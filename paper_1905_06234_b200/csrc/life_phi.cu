@@ -778,6 +778,27 @@ int life_phi_destroy(life_phi *phi)
     return ok();
 }
 
+int life_phi_set_fix_bounds(life_phi *phi, double vmax, double dmax, int64_t fmax_nnz)
+{
+    if (!phi) return fail(LIFE_ERR_INVALID_ARGUMENT, "null handle");
+    if (!(vmax >= 0.0) || !(dmax >= 0.0) || fmax_nnz < 1)
+        return fail(LIFE_ERR_CONFIG_INVALID, "fixed-point bounds must be positive");
+    // never tighter than the handle's own data (the sum must not overflow)
+    phi->vmax = std::max(phi->vmax, vmax);
+    phi->dmax = std::max(phi->dmax, dmax);
+    phi->fmax_nnz = std::max<int64_t>(phi->fmax_nnz, fmax_nnz);
+    return ok();
+}
+
+int life_phi_get_fix_bounds(const life_phi *phi, double *vmax, double *dmax, int64_t *fmax_nnz)
+{
+    if (!phi || !vmax || !dmax || !fmax_nnz) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
+    *vmax = phi->vmax;
+    *dmax = phi->dmax;
+    *fmax_nnz = phi->fmax_nnz;
+    return ok();
+}
+
 int life_phi_get_info(const life_phi *phi, life_phi_info *info)
 {
     if (!phi || !info) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");

@@ -22,10 +22,10 @@ namespace life {
 
 
 struct Scal {
-    double rr, gg, mgmg, mtmg2, alpha, obj, init_obj, final_obj;
+    // rr/skipped_d and mgmg/pad are adjacent: each pair is one all-reduce
+    double rr, skipped_d, mgmg, mg_pad;
+    double gg, mtmg2, alpha, obj, init_obj, final_obj;
     double bb, m1;            // ||b||^2, ||M 1||^2 for the default w0
-    float ymax_r, ymax_mg;
-    unsigned long long skipped;
     unsigned long long t_begin, dsc_ns, wc_ns;
     int done, term, iter, max_iters;
     double grad_tol;
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(BT)
             life_trace_record r;
             r.iteration = it;
             r.zeros = (int)zz;
-            r.dsc_skipped = (int64_t)s->skipped;
+            r.dsc_skipped = (int64_t)s->skipped_d;
             r.objective = s->obj;
             r.alpha = s->alpha;
             r.grad_norm = sqrt(s->gg);
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(BT)
 
 __global__ void k_set_skipped(Scal *s, const unsigned long long *src)
 {
-    if (!s->done) s->skipped = *src;
+    if (!s->done) s->skipped_d = (double)*src;
 }
 
 template <typename T>
@@ -253,7 +253,17 @@ struct Solver {
     unsigned *counter = nullptr;
     unsigned long long *skipped_dev = nullptr;
     int nblk_f = 1;
+    const life_comm *comm = nullptr;
 };
+
+// Enqueue an all-reduce through the caller's communicator (multi-GPU only).
+static int comm_reduce(const Solver &S, void *buf, int64_t count, int dtype, int op)
+{
+    if (!S.comm || S.comm->nranks <= 1) return LIFE_OK;
+    if (S.comm->allreduce(buf, count, dtype, op, S.st, S.comm->ctx) != 0)
+        return fail(LIFE_ERR_NCCL, "solver all-reduce failed");
+    return LIFE_OK;
+}
 
 // One iteration, fp32 fast path.
 static int iter_fast(Solver &S, const float *b, float *w, int even)
@@ -265,15 +275,21 @@ static int iter_fast(Solver &S, const float *b, float *w, int even)
     float *r = (float *)S.r, *mg = (float *)S.mg, *gt = (float *)S.gt,
           *mtmg = (float *)S.mtmg;
     const uint32_t skip = S.skip ? LIFE_SKIP_ZERO : 0u;
+    // r = M w - b; the WC fixed-point scale comes from sqrt(sum r^2), one
+    // scalar that multi-GPU runs reduce together with the skip count
     LIFE_TRY(launch_dsc(phi, w, r, b, LIFE_SUBTRACT_B | skip,
-                        DscOut{&s->skipped, &s->rr, &s->ymax_r}, hd, S.st));
-    LIFE_TRY(launch_wc(phi, r, gt, w, &s->ymax_r, LIFE_PROJECT_GRAD, &s->gg, hw, S.st));
+                        DscOut{nullptr, &s->rr, nullptr, &s->skipped_d}, hd, S.st));
+    LIFE_TRY(comm_reduce(S, &s->rr, 2, LIFE_DT_F64, LIFE_OP_SUM));
+    LIFE_TRY(launch_wc(phi, r, gt, w, nullptr, &s->rr, LIFE_PROJECT_GRAD, &s->gg, hw, S.comm,
+                       S.st));
     k_check_grad<<<1, 1, 0, S.st>>>(s);
     LIFE_CHECK_LAUNCH();
-    LIFE_TRY(launch_dsc(phi, gt, mg, nullptr, skip, DscOut{nullptr, &s->mgmg, &s->ymax_mg},
+    LIFE_TRY(launch_dsc(phi, gt, mg, nullptr, skip, DscOut{nullptr, &s->mgmg, nullptr, nullptr},
                         hd, S.st));
+    LIFE_TRY(comm_reduce(S, &s->mgmg, 1, LIFE_DT_F64, LIFE_OP_SUM));
     if (even)
-        LIFE_TRY(launch_wc(phi, mg, mtmg, nullptr, &s->ymax_mg, 0u, &s->mtmg2, hw, S.st));
+        LIFE_TRY(launch_wc(phi, mg, mtmg, nullptr, nullptr, &s->mgmg, 0u, &s->mtmg2, hw, S.comm,
+                           S.st));
     k_alpha<<<1, 1, 0, S.st>>>(s, even);
     LIFE_CHECK_LAUNCH();
     k_update<float, 256><<<S.nblk_f, 256, 0, S.st>>>(w, gt, phi->nf, s, S.rec, S.part,
@@ -387,6 +403,9 @@ extern "C" int life_sbb_create(life_phi *phi, const void *b_dev, void *w_dev,
     S.exact = exact;
     S.skip = cfg->skip_zero;
     S.nblk_f = blocks_for<float>(phi, phi->nf);
+    S.comm = cfg->comm;
+    if (S.comm && S.comm->nranks > 1 && exact)
+        return fail(LIFE_ERR_CONFIG_INVALID, "voxel-sharded runs use the fp32 path");
     LIFE_CUDA(cudaMalloc(&S.s, sizeof(Scal)));
     LIFE_CUDA(cudaMalloc(&S.rec, sizeof(life_trace_record) * cfg->max_iters));
     LIFE_CUDA(cudaMalloc(&S.r, std::max<int64_t>(ny, 1) * es));
@@ -430,10 +449,11 @@ extern "C" int life_sbb_create(life_phi *phi, const void *b_dev, void *w_dev,
             LIFE_CHECK_LAUNCH();
             CallHooks none{nullptr, nullptr, nullptr};
             LIFE_TRY(launch_dsc(phi, ones, tmp, nullptr, skip,
-                                DscOut{nullptr, &S.s->m1, nullptr}, none, st));
+                                DscOut{nullptr, &S.s->m1, nullptr, nullptr}, none, st));
             k_sumsq<float, 256><<<by, 256, 0, st>>>((const float *)b_dev, ny, S.part,
                                                     S.counter, &S.s->bb);
             LIFE_CHECK_LAUNCH();
+            LIFE_TRY(comm_reduce(S, &S.s->bb, 2, LIFE_DT_F64, LIFE_OP_SUM));  // bb, m1
             k_w0_scale<float><<<bf, 256, 0, st>>>(S.s, (float *)w_dev, phi->nf);
         }
         LIFE_CHECK_LAUNCH();
@@ -445,7 +465,7 @@ extern "C" int life_sbb_create(life_phi *phi, const void *b_dev, void *w_dev,
     }
     if (!exact) {
         LIFE_TRY(prepare_spmv(phi));
-        if (cfg->use_graph) {
+        if (cfg->use_graph && !(S.comm && S.comm->nranks > 1)) {
             // capture one odd+even iteration pair; replays are parity-correct
             // because pairs always start at an odd iteration index
             // (captured on a private stream: the legacy default stream cannot
@@ -550,8 +570,9 @@ extern "C" int life_sbb_finish(life_sbb *x, life_trace_record *records,
         } else {
             CallHooks none{nullptr, nullptr, nullptr};
             LIFE_TRY(launch_dsc(phi, (const float *)x->w, (float *)S.r, (const float *)x->b,
-                                LIFE_SUBTRACT_B | skip, DscOut{nullptr, &S.s->rr, nullptr},
+                                LIFE_SUBTRACT_B | skip, DscOut{nullptr, &S.s->rr, nullptr, nullptr},
                                 none, st));
+            LIFE_TRY(comm_reduce(S, &S.s->rr, 1, LIFE_DT_F64, LIFE_OP_SUM));
         }
         double rr = 0;
         LIFE_CUDA(cudaMemcpyAsync(&rr, &S.s->rr, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
         if (threadIdx.x == 0) {
             if (out.sumsq) *out.sumsq = tsq;
             if (out.skipped) *out.skipped = tsk;
+            if (out.skipped_d) *out.skipped_d = (double)tsk;
             if (out.absmax) *out.absmax = tmax;
             *red.counter = 0;
             if (hooks.t_accum && hooks.t_begin)
@@ -347,11 +348,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
 // ---------------------------------------------------------------------------
 // WC fp32: per-coefficient dots + fixed-point fascicle accumulation
 // ---------------------------------------------------------------------------
-struct WcFix {
-    unsigned long long *wfix;
-    const float *ymax;  // device scalar, max |y|
-    double vmax, dmax, fmax_nnz;
-};
+using WcFix = FixParams;
 
 template <int NT, bool FULL>
 __global__ void __launch_bounds__(kSpmvThreads, 1)
@@ -368,7 +365,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
     __syncthreads();
     unsigned parity = 0;
     const int nt = A.nt;
-    const int ex = wc_fix_exponent(fx.vmax, fx.dmax, (double)nt, fx.fmax_nnz, *fx.ymax);
+    const int ex = fix_exponent(fx, nt);
     const double scale = ldexp(1.0, ex);
     const int vb = A.wpart[gw], ve = A.wpart[gw + 1];
 
@@ -459,7 +456,7 @@ __global__ void __launch_bounds__(BT)
                   double *sumsq_out, const CallHooks hooks)
 {
     if (hooks.done && *hooks.done) return;
-    const int ex = wc_fix_exponent(fx.vmax, fx.dmax, (double)nt, fx.fmax_nnz, *fx.ymax);
+    const int ex = fix_exponent(fx, nt);
     const double inv = ldexp(1.0, -ex);
     const bool accumulate = flags & LIFE_ACCUMULATE;
     const bool project = (flags & LIFE_PROJECT_GRAD) && w_ref != nullptr;
@@ -666,7 +663,7 @@ static int launch_wc_t(life_phi *phi, const float *y, const WcFix &fx,
 
 int launch_dsc_dense(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
                      const DscOut &o, const CallHooks &h, cudaStream_t st);
-int launch_wc_dense(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+int launch_wc_dense(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
                     cudaStream_t st);
 int prepare_dense(life_phi *phi);
 
@@ -693,7 +690,7 @@ static int launch_wc_sparse(life_phi *phi, const float *y, const WcFix &fx,
 int launch_wc_main(life_phi *phi, const float *y, const WcFix &fx,
                    const CallHooks &h, cudaStream_t st)
 {
-    if (phi->has_dense) return launch_wc_dense(phi, y, fx.ymax, h, st);
+    if (phi->has_dense) return launch_wc_dense(phi, fx, y, h, st);
     return launch_wc_sparse(phi, y, fx, h, st);
 }
 
@@ -724,15 +721,22 @@ int prepare_spmv(life_phi *phi)
 }
 
 int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
-              const float *ymax_dev, uint32_t flags, double *sumsq,
-              const CallHooks &h, cudaStream_t st)
+              const float *ymax_dev, const double *ysumsq_dev, uint32_t flags, double *sumsq,
+              const CallHooks &h, const life_comm *comm, cudaStream_t st)
 {
-    if (!ymax_dev) {
+    if (!ymax_dev && !ysumsq_dev) {
         LIFE_TRY(launch_absmax(phi, y, (int64_t)phi->nv * phi->nt, phi->ybound, st));
         ymax_dev = phi->ybound;
     }
-    WcFix fx{phi->wfix, ymax_dev, phi->vmax, phi->dmax, (double)phi->fmax_nnz};
+    WcFix fx{phi->wfix, ymax_dev, ysumsq_dev, phi->vmax, phi->dmax, (double)phi->fmax_nnz};
     LIFE_TRY(launch_wc_main(phi, y, fx, h, st));
+    if (comm && comm->nranks > 1) {
+        // fascicle partial sums of all voxel shards: integer sum, so every
+        // rank gets bit-identical totals whatever the reduction order
+        const int rc = comm->allreduce(phi->wfix, phi->nf, LIFE_DT_I64, LIFE_OP_SUM, st,
+                                       comm->ctx);
+        if (rc != 0) return fail(LIFE_ERR_NCCL, "allreduce(wfix) failed");
+    }
     const int blocks = std::max(1, std::min(phi->sms * 4, (phi->nf + 255) / 256));
     k_wc_finalize<256><<<blocks, 256, 0, st>>>(phi->wfix, w, w_ref, phi->nf, flags, fx,
                                                phi->nt, phi->part_d2, phi->counter2,
@@ -754,8 +758,8 @@ int life_dsc_f32(life_phi *phi, const float *w, float *y, const float *b,
     if (!phi->has_fast && !phi->has_dense)
         return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     if ((flags & LIFE_SUBTRACT_B) && !b) return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_SUBTRACT_B needs b");
-    DscOut o{nullptr, nullptr, nullptr};
-    if (out) o = DscOut{out->skipped, out->sumsq, out->absmax};
+    DscOut o{nullptr, nullptr, nullptr, nullptr};
+    if (out) o = DscOut{out->skipped, out->sumsq, out->absmax, nullptr};
     CallHooks h{nullptr, nullptr, nullptr};
     LIFE_TRY(launch_dsc(phi, w, y, b, flags, o, h, static_cast<cudaStream_t>(stream)));
     return ok();
@@ -771,8 +775,8 @@ int life_wc_f32(life_phi *phi, const float *y, float *w, const float *w_ref,
     if ((flags & LIFE_PROJECT_GRAD) && !w_ref)
         return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_PROJECT_GRAD needs w_ref");
     CallHooks h{nullptr, nullptr, nullptr};
-    LIFE_TRY(launch_wc(phi, y, w, w_ref, y_absmax_dev, flags, out ? out->sumsq : nullptr,
-                       h, static_cast<cudaStream_t>(stream)));
+    LIFE_TRY(launch_wc(phi, y, w, w_ref, y_absmax_dev, nullptr, flags,
+                       out ? out->sumsq : nullptr, h, nullptr, static_cast<cudaStream_t>(stream)));
     return ok();
 }
 

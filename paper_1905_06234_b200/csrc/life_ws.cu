@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         if (threadIdx.x == 0) {
             if (out.sumsq) *out.sumsq = tsq;
             if (out.skipped) *out.skipped = tsk;
+            if (out.skipped_d) *out.skipped_d = (double)tsk;
             if (out.absmax) *out.absmax = tmax;
             *red.counter = 0;
             if (hooks.t_accum && hooks.t_begin) *hooks.t_accum += globaltimer() - *hooks.t_begin;
@@ -465,11 +466,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 // ---------------------------------------------------------------------------
 // WC
 // ---------------------------------------------------------------------------
-struct WsFix {
-    unsigned long long *wfix;
-    const float *ymax;
-    double vmax, dmax, fmax_nnz;
-};
+using WsFix = FixParams;
 
 template <int DPL>
 __global__ void __launch_bounds__(kWsThreads, 1)
@@ -587,7 +584,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     } else {
         // ===== producers: D chunks via TMA; scatter value * Z[cell] =====
         const int p = warp - kWsCons;
-        const int ex = wc_fix_exponent(fx.vmax, fx.dmax, (double)A.nt, fx.fmax_nnz, *fx.ymax);
+        const int ex = fix_exponent(fx, A.nt);
         const double scale = ldexp(1.0, ex);
         // z * 2^ex is exact in fp32 (power-of-two scale) when the exponent
         // stays in range, so the fixed-point term needs no fp64 arithmetic
@@ -663,13 +660,12 @@ static int ws_dsc_t(life_phi *phi, const float *w, float *y, const float *b, uin
 }
 
 template <int DPL>
-static int ws_wc_t(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+static int ws_wc_t(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
                    cudaStream_t st)
 {
     LIFE_TRY(ensure_smem(k_wc_ws<DPL>, phi->d_smem));
     WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_D,
              phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
-    WsFix fx{phi->wfix, ymax, phi->vmax, phi->dmax, (double)phi->fmax_nnz};
     k_wc_ws<DPL><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, y, fx, h);
     LIFE_CHECK_LAUNCH();
     return LIFE_OK;
@@ -697,10 +693,10 @@ int launch_dsc_ws(life_phi *phi, const float *w, float *y, const float *b, uint3
     LIFE_WS_DISPATCH(ws_dsc_t, phi, w, y, b, flags, o, h, st);
 }
 
-int launch_wc_ws(life_phi *phi, const float *y, const float *ymax, const CallHooks &h,
+int launch_wc_ws(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
                  cudaStream_t st)
 {
-    LIFE_WS_DISPATCH(ws_wc_t, phi, y, ymax, h, st);
+    LIFE_WS_DISPATCH(ws_wc_t, phi, fx, y, h, st);
 }
 
 int prepare_ws(life_phi *phi) { LIFE_WS_DISPATCH(ws_prepare_t, phi); }

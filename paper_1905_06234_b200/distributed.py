@@ -1,0 +1,186 @@
+"""Voxel-sharded SBBNNLS over several GPUs.
+
+One process per GPU.  Phi is cut into contiguous voxel ranges balanced by
+coefficient count; a boundary never splits a voxel's coefficients -- exactly
+the reference's synchronization-free rule (engine.build_plan with
+PartitionStrategy("coefficient", sync_free=True), engine.py:113-184) with
+one "thread" per GPU.  Each rank holds its Phi slice (voxels renumbered
+from 0), the full dictionary, its slice of the signal and the replicated
+weights.
+
+Per iteration the exchange is: DSC local (one all-reduce of two doubles:
+sum of squares and skip count), WC local partial sums of the Nf fascicle
+weights in 64-bit fixed point followed by one all-reduce (int64 sum, so the
+result is bit-identical on all ranks and independent of the reduction
+order).  All Nf-space solver work (projection, step size, update) then runs
+redundantly and identically on every rank: there is no broadcast.
+
+The collectives are torch.distributed calls (NCCL over NVLink/NVSwitch for
+the CUDA backend; gloo works too, for tests) enqueued on the solver's stream
+from a ctypes callback that liblife_b200 invokes between its kernels.
+"""
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigInvalid
+from .tensor import Dictionary, Dims, PhiTensor
+
+
+def shard_voxel_ranges(voxel_counts, nranks):
+    """Contiguous voxel ranges [v0, v1) per rank.
+
+    The coefficient range of the voxel-sorted tensor is split into
+    ceil(Nc/nranks) chunks whose interior boundaries are snapped to voxel-run
+    boundaries (engine.snap_to_run_boundaries), then mapped back to voxels.
+    ``voxel_counts[v]`` is the number of coefficients of voxel v."""
+    counts = np.asarray(voxel_counts, dtype=np.int64)
+    nv = counts.size
+    nc = int(counts.sum())
+    if nranks < 1:
+        raise ConfigInvalid("nranks must be >= 1")
+    starts = np.concatenate(([0], np.cumsum(counts)))
+    step = math.ceil(nc / nranks) if nc else 0
+    bounds = [min(i * step, nc) for i in range(nranks + 1)]
+    # the voxel key array of the sorted tensor, implicitly: run v covers
+    # [starts[v], starts[v+1]); snap on that run table (same result as
+    # snap_to_run_boundaries on the expanded key array, tested)
+    bounds = _snap_runs(starts, bounds)
+    # coefficient boundary -> voxel boundary (first voxel starting at it)
+    vb = [0]
+    for b in bounds[1:-1]:
+        vb.append(int(np.searchsorted(starts, b, side="left")))
+    vb.append(nv)
+    for i in range(1, len(vb)):
+        vb[i] = max(vb[i], vb[i - 1])
+    return [(vb[i], vb[i + 1]) for i in range(nranks)]
+
+
+def _snap_runs(starts, bounds):
+    """snap_to_run_boundaries on the run table (no per-coefficient keys)."""
+    nc = int(starts[-1])
+    out = list(bounds)
+    for i in range(1, len(out) - 1):
+        b = out[i]
+        if 0 < b < nc:
+            v = int(np.searchsorted(starts, b, side="right")) - 1  # run containing b
+            lo, hi = int(starts[v]), int(starts[v + 1])
+            if lo < b < hi:
+                out[i] = lo if (b - lo) <= (hi - b) else hi
+    for i in range(1, len(out)):
+        out[i] = max(out[i], out[i - 1])
+    return out
+
+
+def shard_problem(tensor, dictionary, y, v0, v1):
+    """The local problem of voxel range [v0, v1): (PhiTensor, Dictionary, b)."""
+    d = tensor.dims
+    sel = (tensor.voxels >= v0) & (tensor.voxels < v1)
+    idx = np.flatnonzero(sel)
+    local = Dims(n_atoms=d.n_atoms, n_voxels=max(1, v1 - v0), n_fibers=d.n_fibers,
+                 n_dirs=d.n_dirs, n_coeffs=int(idx.size))
+    t = PhiTensor(atoms=tensor.atoms[idx], voxels=tensor.voxels[idx] - np.uint32(v0),
+                  fibers=tensor.fibers[idx], values=tensor.values[idx], dims=local)
+    dic = Dictionary(data=dictionary.data, dims=local)
+    b = np.zeros(local.signal_len)
+    if v1 > v0:
+        b[:] = np.asarray(y)[v0 * d.n_dirs:v1 * d.n_dirs]
+    return t, dic, b
+
+
+def global_fix_bounds(tensor):
+    """(max |value|, longest fascicle) over the whole problem: every rank must
+    derive the same fixed-point exponent for the WC all-reduce."""
+    vmax = float(np.max(np.abs(tensor.values))) if tensor.dims.n_coeffs else 0.0
+    fmax = int(np.bincount(tensor.fibers, minlength=1).max()) if tensor.dims.n_coeffs else 1
+    return vmax * (1.0 + 1e-6), max(fmax, 1)
+
+
+class _CudaArray:
+    """Zero-copy torch view of a raw device pointer (__cuda_array_interface__)."""
+
+    _TYPES = {N.DT_F64: "<f8", N.DT_F32: "<f4", N.DT_I64: "<i8"}
+
+    def __init__(self, ptr, count, dtype):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": self._TYPES[dtype],
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+class TorchComm:
+    """life_comm backed by torch.distributed (NCCL on GPUs, gloo in tests)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.nranks = dist.get_world_size(group)
+        self.error = None
+        self.host_staged = dist.get_backend(group) == "gloo"
+
+        def _allreduce(buf, count, dtype, op, stream, ctx):
+            try:
+                import torch
+                t = torch.as_tensor(_CudaArray(buf, count, dtype), device="cuda")
+                red = dist.ReduceOp.SUM if op == N.OP_SUM else dist.ReduceOp.MAX
+                s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+                with torch.cuda.stream(s):
+                    if self.host_staged:  # gloo (tests): through host memory
+                        h = t.cpu()
+                        dist.all_reduce(h, op=red, group=self.group)
+                        t.copy_(h)
+                    else:                 # NCCL: enqueued, stream-ordered
+                        dist.all_reduce(t, op=red, group=self.group)
+                return 0
+            except Exception as exc:  # reported by the C side as LIFE_ERR_NCCL
+                self.error = exc
+                return 1
+
+        self._fn = N.ALLREDUCE_FN(_allreduce)
+        self.c = N.CommC(allreduce=self._fn, ctx=None, rank=self.rank, nranks=self.nranks)
+
+
+def solve_sharded(problem, config=None, group=None, w0=None, ranges=None):
+    """SBBNNLS with Phi voxel-sharded over the ranks of a torch.distributed
+    group (every rank calls it with the same problem).  Returns (w, trace);
+    both are identical on all ranks."""
+    import torch
+
+    from . import device
+    from .sbbnnls import SolverConfig, SolverSession, trace_from
+
+    config = config or SolverConfig()
+    if config.precision != "fp32":
+        raise ConfigInvalid("voxel-sharded solves run the fp32 path")
+    comm = TorchComm(group)
+    counts = np.bincount(problem.tensor.voxels, minlength=problem.dims.n_voxels)
+    ranges = ranges or shard_voxel_ranges(counts, comm.nranks)
+    v0, v1 = ranges[comm.rank]
+    t, dic, b_host = shard_problem(problem.tensor, problem.dictionary, problem.y, v0, v1)
+    op = device.DeviceOperator(t, dic)
+    vmax, fmax = global_fix_bounds(problem.tensor)
+    N.check(N.lib().life_phi_set_fix_bounds(op.handle, vmax, 0.0, fmax))
+    b = torch.from_numpy(b_host).to(device="cuda", dtype=torch.float32)
+    if w0 is None:
+        w = torch.empty(problem.dims.n_fibers, dtype=torch.float32, device="cuda")
+    else:
+        w = torch.from_numpy(np.asarray(w0, dtype=np.float64)).to(device="cuda",
+                                                                  dtype=torch.float32)
+    sess = SolverSession(op, b, w, config, has_w0=w0 is not None, comm=comm)
+    done = False
+    while not done:
+        sess.iterate(config.poll_every)
+        done = sess.poll()
+    if comm.error is not None:
+        raise comm.error
+    res, recs = sess.finish()
+    sess.close()
+    return w.double().cpu().numpy(), trace_from(res, recs)
+
+
+__all__ = ["TorchComm", "global_fix_bounds", "shard_problem", "shard_voxel_ranges",
+           "solve_sharded"]

@@ -150,7 +150,7 @@ def solve_device(op, b, w, config, stream=None):
                           exact_f64=int(config.precision == "fp64"),
                           has_w0=int(getattr(config, "_has_w0", False)),
                           grad_tol=float(config.grad_tol), poll_every=int(config.poll_every),
-                          use_graph=int(config.use_graph))
+                          use_graph=int(config.use_graph), comm=None)
     recs = (N.TraceRecordC * config.max_iters)()
     res = N.SolverResultC()
     N.check(N.lib().life_solve(op.handle, ctypes.c_void_p(b.data_ptr()),
@@ -167,15 +167,17 @@ class SolverSession:
     w0 when ``has_w0`` and receives the iterates.  Used by bench.py to time
     exactly N iterations, and by the multi-GPU driver."""
 
-    def __init__(self, op, b, w, config, has_w0=False, stream=None):
+    def __init__(self, op, b, w, config, has_w0=False, stream=None, comm=None):
         N.require_cuda()
         self.config = config
         self._b, self._w, self._stream = b, w, stream
+        self._comm = comm  # keeps the ctypes callback alive for the session
         cfg = N.SolverConfigC(max_iters=config.max_iters, skip_zero=int(config.skip_zero),
                               exact_f64=int(config.precision == "fp64"), has_w0=int(has_w0),
                               grad_tol=float(config.grad_tol),
                               poll_every=int(config.poll_every),
-                              use_graph=int(config.use_graph))
+                              use_graph=int(config.use_graph),
+                              comm=ctypes.pointer(comm.c) if comm is not None else None)
         h = ctypes.c_void_p()
         N.check(N.lib().life_sbb_create(op.handle, ctypes.c_void_p(b.data_ptr()),
                                         ctypes.c_void_p(w.data_ptr()), ctypes.byref(cfg),
@@ -210,6 +212,24 @@ class SolverSession:
             pass
 
 
+def trace_from(res, recs, setup_seconds=0.0):
+    """SolverTrace from the C result and trace records."""
+    trace = SolverTrace(termination=N.TERM_NAMES.get(res.termination, "max_iters"),
+                        initial_objective=res.initial_objective,
+                        final_objective=res.final_objective,
+                        total_dsc_calls=int(res.total_dsc_calls),
+                        total_wc_calls=int(res.total_wc_calls),
+                        loop_seconds=res.loop_seconds, setup_seconds=setup_seconds)
+    for i in range(res.iterations):
+        r = recs[i]
+        trace.records.append(TraceRecord(
+            iteration=r.iteration, objective=r.objective, alpha=r.alpha,
+            grad_norm=r.grad_norm, zeros=r.zeros, dsc_seconds=r.dsc_seconds,
+            wc_seconds=r.wc_seconds, dsc_calls=r.dsc_calls, wc_calls=r.wc_calls,
+            dsc_skipped=int(r.dsc_skipped), w_min=r.w_min))
+    return trace
+
+
 def solve(problem, w0=None, config=None):
     """Run the solver on the B200; returns (weights, trace) like
     sbbnnls.solve (sbbnnls.py:223-291)."""
@@ -233,17 +253,4 @@ def solve(problem, w0=None, config=None):
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     res, recs = solve_device(op, b, w, config)
-    trace = SolverTrace(termination=N.TERM_NAMES.get(res.termination, "max_iters"),
-                        initial_objective=res.initial_objective,
-                        final_objective=res.final_objective,
-                        total_dsc_calls=int(res.total_dsc_calls),
-                        total_wc_calls=int(res.total_wc_calls),
-                        loop_seconds=res.loop_seconds, setup_seconds=t_setup)
-    for i in range(res.iterations):
-        r = recs[i]
-        trace.records.append(TraceRecord(
-            iteration=r.iteration, objective=r.objective, alpha=r.alpha,
-            grad_norm=r.grad_norm, zeros=r.zeros, dsc_seconds=r.dsc_seconds,
-            wc_seconds=r.wc_seconds, dsc_calls=r.dsc_calls, wc_calls=r.wc_calls,
-            dsc_skipped=int(r.dsc_skipped), w_min=r.w_min))
-    return w.double().cpu().numpy(), trace
+    return w.double().cpu().numpy(), trace_from(res, recs, t_setup)
