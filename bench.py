@@ -229,14 +229,30 @@ def run_ours(args, dims):
 
     # ---- device-resident timing of exactly K iterations ---------------------
     total_iters = args.warmup + args.steps
-    op = L.DeviceOperator(problem.tensor, problem.dictionary)
+    comm = None
+    if world > 1:
+        from paper_1905_06234_b200 import distributed as D
+        comm = D.TorchComm()
+        counts = np.bincount(problem.tensor.voxels, minlength=nv)
+        v0, v1 = D.shard_voxel_ranges(counts, world)[rank]
+        t_loc, dic_loc, b_loc = D.shard_problem(problem.tensor, problem.dictionary,
+                                                problem.y, v0, v1)
+        op = L.DeviceOperator(t_loc, dic_loc)
+        vmax, fmax = D.global_fix_bounds(problem.tensor)
+        _native.check(_native.lib().life_phi_set_fix_bounds(op.handle, vmax, 0.0, fmax))
+        b = torch.from_numpy(b_loc).to(device="cuda", dtype=torch.float32)
+        local_dims = (na, t_loc.dims.n_voxels, nf, nt, t_loc.dims.n_coeffs)
+        info["shard"] = {"voxels": [int(v0), int(v1)], "n_coeffs": int(t_loc.dims.n_coeffs)}
+    else:
+        op = L.DeviceOperator(problem.tensor, problem.dictionary)
+        b = torch.from_numpy(problem.y).to(device="cuda", dtype=torch.float32)
+        local_dims = dims
     info["restructure_ms"] = round(op.info.sort_ms, 1)
     info["atom_groups"] = op.info.atom_groups
     info["kernels"] = op.kind
-    b = torch.from_numpy(problem.y).to(device="cuda", dtype=torch.float32)
     w = torch.empty(nf, dtype=torch.float32, device="cuda")
     scfg = L.SolverConfig(max_iters=total_iters, grad_tol=0.0)
-    sess = L.sbbnnls.SolverSession(op, b, w, scfg)
+    sess = L.sbbnnls.SolverSession(op, b, w, scfg, comm=comm)
     sess.iterate(args.warmup)
     torch.cuda.synchronize()
     if world > 1:
@@ -255,17 +271,16 @@ def run_ours(args, dims):
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    terminated_early = sess.poll() and False
     res, recs = sess.finish()
     if res.iterations < total_iters:
         raise RuntimeError(f"solver stopped after {res.iterations} < {total_iters} iterations "
                            f"({res.termination}); timed region would contain no-op steps")
     value = args.steps / (ms * 1e-3)
-    del terminated_early
 
     # ---- kernel-level timing (DSC / WC) for the roofline -------------------
-    dsc_b, wc_b = spmv_bytes(dims)
-    y = torch.empty(nv * nt, dtype=torch.float32, device="cuda")
+    # (this rank's shard when N > 1: local bytes over local kernel time)
+    dsc_b, wc_b = spmv_bytes(local_dims)
+    y = torch.empty(local_dims[1] * nt, dtype=torch.float32, device="cuda")
     g = torch.empty(nf, dtype=torch.float32, device="cuda")
     ymax = torch.zeros(1, dtype=torch.float32, device="cuda")
     iso = max(5, min(20, args.steps))
@@ -309,12 +324,16 @@ def run_ours(args, dims):
         fresh = L.PhiTensor(atoms=t.atoms, voxels=t.voxels, fibers=t.fibers, values=t.values,
                             dims=t.dims)
         p2 = L.Problem(tensor=fresh, dictionary=problem.dictionary, y=problem.y)
+        sess.close()
         del op, sess
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        w_host, tr = L.solve(p2, config=L.SolverConfig(max_iters=args.steps, grad_tol=0.0))
+        if world > 1:
+            w_host, tr = D.solve_sharded(p2, L.SolverConfig(max_iters=args.steps, grad_tol=0.0))
+        else:
+            w_host, tr = L.solve(p2, config=L.SolverConfig(max_iters=args.steps, grad_tol=0.0))
         e2e_s = time.perf_counter() - t0
         if world > 1:
             tt = torch.tensor([e2e_s], device="cuda")
