@@ -107,6 +107,8 @@ struct life_phi {
     int n_tiles = 0, n_chunks = 0, nt_pad = 0, d_blocks = 0, d_W = 0;
     int d_kind = 0;       // 1: register-tiled v1 (life_dense.cu), 2: warp-specialized (life_ws.cu)
     int d_tv = 0;         // voxels per tile
+    uint32_t *d_t1 = nullptr;  // ws layout: start of each segment's rank>=1 region
+    int64_t d_npad = 0;        // ws layout: padded coefficient count
     size_t d_smem = 0;
 
     // fixed-point WC accumulator and its scale inputs

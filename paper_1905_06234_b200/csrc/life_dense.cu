@@ -555,6 +555,65 @@ __global__ void k_dense_tptr(const unsigned long long *sk2, int64_t n, int64_t n
     }
 }
 
+// ---- warp-specialized layout: per (tile, chunk) segment a rank-0 region
+// (distinct cells) and a rank>=1 region, each padded to a multiple of 4
+// entries (fiber = kWsSentinel) so producer warps stream 16-byte vectors.
+constexpr uint32_t kWsSentinel = 0xFFFFFFFFu;
+
+__global__ void k_ws_bounds(const unsigned long long *sk2, int64_t n, int64_t ntc, int cell_bits,
+                            uint32_t *s0, uint32_t *s1)
+{
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntc;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k0 = (unsigned long long)t << 32;
+        const unsigned long long k1 = k0 | (1ull << cell_bits);
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (sk2[mid] < k0) lo = mid + 1; else hi = mid;
+        }
+        s0[t] = (uint32_t)lo;
+        hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (sk2[mid] < k1) lo = mid + 1; else hi = mid;
+        }
+        s1[t] = (uint32_t)lo;
+    }
+}
+
+__global__ void k_ws_scatter(const unsigned long long *sk2, const uint32_t *perm, int64_t n,
+                             const uint32_t *f, const double *val, const uint32_t *s0,
+                             const uint32_t *s1, const uint32_t *P, const uint32_t *T1,
+                             int cell_bits, uint32_t *cr_out, uint32_t *f_out, float *val_out)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = sk2[i];
+        const uint32_t tc = (uint32_t)(k >> 32);
+        uint32_t cr = (uint32_t)(k & 0xFFFFFFFFull);
+        const uint32_t rank = cr >> cell_bits;
+        int64_t dest;
+        if (rank == 0) {
+            dest = (int64_t)P[tc] + (i - (int64_t)s0[tc]);
+        } else {
+            const int64_t o = i - (int64_t)s1[tc];
+            dest = (int64_t)T1[tc] + o;
+            // windows of 32 counted from the start of the rank>=1 region
+            const int64_t w0 = (int64_t)s1[tc] + (o / 32) * 32;
+            const int64_t end = s0[tc + 1];
+            const int64_t w1 = (w0 + 32 < end ? w0 + 32 : end) - 1;
+            const uint32_t r0 = (uint32_t)(sk2[w0] & 0xFFFFFFFFull) >> cell_bits;
+            const uint32_t r1 = (uint32_t)(sk2[w1] & 0xFFFFFFFFull) >> cell_bits;
+            if (r0 != r1) cr |= 0x80000000u;
+        }
+        const uint32_t p = perm[i];
+        cr_out[dest] = cr;
+        f_out[dest] = f[p];
+        val_out[dest] = (float)val[p];
+    }
+}
+
 static int gridn(int64_t n)
 {
     int64_t b = (n + 255) / 256;
@@ -579,6 +638,7 @@ static int pad_dirs(int nt)
 }
 
 size_t ws_smem_bytes(int nt_pad);
+int ws_warps();
 
 int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
                 const double *val, const std::vector<double> &hdict, cudaStream_t st)
@@ -646,16 +706,57 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     g_launches.fetch_add(4, std::memory_order_relaxed);
     LIFE_CUDA(cudaFreeAsync(k2, st));
     LIFE_CUDA(cudaFreeAsync(perm1, st));
-    LIFE_TRY(dalloc(phi, &phi->d_cr, n));
-    LIFE_TRY(dalloc(phi, &phi->d_fiber, n));
-    LIFE_TRY(dalloc(phi, &phi->d_val, n));
-    LIFE_TRY(dalloc(phi, &phi->d_tptr, ntc + 1));
-    k_dense_tptr<<<gridn(ntc + 1), 256, 0, st>>>(sk2, n, ntc, phi->d_tptr);
-    LIFE_CHECK_LAUNCH();
-    k_dense_gather<<<gridn(n), 256, 0, st>>>(sk2, perm, n, f, val, phi->d_tptr, cell_bits,
-                                             kind == 2 ? 1 : 0, phi->d_cr, phi->d_fiber,
-                                             phi->d_val);
-    LIFE_CHECK_LAUNCH();
+    if (kind == 2) {
+        uint32_t *s0 = nullptr, *s1 = nullptr, *Pd = nullptr, *T1d = nullptr;
+        LIFE_CUDA(cudaMallocAsync(&s0, (ntc + 1) * 4, st));
+        LIFE_CUDA(cudaMallocAsync(&s1, (ntc + 1) * 4, st));
+        k_ws_bounds<<<gridn(ntc + 1), 256, 0, st>>>(sk2, n, ntc, cell_bits, s0, s1);
+        LIFE_CHECK_LAUNCH();
+        std::vector<uint32_t> h0(ntc + 1), h1(ntc + 1), hP(ntc + 1), hT(ntc + 1);
+        LIFE_CUDA(cudaMemcpyAsync(h0.data(), s0, (ntc + 1) * 4, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaMemcpyAsync(h1.data(), s1, (ntc + 1) * 4, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        int64_t pos = 0;
+        for (int64_t t = 0; t < ntc; ++t) {
+            const int64_t n0 = (int64_t)h1[t] - h0[t], n1 = (int64_t)h0[t + 1] - h1[t];
+            hP[t] = (uint32_t)pos;
+            hT[t] = (uint32_t)(pos + (n0 + 3) / 4 * 4);
+            pos += (n0 + 3) / 4 * 4 + (n1 + 3) / 4 * 4;
+        }
+        hP[ntc] = hT[ntc] = (uint32_t)pos;
+        if (pos >= 0xFFFFFFFFll) return fail(LIFE_ERR_CONFIG_INVALID, "padded layout exceeds u32");
+        const int64_t npad = std::max<int64_t>(pos, 1);
+        LIFE_TRY(dalloc(phi, &phi->d_cr, npad));
+        LIFE_TRY(dalloc(phi, &phi->d_fiber, npad));
+        LIFE_TRY(dalloc(phi, &phi->d_val, npad));
+        LIFE_TRY(dalloc(phi, &phi->d_tptr, ntc + 1));
+        LIFE_TRY(dalloc(phi, &phi->d_t1, ntc + 1));
+        LIFE_CUDA(cudaMemsetAsync(phi->d_cr, 0, npad * 4, st));
+        LIFE_CUDA(cudaMemsetAsync(phi->d_fiber, 0xFF, npad * 4, st));  // kWsSentinel
+        LIFE_CUDA(cudaMemsetAsync(phi->d_val, 0, npad * 4, st));
+        LIFE_CUDA(cudaMemcpyAsync(phi->d_tptr, hP.data(), (ntc + 1) * 4, cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaMemcpyAsync(phi->d_t1, hT.data(), (ntc + 1) * 4, cudaMemcpyHostToDevice, st));
+        k_ws_scatter<<<gridn(n), 256, 0, st>>>(sk2, perm, n, f, val, s0, s1, phi->d_tptr,
+                                               phi->d_t1, cell_bits, phi->d_cr, phi->d_fiber,
+                                               phi->d_val);
+        LIFE_CHECK_LAUNCH();
+        phi->d_npad = pos;
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        LIFE_CUDA(cudaFreeAsync(s0, st));
+        LIFE_CUDA(cudaFreeAsync(s1, st));
+        (void)Pd;
+        (void)T1d;
+    } else {
+        LIFE_TRY(dalloc(phi, &phi->d_cr, n));
+        LIFE_TRY(dalloc(phi, &phi->d_fiber, n));
+        LIFE_TRY(dalloc(phi, &phi->d_val, n));
+        LIFE_TRY(dalloc(phi, &phi->d_tptr, ntc + 1));
+        k_dense_tptr<<<gridn(ntc + 1), 256, 0, st>>>(sk2, n, ntc, phi->d_tptr);
+        LIFE_CHECK_LAUNCH();
+        k_dense_gather<<<gridn(n), 256, 0, st>>>(sk2, perm, n, f, val, phi->d_tptr, cell_bits, 0,
+                                                 phi->d_cr, phi->d_fiber, phi->d_val);
+        LIFE_CHECK_LAUNCH();
+    }
     LIFE_CUDA(cudaFreeAsync(sk2, st));
     LIFE_CUDA(cudaFreeAsync(perm, st));
     LIFE_CUDA(cudaFreeAsync(mr, st));
@@ -670,7 +771,7 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     if (kind == 2) {
         phi->d_smem = ws_smem_bytes(nt_pad);
         phi->d_blocks = phi->sms;
-        phi->d_W = phi->d_blocks * 12;
+        phi->d_W = phi->d_blocks * ws_warps();
     } else {
         phi->d_smem = ((size_t)2 * kCA * nt_pad + (size_t)kDenseWarps * kCells) * sizeof(float);
         // residency: 2 CTAs per SM when shared memory allows

@@ -28,21 +28,48 @@ namespace life {
 
 constexpr int kWsCons = 8;
 constexpr int kWsProd = 4;
+constexpr int kTPP = kWsCons / kWsProd;   // consumer tiles per producer warp
 constexpr int kWsWarps = kWsCons + kWsProd;
 constexpr int kWsThreads = kWsWarps * 32;
 constexpr int kWsTV = 32;                  // voxels per consumer tile
 constexpr int kWsCA = 64;                  // atoms per chunk
 constexpr int kWsCells = kWsTV * kWsCA;    // 2048
 constexpr int kWsCellBits = 11;
+// optional register split between the roles (setmaxnreg, warpgroup-aligned).
+// 8 producer warps at 88 registers measured slower than 4 at 168 (C2: DSC
+// 1.93 vs 1.72 ms), so the split is off by default.
+constexpr bool kSplitRegs = false;
+constexpr int kRegCons = 168;
+constexpr int kRegProd = 88;
+static_assert(kWsCons % 4 == 0 && kWsProd % 4 == 0, "roles must be whole warpgroups");
+static_assert(!kSplitRegs || kWsCons * kRegCons + kWsProd * kRegProd <= 2048, "register file");
 
 struct WsArgs {
     const uint32_t *cr;
     const uint32_t *fiber;
     const float *val;
-    const uint32_t *tptr;
+    const uint32_t *tptr;   // padded segment starts, [n_tiles*nch + 1]
+    const uint32_t *t1;     // start of each segment's rank>=1 region
     const float *D;
     int nv, nt, nt_pad, nch, n_tiles, na;
 };
+constexpr uint32_t kSent = 0xFFFFFFFFu;  // padding entry (fiber field)
+// Diagnostic isolation, compiled in only with -DLIFE_WS_DIAG (tools/ws_isolate.py):
+// c_ws_isolate 1 = producers only, 2 = consumers only (results are garbage);
+// c_ws_flags 1 = no L2 prefetch, 2 = __ldg streams, 4 = no gather.
+#ifdef LIFE_WS_DIAG
+__constant__ int c_ws_isolate = 0;
+__constant__ int c_ws_flags = 0;
+#else
+constexpr int c_ws_isolate = 0;
+constexpr int c_ws_flags = 0;
+#endif
+
+template <typename T>
+__device__ __forceinline__ T ld_s(const T *p)
+{
+    return (c_ws_flags & 2) ? __ldg(p) : ld_stream(p);
+}
 
 __device__ __forceinline__ unsigned long long wpk(float a, float b)
 {
@@ -147,39 +174,27 @@ __device__ __forceinline__ bool ws_last_block(unsigned *counter)
 }
 
 // ---- producer: coefficient tile build (DSC) ---------------------------------
-// A producer warp builds two consumer tiles per step.  Their segments are
-// walked as one sequence of groups (4 rounds x 32 coefficients); a 4-deep
-// software pipeline keeps stream loads three groups ahead and w-gathers one
-// group ahead of the group being applied, and the next step's segments are
-// prefetched into L2 (cp.async.bulk.prefetch) a whole step in advance.
-struct BGroup {
-    uint32_t cr[4], f[4];
-    float v[4], wv[4];
-    bool ok[4];
-    int t;
+// Segment of one (voxel tile, atom chunk): [p0, q0) holds each cell's first
+// coefficient (rank 0, distinct cells) and [q0, p1) the repeats (rank >= 1);
+// both regions are padded to 4-entry multiples, so the rank-0 region (~75%
+// of all coefficients at C2) streams as 16-byte vectors, 4 coefficients per
+// lane, with one plain STS per coefficient.  Repeats are added afterwards in
+// rank order (windows straddling two ranks, flagged at build time, are
+// applied rank by rank).  The next step's segments are prefetched into L2.
+struct Seg1 {
+    uint32_t p0, q0, p1;
 };
 
-struct Segs {
-    uint32_t p0[2], p1[2];
-    int ng0, ng;
-};
-
-__device__ __forceinline__ void seg_init(Segs &S, const WsArgs &A, int ct, int c, int p)
+__device__ __forceinline__ Seg1 seg_of(const WsArgs &A, int wt, int c)
 {
-    S.ng = 0;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int wt = ct * kWsCons + p * 2 + q;
-        if (wt < A.n_tiles) {
-            const uint32_t *tp = A.tptr + (size_t)wt * A.nch + c;
-            S.p0[q] = tp[0];
-            S.p1[q] = tp[1];
-        } else {
-            S.p0[q] = S.p1[q] = 0;
-        }
+    Seg1 S{0u, 0u, 0u};
+    if (wt < A.n_tiles) {
+        const size_t tc = (size_t)wt * A.nch + c;
+        S.p0 = A.tptr[tc];
+        S.q0 = A.t1[tc];
+        S.p1 = A.tptr[tc + 1];
     }
-    S.ng0 = (int)((S.p1[0] - S.p0[0] + 127) / 128);
-    S.ng = S.ng0 + (int)((S.p1[1] - S.p0[1] + 127) / 128);
+    return S;
 }
 
 __device__ __forceinline__ void prefetch_l2(const void *ptr, uint32_t bytes)
@@ -188,72 +203,108 @@ __device__ __forceinline__ void prefetch_l2(const void *ptr, uint32_t bytes)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void prefetch_range(const WsArgs &A, uint32_t p0, uint32_t p1)
+__device__ __forceinline__ void prefetch_seg(const WsArgs &A, const Seg1 &S)
 {
-    if (p1 <= p0) return;
-    const uint32_t a0 = p0 & ~3u, a1 = (p1 + 3u) & ~3u;  // 16-byte aligned u32/f32 ranges
-    const uint32_t bytes = (a1 - a0) * 4u;
-    prefetch_l2(A.cr + a0, bytes);
-    prefetch_l2(A.fiber + a0, bytes);
-    prefetch_l2(A.val + a0, bytes);
+    if (S.p1 <= S.p0 || (c_ws_flags & 1)) return;
+    const uint32_t bytes = (S.p1 - S.p0) * 4u;  // padded segments are 16-byte aligned
+    prefetch_l2(A.cr + S.p0, bytes);
+    prefetch_l2(A.fiber + S.p0, bytes);
+    prefetch_l2(A.val + S.p0, bytes);
 }
 
-__device__ __forceinline__ void bg_load(BGroup &G, const WsArgs &A, const Segs &S, int g, int lane)
+// 4 consecutive coefficients per lane (a 128-coefficient block per warp)
+struct VBlk {
+    uint4 cr, f;
+    float4 v;
+    float w[4];
+    bool ok;
+};
+
+__device__ __forceinline__ void vb_load(VBlk &B, const WsArgs &A, uint32_t base, uint32_t end,
+                                        int lane)
 {
-    int t = 0;
-    uint32_t base = 0, p1 = 0;
-    if (g < S.ng0) {
-        base = S.p0[0] + (uint32_t)g * 128u;
-        p1 = S.p1[0];
-    } else if (g < S.ng) {
-        t = 1;
-        base = S.p0[1] + (uint32_t)(g - S.ng0) * 128u;
-        p1 = S.p1[1];
+    const uint32_t k = base + 4u * (uint32_t)lane;
+    B.ok = k < end;
+    if (B.ok) {
+        B.cr = ld_s(reinterpret_cast<const uint4 *>(A.cr + k));
+        B.f = ld_s(reinterpret_cast<const uint4 *>(A.fiber + k));
+        B.v = ld_s(reinterpret_cast<const float4 *>(A.val + k));
+    } else {
+        B.cr = make_uint4(0u, 0u, 0u, 0u);
+        B.f = make_uint4(kSent, kSent, kSent, kSent);
+        B.v = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    G.t = t;
+}
+
+__device__ __forceinline__ void vb_gather(VBlk &B, const float *__restrict__ w)
+{
+    const uint32_t f[4] = {B.f.x, B.f.y, B.f.z, B.f.w};
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const uint32_t k = base + 32 * r + lane;
-        G.ok[r] = k < p1;
-        G.cr[r] = G.ok[r] ? ld_stream(A.cr + k) : 0u;
-        G.f[r] = G.ok[r] ? ld_stream(A.fiber + k) : 0u;
-        G.v[r] = G.ok[r] ? ld_stream(A.val + k) : 0.f;
+    for (int e = 0; e < 4; ++e)
+        B.w[e] = f[e] != kSent ? ((c_ws_flags & 4) ? 1.f : __ldg(w + f[e])) : 0.f;
+}
+
+__device__ __forceinline__ void vb_assign(const VBlk &B, float *C, unsigned &zeros)
+{
+    const uint32_t f[4] = {B.f.x, B.f.y, B.f.z, B.f.w};
+    const uint32_t cr[4] = {B.cr.x, B.cr.y, B.cr.z, B.cr.w};
+    const float v[4] = {B.v.x, B.v.y, B.v.z, B.v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (f[e] != kSent) {
+            const float s = __fmul_rn(B.w[e], v[e]);
+            zeros += (s == 0.f) ? 1u : 0u;
+            C[cr[e] & (kWsCells - 1)] = s;
+        }
     }
 }
 
-__device__ __forceinline__ void bg_gather(BGroup &G, const float *__restrict__ w)
+// Rounds of the rank>=1 region: their loads are issued at the start of the
+// tile build (hidden behind the rank-0 stream), gathered and applied after.
+constexpr int kSlowRounds = 8;
+struct SlowRounds {
+    uint32_t cr[kSlowRounds], f[kSlowRounds];
+    float v[kSlowRounds], w[kSlowRounds];
+};
+
+__device__ __forceinline__ void sr_load(SlowRounds &R, const WsArgs &A, uint32_t base,
+                                        uint32_t p1, int lane)
 {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) G.wv[r] = G.ok[r] ? __ldg(w + G.f[r]) : 0.f;
+    for (int r = 0; r < kSlowRounds; ++r) {
+        const uint32_t k = base + 32u * r + (uint32_t)lane;
+        const bool in = k < p1;
+        R.cr[r] = in ? ld_s(A.cr + k) : 0u;
+        R.f[r] = in ? ld_s(A.fiber + k) : kSent;
+        R.v[r] = in ? ld_s(A.val + k) : 0.f;
+    }
 }
 
-// Apply one group to the tile.  Windows whose entries share one rank touch
-// distinct cells (one STS or LDS+FADD+STS per lane); a window straddling
-// rank levels ("mixed", precomputed bit 31 of cr) is applied rank by rank.
-// Zero products are counted per lane (summed once per kernel).
-__device__ __forceinline__ void bg_apply(const BGroup &G, float *C0, float *C1, unsigned &zeros)
+__device__ __forceinline__ void sr_gather(SlowRounds &R, const float *__restrict__ w)
 {
-    float *C = G.t ? C1 : C0;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const bool ok = G.ok[r];
-        const float s = __fmul_rn(G.wv[r], G.v[r]);
+    for (int r = 0; r < kSlowRounds; ++r) R.w[r] = R.f[r] != kSent ? __ldg(w + R.f[r]) : 0.f;
+}
+
+// apply rounds in order; a round whose 32 entries straddle two rank levels
+// (flag bit 31, set at build time) is applied rank by rank
+__device__ __forceinline__ void sr_apply(const SlowRounds &R, float *C, unsigned &zeros)
+{
+#pragma unroll
+    for (int r = 0; r < kSlowRounds; ++r) {
+        const bool ok = R.f[r] != kSent;
+        if (!__any_sync(0xffffffffu, ok)) break;
+        const float s = __fmul_rn(R.w[r], R.v[r]);
         zeros += (ok && s == 0.f) ? 1u : 0u;
-        const uint32_t cr = G.cr[r];
+        const uint32_t cr = R.cr[r];
         const uint32_t rank = (cr >> kWsCellBits) & 0xFFFFFu, cell = cr & (kWsCells - 1);
         if (!__any_sync(0xffffffffu, ok && (cr >> 31))) {
-            if (ok) {
-                if (rank == 0) C[cell] = s;
-                else C[cell] += s;
-            }
+            if (ok) C[cell] += s;
         } else {
             const uint32_t rmin = __reduce_min_sync(0xffffffffu, ok ? rank : 0xFFFFFFFFu);
             const uint32_t rmax = __reduce_max_sync(0xffffffffu, ok ? rank : 0u);
             for (uint32_t rr = rmin; rr <= rmax; ++rr) {
-                if (ok && rank == rr) {
-                    if (rr == 0) C[cell] = s;
-                    else C[cell] += s;
-                }
+                if (ok && rank == rr) C[cell] += s;
                 __syncwarp();
             }
         }
@@ -261,32 +312,35 @@ __device__ __forceinline__ void bg_apply(const BGroup &G, float *C0, float *C1, 
     }
 }
 
-__device__ __forceinline__ unsigned build_step(float *C0, float *C1, const WsArgs &A,
-                                               const float *__restrict__ w, const Segs &S,
+__device__ __forceinline__ unsigned build_tile(float *C, const WsArgs &A,
+                                               const float *__restrict__ w, const Seg1 &S,
                                                int lane)
 {
-    float4 *Z0 = reinterpret_cast<float4 *>(C0);
-    float4 *Z1 = reinterpret_cast<float4 *>(C1);
+    SlowRounds R;
+    sr_load(R, A, S.q0, S.p1, lane);  // in flight during the rank-0 stream
+    float4 *Z = reinterpret_cast<float4 *>(C);
 #pragma unroll 4
-    for (int i = 0; i < kWsCells / 4 / 32; ++i) {
-        Z0[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        Z1[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int i = 0; i < kWsCells / 4 / 32; ++i) Z[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
     unsigned zeros = 0;
-    if (S.ng == 0) return 0;
-    BGroup G0, G1, G2, G3;
-    bg_load(G0, A, S, 0, lane);
-    bg_load(G1, A, S, 1, lane);
-    bg_load(G2, A, S, 2, lane);
-    bg_gather(G0, w);
-    for (int g = 0; g < S.ng; ++g) {
-        bg_load(G3, A, S, g + 3, lane);
-        bg_gather(G1, w);
-        bg_apply(G0, C0, C1, zeros);
-        G0 = G1;
-        G1 = G2;
-        G2 = G3;
+    // rank-0 region in batches of kFastBlocks x 128 coefficients: all loads of
+    // a batch in flight, then all w-gathers, then the stores (two latency
+    // epochs per batch; at C2 a tile's rank-0 region is ~6 blocks)
+    constexpr int kFastBlocks = 6;
+    for (uint32_t b0 = S.p0; b0 < S.q0; b0 += 128u * kFastBlocks) {
+        VBlk B[kFastBlocks];
+#pragma unroll
+        for (int j = 0; j < kFastBlocks; ++j) vb_load(B[j], A, b0 + 128u * j, S.q0, lane);
+#pragma unroll
+        for (int j = 0; j < kFastBlocks; ++j) vb_gather(B[j], w);
+#pragma unroll
+        for (int j = 0; j < kFastBlocks; ++j) vb_assign(B[j], C, zeros);
+    }
+    __syncwarp();
+    for (uint32_t base = S.q0; base < S.p1; base += 32u * kSlowRounds) {
+        if (base != S.q0) sr_load(R, A, base, S.p1, lane);
+        sr_gather(R, w);
+        sr_apply(R, C, zeros);
     }
     return zeros;
 }
@@ -333,6 +387,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 
     if (warp < kWsCons) {
         // ===== consumers: register-tiled FFMA2 =====
+        if constexpr (kSplitRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegCons));
         const int vg = lane >> 3, dg = lane & 7;
         const bool accumulate = flags & LIFE_ACCUMULATE;
         const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
@@ -351,7 +406,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             for (int c = 0; c < A.nch; ++c, ++k) {
                 const int s = k & 1;
                 bar_wait(&full[s], (k >> 1) & 1);
-                if (tile_ok) {
+                if (tile_ok && c_ws_isolate != 1) {
                     const float *C = Cbuf + (s * kWsCons + warp) * kWsCells + vg * 8;
                     const float *D = Dbuf + s * chunk_floats + dg * DPL;
                     const int na_c = min(kWsCA, A.na - c * kWsCA);
@@ -406,28 +461,29 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
     } else {
         // ===== producers: TMA for D, coefficient tiles =====
+        if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProd));
         const int p = warp - kWsCons;
         int k = 0;
         for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
             for (int c = 0; c < A.nch; ++c, ++k) {
                 const int s = k & 1;
-                Segs S;
-                seg_init(S, A, ct, c, p);
                 {   // warm L2 with the next step's coefficient segments
                     int nct = ct, nc = c;
                     next_step(nct, nc, A.nch);
-                    if (nct < n_ct && lane < 2) {
-                        Segs Sn;
-                        seg_init(Sn, A, nct, nc, p);
-                        prefetch_range(A, lane ? Sn.p0[1] : Sn.p0[0], lane ? Sn.p1[1] : Sn.p1[0]);
-                    }
+                    if (nct < n_ct && lane < kTPP)
+                        prefetch_seg(A, seg_of(A, nct * kWsCons + p * kTPP + lane, nc));
                 }
                 if (k >= 2) bar_wait(&empty[s], ((k - 2) >> 1) & 1);
                 if (p == 0 && lane == 0)
                     tma_chunk(Dbuf + s * chunk_floats, A.D + (size_t)c * chunk_floats,
                               chunk_bytes, &full[s]);
-                skipped += build_step(Cbuf + (s * kWsCons + 2 * p) * kWsCells,
-                                      Cbuf + (s * kWsCons + 2 * p + 1) * kWsCells, A, w, S, lane);
+#pragma unroll 1
+                for (int q = 0; q < kTPP; ++q) {
+                    const int tw = kTPP * p + q;
+                    if (c_ws_isolate != 2)
+                        skipped += build_tile(Cbuf + (s * kWsCons + tw) * kWsCells, A, w,
+                                              seg_of(A, ct * kWsCons + tw, c), lane);
+                }
                 __syncwarp();
                 if (lane == 0) bar_arrive(&full[s]);
             }
@@ -496,6 +552,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     __syncthreads();
     if (warp < kWsCons) {
         // ===== consumers: Z = Y . D^T =====
+        if constexpr (kSplitRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegCons));
         const int vg = lane >> 3, dg = lane & 7;
         const int b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
         int k = 0;
@@ -583,6 +640,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
     } else {
         // ===== producers: D chunks via TMA; scatter value * Z[cell] =====
+        if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProd));
         const int p = warp - kWsCons;
         const int ex = fix_exponent(fx, A.nt);
         const double scale = ldexp(1.0, ex);
@@ -604,37 +662,37 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                               chunk_bytes, &dfull[s1]);
                 }
                 __syncwarp();
-                Segs S;
-                seg_init(S, A, ct, c, p);
                 {
                     int nct = ct, nc = c;
                     next_step(nct, nc, A.nch);
-                    if (nct < n_ct && lane < 2) {
-                        Segs Sn;
-                        seg_init(Sn, A, nct, nc, p);
-                        prefetch_range(A, lane ? Sn.p0[1] : Sn.p0[0], lane ? Sn.p1[1] : Sn.p1[0]);
-                    }
+                    if (nct < n_ct && lane < kTPP)
+                        prefetch_seg(A, seg_of(A, nct * kWsCons + p * kTPP + lane, nc));
                 }
-                BGroup G0, G1, G2;
-                bg_load(G0, A, S, 0, lane);
-                bg_load(G1, A, S, 1, lane);
+                const Seg1 S0 = seg_of(A, ct * kWsCons + kTPP * p, c);
+                VBlk B0, B1;
+                vb_load(B0, A, S0.p0, S0.p1, lane);
                 bar_wait(&zfull[s], (k >> 1) & 1);
-                const float *Z0 = Zbuf + (s * kWsCons + 2 * p) * kWsCells;
-                const float *Z1 = Z0 + kWsCells;
-                for (int g = 0; g < S.ng; ++g) {
-                    bg_load(G2, A, S, g + 2, lane);
-                    const float *Z = G0.t ? Z1 : Z0;
+#pragma unroll 1
+                for (int q = 0; q < kTPP; ++q) {
+                    const Seg1 S = q ? seg_of(A, ct * kWsCons + kTPP * p + q, c) : S0;
+                    const float *Z = Zbuf + (s * kWsCons + kTPP * p + q) * kWsCells;
+                    if (q) vb_load(B0, A, S.p0, S.p1, lane);
+                    for (uint32_t base = S.p0; base < S.p1; base += 128u) {
+                        vb_load(B1, A, base + 128u, S.p1, lane);
+                        const uint32_t f[4] = {B0.f.x, B0.f.y, B0.f.z, B0.f.w};
+                        const uint32_t cr[4] = {B0.cr.x, B0.cr.y, B0.cr.z, B0.cr.w};
+                        const float v[4] = {B0.v.x, B0.v.y, B0.v.z, B0.v.w};
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        if (G0.ok[r]) {
-                            const float z = Z[G0.cr[r] & (kWsCells - 1)] * G0.v[r];
-                            const long long qv = f32_scale ? __float2ll_rn(z * scalef)
-                                                           : __double2ll_rn((double)z * scale);
-                            atomicAdd(fx.wfix + G0.f[r], static_cast<unsigned long long>(qv));
+                        for (int e = 0; e < 4; ++e) {
+                            if (f[e] != kSent) {
+                                const float z = Z[cr[e] & (kWsCells - 1)] * v[e];
+                                const long long qv = f32_scale ? __float2ll_rn(z * scalef)
+                                                               : __double2ll_rn((double)z * scale);
+                                atomicAdd(fx.wfix + f[e], static_cast<unsigned long long>(qv));
+                            }
                         }
+                        B0 = B1;
                     }
-                    G0 = G1;
-                    G1 = G2;
                 }
                 __syncwarp();
                 if (lane == 0) bar_arrive(&zempty[s]);
@@ -651,7 +709,7 @@ static int ws_dsc_t(life_phi *phi, const float *w, float *y, const float *b, uin
                     const DscOut &o, const CallHooks &h, cudaStream_t st)
 {
     LIFE_TRY(ensure_smem(k_dsc_ws<DPL>, phi->d_smem));
-    WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_D,
+    WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_t1, phi->d_D,
              phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
     k_dsc_ws<DPL><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, w, y, b, flags, phi->red,
                                                                    o, h);
@@ -664,7 +722,7 @@ static int ws_wc_t(life_phi *phi, const FixParams &fx, const float *y, const Cal
                    cudaStream_t st)
 {
     LIFE_TRY(ensure_smem(k_wc_ws<DPL>, phi->d_smem));
-    WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_D,
+    WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_t1, phi->d_D,
              phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
     k_wc_ws<DPL><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, y, fx, h);
     LIFE_CHECK_LAUNCH();
@@ -700,6 +758,21 @@ int launch_wc_ws(life_phi *phi, const FixParams &fx, const float *y, const CallH
 }
 
 int prepare_ws(life_phi *phi) { LIFE_WS_DISPATCH(ws_prepare_t, phi); }
+
+}  // namespace life
+
+#ifdef LIFE_WS_DIAG
+extern "C" LIFE_API int life_debug_ws_isolate(int mode)
+{
+    const int iso = mode & 0xFF, fl = mode >> 8;
+    if (cudaMemcpyToSymbol(life::c_ws_isolate, &iso, sizeof(int)) != cudaSuccess) return 20;
+    return cudaMemcpyToSymbol(life::c_ws_flags, &fl, sizeof(int)) == cudaSuccess ? 0 : 20;
+}
+#endif
+
+namespace life {
+
+int ws_warps() { return kWsWarps; }
 
 size_t ws_smem_bytes(int nt_pad)
 {
