@@ -11,7 +11,8 @@ import os
 from .errors import DeviceError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblife_b200.so")
+# LIFE_B200_LIB overrides the path (diagnostic builds, tools/ only)
+LIB_PATH = os.environ.get("LIFE_B200_LIB") or os.path.join(_HERE, "liblife_b200.so")
 
 c_i32, c_i64, c_u32, c_u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
 c_void_p, c_double = ctypes.c_void_p, ctypes.c_double

@@ -109,6 +109,11 @@ struct life_phi {
     int d_tv = 0;         // voxels per tile
     uint32_t *d_t1 = nullptr;  // ws layout: start of each segment's rank>=1 region
     int64_t d_npad = 0;        // ws layout: padded coefficient count
+    int d_ca = 0;              // atoms per chunk (ws layout: 32, v1: 64)
+    int64_t d_maxpw = 0;       // ws layout: largest per-producer-warp step range
+    bool d_staged = false;     // ws layout: producer ranges staged by TMA bulk copies
+    uint32_t *d_vslot = nullptr;  // ws layout: tile slot of each voxel (load-balanced order)
+    int *d_slotv = nullptr;       // ws layout: voxel of each tile slot, -1 = padding
     size_t d_smem = 0;
 
     // fixed-point WC accumulator and its scale inputs

@@ -28,6 +28,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "life_common.cuh"
@@ -491,6 +493,31 @@ __global__ void k_dense_key1(const uint32_t *a, const uint32_t *v, int64_t n, in
     }
 }
 
+// warp-specialized layout: segments ordered by (CTA tile round ct, atom
+// chunk, warp tile q in the round), so one step (ct, chunk) of a CTA -- and
+// the two tiles a producer warp owns in it -- is a contiguous range
+__global__ void k_voxel_hist(const uint32_t *v, int64_t n, unsigned *cnt)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(cnt + v[i], 1u);
+}
+
+__global__ void k_ws_key1(const uint32_t *a, const uint32_t *v, const uint32_t *vslot, int64_t n,
+                          int nch, int ca, unsigned long long *key, uint32_t *iota)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t at = a[i], vx = vslot[v[i]];
+        const uint32_t tile = vx / 32u;
+        const unsigned long long tc =
+            ((unsigned long long)(tile / 8u) * nch + at / ca) * 8u + tile % 8u;
+        const uint32_t cell = (at % ca) * 32u + vx % 32u;
+        key[i] = (tc << 10) | cell;
+        iota[i] = (uint32_t)i;
+    }
+}
+
 // rank = position within the run of equal keys;
 // key2 = tc<<32 | rank<<cell_bits | cell
 __global__ void k_dense_key2(const unsigned long long *sk, int64_t n, int cell_bits,
@@ -637,8 +664,10 @@ static int pad_dirs(int nt)
     return p;
 }
 
-size_t ws_smem_bytes(int nt_pad);
+size_t ws_smem_bytes(int nt_pad, bool staged);
 int ws_warps();
+int ws_chunk_atoms();
+int ws_ring_entries();
 
 int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
                 const double *val, const std::vector<double> &hdict, cudaStream_t st)
@@ -646,22 +675,26 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     const int64_t n = phi->nc;
     // warp-specialized kernels (life_ws.cu) for n_dirs <= 96, the v1
     // register-tiled kernels above for n_dirs <= 160, else sparse only
-    int kind = 2, tv = 32, cell_bits = 11;
+    int kind = 2, tv = 32, cell_bits = 10, ca = ws_chunk_atoms();
     int nt_pad = (phi->nt + 31) / 32 * 32;
     if (nt_pad > 96) {
         kind = 1;
         tv = kTV;
         cell_bits = 10;
+        ca = kCA;
         nt_pad = pad_dirs(phi->nt);
         if (!dense_supported_dpl(nt_pad)) return LIFE_OK;
     }
     if (n == 0) return LIFE_OK;
     phi->d_kind = kind;
     phi->d_tv = tv;
+    phi->d_ca = ca;
     phi->nt_pad = nt_pad;
     phi->n_tiles = (phi->nv + tv - 1) / tv;
-    phi->n_chunks = (phi->na + kCA - 1) / kCA;
-    const int64_t ntc = (int64_t)phi->n_tiles * phi->n_chunks;
+    phi->n_chunks = (phi->na + ca - 1) / ca;
+    // ws: whole CTA rounds of 8 tiles (segments of missing tiles stay empty)
+    const int64_t n_ct = ((int64_t)phi->n_tiles + 7) / 8;
+    const int64_t ntc = kind == 2 ? n_ct * phi->n_chunks * 8 : (int64_t)phi->n_tiles * phi->n_chunks;
     if (ntc >= (1ll << 31)) return LIFE_OK;
     unsigned long long *k1 = nullptr, *sk1 = nullptr, *k2 = nullptr, *sk2 = nullptr;
     uint32_t *iota = nullptr, *perm1 = nullptr, *perm = nullptr;
@@ -672,7 +705,45 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     LIFE_CUDA(cudaMallocAsync(&perm1, n * 4, st));
     LIFE_CUDA(cudaMallocAsync(&mr, 4, st));
     LIFE_CUDA(cudaMemsetAsync(mr, 0, 4, st));
-    k_dense_key1<<<gridn(n), 256, 0, st>>>(a, v, n, phi->n_chunks, tv, cell_bits, k1, iota);
+    if (kind == 2) {
+        // Load balance: voxels sorted by coefficient count are dealt to the
+        // tiles in snake order (round r gives tile i, or T-1-i on odd rounds,
+        // its r-th slot), so every 32-voxel tile -- and every CTA's step --
+        // carries about the same number of coefficients.  y rows are read and
+        // written through slot -> voxel; the arithmetic per voxel is unchanged.
+        unsigned *cnt = nullptr;
+        LIFE_CUDA(cudaMallocAsync(&cnt, (size_t)phi->nv * 4, st));
+        LIFE_CUDA(cudaMemsetAsync(cnt, 0, (size_t)phi->nv * 4, st));
+        k_voxel_hist<<<gridn(n), 256, 0, st>>>(v, n, cnt);
+        LIFE_CHECK_LAUNCH();
+        std::vector<unsigned> hc(phi->nv);
+        LIFE_CUDA(cudaMemcpyAsync(hc.data(), cnt, (size_t)phi->nv * 4, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        LIFE_CUDA(cudaFreeAsync(cnt, st));
+        std::vector<uint32_t> order(phi->nv);
+        for (int i = 0; i < phi->nv; ++i) order[i] = (uint32_t)i;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](uint32_t x, uint32_t y) { return hc[x] > hc[y]; });
+        const int64_t T = phi->n_tiles, nslots = n_ct * 8 * 32;
+        std::vector<uint32_t> vslot(phi->nv);
+        std::vector<int> slotv(nslots, -1);
+        for (int64_t i = 0; i < phi->nv; ++i) {
+            const int64_t r = i / T, q = i % T, tile = (r & 1) ? T - 1 - q : q;
+            const int64_t slot = tile * 32 + r;
+            vslot[order[i]] = (uint32_t)slot;
+            slotv[slot] = (int)order[i];
+        }
+        LIFE_TRY(dalloc(phi, &phi->d_vslot, (size_t)phi->nv));
+        LIFE_TRY(dalloc(phi, &phi->d_slotv, (size_t)nslots));
+        LIFE_CUDA(cudaMemcpyAsync(phi->d_vslot, vslot.data(), (size_t)phi->nv * 4,
+                                  cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaMemcpyAsync(phi->d_slotv, slotv.data(), (size_t)nslots * 4,
+                                  cudaMemcpyHostToDevice, st));
+        k_ws_key1<<<gridn(n), 256, 0, st>>>(a, v, phi->d_vslot, n, phi->n_chunks, ca, k1, iota);
+        LIFE_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    }
+    else
+        k_dense_key1<<<gridn(n), 256, 0, st>>>(a, v, n, phi->n_chunks, tv, cell_bits, k1, iota);
     LIFE_CHECK_LAUNCH();
     int bits_tc = 1;
     while (bits_tc < 40 && (ntc >> bits_tc) != 0) ++bits_tc;
@@ -725,6 +796,37 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
         }
         hP[ntc] = hT[ntc] = (uint32_t)pos;
         if (pos >= 0xFFFFFFFFll) return fail(LIFE_ERR_CONFIG_INVALID, "padded layout exceeds u32");
+        // staged producers keep two consecutive steps of a warp (its two
+        // tiles of (ct, c) and of the next step) in a ring of
+        // ws_ring_entries(); check the largest such pair for this grid
+        int64_t maxpw = 0, maxpair = 0;
+        {
+            const int64_t nch = phi->n_chunks, grid = phi->sms;
+            auto rng = [&](int64_t ct, int64_t c, int p) {
+                const int64_t t = (ct * nch + c) * 8 + 2 * p;
+                return (int64_t)hP[t + 2] - hP[t];
+            };
+            for (int64_t b = 0; b < std::min<int64_t>(grid, n_ct); ++b) {
+                const int64_t my = (n_ct - 1 - b) / grid + 1, total = my * nch;
+                for (int p = 0; p < 4; ++p) {
+                    int64_t prev = -1;
+                    for (int64_t j = 0; j < total; ++j) {
+                        const int64_t r = rng(b + (j / nch) * grid, j % nch, p);
+                        maxpw = std::max(maxpw, r);
+                        if (prev >= 0) maxpair = std::max(maxpair, prev + r);
+                        prev = r;
+                    }
+                }
+            }
+        }
+        maxpair = std::max(maxpair, maxpw);  // a lone step must fit as well
+        phi->d_maxpw = maxpair;
+        const char *unstaged = getenv("LIFE_WS_UNSTAGED");  // A/B diagnostics
+        phi->d_staged = maxpair <= ws_ring_entries() && !(unstaged && unstaged[0] == '1');
+        if (getenv("LIFE_DEBUG"))
+            fprintf(stderr, "[life] ws layout: ntc=%lld padded=%lld maxpw=%lld maxpair=%lld staged=%d\n",
+                    (long long)ntc, (long long)pos, (long long)maxpw, (long long)maxpair,
+                    (int)phi->d_staged);
         const int64_t npad = std::max<int64_t>(pos, 1);
         LIFE_TRY(dalloc(phi, &phi->d_cr, npad));
         LIFE_TRY(dalloc(phi, &phi->d_fiber, npad));
@@ -760,8 +862,8 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     LIFE_CUDA(cudaFreeAsync(sk2, st));
     LIFE_CUDA(cudaFreeAsync(perm, st));
     LIFE_CUDA(cudaFreeAsync(mr, st));
-    // zero-padded dictionary chunks [n_chunks][64][nt_pad]
-    std::vector<float> hD((size_t)phi->n_chunks * kCA * nt_pad, 0.f);
+    // zero-padded dictionary chunks [n_chunks][ca][nt_pad]
+    std::vector<float> hD((size_t)phi->n_chunks * ca * nt_pad, 0.f);
     for (int at = 0; at < phi->na; ++at)
         for (int t = 0; t < phi->nt; ++t)
             hD[(size_t)at * nt_pad + t] = (float)hdict[(size_t)at * phi->nt + t];
@@ -769,7 +871,7 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     LIFE_CUDA(cudaMemcpyAsync(phi->d_D, hD.data(), hD.size() * 4, cudaMemcpyHostToDevice, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
     if (kind == 2) {
-        phi->d_smem = ws_smem_bytes(nt_pad);
+        phi->d_smem = ws_smem_bytes(nt_pad, phi->d_staged);
         phi->d_blocks = phi->sms;
         phi->d_W = phi->d_blocks * ws_warps();
     } else {

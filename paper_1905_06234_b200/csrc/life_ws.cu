@@ -1,12 +1,12 @@
 // life_ws.cu -- warp-specialized dense DSC / WC (the C2 hot path).
 //
 // Same contraction as life_dense.cu (Y_tile += C_tile . D_chunk for DSC,
-// Z_tile = Y_tile . D_chunk^T then value*Z[cell] -> fascicles for WC), but
-// split between two roles inside one persistent CTA per SM:
+// Z_tile = Y_tile . D_chunk^T then value*Z[cell] -> fascicles for WC), split
+// between two roles inside one persistent CTA per SM:
 //
-//   4 producer warps  stream the sorted coefficient segment of the next
-//                     (voxel tile, atom chunk) step, gather w[f], and build
-//                     the 64 x 32 coefficient tile C in shared memory (DSC);
+//   4 producer warps  build the 32 x 32 coefficient tiles C of the next
+//                     (voxel tile, atom chunk) step in shared memory from the
+//                     sorted coefficient stream and the gathered w[f] (DSC),
 //                     or scatter value * Z[cell] into the fixed-point fascicle
 //                     sums with RED.ADD (WC).  Producer warp 0 also issues
 //                     the TMA bulk copy of the next dictionary chunk.
@@ -14,12 +14,21 @@
 //                     8 voxels x 12 directions (96 fp32 accumulators), so a
 //                     dictionary value feeds 8 FMAs and a coefficient 12.
 //
-// Steps are double buffered (C/Z tiles and dictionary chunks) and handed
-// over with mbarriers (full/empty), so coefficient latency hides behind the
-// consumers' FMA stream.  Each LDS.128 costs four shared-memory wavefronts on
-// sm_100 (measured, tools/ubench); the 8x12 lane tile needs 5 of them per 96
-// FMAs per lane, keeping shared memory (80 wavefronts per 96-cycle FMA step
-// per SM) below the FP32 pipe.
+// Coefficient staging (the "staged" producer): the layout orders segments by
+// (CTA tile round, atom chunk, warp tile, rank, cell), so the two tiles a
+// producer warp owns in one step are ONE contiguous range of the stream.
+// Lane 0 of each producer warp copies the next step's range into its own
+// double-buffered shared-memory slot with three cp.async.bulk copies
+// (index / fascicle / value arrays, mbarrier complete_tx) and prefetches the
+// step after that into L2, so the producers see shared-memory latency for
+// the stream and only the w[f] gathers (DSC) or RED.ADDs (WC) go to L2.
+// Operators whose per-warp step range exceeds a slot fall back to the
+// register-streaming producer (same results, bit for bit).
+//
+// Steps are double buffered (C/Z tiles and dictionary chunks) and handed over
+// with mbarriers (full/empty).  Each LDS.128 costs four shared-memory
+// wavefronts on sm_100 (measured, tools/ubench); the 8x12 lane tile needs 5 of
+// them per 96 FMAs per lane, keeping shared memory below the FP32 pipe.
 #include <algorithm>
 
 #include "life_common.cuh"
@@ -32,31 +41,31 @@ constexpr int kTPP = kWsCons / kWsProd;   // consumer tiles per producer warp
 constexpr int kWsWarps = kWsCons + kWsProd;
 constexpr int kWsThreads = kWsWarps * 32;
 constexpr int kWsTV = 32;                  // voxels per consumer tile
-constexpr int kWsCA = 64;                  // atoms per chunk
-constexpr int kWsCells = kWsTV * kWsCA;    // 2048
-constexpr int kWsCellBits = 11;
-// optional register split between the roles (setmaxnreg, warpgroup-aligned).
-// 8 producer warps at 88 registers measured slower than 4 at 168 (C2: DSC
-// 1.93 vs 1.72 ms), so the split is off by default.
-constexpr bool kSplitRegs = false;
-constexpr int kRegCons = 168;
-constexpr int kRegProd = 88;
-static_assert(kWsCons % 4 == 0 && kWsProd % 4 == 0, "roles must be whole warpgroups");
-static_assert(!kSplitRegs || kWsCons * kRegCons + kWsProd * kRegProd <= 2048, "register file");
+constexpr int kWsCA = 32;                  // atoms per chunk
+constexpr int kWsCells = kWsTV * kWsCA;    // 1024
+constexpr int kWsCellBits = 10;
+constexpr int kWsRing = 2880;              // staged entries per producer warp (ring)
+// load and gather the first rank>=1 batch together with the first rank-0 batch
+#ifndef LIFE_WS_EARLY_SLOW
+#define LIFE_WS_EARLY_SLOW 0
+#endif
+constexpr bool kEarlySlow = LIFE_WS_EARLY_SLOW;
+static_assert(kTPP == 2, "a producer warp owns two adjacent tiles");
 
 struct WsArgs {
     const uint32_t *cr;
     const uint32_t *fiber;
     const float *val;
-    const uint32_t *tptr;   // padded segment starts, [n_tiles*nch + 1]
+    const uint32_t *tptr;   // padded segment starts, [n_ct*nch*8 + 1]
     const uint32_t *t1;     // start of each segment's rank>=1 region
     const float *D;
+    const int *slotv;       // voxel of each tile slot (tile*32 + i), -1 for padding
     int nv, nt, nt_pad, nch, n_tiles, na;
 };
 constexpr uint32_t kSent = 0xFFFFFFFFu;  // padding entry (fiber field)
 // Diagnostic isolation, compiled in only with -DLIFE_WS_DIAG (tools/ws_isolate.py):
 // c_ws_isolate 1 = producers only, 2 = consumers only (results are garbage);
-// c_ws_flags 1 = no L2 prefetch, 2 = __ldg streams, 4 = no gather.
+// c_ws_flags 1 = no L2 prefetch, 4 = no gather.
 #ifdef LIFE_WS_DIAG
 __constant__ int c_ws_isolate = 0;
 __constant__ int c_ws_flags = 0;
@@ -64,12 +73,6 @@ __constant__ int c_ws_flags = 0;
 constexpr int c_ws_isolate = 0;
 constexpr int c_ws_flags = 0;
 #endif
-
-template <typename T>
-__device__ __forceinline__ T ld_s(const T *p)
-{
-    return (c_ws_flags & 2) ? __ldg(p) : ld_stream(p);
-}
 
 __device__ __forceinline__ unsigned long long wpk(float a, float b)
 {
@@ -115,19 +118,21 @@ __device__ __forceinline__ void bar_wait(uint64_t *b, unsigned parity)
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *b)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smaddr(dst)),
+        "l"(src), "r"(bytes), "r"(smaddr(b))
+        : "memory");
+}
 __device__ __forceinline__ void tma_chunk(float *dst, const float *src, unsigned bytes, uint64_t *b)
 {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     bar_arrive_tx(b, bytes);
     const char *s = reinterpret_cast<const char *>(src);
     char *d = reinterpret_cast<char *>(dst);
-    for (unsigned off = 0; off < bytes; off += 32768u) {
-        const unsigned sz = min(32768u, bytes - off);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smaddr(d + off)),
-            "l"(s + off), "r"(sz), "r"(smaddr(b))
-            : "memory");
-    }
+    for (unsigned off = 0; off < bytes; off += 32768u)
+        bulk_g2s(d + off, s + off, min(32768u, bytes - off), b);
 }
 
 template <typename T, typename Op>
@@ -173,43 +178,102 @@ __device__ __forceinline__ bool ws_last_block(unsigned *counter)
     return s_last;
 }
 
-// ---- producer: coefficient tile build (DSC) ---------------------------------
-// Segment of one (voxel tile, atom chunk): [p0, q0) holds each cell's first
-// coefficient (rank 0, distinct cells) and [q0, p1) the repeats (rank >= 1);
-// both regions are padded to 4-entry multiples, so the rank-0 region (~75%
-// of all coefficients at C2) streams as 16-byte vectors, 4 coefficients per
-// lane, with one plain STS per coefficient.  Repeats are added afterwards in
-// rank order (windows straddling two ranks, flagged at build time, are
-// applied rank by rank).  The next step's segments are prefetched into L2.
-struct Seg1 {
-    uint32_t p0, q0, p1;
-};
-
-__device__ __forceinline__ Seg1 seg_of(const WsArgs &A, int wt, int c)
-{
-    Seg1 S{0u, 0u, 0u};
-    if (wt < A.n_tiles) {
-        const size_t tc = (size_t)wt * A.nch + c;
-        S.p0 = A.tptr[tc];
-        S.q0 = A.t1[tc];
-        S.p1 = A.tptr[tc + 1];
-    }
-    return S;
-}
-
 __device__ __forceinline__ void prefetch_l2(const void *ptr, uint32_t bytes)
 {
     if (bytes == 0) return;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void prefetch_seg(const WsArgs &A, const Seg1 &S)
+// ---- a producer warp's step: its two tiles (2p, 2p+1) of one (ct, chunk) --
+// Segment of one (tile, chunk): [p0, q0) holds each cell's first coefficient
+// (rank 0, distinct cells) and [q0, p1) the repeats (rank >= 1); both regions
+// are padded to 4-entry multiples (fiber = kSent), so the rank-0 region
+// streams as 16-byte vectors, 4 coefficients per lane, with one plain STS per
+// coefficient.  Repeats are added afterwards in rank order (32-entry windows
+// straddling two ranks, flagged at build time, are applied rank by rank).
+struct Seg2 {
+    uint32_t a, q0, b, q1, e;  // tile 0 [a, q0) [q0, b); tile 1 [b, q1) [q1, e)
+};
+
+__device__ __forceinline__ size_t tc_of(const WsArgs &A, int ct, int c, int q)
 {
-    if (S.p1 <= S.p0 || (c_ws_flags & 1)) return;
-    const uint32_t bytes = (S.p1 - S.p0) * 4u;  // padded segments are 16-byte aligned
-    prefetch_l2(A.cr + S.p0, bytes);
-    prefetch_l2(A.fiber + S.p0, bytes);
-    prefetch_l2(A.val + S.p0, bytes);
+    return ((size_t)ct * A.nch + c) * kWsCons + q;
+}
+
+__device__ __forceinline__ Seg2 seg2_of(const WsArgs &A, int ct, int c, int p)
+{
+    const size_t tc = tc_of(A, ct, c, kTPP * p);
+    Seg2 S;
+    S.a = __ldg(A.tptr + tc);
+    S.q0 = __ldg(A.t1 + tc);
+    S.b = __ldg(A.tptr + tc + 1);
+    S.q1 = __ldg(A.t1 + tc + 1);
+    S.e = __ldg(A.tptr + tc + 2);
+    return S;
+}
+
+// the CTA's j-th step: (ct, c)
+__device__ __forceinline__ void step_of(int j, int nch, int &ct, int &c)
+{
+    ct = (int)blockIdx.x + (j / nch) * (int)gridDim.x;
+    c = j % nch;
+}
+
+__device__ __forceinline__ void prefetch_range(const WsArgs &A, const Seg2 &S, int lane)
+{
+    if ((c_ws_flags & 1) || S.e <= S.a || lane >= 3) return;
+    const uint32_t bytes = (S.e - S.a) * 4u;  // padded ranges are 16-byte aligned
+    const void *base = lane == 0 ? (const void *)(A.cr + S.a)
+                     : lane == 1 ? (const void *)(A.fiber + S.a)
+                                 : (const void *)(A.val + S.a);
+    prefetch_l2(base, bytes);
+}
+
+// staging ring of one producer warp: three arrays of kWsRing entries; a step's
+// range occupies [off, off + n) modulo kWsRing (offsets and sizes are
+// multiples of 4, so a 16-byte vector never wraps).  The host checks that two
+// consecutive steps of a warp always fit (life_dense.cu: build_dense).
+struct Slot {
+    uint32_t *cr;
+    uint32_t *f;
+    float *v;
+    uint32_t off;
+    __device__ __forceinline__ uint32_t at(uint32_t i) const
+    {
+        const uint32_t x = off + i;
+        return x >= (uint32_t)kWsRing ? x - (uint32_t)kWsRing : x;
+    }
+};
+
+__device__ __forceinline__ uint32_t ring_wrap(uint32_t x)
+{
+    return x >= (uint32_t)kWsRing ? x - (uint32_t)kWsRing : x;
+}
+
+__device__ __forceinline__ Slot slot_at(float *slots, int p, uint32_t off)
+{
+    uint32_t *base = reinterpret_cast<uint32_t *>(slots) + (size_t)p * 3 * kWsRing;
+    return Slot{base, base + kWsRing, reinterpret_cast<float *>(base + 2 * kWsRing), off};
+}
+
+// lane 0: copy the step's range [S.a, S.e) into the ring at D.off
+// (three arrays, split in two where the range wraps)
+__device__ __forceinline__ void stage_issue(const WsArgs &A, const Seg2 &S, const Slot &D,
+                                            uint64_t *bar)
+{
+    const unsigned n = S.e - S.a;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    bar_arrive_tx(bar, 12u * n);
+    if (n == 0) return;
+    const unsigned n1 = min(n, (unsigned)kWsRing - D.off), n2 = n - n1;
+    bulk_g2s(D.cr + D.off, A.cr + S.a, 4u * n1, bar);
+    bulk_g2s(D.f + D.off, A.fiber + S.a, 4u * n1, bar);
+    bulk_g2s(D.v + D.off, A.val + S.a, 4u * n1, bar);
+    if (n2) {
+        bulk_g2s(D.cr, A.cr + S.a + n1, 4u * n2, bar);
+        bulk_g2s(D.f, A.fiber + S.a + n1, 4u * n2, bar);
+        bulk_g2s(D.v, A.val + S.a + n1, 4u * n2, bar);
+    }
 }
 
 // 4 consecutive coefficients per lane (a 128-coefficient block per warp)
@@ -217,22 +281,37 @@ struct VBlk {
     uint4 cr, f;
     float4 v;
     float w[4];
-    bool ok;
 };
 
-__device__ __forceinline__ void vb_load(VBlk &B, const WsArgs &A, uint32_t base, uint32_t end,
-                                        int lane)
+__device__ __forceinline__ void vb_empty(VBlk &B)
 {
-    const uint32_t k = base + 4u * (uint32_t)lane;
-    B.ok = k < end;
-    if (B.ok) {
-        B.cr = ld_s(reinterpret_cast<const uint4 *>(A.cr + k));
-        B.f = ld_s(reinterpret_cast<const uint4 *>(A.fiber + k));
-        B.v = ld_s(reinterpret_cast<const float4 *>(A.val + k));
+    B.cr = make_uint4(0u, 0u, 0u, 0u);
+    B.f = make_uint4(kSent, kSent, kSent, kSent);
+    B.v = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// staged: from the slot (k relative to the slot start)
+__device__ __forceinline__ void vb_lds(VBlk &B, const Slot &S, uint32_t k, bool ok)
+{
+    if (ok) {
+        const uint32_t x = S.at(k);
+        B.cr = *reinterpret_cast<const uint4 *>(S.cr + x);
+        B.f = *reinterpret_cast<const uint4 *>(S.f + x);
+        B.v = *reinterpret_cast<const float4 *>(S.v + x);
     } else {
-        B.cr = make_uint4(0u, 0u, 0u, 0u);
-        B.f = make_uint4(kSent, kSent, kSent, kSent);
-        B.v = make_float4(0.f, 0.f, 0.f, 0.f);
+        vb_empty(B);
+    }
+}
+
+// streamed: straight from global memory (fallback producer)
+__device__ __forceinline__ void vb_ldg(VBlk &B, const WsArgs &A, uint32_t k, bool ok)
+{
+    if (ok) {
+        B.cr = ld_stream(reinterpret_cast<const uint4 *>(A.cr + k));
+        B.f = ld_stream(reinterpret_cast<const uint4 *>(A.fiber + k));
+        B.v = ld_stream(reinterpret_cast<const float4 *>(A.val + k));
+    } else {
+        vb_empty(B);
     }
 }
 
@@ -259,45 +338,34 @@ __device__ __forceinline__ void vb_assign(const VBlk &B, float *C, unsigned &zer
     }
 }
 
-// Rounds of the rank>=1 region: their loads are issued at the start of the
-// tile build (hidden behind the rank-0 stream), gathered and applied after.
+// one 32-entry window of a rank>=1 region per round
 constexpr int kSlowRounds = 8;
 struct SlowRounds {
     uint32_t cr[kSlowRounds], f[kSlowRounds];
     float v[kSlowRounds], w[kSlowRounds];
+    bool t1[kSlowRounds];  // window belongs to tile 1
 };
-
-__device__ __forceinline__ void sr_load(SlowRounds &R, const WsArgs &A, uint32_t base,
-                                        uint32_t p1, int lane)
-{
-#pragma unroll
-    for (int r = 0; r < kSlowRounds; ++r) {
-        const uint32_t k = base + 32u * r + (uint32_t)lane;
-        const bool in = k < p1;
-        R.cr[r] = in ? ld_s(A.cr + k) : 0u;
-        R.f[r] = in ? ld_s(A.fiber + k) : kSent;
-        R.v[r] = in ? ld_s(A.val + k) : 0.f;
-    }
-}
 
 __device__ __forceinline__ void sr_gather(SlowRounds &R, const float *__restrict__ w)
 {
 #pragma unroll
-    for (int r = 0; r < kSlowRounds; ++r) R.w[r] = R.f[r] != kSent ? __ldg(w + R.f[r]) : 0.f;
+    for (int r = 0; r < kSlowRounds; ++r)
+        R.w[r] = R.f[r] != kSent ? ((c_ws_flags & 4) ? 1.f : __ldg(w + R.f[r])) : 0.f;
 }
 
 // apply rounds in order; a round whose 32 entries straddle two rank levels
 // (flag bit 31, set at build time) is applied rank by rank
-__device__ __forceinline__ void sr_apply(const SlowRounds &R, float *C, unsigned &zeros)
+__device__ __forceinline__ void sr_apply(const SlowRounds &R, float *C0, float *C1, unsigned &zeros)
 {
 #pragma unroll
     for (int r = 0; r < kSlowRounds; ++r) {
         const bool ok = R.f[r] != kSent;
-        if (!__any_sync(0xffffffffu, ok)) break;
+        if (!__any_sync(0xffffffffu, ok)) continue;
+        float *C = R.t1[r] ? C1 : C0;
         const float s = __fmul_rn(R.w[r], R.v[r]);
         zeros += (ok && s == 0.f) ? 1u : 0u;
         const uint32_t cr = R.cr[r];
-        const uint32_t rank = (cr >> kWsCellBits) & 0xFFFFFu, cell = cr & (kWsCells - 1);
+        const uint32_t rank = (cr >> kWsCellBits) & 0x1FFFFFu, cell = cr & (kWsCells - 1);
         if (!__any_sync(0xffffffffu, ok && (cr >> 31))) {
             if (ok) C[cell] += s;
         } else {
@@ -312,59 +380,96 @@ __device__ __forceinline__ void sr_apply(const SlowRounds &R, float *C, unsigned
     }
 }
 
-__device__ __forceinline__ unsigned build_tile(float *C, const WsArgs &A,
-                                               const float *__restrict__ w, const Seg1 &S,
-                                               int lane)
+// Build the producer warp's two coefficient tiles of one step.  STAGED reads
+// the range from the warp's shared-memory slot (entry k at slot[k - S.a]),
+// otherwise straight from global memory.
+template <bool STAGED>
+__device__ __forceinline__ unsigned build_pair(float *C0, float *C1, const WsArgs &A,
+                                               const float *__restrict__ w, const Seg2 &S,
+                                               const Slot &sl, int lane)
 {
-    SlowRounds R;
-    sr_load(R, A, S.q0, S.p1, lane);  // in flight during the rank-0 stream
-    float4 *Z = reinterpret_cast<float4 *>(C);
-#pragma unroll 4
-    for (int i = 0; i < kWsCells / 4 / 32; ++i) Z[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 *Z0 = reinterpret_cast<float4 *>(C0);
+    float4 *Z1 = reinterpret_cast<float4 *>(C1);
+#pragma unroll
+    for (int i = 0; i < kWsCells / 4 / 32; ++i) {
+        Z0[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        Z1[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     __syncwarp();
     unsigned zeros = 0;
-    // rank-0 region in batches of kFastBlocks x 128 coefficients: all loads of
-    // a batch in flight, then all w-gathers, then the stores (two latency
-    // epochs per batch; at C2 a tile's rank-0 region is ~6 blocks)
+    // rank-0 regions of both tiles in batches of kFastBlocks x 128 entries
+    // (all loads of a batch, then all w gathers, then the stores); the first
+    // batch of rank>=1 windows is loaded and gathered together with the first
+    // rank-0 batch, so a typical step has one gather round trip
     constexpr int kFastBlocks = 6;
-    for (uint32_t b0 = S.p0; b0 < S.q0; b0 += 128u * kFastBlocks) {
-        VBlk B[kFastBlocks];
+    const int n0 = (int)((S.q0 - S.a + 127u) / 128u), n1 = (int)((S.q1 - S.b + 127u) / 128u);
+    const int m0 = (int)((S.b - S.q0 + 31u) / 32u), m1 = (int)((S.e - S.q1 + 31u) / 32u);
+    SlowRounds R;
+    auto load_slow = [&](int r0) {
 #pragma unroll
-        for (int j = 0; j < kFastBlocks; ++j) vb_load(B[j], A, b0 + 128u * j, S.q0, lane);
+        for (int r = 0; r < kSlowRounds; ++r) {
+            const int g = r0 + r;
+            R.t1[r] = g >= m0;
+            const uint32_t base = R.t1[r] ? S.q1 + 32u * (uint32_t)(g - m0) : S.q0 + 32u * (uint32_t)g;
+            const uint32_t end = R.t1[r] ? S.e : S.b;
+            const uint32_t k = base + (uint32_t)lane;
+            const bool in = g < m0 + m1 && k < end;
+            if (STAGED) {
+                const uint32_t x = sl.at(k - S.a);
+                R.cr[r] = in ? sl.cr[x] : 0u;
+                R.f[r] = in ? sl.f[x] : kSent;
+                R.v[r] = in ? sl.v[x] : 0.f;
+            } else {
+                R.cr[r] = in ? ld_stream(A.cr + k) : 0u;
+                R.f[r] = in ? ld_stream(A.fiber + k) : kSent;
+                R.v[r] = in ? ld_stream(A.val + k) : 0.f;
+            }
+        }
+    };
+    if (kEarlySlow) load_slow(0);
+    for (int g0 = 0; g0 < n0 + n1; g0 += kFastBlocks) {
+        VBlk B[kFastBlocks];
+        bool second[kFastBlocks];
+#pragma unroll
+        for (int j = 0; j < kFastBlocks; ++j) {
+            const int g = g0 + j;
+            second[j] = g >= n0;
+            const uint32_t base = second[j] ? S.b + 128u * (uint32_t)(g - n0) : S.a + 128u * (uint32_t)g;
+            const uint32_t end = second[j] ? S.q1 : S.q0;
+            const uint32_t k = base + 4u * (uint32_t)lane;
+            const bool ok = g < n0 + n1 && k < end;
+            if (STAGED) vb_lds(B[j], sl, k - S.a, ok);
+            else vb_ldg(B[j], A, k, ok);
+        }
 #pragma unroll
         for (int j = 0; j < kFastBlocks; ++j) vb_gather(B[j], w);
+        if (kEarlySlow && g0 == 0) sr_gather(R, w);
 #pragma unroll
-        for (int j = 0; j < kFastBlocks; ++j) vb_assign(B[j], C, zeros);
+        for (int j = 0; j < kFastBlocks; ++j) vb_assign(B[j], second[j] ? C1 : C0, zeros);
     }
     __syncwarp();
-    for (uint32_t base = S.q0; base < S.p1; base += 32u * kSlowRounds) {
-        if (base != S.q0) sr_load(R, A, base, S.p1, lane);
-        sr_gather(R, w);
-        sr_apply(R, C, zeros);
+    // rank>=1 windows, in order, after every rank-0 store
+    for (int r0 = 0; r0 < m0 + m1; r0 += kSlowRounds) {
+        if (r0 || !kEarlySlow || n0 + n1 == 0) {
+            load_slow(r0);
+            sr_gather(R, w);
+        }
+        sr_apply(R, C0, C1, zeros);
     }
     return zeros;
-}
-
-// next (ct, c) step of this CTA, or ct >= n_ct when none
-__device__ __forceinline__ void next_step(int &ct, int &c, int nch)
-{
-    if (++c == nch) {
-        c = 0;
-        ct += gridDim.x;
-    }
 }
 
 // ---------------------------------------------------------------------------
 // DSC
 // ---------------------------------------------------------------------------
-template <int DPL>
+template <int DPL, bool STAGED>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_dsc_ws(const WsArgs A, const float *__restrict__ w, float *__restrict__ y,
              const float *__restrict__ b, const uint32_t flags, const ReduceSlots red,
              const DscOut out, const CallHooks hooks)
 {
     extern __shared__ __align__(128) float sm[];
-    __shared__ __align__(8) uint64_t full[2], empty[2];
+    __shared__ __align__(8) uint64_t full[2], empty[2], slotbar[kWsProd][2];
     if (hooks.done && *hooks.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
@@ -372,11 +477,15 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const unsigned chunk_bytes = (unsigned)chunk_floats * 4u;
     float *Dbuf = sm;
     float *Cbuf = sm + 2 * chunk_floats;
+    float *slots = Cbuf + 2 * kWsCons * kWsCells;
     const int n_ct = (A.n_tiles + kWsCons - 1) / kWsCons;
+    const int my_ct = (int)blockIdx.x < n_ct ? (n_ct - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int total = my_ct * A.nch;
     if (threadIdx.x == 0) {
         for (int s = 0; s < 2; ++s) {
             bar_init(&full[s], kWsProd + 1);
             bar_init(&empty[s], kWsCons);
+            for (int p = 0; p < kWsProd; ++p) bar_init(&slotbar[p][s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -387,7 +496,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 
     if (warp < kWsCons) {
         // ===== consumers: register-tiled FFMA2 =====
-        if constexpr (kSplitRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegCons));
         const int vg = lane >> 3, dg = lane & 7;
         const bool accumulate = flags & LIFE_ACCUMULATE;
         const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
@@ -409,8 +517,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 if (tile_ok && c_ws_isolate != 1) {
                     const float *C = Cbuf + (s * kWsCons + warp) * kWsCells + vg * 8;
                     const float *D = Dbuf + s * chunk_floats + dg * DPL;
-                    const int na_c = min(kWsCA, A.na - c * kWsCA);
-#pragma unroll 32
+#pragma unroll
                     for (int a = 0; a < kWsCA; ++a) {
                         const float4 c0 = *reinterpret_cast<const float4 *>(C + a * kWsTV);
                         const float4 c1 = *reinterpret_cast<const float4 *>(C + a * kWsTV + 4);
@@ -438,8 +545,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 for (int vp = 0; vp < 4; ++vp) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int voxel = wt * kWsTV + vg * 8 + 2 * vp + h;
-                        if (voxel >= A.nv) continue;
+                        const int voxel = __ldg(A.slotv + wt * kWsTV + vg * 8 + 2 * vp + h);
+                        if (voxel < 0) continue;
                         const size_t yo = (size_t)voxel * A.nt;
 #pragma unroll
                         for (int j = 0; j < DPL; ++j) {
@@ -460,33 +567,52 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             }
         }
     } else {
-        // ===== producers: TMA for D, coefficient tiles =====
-        if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProd));
+        // ===== producers: TMA for D and the coefficient ranges, tile build =====
         const int p = warp - kWsCons;
-        int k = 0;
-        for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
-            for (int c = 0; c < A.nch; ++c, ++k) {
-                const int s = k & 1;
-                {   // warm L2 with the next step's coefficient segments
-                    int nct = ct, nc = c;
-                    next_step(nct, nc, A.nch);
-                    if (nct < n_ct && lane < kTPP)
-                        prefetch_seg(A, seg_of(A, nct * kWsCons + p * kTPP + lane, nc));
-                }
-                if (k >= 2) bar_wait(&empty[s], ((k - 2) >> 1) & 1);
-                if (p == 0 && lane == 0)
-                    tma_chunk(Dbuf + s * chunk_floats, A.D + (size_t)c * chunk_floats,
-                              chunk_bytes, &full[s]);
-#pragma unroll 1
-                for (int q = 0; q < kTPP; ++q) {
-                    const int tw = kTPP * p + q;
-                    if (c_ws_isolate != 2)
-                        skipped += build_tile(Cbuf + (s * kWsCons + tw) * kWsCells, A, w,
-                                              seg_of(A, ct * kWsCons + tw, c), lane);
-                }
-                __syncwarp();
-                if (lane == 0) bar_arrive(&full[s]);
+        Seg2 cur{}, nxt{};
+        uint32_t off_cur = 0u, off_nxt = 0u;
+        if (total > 0) {
+            int ct, c;
+            step_of(0, A.nch, ct, c);
+            cur = seg2_of(A, ct, c, p);
+            if (STAGED && lane == 0) stage_issue(A, cur, slot_at(slots, p, 0u), &slotbar[p][0]);
+            off_nxt = ring_wrap(cur.e - cur.a);
+        }
+        if (total > 1) {
+            int ct, c;
+            step_of(1, A.nch, ct, c);
+            nxt = seg2_of(A, ct, c, p);
+            prefetch_range(A, nxt, lane);
+        }
+        for (int k = 0; k < total; ++k) {
+            const int s = k & 1;
+            int ct, c;
+            step_of(k, A.nch, ct, c);
+            Seg2 nn{};
+            if (k + 2 < total) {
+                int ct2, c2;
+                step_of(k + 2, A.nch, ct2, c2);
+                nn = seg2_of(A, ct2, c2, p);
             }
+            // slot s^1 was last read in step k-1, which this warp finished
+            if (STAGED && k + 1 < total && lane == 0)
+                stage_issue(A, nxt, slot_at(slots, p, off_nxt), &slotbar[p][s ^ 1]);
+            if (k >= 2) bar_wait(&empty[s], ((k - 2) >> 1) & 1);
+            if (p == 0 && lane == 0)
+                tma_chunk(Dbuf + s * chunk_floats, A.D + (size_t)c * chunk_floats, chunk_bytes,
+                          &full[s]);
+            if (k + 2 < total) prefetch_range(A, nn, lane);
+            if (STAGED) bar_wait(&slotbar[p][s], (k >> 1) & 1);
+            if (c_ws_isolate != 2)
+                skipped += build_pair<STAGED>(Cbuf + (s * kWsCons + kTPP * p) * kWsCells,
+                                              Cbuf + (s * kWsCons + kTPP * p + 1) * kWsCells, A,
+                                              w, cur, slot_at(slots, p, off_cur), lane);
+            __syncwarp();
+            if (lane == 0) bar_arrive(&full[s]);
+            off_cur = off_nxt;
+            off_nxt = ring_wrap(off_nxt + (nxt.e - nxt.a));
+            cur = nxt;
+            nxt = nn;
         }
     }
 
@@ -524,12 +650,30 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 // ---------------------------------------------------------------------------
 using WsFix = FixParams;
 
-template <int DPL>
+// value * Z[cell] of 4 consecutive entries -> fixed-point fascicle sums
+__device__ __forceinline__ void wc_scatter4(const VBlk &B, const float *Z, const WsFix &fx,
+                                            bool f32_scale, float scalef, double scale)
+{
+    const uint32_t f[4] = {B.f.x, B.f.y, B.f.z, B.f.w};
+    const uint32_t cr[4] = {B.cr.x, B.cr.y, B.cr.z, B.cr.w};
+    const float v[4] = {B.v.x, B.v.y, B.v.z, B.v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (f[e] != kSent) {
+            const float z = Z[cr[e] & (kWsCells - 1)] * v[e];
+            const long long qv = f32_scale ? __float2ll_rn(z * scalef)
+                                           : __double2ll_rn((double)z * scale);
+            atomicAdd(fx.wfix + f[e], static_cast<unsigned long long>(qv));
+        }
+    }
+}
+
+template <int DPL, bool STAGED>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_wc_ws(const WsArgs A, const float *__restrict__ y, const WsFix fx, const CallHooks hooks)
 {
     extern __shared__ __align__(128) float sm[];
-    __shared__ __align__(8) uint64_t dfull[2], dempty[2], zfull[2], zempty[2];
+    __shared__ __align__(8) uint64_t dfull[2], dempty[2], zfull[2], zempty[2], slotbar[kWsProd][2];
     if (hooks.done && *hooks.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
@@ -537,6 +681,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const unsigned chunk_bytes = (unsigned)chunk_floats * 4u;
     float *Dbuf = sm;
     float *Zbuf = sm + 2 * chunk_floats;
+    float *slots = Zbuf + 2 * kWsCons * kWsCells;
     const int n_ct = (A.n_tiles + kWsCons - 1) / kWsCons;
     const int my_ct = (int)blockIdx.x < n_ct ? (n_ct - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int total = my_ct * A.nch;
@@ -546,30 +691,32 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             bar_init(&dempty[s], kWsCons);
             bar_init(&zfull[s], kWsCons);
             bar_init(&zempty[s], kWsProd);
+            for (int p = 0; p < kWsProd; ++p) bar_init(&slotbar[p][s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (warp < kWsCons) {
         // ===== consumers: Z = Y . D^T =====
-        if constexpr (kSplitRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegCons));
+        // Lane (vg, dg) holds 12 directions of 8 voxels; partial dots are
+        // summed over the 8 direction lanes of a voxel group by a butterfly.
+        // Slot u of the lane's 8 voxels holds voxel vg*8 + (u ^ dg), so every
+        // butterfly stage keeps the low half of its values and sends the high
+        // half (no lane-dependent selects), and slot 0 ends up holding
+        // voxel vg*8 + dg, summed over all 96 directions.
         const int vg = lane >> 3, dg = lane & 7;
-        const int b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
         int k = 0;
         for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
             const int wt = ct * kWsCons + warp;
             const bool tile_ok = wt < A.n_tiles;
-            // yv[vp][t] = (y[2vp][t], y[2vp+1][t]) over this lane's DPL
-            // directions: pairs across voxels, so each dictionary value is a
-            // broadcast scalar operand and partial dots come out as voxel pairs
-            unsigned long long yv[4][DPL];
+            unsigned long long yv[4][DPL];  // (slot 2vp, slot 2vp+1) per direction
 #pragma unroll
             for (int vp = 0; vp < 4; ++vp) {
                 float e[2][DPL];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int voxel = wt * kWsTV + vg * 8 + 2 * vp + h;
-                    const bool ok = tile_ok && voxel < A.nv;
+                    const int voxel = tile_ok ? __ldg(A.slotv + wt * kWsTV + vg * 8 + ((2 * vp + h) ^ dg)) : -1;
+                    const bool ok = voxel >= 0;
                     const size_t yo = (size_t)(ok ? voxel : 0) * A.nt;
 #pragma unroll
                     for (int j = 0; j < DPL; ++j) {
@@ -584,12 +731,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 const int s = k & 1;
                 bar_wait(&dfull[s], (k >> 1) & 1);
                 if (k >= 2) bar_wait(&zempty[s], ((k - 2) >> 1) & 1);
-                if (tile_ok) {
-                    float *Z = Zbuf + (s * kWsCons + warp) * kWsCells;
+                if (tile_ok && c_ws_isolate != 1) {
+                    float *Z = Zbuf + (s * kWsCons + warp) * kWsCells + vg * 8 + dg;
                     const float *D = Dbuf + s * chunk_floats + dg * DPL;
-                    const int na_c = min(kWsCA, A.na - c * kWsCA);
-#pragma unroll 1
-                    for (int a0 = 0; a0 < na_c; a0 += 2) {
+#pragma unroll 2
+                    for (int a0 = 0; a0 < kWsCA; a0 += 2) {
                         unsigned long long pp[2][4];
 #pragma unroll
                         for (int aa = 0; aa < 2; ++aa) {
@@ -608,27 +754,18 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                                 }
                             }
                         }
-                        float q[16];
 #pragma unroll
-                        for (int aa = 0; aa < 2; ++aa)
+                        for (int aa = 0; aa < 2; ++aa) {
+                            float q[8];
 #pragma unroll
-                            for (int vp = 0; vp < 4; ++vp)
-                                wupk(pp[aa][vp], q[aa * 8 + 2 * vp], q[aa * 8 + 2 * vp + 1]);
-                        // butterfly over the 8 direction lanes of this voxel group
+                            for (int vp = 0; vp < 4; ++vp) wupk(pp[aa][vp], q[2 * vp], q[2 * vp + 1]);
 #pragma unroll
-                        for (int m = 4, h = 8; m >= 1; m >>= 1, h >>= 1) {
-                            const bool up = (lane & m) != 0;
+                            for (int m = 4; m >= 1; m >>= 1)
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                if (i < h) {
-                                    const float send = up ? q[i] : q[i + h];
-                                    const float keep = up ? q[i + h] : q[i];
-                                    q[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-                                }
-                            }
+                                for (int i = 0; i < 4; ++i)
+                                    if (i < m) q[i] += __shfl_xor_sync(0xffffffffu, q[i + m], m);
+                            Z[(a0 + aa) * kWsTV] = q[0];
                         }
-                        *reinterpret_cast<float2 *>(Z + (a0 + b2) * kWsTV + vg * 8 + 4 * b1 + 2 * b0) =
-                            make_float2(q[0], q[1]);
                     }
                 }
                 __syncwarp();
@@ -640,7 +777,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
     } else {
         // ===== producers: D chunks via TMA; scatter value * Z[cell] =====
-        if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProd));
         const int p = warp - kWsCons;
         const int ex = fix_exponent(fx, A.nt);
         const double scale = ldexp(1.0, ex);
@@ -648,55 +784,70 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         // stays in range, so the fixed-point term needs no fp64 arithmetic
         const bool f32_scale = ex >= -120 && ex <= 120;
         const float scalef = f32_scale ? ldexpf(1.f, ex) : 1.f;
-        if (p == 0 && lane == 0 && total > 0)
-            tma_chunk(Dbuf, A.D, chunk_bytes, &dfull[0]);
-        int k = 0;
-        for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
-            for (int c = 0; c < A.nch; ++c, ++k) {
-                const int s = k & 1;
-                if (p == 0 && lane == 0 && k + 1 < total) {
-                    const int s1 = (k + 1) & 1;
-                    if (k + 1 >= 2) bar_wait(&dempty[s1], ((k - 1) >> 1) & 1);
-                    const int c1 = (c + 1) % A.nch;
-                    tma_chunk(Dbuf + s1 * chunk_floats, A.D + (size_t)c1 * chunk_floats,
-                              chunk_bytes, &dfull[s1]);
-                }
-                __syncwarp();
-                {
-                    int nct = ct, nc = c;
-                    next_step(nct, nc, A.nch);
-                    if (nct < n_ct && lane < kTPP)
-                        prefetch_seg(A, seg_of(A, nct * kWsCons + p * kTPP + lane, nc));
-                }
-                const Seg1 S0 = seg_of(A, ct * kWsCons + kTPP * p, c);
-                VBlk B0, B1;
-                vb_load(B0, A, S0.p0, S0.p1, lane);
-                bar_wait(&zfull[s], (k >> 1) & 1);
-#pragma unroll 1
-                for (int q = 0; q < kTPP; ++q) {
-                    const Seg1 S = q ? seg_of(A, ct * kWsCons + kTPP * p + q, c) : S0;
-                    const float *Z = Zbuf + (s * kWsCons + kTPP * p + q) * kWsCells;
-                    if (q) vb_load(B0, A, S.p0, S.p1, lane);
-                    for (uint32_t base = S.p0; base < S.p1; base += 128u) {
-                        vb_load(B1, A, base + 128u, S.p1, lane);
-                        const uint32_t f[4] = {B0.f.x, B0.f.y, B0.f.z, B0.f.w};
-                        const uint32_t cr[4] = {B0.cr.x, B0.cr.y, B0.cr.z, B0.cr.w};
-                        const float v[4] = {B0.v.x, B0.v.y, B0.v.z, B0.v.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            if (f[e] != kSent) {
-                                const float z = Z[cr[e] & (kWsCells - 1)] * v[e];
-                                const long long qv = f32_scale ? __float2ll_rn(z * scalef)
-                                                               : __double2ll_rn((double)z * scale);
-                                atomicAdd(fx.wfix + f[e], static_cast<unsigned long long>(qv));
-                            }
-                        }
-                        B0 = B1;
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) bar_arrive(&zempty[s]);
+        if (p == 0 && lane == 0 && total > 0) tma_chunk(Dbuf, A.D, chunk_bytes, &dfull[0]);
+        Seg2 cur{}, nxt{};
+        uint32_t off_cur = 0u, off_nxt = 0u;
+        if (total > 0) {
+            int ct, c;
+            step_of(0, A.nch, ct, c);
+            cur = seg2_of(A, ct, c, p);
+            if (STAGED && lane == 0) stage_issue(A, cur, slot_at(slots, p, 0u), &slotbar[p][0]);
+            off_nxt = ring_wrap(cur.e - cur.a);
+        }
+        if (total > 1) {
+            int ct, c;
+            step_of(1, A.nch, ct, c);
+            nxt = seg2_of(A, ct, c, p);
+            prefetch_range(A, nxt, lane);
+        }
+        for (int k = 0; k < total; ++k) {
+            const int s = k & 1;
+            int ct, c;
+            step_of(k, A.nch, ct, c);
+            if (p == 0 && lane == 0 && k + 1 < total) {
+                const int s1 = (k + 1) & 1;
+                if (k + 1 >= 2) bar_wait(&dempty[s1], ((k - 1) >> 1) & 1);
+                const int c1 = (c + 1) % A.nch;
+                tma_chunk(Dbuf + s1 * chunk_floats, A.D + (size_t)c1 * chunk_floats, chunk_bytes,
+                          &dfull[s1]);
             }
+            __syncwarp();
+            Seg2 nn{};
+            if (k + 2 < total) {
+                int ct2, c2;
+                step_of(k + 2, A.nch, ct2, c2);
+                nn = seg2_of(A, ct2, c2, p);
+            }
+            if (STAGED && k + 1 < total && lane == 0)
+                stage_issue(A, nxt, slot_at(slots, p, off_nxt), &slotbar[p][s ^ 1]);
+            if (k + 2 < total) prefetch_range(A, nn, lane);
+            const Slot sl = slot_at(slots, p, off_cur);
+            if (STAGED) bar_wait(&slotbar[p][s], (k >> 1) & 1);
+            bar_wait(&zfull[s], (k >> 1) & 1);
+            const float *Z0 = Zbuf + (s * kWsCons + kTPP * p) * kWsCells;
+            // the pair's range [a, e) in 128-entry blocks; tile 1 starts at b
+            // (a 4-aligned boundary, so no 4-entry group straddles it)
+            constexpr int kB = 4;
+            for (uint32_t base = cur.a; base < (c_ws_isolate == 2 ? cur.a : cur.e); base += 128u * kB) {
+                VBlk B[kB];
+#pragma unroll
+                for (int j = 0; j < kB; ++j) {
+                    const uint32_t kk = base + 128u * j + 4u * (uint32_t)lane;
+                    if (STAGED) vb_lds(B[j], sl, kk - cur.a, kk < cur.e);
+                    else vb_ldg(B[j], A, kk, kk < cur.e);
+                }
+#pragma unroll
+                for (int j = 0; j < kB; ++j) {
+                    const uint32_t kk = base + 128u * j + 4u * (uint32_t)lane;
+                    wc_scatter4(B[j], kk < cur.b ? Z0 : Z0 + kWsCells, fx, f32_scale, scalef, scale);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(&zempty[s]);
+            off_cur = off_nxt;
+            off_nxt = ring_wrap(off_nxt + (nxt.e - nxt.a));
+            cur = nxt;
+            nxt = nn;
         }
     }
 }
@@ -704,46 +855,49 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
-template <int DPL>
+template <int DPL, bool STAGED>
 static int ws_dsc_t(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
                     const DscOut &o, const CallHooks &h, cudaStream_t st)
 {
-    LIFE_TRY(ensure_smem(k_dsc_ws<DPL>, phi->d_smem));
+    LIFE_TRY(ensure_smem(k_dsc_ws<DPL, STAGED>, phi->d_smem));
     WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_t1, phi->d_D,
-             phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
-    k_dsc_ws<DPL><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, w, y, b, flags, phi->red,
-                                                                   o, h);
+             phi->d_slotv, phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
+    k_dsc_ws<DPL, STAGED><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, w, y, b, flags,
+                                                                           phi->red, o, h);
     LIFE_CHECK_LAUNCH();
     return LIFE_OK;
 }
 
-template <int DPL>
+template <int DPL, bool STAGED>
 static int ws_wc_t(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
                    cudaStream_t st)
 {
-    LIFE_TRY(ensure_smem(k_wc_ws<DPL>, phi->d_smem));
+    LIFE_TRY(ensure_smem(k_wc_ws<DPL, STAGED>, phi->d_smem));
     WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_t1, phi->d_D,
-             phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
-    k_wc_ws<DPL><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, y, fx, h);
+             phi->d_slotv, phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
+    k_wc_ws<DPL, STAGED><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, y, fx, h);
     LIFE_CHECK_LAUNCH();
     return LIFE_OK;
 }
 
-template <int DPL>
+template <int DPL, bool STAGED>
 static int ws_prepare_t(life_phi *phi)
 {
-    LIFE_TRY(ensure_smem(k_dsc_ws<DPL>, phi->d_smem));
-    LIFE_TRY(ensure_smem(k_wc_ws<DPL>, phi->d_smem));
+    LIFE_TRY(ensure_smem(k_dsc_ws<DPL, STAGED>, phi->d_smem));
+    LIFE_TRY(ensure_smem(k_wc_ws<DPL, STAGED>, phi->d_smem));
     return LIFE_OK;
 }
 
 #define LIFE_WS_DISPATCH(FN, ...)                                              \
-    switch (phi->nt_pad / 8) {                                                 \
-    case 4: return FN<4>(__VA_ARGS__);                                         \
-    case 8: return FN<8>(__VA_ARGS__);                                         \
-    case 12: return FN<12>(__VA_ARGS__);                                       \
-    default: return fail(LIFE_ERR_CONFIG_INVALID, "ws layout: unsupported n_dirs"); \
-    }
+    do {                                                                       \
+        const bool staged_ = phi->d_staged;                                    \
+        switch (phi->nt_pad / 8) {                                             \
+        case 4: return staged_ ? FN<4, true>(__VA_ARGS__) : FN<4, false>(__VA_ARGS__);    \
+        case 8: return staged_ ? FN<8, true>(__VA_ARGS__) : FN<8, false>(__VA_ARGS__);    \
+        case 12: return staged_ ? FN<12, true>(__VA_ARGS__) : FN<12, false>(__VA_ARGS__); \
+        default: return fail(LIFE_ERR_CONFIG_INVALID, "ws layout: unsupported n_dirs"); \
+        }                                                                      \
+    } while (0)
 
 int launch_dsc_ws(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
                   const DscOut &o, const CallHooks &h, cudaStream_t st)
@@ -773,10 +927,14 @@ extern "C" LIFE_API int life_debug_ws_isolate(int mode)
 namespace life {
 
 int ws_warps() { return kWsWarps; }
+int ws_chunk_atoms() { return kWsCA; }
+int ws_ring_entries() { return kWsRing; }
 
-size_t ws_smem_bytes(int nt_pad)
+size_t ws_smem_bytes(int nt_pad, bool staged)
 {
-    return ((size_t)2 * kWsCA * nt_pad + (size_t)2 * kWsCons * kWsCells) * sizeof(float);
+    size_t b = ((size_t)2 * kWsCA * nt_pad + (size_t)2 * kWsCons * kWsCells) * sizeof(float);
+    if (staged) b += (size_t)kWsProd * 3 * kWsRing * 4;
+    return b;
 }
 
 }  // namespace life

@@ -1,24 +1,33 @@
-"""Time k_dsc_ws with consumers or producers disabled (diagnostic)."""
-import ctypes, os, sys
-import numpy as np, torch
+"""Time k_dsc_ws / k_wc_ws with consumers or producers disabled (diagnostic build):
+  make -C paper_1905_06234_b200/csrc diag
+  LIFE_B200_LIB=$PWD/build/diag/liblife_b200.so python tools/ws_isolate.py [--mrl 520]
+mode: 0 full, 1 producers only, 2 consumers only; flags<<8: 1 no L2 prefetch, 4 no gather."""
+import argparse, ctypes, os, sys
+import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import paper_1905_06234_b200 as L
-from paper_1905_06234_b200 import _native, datagen
+import paper_1905_06234_b200 as L  # noqa: E402
+from paper_1905_06234_b200 import _native, datagen  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--mrl", type=float, default=520.0)
+args = ap.parse_args()
 dims = (1057, 200_000, 500_000, 96, 100_000_000)
-cfg = L.GenConfig(dims=L.Dims(*dims), mean_run_length=520.0, seed=0, noise_sigma=0.1)
+cfg = L.GenConfig(dims=L.Dims(*dims), mean_run_length=args.mrl, seed=0, noise_sigma=0.1)
 t, dic, w_true, _ = datagen.draw_arrays(cfg)
 op = L.DeviceOperator(t, dic)
 lib = _native.lib()
 lib.life_debug_ws_isolate.argtypes = [ctypes.c_int]
 w = torch.from_numpy(w_true).float().cuda()
 y = torch.empty(dims[1] * dims[3], device="cuda"); g = torch.empty(dims[2], device="cuda")
-ym = torch.zeros(1, device="cuda")
-for mode in [0, 1, 2] + [1 | (f << 8) for f in (1, 2, 4, 3, 7)] + [0]:
-    lib.life_debug_ws_isolate(mode)
-    for _ in range(2): op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absmax=ym)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(10): op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absmax=ym)
-    e1.record(); torch.cuda.synchronize()
-    print("mode", mode, "dsc ms", e0.elapsed_time(e1) / 10, flush=True)
+ym = torch.ones(1, device="cuda")
+for name, fn in (("dsc", lambda: op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absmax=ym)),
+                 ("wc", lambda: op.wc_f32(y, g, y_absmax=ym))):
+    for mode in [0, 1, 2, 1 | (1 << 8), 1 | (4 << 8)]:
+        lib.life_debug_ws_isolate(mode)
+        for _ in range(2): fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10): fn()
+        e1.record(); torch.cuda.synchronize()
+        print(f"mrl={args.mrl} {name} mode {mode:#x} ms {e0.elapsed_time(e1) / 10:.4f}", flush=True)
 lib.life_debug_ws_isolate(0)
