@@ -493,9 +493,9 @@ __global__ void k_dense_key1(const uint32_t *a, const uint32_t *v, int64_t n, in
     }
 }
 
-// warp-specialized layout: segments ordered by (CTA tile round ct, atom
-// chunk, warp tile q in the round), so one step (ct, chunk) of a CTA -- and
-// the two tiles a producer warp owns in it -- is a contiguous range
+// warp-specialized layout: one segment per (CTA tile round ct, atom chunk,
+// producer warp p) = a pair of adjacent tiles, so one producer warp's step is
+// one segment; cell (11 bits) = tile-in-pair, atom in chunk, voxel slot
 __global__ void k_voxel_hist(const uint32_t *v, int64_t n, unsigned *cnt)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -504,16 +504,17 @@ __global__ void k_voxel_hist(const uint32_t *v, int64_t n, unsigned *cnt)
 }
 
 __global__ void k_ws_key1(const uint32_t *a, const uint32_t *v, const uint32_t *vslot, int64_t n,
-                          int nch, int ca, unsigned long long *key, uint32_t *iota)
+                          int nch, int ca, int nprod, unsigned long long *key, uint32_t *iota)
 {
+    const int tpp = 8 / nprod, cbits = tpp == 2 ? 11 : 10;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t at = a[i], vx = vslot[v[i]];
-        const uint32_t tile = vx / 32u;
-        const unsigned long long tc =
-            ((unsigned long long)(tile / 8u) * nch + at / ca) * 8u + tile % 8u;
-        const uint32_t cell = (at % ca) * 32u + vx % 32u;
-        key[i] = (tc << 10) | cell;
+        const uint32_t at = a[i], slot = vslot[v[i]];
+        const uint32_t tile = slot / 32u;
+        const unsigned long long seg =
+            ((unsigned long long)(tile / 8u) * nch + at / ca) * nprod + (tile % 8u) / tpp;
+        const uint32_t cell = (tile % tpp) << 10 | (at % ca) * 32u + slot % 32u;
+        key[i] = (seg << cbits) | cell;
         iota[i] = (uint32_t)i;
     }
 }
@@ -667,7 +668,8 @@ static int pad_dirs(int nt)
 size_t ws_smem_bytes(int nt_pad, bool staged);
 int ws_warps();
 int ws_chunk_atoms();
-int ws_ring_entries();
+int ws_slot_entries();
+int ws_producers();
 
 int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
                 const double *val, const std::vector<double> &hdict, cudaStream_t st)
@@ -675,7 +677,8 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     const int64_t n = phi->nc;
     // warp-specialized kernels (life_ws.cu) for n_dirs <= 96, the v1
     // register-tiled kernels above for n_dirs <= 160, else sparse only
-    int kind = 2, tv = 32, cell_bits = 10, ca = ws_chunk_atoms();
+    int kind = 2, tv = 32, ca = ws_chunk_atoms();
+    int cell_bits = ws_producers() == 4 ? 11 : 10;
     int nt_pad = (phi->nt + 31) / 32 * 32;
     if (nt_pad > 96) {
         kind = 1;
@@ -694,7 +697,9 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     phi->n_chunks = (phi->na + ca - 1) / ca;
     // ws: whole CTA rounds of 8 tiles (segments of missing tiles stay empty)
     const int64_t n_ct = ((int64_t)phi->n_tiles + 7) / 8;
-    const int64_t ntc = kind == 2 ? n_ct * phi->n_chunks * 8 : (int64_t)phi->n_tiles * phi->n_chunks;
+    // ws: one segment per producer warp and step (its one or two tiles)
+    const int64_t ntc = kind == 2 ? n_ct * phi->n_chunks * ws_producers()
+                                  : (int64_t)phi->n_tiles * phi->n_chunks;
     if (ntc >= (1ll << 31)) return LIFE_OK;
     unsigned long long *k1 = nullptr, *sk1 = nullptr, *k2 = nullptr, *sk2 = nullptr;
     uint32_t *iota = nullptr, *perm1 = nullptr, *perm = nullptr;
@@ -739,7 +744,8 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
                                   cudaMemcpyHostToDevice, st));
         LIFE_CUDA(cudaMemcpyAsync(phi->d_slotv, slotv.data(), (size_t)nslots * 4,
                                   cudaMemcpyHostToDevice, st));
-        k_ws_key1<<<gridn(n), 256, 0, st>>>(a, v, phi->d_vslot, n, phi->n_chunks, ca, k1, iota);
+        k_ws_key1<<<gridn(n), 256, 0, st>>>(a, v, phi->d_vslot, n, phi->n_chunks, ca,
+                                             ws_producers(), k1, iota);
         LIFE_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
     }
     else
@@ -762,7 +768,8 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
     unsigned hmr = 0;
     LIFE_CUDA(cudaMemcpyAsync(&hmr, mr, 4, cudaMemcpyDeviceToHost, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
-    if (hmr >= (1u << (31 - cell_bits))) {
+    // rank field: ws bits cell_bits..29 (bit 30 = pad, 31 = mixed); v1 bits 10..31
+    if (hmr >= (kind == 2 ? (1u << (30 - cell_bits)) : (1u << (31 - cell_bits)))) {
         cudaFreeAsync(sk1, st); cudaFreeAsync(perm1, st); cudaFreeAsync(k2, st); cudaFreeAsync(mr, st);
         return LIFE_OK;  // pathological duplicate counts: stay sparse
     }
@@ -796,33 +803,13 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
         }
         hP[ntc] = hT[ntc] = (uint32_t)pos;
         if (pos >= 0xFFFFFFFFll) return fail(LIFE_ERR_CONFIG_INVALID, "padded layout exceeds u32");
-        // staged producers keep two consecutive steps of a warp (its two
-        // tiles of (ct, c) and of the next step) in a ring of
-        // ws_ring_entries(); check the largest such pair for this grid
-        int64_t maxpw = 0, maxpair = 0;
-        {
-            const int64_t nch = phi->n_chunks, grid = phi->sms;
-            auto rng = [&](int64_t ct, int64_t c, int p) {
-                const int64_t t = (ct * nch + c) * 8 + 2 * p;
-                return (int64_t)hP[t + 2] - hP[t];
-            };
-            for (int64_t b = 0; b < std::min<int64_t>(grid, n_ct); ++b) {
-                const int64_t my = (n_ct - 1 - b) / grid + 1, total = my * nch;
-                for (int p = 0; p < 4; ++p) {
-                    int64_t prev = -1;
-                    for (int64_t j = 0; j < total; ++j) {
-                        const int64_t r = rng(b + (j / nch) * grid, j % nch, p);
-                        maxpw = std::max(maxpw, r);
-                        if (prev >= 0) maxpair = std::max(maxpair, prev + r);
-                        prev = r;
-                    }
-                }
-            }
-        }
-        maxpair = std::max(maxpair, maxpw);  // a lone step must fit as well
-        phi->d_maxpw = maxpair;
+        // staged producers copy one segment per step into a fixed slot
+        int64_t maxpw = 0;
+        for (int64_t t = 0; t < ntc; ++t) maxpw = std::max<int64_t>(maxpw, (int64_t)hP[t + 1] - hP[t]);
+        const int64_t maxpair = maxpw;
+        phi->d_maxpw = maxpw;
         const char *unstaged = getenv("LIFE_WS_UNSTAGED");  // A/B diagnostics
-        phi->d_staged = maxpair <= ws_ring_entries() && !(unstaged && unstaged[0] == '1');
+        phi->d_staged = maxpw <= ws_slot_entries() && !(unstaged && unstaged[0] == '1');
         if (getenv("LIFE_DEBUG"))
             fprintf(stderr, "[life] ws layout: ntc=%lld padded=%lld maxpw=%lld maxpair=%lld staged=%d\n",
                     (long long)ntc, (long long)pos, (long long)maxpw, (long long)maxpair,
@@ -833,7 +820,7 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
         LIFE_TRY(dalloc(phi, &phi->d_val, npad));
         LIFE_TRY(dalloc(phi, &phi->d_tptr, ntc + 1));
         LIFE_TRY(dalloc(phi, &phi->d_t1, ntc + 1));
-        LIFE_CUDA(cudaMemsetAsync(phi->d_cr, 0, npad * 4, st));
+        LIFE_CUDA(cudaMemsetAsync(phi->d_cr, 0x40, npad * 4, st));  // pad bit 30
         LIFE_CUDA(cudaMemsetAsync(phi->d_fiber, 0xFF, npad * 4, st));  // kWsSentinel
         LIFE_CUDA(cudaMemsetAsync(phi->d_val, 0, npad * 4, st));
         LIFE_CUDA(cudaMemcpyAsync(phi->d_tptr, hP.data(), (ntc + 1) * 4, cudaMemcpyHostToDevice, st));

@@ -14,16 +14,23 @@
 //                     8 voxels x 12 directions (96 fp32 accumulators), so a
 //                     dictionary value feeds 8 FMAs and a coefficient 12.
 //
-// Coefficient staging (the "staged" producer): the layout orders segments by
-// (CTA tile round, atom chunk, warp tile, rank, cell), so the two tiles a
-// producer warp owns in one step are ONE contiguous range of the stream.
-// Lane 0 of each producer warp copies the next step's range into its own
-// double-buffered shared-memory slot with three cp.async.bulk copies
-// (index / fascicle / value arrays, mbarrier complete_tx) and prefetches the
-// step after that into L2, so the producers see shared-memory latency for
-// the stream and only the w[f] gathers (DSC) or RED.ADDs (WC) go to L2.
-// Operators whose per-warp step range exceeds a slot fall back to the
-// register-streaming producer (same results, bit for bit).
+// Layout: one segment per (CTA tile round ct, atom chunk c, producer warp
+// p), i.e. per PAIR of consumer tiles (2p, 2p+1): a rank-0 region (each
+// cell's first coefficient; cells are 11 bits = tile-in-pair, atom, voxel
+// slot, all distinct) then a rank>=1 region (repeats, sorted by rank), each
+// padded to a multiple of 4 entries with pad entries (cr bit 30).  The pair's
+// two C tiles are adjacent in shared memory, so an entry's tile is just bit 10
+// of its cell.  Voxels are dealt to tile slots by coefficient count
+// (life_dense.cu), so every segment carries about the same work.
+//
+// Coefficient staging (the "staged" producer): lane 0 of each producer warp
+// copies the next step's segment into one of the warp's two shared-memory
+// slots with three cp.async.bulk copies (index / fascicle / value arrays,
+// mbarrier complete_tx) and prefetches the step after that into L2, so the
+// producers see shared-memory latency for the stream and only the w[f]
+// gathers (DSC) or RED.ADDs (WC) go to L2.  Operators with a segment larger
+// than a slot fall back to the register-streaming producer (same results,
+// bit for bit).
 //
 // Steps are double buffered (C/Z tiles and dictionary chunks) and handed over
 // with mbarriers (full/empty).  Each LDS.128 costs four shared-memory
@@ -36,40 +43,63 @@
 namespace life {
 
 constexpr int kWsCons = 8;
-constexpr int kWsProd = 4;
+#ifndef LIFE_WS_PROD
+#define LIFE_WS_PROD 8
+#endif
+#if LIFE_WS_PROD != 8
+#error "the WC kernel pairs up the per-tile segments of the 8-producer layout"
+#endif
+constexpr int kWsProd = LIFE_WS_PROD;      // producer warps (4 or 8)
 constexpr int kTPP = kWsCons / kWsProd;   // consumer tiles per producer warp
 constexpr int kWsWarps = kWsCons + kWsProd;
+// 8 producer warps: registers are split between the roles with setmaxnreg
+// (consumers 168 for their 96 accumulators, producers 88)
+constexpr bool kSplitRegs = kWsProd == 8;
+constexpr int kRegCons = 168;
+constexpr int kRegProd = 88;
+static_assert(!kSplitRegs || kWsCons * kRegCons + kWsProd * kRegProd <= 2048, "register file");
 constexpr int kWsThreads = kWsWarps * 32;
 constexpr int kWsTV = 32;                  // voxels per consumer tile
 constexpr int kWsCA = 32;                  // atoms per chunk
-constexpr int kWsCells = kWsTV * kWsCA;    // 1024
-constexpr int kWsCellBits = 10;
-constexpr int kWsRing = 2880;              // staged entries per producer warp (ring)
-// load and gather the first rank>=1 batch together with the first rank-0 batch
-#ifndef LIFE_WS_EARLY_SLOW
-#define LIFE_WS_EARLY_SLOW 0
+constexpr int kWsCells = kWsTV * kWsCA;    // 1024 cells per tile
+constexpr int kWsCellBits = kTPP == 2 ? 11 : 10;  // cell within a producer's tiles
+constexpr uint32_t kCellMask = kTPP * kWsCells - 1;
+constexpr uint32_t kPadBit = 0x40000000u;  // pad entry
+constexpr uint32_t kMixedBit = 0x80000000u;  // 32-window straddles two ranks
+constexpr uint32_t kRankMask = (1u << (30 - kWsCellBits)) - 1;  // rank: bits cellbits..29
+#ifndef LIFE_WS_CPASYNC
+#define LIFE_WS_CPASYNC 0
 #endif
-constexpr bool kEarlySlow = LIFE_WS_EARLY_SLOW;
-static_assert(kTPP == 2, "a producer warp owns two adjacent tiles");
+// staged producers: gather w with cp.async into the slot one step ahead (1)
+// or into registers within the step (0)
+constexpr bool kCpAsyncGather = LIFE_WS_CPASYNC;
+constexpr int kWsSlot = 720 * kTPP;        // staged entries per (producer warp, slot)
+static_assert(kTPP == 1 || kTPP == 2, "a producer warp owns one or two adjacent tiles");
 
 struct WsArgs {
     const uint32_t *cr;
     const uint32_t *fiber;
     const float *val;
-    const uint32_t *tptr;   // padded segment starts, [n_ct*nch*8 + 1]
+    const uint32_t *tptr;   // padded pair-segment starts, [n_ct*nch*4 + 1]
     const uint32_t *t1;     // start of each segment's rank>=1 region
     const float *D;
     const int *slotv;       // voxel of each tile slot (tile*32 + i), -1 for padding
     int nv, nt, nt_pad, nch, n_tiles, na;
 };
-constexpr uint32_t kSent = 0xFFFFFFFFu;  // padding entry (fiber field)
 // Diagnostic isolation, compiled in only with -DLIFE_WS_DIAG (tools/ws_isolate.py):
 // c_ws_isolate 1 = producers only, 2 = consumers only (results are garbage);
 // c_ws_flags 1 = no L2 prefetch, 4 = no gather.
 #ifdef LIFE_WS_DIAG
 __constant__ int c_ws_isolate = 0;
 __constant__ int c_ws_flags = 0;
+// producer-warp cycle counters: [0] slot wait, [1] empty wait, [2] build, [3] steps,
+// [4] consumer full wait, [5] consumer compute
+__device__ unsigned long long g_ws_cyc[8];
+#define WS_T0(v) const long long v = clock64()
+#define WS_ACC(i, v) atomicAdd(&g_ws_cyc[i], (unsigned long long)(clock64() - (v)))
 #else
+#define WS_T0(v)
+#define WS_ACC(i, v)
 constexpr int c_ws_isolate = 0;
 constexpr int c_ws_flags = 0;
 #endif
@@ -178,283 +208,331 @@ __device__ __forceinline__ bool ws_last_block(unsigned *counter)
     return s_last;
 }
 
+// L2 policies: the coefficient stream (read once per SpMV, 1.2 GB at C2) is
+// evict-first so it does not push the gathered / scattered Nf-vectors (w,
+// the fixed-point sums) out of L2; those are evict-last.
+__device__ __forceinline__ uint64_t policy_stream()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_keep()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void prefetch_l2(const void *ptr, uint32_t bytes)
 {
     if (bytes == 0) return;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(ptr), "r"(bytes),
+                 "l"(policy_stream())
+                 : "memory");
 }
 
-// ---- a producer warp's step: its two tiles (2p, 2p+1) of one (ct, chunk) --
-// Segment of one (tile, chunk): [p0, q0) holds each cell's first coefficient
-// (rank 0, distinct cells) and [q0, p1) the repeats (rank >= 1); both regions
-// are padded to 4-entry multiples (fiber = kSent), so the rank-0 region
-// streams as 16-byte vectors, 4 coefficients per lane, with one plain STS per
-// coefficient.  Repeats are added afterwards in rank order (32-entry windows
-// straddling two ranks, flagged at build time, are applied rank by rank).
-struct Seg2 {
-    uint32_t a, q0, b, q1, e;  // tile 0 [a, q0) [q0, b); tile 1 [b, q1) [q1, e)
+__device__ __forceinline__ void bulk_g2s_stream(void *dst, const void *src, unsigned bytes,
+                                                uint64_t *b)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(smaddr(dst)),
+        "l"(src), "r"(bytes), "r"(smaddr(b)), "l"(policy_stream())
+        : "memory");
+}
+
+__device__ __forceinline__ float ld_keep(const float *p, uint64_t pol)
+{
+    float r;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ void red_keep(unsigned long long *p, unsigned long long v, uint64_t pol)
+{
+    asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
+// ---- a producer warp's step: the pair segment of (ct, chunk, p) ------------
+struct Seg {
+    uint32_t p0, q0, p1;  // rank-0 region [p0, q0), rank>=1 region [q0, p1)
 };
 
-__device__ __forceinline__ size_t tc_of(const WsArgs &A, int ct, int c, int q)
+__device__ __forceinline__ Seg seg_of(const WsArgs &A, int ct, int c, int p)
 {
-    return ((size_t)ct * A.nch + c) * kWsCons + q;
-}
-
-__device__ __forceinline__ Seg2 seg2_of(const WsArgs &A, int ct, int c, int p)
-{
-    const size_t tc = tc_of(A, ct, c, kTPP * p);
-    Seg2 S;
-    S.a = __ldg(A.tptr + tc);
-    S.q0 = __ldg(A.t1 + tc);
-    S.b = __ldg(A.tptr + tc + 1);
-    S.q1 = __ldg(A.t1 + tc + 1);
-    S.e = __ldg(A.tptr + tc + 2);
+    const size_t t = ((size_t)ct * A.nch + c) * kWsProd + p;
+    Seg S;
+    S.p0 = __ldg(A.tptr + t);
+    S.q0 = __ldg(A.t1 + t);
+    S.p1 = __ldg(A.tptr + t + 1);
     return S;
 }
 
-// the CTA's j-th step: (ct, c)
-__device__ __forceinline__ void step_of(int j, int nch, int &ct, int &c)
+// the CTA's steps in order: (ct, c), c fastest
+__device__ __forceinline__ void step_next(int &ct, int &c, int nch)
 {
-    ct = (int)blockIdx.x + (j / nch) * (int)gridDim.x;
-    c = j % nch;
+    if (++c == nch) {
+        c = 0;
+        ct += gridDim.x;
+    }
 }
 
-__device__ __forceinline__ void prefetch_range(const WsArgs &A, const Seg2 &S, int lane)
+__device__ __forceinline__ void prefetch_seg(const WsArgs &A, const Seg &S, int lane)
 {
-    if ((c_ws_flags & 1) || S.e <= S.a || lane >= 3) return;
-    const uint32_t bytes = (S.e - S.a) * 4u;  // padded ranges are 16-byte aligned
-    const void *base = lane == 0 ? (const void *)(A.cr + S.a)
-                     : lane == 1 ? (const void *)(A.fiber + S.a)
-                                 : (const void *)(A.val + S.a);
+    if ((c_ws_flags & 1) || S.p1 <= S.p0 || lane >= 3) return;
+    const uint32_t bytes = (S.p1 - S.p0) * 4u;  // padded segments are 16-byte aligned
+    const void *base = lane == 0 ? (const void *)(A.cr + S.p0)
+                     : lane == 1 ? (const void *)(A.fiber + S.p0)
+                                 : (const void *)(A.val + S.p0);
     prefetch_l2(base, bytes);
 }
 
-// staging ring of one producer warp: three arrays of kWsRing entries; a step's
-// range occupies [off, off + n) modulo kWsRing (offsets and sizes are
-// multiples of 4, so a 16-byte vector never wraps).  The host checks that two
-// consecutive steps of a warp always fit (life_dense.cu: build_dense).
-struct Slot {
-    uint32_t *cr;
-    uint32_t *f;
-    float *v;
-    uint32_t off;
-    __device__ __forceinline__ uint32_t at(uint32_t i) const
-    {
-        const uint32_t x = off + i;
-        return x >= (uint32_t)kWsRing ? x - (uint32_t)kWsRing : x;
-    }
+// A segment's entries, relative to its start: a shared-memory slot (staged)
+// or the global arrays offset by p0 (fallback).
+struct View {
+    const uint32_t *cr;
+    const uint32_t *f;
+    const float *v;
 };
 
-__device__ __forceinline__ uint32_t ring_wrap(uint32_t x)
+__device__ __forceinline__ View slot_view(float *slots, int p, int s)
 {
-    return x >= (uint32_t)kWsRing ? x - (uint32_t)kWsRing : x;
+    uint32_t *base = reinterpret_cast<uint32_t *>(slots) + (size_t)(p * 2 + s) * 3 * kWsSlot;
+    return View{base, base + kWsSlot, reinterpret_cast<const float *>(base + 2 * kWsSlot)};
 }
 
-__device__ __forceinline__ Slot slot_at(float *slots, int p, uint32_t off)
+__device__ __forceinline__ View global_view(const WsArgs &A, const Seg &S)
 {
-    uint32_t *base = reinterpret_cast<uint32_t *>(slots) + (size_t)p * 3 * kWsRing;
-    return Slot{base, base + kWsRing, reinterpret_cast<float *>(base + 2 * kWsRing), off};
+    return View{A.cr + S.p0, A.fiber + S.p0, A.val + S.p0};
 }
 
-// lane 0: copy the step's range [S.a, S.e) into the ring at D.off
-// (three arrays, split in two where the range wraps)
-__device__ __forceinline__ void stage_issue(const WsArgs &A, const Seg2 &S, const Slot &D,
-                                            uint64_t *bar)
+template <bool STAGED, typename T>
+__device__ __forceinline__ T ldv(const T *p)
 {
-    const unsigned n = S.e - S.a;
+    if constexpr (STAGED) return *p;
+    else return ld_stream(p);
+}
+
+// lane 0: copy segment S into the warp's slot (three bulk copies)
+__device__ __forceinline__ void stage_issue(const WsArgs &A, const Seg &S, float *slots, int p,
+                                            int s, uint64_t *bar)
+{
+    const unsigned n = S.p1 - S.p0, bytes = n * 4u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    bar_arrive_tx(bar, 12u * n);
-    if (n == 0) return;
-    const unsigned n1 = min(n, (unsigned)kWsRing - D.off), n2 = n - n1;
-    bulk_g2s(D.cr + D.off, A.cr + S.a, 4u * n1, bar);
-    bulk_g2s(D.f + D.off, A.fiber + S.a, 4u * n1, bar);
-    bulk_g2s(D.v + D.off, A.val + S.a, 4u * n1, bar);
-    if (n2) {
-        bulk_g2s(D.cr, A.cr + S.a + n1, 4u * n2, bar);
-        bulk_g2s(D.f, A.fiber + S.a + n1, 4u * n2, bar);
-        bulk_g2s(D.v, A.val + S.a + n1, 4u * n2, bar);
+    bar_arrive_tx(bar, 3u * bytes);
+    if (n) {
+        const View D = slot_view(slots, p, s);
+        bulk_g2s_stream((void *)D.cr, A.cr + S.p0, bytes, bar);
+        bulk_g2s_stream((void *)D.f, A.fiber + S.p0, bytes, bar);
+        bulk_g2s_stream((void *)D.v, A.val + S.p0, bytes, bar);
     }
 }
 
-// 4 consecutive coefficients per lane (a 128-coefficient block per warp)
-struct VBlk {
-    uint4 cr, f;
-    float4 v;
-    float w[4];
-};
+constexpr uint32_t kSent = 0xFFFFFFFFu;  // fascicle field of pad entries
 
-__device__ __forceinline__ void vb_empty(VBlk &B)
+__device__ __forceinline__ float gather_w(const float *__restrict__ w, uint32_t f)
 {
-    B.cr = make_uint4(0u, 0u, 0u, 0u);
-    B.f = make_uint4(kSent, kSent, kSent, kSent);
-    B.v = make_float4(0.f, 0.f, 0.f, 0.f);
+    return f == kSent ? 0.f : ((c_ws_flags & 4) ? 1.f : ld_keep(w + f, policy_keep()));
 }
 
-// staged: from the slot (k relative to the slot start)
-__device__ __forceinline__ void vb_lds(VBlk &B, const Slot &S, uint32_t k, bool ok)
-{
-    if (ok) {
-        const uint32_t x = S.at(k);
-        B.cr = *reinterpret_cast<const uint4 *>(S.cr + x);
-        B.f = *reinterpret_cast<const uint4 *>(S.f + x);
-        B.v = *reinterpret_cast<const float4 *>(S.v + x);
-    } else {
-        vb_empty(B);
-    }
-}
+// Build the producer warp's two coefficient tiles (C: 2 x 1024 floats) from
+// its segment.  Two phases per batch keep few registers live: first every
+// lane issues the w[f] gathers of its entries (4 per 128-entry block, one
+// per 32-entry window), then it reloads index and value and stores
+// C[cell] = w * value.  The first batch of rank>=1 windows is gathered with
+// the rank-0 batch, so a typical step has one gather round trip.  Repeats
+// are added after every rank-0 store, window by window in rank order; a
+// window straddling two rank levels (kMixedBit) is applied rank by rank.
+constexpr int kFastBlocks = kWsProd == 8 ? 4 : 8;
+#ifndef LIFE_WC_ATOMS
+#define LIFE_WC_ATOMS 4
+#endif
+constexpr int kWcAtoms = LIFE_WC_ATOMS;  // atoms per WC consumer iteration
+constexpr int kSlowRounds = 8;
 
-// streamed: straight from global memory (fallback producer)
-__device__ __forceinline__ void vb_ldg(VBlk &B, const WsArgs &A, uint32_t k, bool ok)
+template <bool STAGED>
+__device__ __forceinline__ unsigned build_pair(float *C, const float *__restrict__ w,
+                                               const Seg &S, const View &V, int junk,
+                                               int lane)
 {
-    if (ok) {
-        B.cr = ld_stream(reinterpret_cast<const uint4 *>(A.cr + k));
-        B.f = ld_stream(reinterpret_cast<const uint4 *>(A.fiber + k));
-        B.v = ld_stream(reinterpret_cast<const float4 *>(A.val + k));
-    } else {
-        vb_empty(B);
-    }
-}
-
-__device__ __forceinline__ void vb_gather(VBlk &B, const float *__restrict__ w)
-{
-    const uint32_t f[4] = {B.f.x, B.f.y, B.f.z, B.f.w};
+    WS_T0(t_fast);
+    float4 *Z = reinterpret_cast<float4 *>(C);
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-        B.w[e] = f[e] != kSent ? ((c_ws_flags & 4) ? 1.f : __ldg(w + f[e])) : 0.f;
-}
-
-__device__ __forceinline__ void vb_assign(const VBlk &B, float *C, unsigned &zeros)
-{
-    const uint32_t f[4] = {B.f.x, B.f.y, B.f.z, B.f.w};
-    const uint32_t cr[4] = {B.cr.x, B.cr.y, B.cr.z, B.cr.w};
-    const float v[4] = {B.v.x, B.v.y, B.v.z, B.v.w};
+    for (int i = 0; i < kTPP * kWsCells / 4 / 32; ++i) Z[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+    unsigned zeros = 0;
+    const uint32_t nf = S.q0 - S.p0, n = S.p1 - S.p0;
+    const int nb = (int)((nf + 127u) / 128u), nw = (int)((n - nf + 31u) / 32u);
+    float ws[kSlowRounds];
+    auto gather_slow = [&](int r0) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        if (f[e] != kSent) {
-            const float s = __fmul_rn(B.w[e], v[e]);
-            zeros += (s == 0.f) ? 1u : 0u;
-            C[cr[e] & (kWsCells - 1)] = s;
+        for (int r = 0; r < kSlowRounds; ++r) {
+            const uint32_t k = nf + 32u * (uint32_t)(r0 + r) + (uint32_t)lane;
+            ws[r] = 0.f;
+            if (r0 + r < nw && k < n) ws[r] = gather_w(w, ldv<STAGED>(V.f + k));
+        }
+    };
+    for (int b0 = 0; b0 < nb || (b0 == 0 && nw > 0); b0 += kFastBlocks) {
+        float wf[kFastBlocks][4];
+#pragma unroll
+        for (int j = 0; j < kFastBlocks; ++j) {
+            const uint32_t k = 128u * (uint32_t)(b0 + j) + 4u * (uint32_t)lane;
+            if (b0 + j < nb && k < nf) {
+                const uint4 f = ldv<STAGED>(reinterpret_cast<const uint4 *>(V.f + k));
+                wf[j][0] = gather_w(w, f.x);
+                wf[j][1] = gather_w(w, f.y);
+                wf[j][2] = gather_w(w, f.z);
+                wf[j][3] = gather_w(w, f.w);
+            }
+        }
+        if (b0 == 0) gather_slow(0);
+#pragma unroll
+        for (int j = 0; j < kFastBlocks; ++j) {
+            const uint32_t k = 128u * (uint32_t)(b0 + j) + 4u * (uint32_t)lane;
+            if (b0 + j < nb && k < nf) {
+                const uint4 c4 = ldv<STAGED>(reinterpret_cast<const uint4 *>(V.cr + k));
+                const float4 v4 = ldv<STAGED>(reinterpret_cast<const float4 *>(V.v + k));
+                const uint32_t cr[4] = {c4.x, c4.y, c4.z, c4.w};
+                const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    // branch-free: pad entries store into the warp's junk word
+                    const bool ok = !(cr[e] & kPadBit);
+                    const float sv = __fmul_rn(wf[j][e], v[e]);
+                    zeros += (ok && sv == 0.f) ? 1u : 0u;
+                    C[ok ? (int)(cr[e] & kCellMask) : junk] = sv;
+                }
+            }
         }
     }
+    __syncwarp();
+    if (lane == 0) WS_ACC(6, t_fast);
+    WS_T0(t_slow);
+    for (int r0 = 0; r0 < nw; r0 += kSlowRounds) {
+        if (r0) gather_slow(r0);
+#pragma unroll
+        for (int r = 0; r < kSlowRounds; ++r) {
+            if (r0 + r >= nw) break;  // warp-uniform
+            const uint32_t k = nf + 32u * (uint32_t)(r0 + r) + (uint32_t)lane;
+            const uint32_t cr = k < n ? ldv<STAGED>(V.cr + k) : kPadBit;
+            const bool ok = !(cr & kPadBit);
+            const float sv = ok ? __fmul_rn(ws[r], ldv<STAGED>(V.v + k)) : 0.f;
+            zeros += (ok && sv == 0.f) ? 1u : 0u;
+            const uint32_t cell = cr & kCellMask;
+            if (!__any_sync(0xffffffffu, ok && (cr & kMixedBit))) {
+                if (ok) C[cell] += sv;
+            } else {
+                const uint32_t rank = (cr >> kWsCellBits) & kRankMask;
+                const uint32_t rmin = __reduce_min_sync(0xffffffffu, ok ? rank : 0xFFFFFFFFu);
+                const uint32_t rmax = __reduce_max_sync(0xffffffffu, ok ? rank : 0u);
+                for (uint32_t rr = rmin; rr <= rmax; ++rr) {
+                    if (ok && rank == rr) C[cell] += sv;
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (lane == 0) WS_ACC(7, t_slow);
+    return zeros;
 }
 
-// one 32-entry window of a rank>=1 region per round
-constexpr int kSlowRounds = 8;
-struct SlowRounds {
-    uint32_t cr[kSlowRounds], f[kSlowRounds];
-    float v[kSlowRounds], w[kSlowRounds];
-    bool t1[kSlowRounds];  // window belongs to tile 1
-};
-
-__device__ __forceinline__ void sr_gather(SlowRounds &R, const float *__restrict__ w)
+// ---- staged, pipelined producer ---------------------------------------------
+// The w[f] gathers of step k+1 are issued during step k as 4-byte cp.async
+// copies (LDGSTS) that overwrite the slot's fascicle array in place with the
+// gathered weights, so the L2 round trips of the gathers (bounded by the L2's
+// random-sector rate, ~1 per cycle per SM) overlap the tile build of step k
+// instead of stalling it.  Each lane gathers exactly the entries it later
+// reads (4 per 128-entry block in the rank-0 region, 1 per 32-entry window
+// after it), so cp.async.wait_group alone makes its values visible.
+__device__ __forceinline__ void cp_async4(void *dst, const void *src, uint64_t pol)
 {
-#pragma unroll
-    for (int r = 0; r < kSlowRounds; ++r)
-        R.w[r] = R.f[r] != kSent ? ((c_ws_flags & 4) ? 1.f : __ldg(w + R.f[r])) : 0.f;
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(smaddr(dst)),
+                 "l"(src), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void gather_to_slot(const Seg &S, const View &V,
+                                               const float *__restrict__ w, int lane)
+{
+    const uint64_t pol = policy_keep();
+    uint32_t *F = const_cast<uint32_t *>(V.f);
+    const uint32_t nf = S.q0 - S.p0, n = S.p1 - S.p0;
+    if (!(c_ws_flags & 4)) {
+        for (uint32_t k = 4u * (uint32_t)lane; k < nf; k += 128u) {
+            const uint4 f = *reinterpret_cast<const uint4 *>(F + k);
+            if (f.x != kSent) cp_async4(F + k, w + f.x, pol);
+            if (f.y != kSent) cp_async4(F + k + 1, w + f.y, pol);
+            if (f.z != kSent) cp_async4(F + k + 2, w + f.z, pol);
+            if (f.w != kSent) cp_async4(F + k + 3, w + f.w, pol);
+        }
+        for (uint32_t k = nf + (uint32_t)lane; k < n; k += 32u) {
+            const uint32_t f = F[k];
+            if (f != kSent) cp_async4(F + k, w + f, pol);
+        }
+    }
+    cp_async_commit();
 }
 
-// apply rounds in order; a round whose 32 entries straddle two rank levels
-// (flag bit 31, set at build time) is applied rank by rank
-__device__ __forceinline__ void sr_apply(const SlowRounds &R, float *C0, float *C1, unsigned &zeros)
+// zero + rank-0 stores, from a slot whose fascicle array holds the gathered w
+__device__ __forceinline__ unsigned build_fast_staged(float *C, const Seg &S, const View &V,
+                                                      int junk, int lane)
 {
+    float4 *Z = reinterpret_cast<float4 *>(C);
 #pragma unroll
-    for (int r = 0; r < kSlowRounds; ++r) {
-        const bool ok = R.f[r] != kSent;
-        if (!__any_sync(0xffffffffu, ok)) continue;
-        float *C = R.t1[r] ? C1 : C0;
-        const float s = __fmul_rn(R.w[r], R.v[r]);
-        zeros += (ok && s == 0.f) ? 1u : 0u;
-        const uint32_t cr = R.cr[r];
-        const uint32_t rank = (cr >> kWsCellBits) & 0x1FFFFFu, cell = cr & (kWsCells - 1);
-        if (!__any_sync(0xffffffffu, ok && (cr >> 31))) {
-            if (ok) C[cell] += s;
+    for (int i = 0; i < kTPP * kWsCells / 4 / 32; ++i) Z[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+    unsigned zeros = 0;
+    const uint32_t nf = S.q0 - S.p0;
+    const float *W = reinterpret_cast<const float *>(V.f);
+#pragma unroll 2
+    for (uint32_t k = 4u * (uint32_t)lane; k < nf; k += 128u) {
+        const uint4 c4 = *reinterpret_cast<const uint4 *>(V.cr + k);
+        const float4 w4 = *reinterpret_cast<const float4 *>(W + k);
+        const float4 v4 = *reinterpret_cast<const float4 *>(V.v + k);
+        const uint32_t cr[4] = {c4.x, c4.y, c4.z, c4.w};
+        const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+        const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const bool ok = !(cr[e] & kPadBit);
+            const float sv = __fmul_rn((c_ws_flags & 4) ? 1.f : wv[e], v[e]);
+            zeros += (ok && sv == 0.f) ? 1u : 0u;
+            C[ok ? (int)(cr[e] & kCellMask) : junk] = sv;
+        }
+    }
+    __syncwarp();
+    return zeros;
+}
+
+// rank>=1 windows in order (after every rank-0 store of the tile)
+__device__ __forceinline__ unsigned build_slow_staged(float *C, const Seg &S, const View &V,
+                                                      int lane)
+{
+    unsigned zeros = 0;
+    const uint32_t nf = S.q0 - S.p0, n = S.p1 - S.p0;
+    const float *W = reinterpret_cast<const float *>(V.f);
+    for (uint32_t base = nf; base < n; base += 32u) {
+        const uint32_t k = base + (uint32_t)lane;
+        const uint32_t cr = k < n ? V.cr[k] : kPadBit;
+        const bool ok = !(cr & kPadBit);
+        const float sv = ok ? __fmul_rn((c_ws_flags & 4) ? 1.f : W[k], V.v[k]) : 0.f;
+        zeros += (ok && sv == 0.f) ? 1u : 0u;
+        const uint32_t cell = cr & kCellMask;
+        if (!__any_sync(0xffffffffu, ok && (cr & kMixedBit))) {
+            if (ok) C[cell] += sv;
         } else {
+            const uint32_t rank = (cr >> kWsCellBits) & kRankMask;
             const uint32_t rmin = __reduce_min_sync(0xffffffffu, ok ? rank : 0xFFFFFFFFu);
             const uint32_t rmax = __reduce_max_sync(0xffffffffu, ok ? rank : 0u);
             for (uint32_t rr = rmin; rr <= rmax; ++rr) {
-                if (ok && rank == rr) C[cell] += s;
+                if (ok && rank == rr) C[cell] += sv;
                 __syncwarp();
             }
         }
         __syncwarp();
-    }
-}
-
-// Build the producer warp's two coefficient tiles of one step.  STAGED reads
-// the range from the warp's shared-memory slot (entry k at slot[k - S.a]),
-// otherwise straight from global memory.
-template <bool STAGED>
-__device__ __forceinline__ unsigned build_pair(float *C0, float *C1, const WsArgs &A,
-                                               const float *__restrict__ w, const Seg2 &S,
-                                               const Slot &sl, int lane)
-{
-    float4 *Z0 = reinterpret_cast<float4 *>(C0);
-    float4 *Z1 = reinterpret_cast<float4 *>(C1);
-#pragma unroll
-    for (int i = 0; i < kWsCells / 4 / 32; ++i) {
-        Z0[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        Z1[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    __syncwarp();
-    unsigned zeros = 0;
-    // rank-0 regions of both tiles in batches of kFastBlocks x 128 entries
-    // (all loads of a batch, then all w gathers, then the stores); the first
-    // batch of rank>=1 windows is loaded and gathered together with the first
-    // rank-0 batch, so a typical step has one gather round trip
-    constexpr int kFastBlocks = 6;
-    const int n0 = (int)((S.q0 - S.a + 127u) / 128u), n1 = (int)((S.q1 - S.b + 127u) / 128u);
-    const int m0 = (int)((S.b - S.q0 + 31u) / 32u), m1 = (int)((S.e - S.q1 + 31u) / 32u);
-    SlowRounds R;
-    auto load_slow = [&](int r0) {
-#pragma unroll
-        for (int r = 0; r < kSlowRounds; ++r) {
-            const int g = r0 + r;
-            R.t1[r] = g >= m0;
-            const uint32_t base = R.t1[r] ? S.q1 + 32u * (uint32_t)(g - m0) : S.q0 + 32u * (uint32_t)g;
-            const uint32_t end = R.t1[r] ? S.e : S.b;
-            const uint32_t k = base + (uint32_t)lane;
-            const bool in = g < m0 + m1 && k < end;
-            if (STAGED) {
-                const uint32_t x = sl.at(k - S.a);
-                R.cr[r] = in ? sl.cr[x] : 0u;
-                R.f[r] = in ? sl.f[x] : kSent;
-                R.v[r] = in ? sl.v[x] : 0.f;
-            } else {
-                R.cr[r] = in ? ld_stream(A.cr + k) : 0u;
-                R.f[r] = in ? ld_stream(A.fiber + k) : kSent;
-                R.v[r] = in ? ld_stream(A.val + k) : 0.f;
-            }
-        }
-    };
-    if (kEarlySlow) load_slow(0);
-    for (int g0 = 0; g0 < n0 + n1; g0 += kFastBlocks) {
-        VBlk B[kFastBlocks];
-        bool second[kFastBlocks];
-#pragma unroll
-        for (int j = 0; j < kFastBlocks; ++j) {
-            const int g = g0 + j;
-            second[j] = g >= n0;
-            const uint32_t base = second[j] ? S.b + 128u * (uint32_t)(g - n0) : S.a + 128u * (uint32_t)g;
-            const uint32_t end = second[j] ? S.q1 : S.q0;
-            const uint32_t k = base + 4u * (uint32_t)lane;
-            const bool ok = g < n0 + n1 && k < end;
-            if (STAGED) vb_lds(B[j], sl, k - S.a, ok);
-            else vb_ldg(B[j], A, k, ok);
-        }
-#pragma unroll
-        for (int j = 0; j < kFastBlocks; ++j) vb_gather(B[j], w);
-        if (kEarlySlow && g0 == 0) sr_gather(R, w);
-#pragma unroll
-        for (int j = 0; j < kFastBlocks; ++j) vb_assign(B[j], second[j] ? C1 : C0, zeros);
-    }
-    __syncwarp();
-    // rank>=1 windows, in order, after every rank-0 store
-    for (int r0 = 0; r0 < m0 + m1; r0 += kSlowRounds) {
-        if (r0 || !kEarlySlow || n0 + n1 == 0) {
-            load_slow(r0);
-            sr_gather(R, w);
-        }
-        sr_apply(R, C0, C1, zeros);
     }
     return zeros;
 }
@@ -470,6 +548,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 {
     extern __shared__ __align__(128) float sm[];
     __shared__ __align__(8) uint64_t full[2], empty[2], slotbar[kWsProd][2];
+    __shared__ float junkbuf[kWsProd * 32];
     if (hooks.done && *hooks.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
@@ -496,6 +575,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 
     if (warp < kWsCons) {
         // ===== consumers: register-tiled FFMA2 =====
+        if constexpr (kSplitRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegCons));
         const int vg = lane >> 3, dg = lane & 7;
         const bool accumulate = flags & LIFE_ACCUMULATE;
         const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
@@ -513,7 +593,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 for (int j = 0; j < DPL; ++j) acc[v][j] = 0ull;
             for (int c = 0; c < A.nch; ++c, ++k) {
                 const int s = k & 1;
+                WS_T0(t_f);
                 bar_wait(&full[s], (k >> 1) & 1);
+                if (lane == 0) WS_ACC(4, t_f);
+                WS_T0(t_c);
                 if (tile_ok && c_ws_isolate != 1) {
                     const float *C = Cbuf + (s * kWsCons + warp) * kWsCells + vg * 8;
                     const float *D = Dbuf + s * chunk_floats + dg * DPL;
@@ -538,6 +621,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     }
                 }
                 __syncwarp();
+                if (lane == 0) WS_ACC(5, t_c);
                 if (lane == 0) bar_arrive(&empty[s]);
             }
             if (tile_ok) {
@@ -567,52 +651,145 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             }
         }
     } else {
-        // ===== producers: TMA for D and the coefficient ranges, tile build =====
+        // ===== producers: TMA for D and the coefficient segments, tile build =====
+        if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProd));
         const int p = warp - kWsCons;
-        Seg2 cur{}, nxt{};
-        uint32_t off_cur = 0u, off_nxt = 0u;
-        if (total > 0) {
-            int ct, c;
-            step_of(0, A.nch, ct, c);
-            cur = seg2_of(A, ct, c, p);
-            if (STAGED && lane == 0) stage_issue(A, cur, slot_at(slots, p, 0u), &slotbar[p][0]);
-            off_nxt = ring_wrap(cur.e - cur.a);
-        }
-        if (total > 1) {
-            int ct, c;
-            step_of(1, A.nch, ct, c);
-            nxt = seg2_of(A, ct, c, p);
-            prefetch_range(A, nxt, lane);
-        }
-        for (int k = 0; k < total; ++k) {
-            const int s = k & 1;
-            int ct, c;
-            step_of(k, A.nch, ct, c);
-            Seg2 nn{};
-            if (k + 2 < total) {
-                int ct2, c2;
-                step_of(k + 2, A.nch, ct2, c2);
-                nn = seg2_of(A, ct2, c2, p);
+        // steps k (current), k+1, k+2, k+3 -- c fastest
+        int ct0 = blockIdx.x, c0 = 0, ct1 = ct0, c1 = 0, ct2, c2, ct3, c3;
+        step_next(ct1, c1, A.nch);
+        ct2 = ct1; c2 = c1;
+        step_next(ct2, c2, A.nch);
+        ct3 = ct2; c3 = c2;
+        step_next(ct3, c3, A.nch);
+        float *Cp = nullptr;
+        auto tiles = [&](int s) { return Cbuf + (s * kWsCons + kTPP * p) * kWsCells; };
+        auto junk_of = [&](int s) { return (int)(junkbuf + p * 32 + lane - tiles(s)); };
+        (void)Cp;
+        if constexpr (STAGED && !kCpAsyncGather) {
+            // segment k+1 is staged while step k builds; w gathered in registers
+            Seg cur{}, nxt{};
+            if (total > 0) {
+                cur = seg_of(A, ct0, c0, p);
+                if (lane == 0) stage_issue(A, cur, slots, p, 0, &slotbar[p][0]);
             }
-            // slot s^1 was last read in step k-1, which this warp finished
-            if (STAGED && k + 1 < total && lane == 0)
-                stage_issue(A, nxt, slot_at(slots, p, off_nxt), &slotbar[p][s ^ 1]);
-            if (k >= 2) bar_wait(&empty[s], ((k - 2) >> 1) & 1);
-            if (p == 0 && lane == 0)
-                tma_chunk(Dbuf + s * chunk_floats, A.D + (size_t)c * chunk_floats, chunk_bytes,
-                          &full[s]);
-            if (k + 2 < total) prefetch_range(A, nn, lane);
-            if (STAGED) bar_wait(&slotbar[p][s], (k >> 1) & 1);
-            if (c_ws_isolate != 2)
-                skipped += build_pair<STAGED>(Cbuf + (s * kWsCons + kTPP * p) * kWsCells,
-                                              Cbuf + (s * kWsCons + kTPP * p + 1) * kWsCells, A,
-                                              w, cur, slot_at(slots, p, off_cur), lane);
-            __syncwarp();
-            if (lane == 0) bar_arrive(&full[s]);
-            off_cur = off_nxt;
-            off_nxt = ring_wrap(off_nxt + (nxt.e - nxt.a));
-            cur = nxt;
-            nxt = nn;
+            if (total > 1) {
+                nxt = seg_of(A, ct1, c1, p);
+                prefetch_seg(A, nxt, lane);
+            }
+            for (int k = 0; k < total; ++k) {
+                const int s = k & 1;
+                Seg nn{};
+                if (k + 2 < total) nn = seg_of(A, ct2, c2, p);
+                if (k + 1 < total && lane == 0) stage_issue(A, nxt, slots, p, s ^ 1, &slotbar[p][s ^ 1]);
+                WS_T0(t_e);
+                if (k >= 2) bar_wait(&empty[s], ((k - 2) >> 1) & 1);
+                if (lane == 0) WS_ACC(1, t_e);
+                if (p == 0 && lane == 0)
+                    tma_chunk(Dbuf + s * chunk_floats, A.D + (size_t)c0 * chunk_floats,
+                              chunk_bytes, &full[s]);
+                if (k + 2 < total) prefetch_seg(A, nn, lane);
+                WS_T0(t_s);
+                bar_wait(&slotbar[p][s], (k >> 1) & 1);
+                if (lane == 0) WS_ACC(0, t_s);
+                WS_T0(t_b);
+                if (c_ws_isolate != 2)
+                    skipped += build_pair<true>(tiles(s), w, cur, slot_view(slots, p, s), junk_of(s),
+                                                lane);
+                __syncwarp();
+                if (lane == 0) WS_ACC(2, t_b);
+                if (lane == 0) bar_arrive(&full[s]);
+                cur = nxt;
+                nxt = nn;
+                ct0 = ct1; c0 = c1;
+                ct1 = ct2; c1 = c2;
+                ct2 = ct3; c2 = c3;
+                step_next(ct3, c3, A.nch);
+            }
+        } else if constexpr (STAGED) {
+            // segment k+1 is staged and its w gathered while step k builds;
+            // segment k+2 is copied into slot k%2 once step k is done with it
+            Seg cur{}, nxt{}, nn{};
+            if (total > 0) {
+                cur = seg_of(A, ct0, c0, p);
+                if (lane == 0) stage_issue(A, cur, slots, p, 0, &slotbar[p][0]);
+            }
+            if (total > 1) {
+                nxt = seg_of(A, ct1, c1, p);
+                if (lane == 0) stage_issue(A, nxt, slots, p, 1, &slotbar[p][1]);
+            }
+            if (total > 2) {
+                nn = seg_of(A, ct2, c2, p);
+                prefetch_seg(A, nn, lane);
+            }
+            if (total > 0) {
+                bar_wait(&slotbar[p][0], 0);
+                gather_to_slot(cur, slot_view(slots, p, 0), w, lane);
+            }
+            for (int k = 0; k < total; ++k) {
+                const int s = k & 1;
+                Seg n3{};
+                if (k + 3 < total) n3 = seg_of(A, ct3, c3, p);
+                WS_T0(t_e);
+                if (k >= 2) bar_wait(&empty[s], ((k - 2) >> 1) & 1);
+                if (lane == 0) WS_ACC(1, t_e);
+                if (p == 0 && lane == 0)
+                    tma_chunk(Dbuf + s * chunk_floats, A.D + (size_t)c0 * chunk_floats,
+                              chunk_bytes, &full[s]);
+                WS_T0(t_s);
+                cp_async_wait_all();
+                __syncwarp();
+                if (lane == 0) WS_ACC(0, t_s);
+                WS_T0(t_b);
+                const View V = slot_view(slots, p, s);
+                if (c_ws_isolate != 2) skipped += build_fast_staged(tiles(s), cur, V, junk_of(s), lane);
+                if (k + 1 < total) {
+                    bar_wait(&slotbar[p][s ^ 1], ((k + 1) >> 1) & 1);
+                    gather_to_slot(nxt, slot_view(slots, p, s ^ 1), w, lane);
+                }
+                if (c_ws_isolate != 2) skipped += build_slow_staged(tiles(s), cur, V, lane);
+                __syncwarp();
+                if (lane == 0) WS_ACC(2, t_b);
+                if (lane == 0) bar_arrive(&full[s]);
+                // slot s is free: stage segment k+2 into it
+                if (k + 2 < total && lane == 0) stage_issue(A, nn, slots, p, s, &slotbar[p][s]);
+                if (k + 3 < total) prefetch_seg(A, n3, lane);
+                cur = nxt;
+                nxt = nn;
+                nn = n3;
+                ct0 = ct1; c0 = c1;
+                ct1 = ct2; c1 = c2;
+                ct2 = ct3; c2 = c3;
+                step_next(ct3, c3, A.nch);
+            }
+        } else {
+            // fallback: segments straight from global memory, gathers in registers
+            Seg cur{}, nxt{};
+            if (total > 0) cur = seg_of(A, ct0, c0, p);
+            if (total > 1) {
+                nxt = seg_of(A, ct1, c1, p);
+                prefetch_seg(A, nxt, lane);
+            }
+            for (int k = 0; k < total; ++k) {
+                const int s = k & 1;
+                Seg nn{};
+                if (k + 2 < total) nn = seg_of(A, ct2, c2, p);
+                if (k >= 2) bar_wait(&empty[s], ((k - 2) >> 1) & 1);
+                if (p == 0 && lane == 0)
+                    tma_chunk(Dbuf + s * chunk_floats, A.D + (size_t)c0 * chunk_floats,
+                              chunk_bytes, &full[s]);
+                if (k + 2 < total) prefetch_seg(A, nn, lane);
+                if (c_ws_isolate != 2)
+                    skipped += build_pair<false>(tiles(s), w, cur, global_view(A, cur), junk_of(s),
+                                                 lane);
+                __syncwarp();
+                if (lane == 0) bar_arrive(&full[s]);
+                cur = nxt;
+                nxt = nn;
+                ct0 = ct1; c0 = c1;
+                ct1 = ct2; c1 = c2;
+                ct2 = ct3; c2 = c3;
+                step_next(ct3, c3, A.nch);
+            }
         }
     }
 
@@ -650,30 +827,63 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 // ---------------------------------------------------------------------------
 using WsFix = FixParams;
 
-// value * Z[cell] of 4 consecutive entries -> fixed-point fascicle sums
-__device__ __forceinline__ void wc_scatter4(const VBlk &B, const float *Z, const WsFix &fx,
-                                            bool f32_scale, float scalef, double scale)
+// value * Z[cell] -> fixed-point fascicle sum (pad entries skipped)
+__device__ __forceinline__ void wc_scatter1(uint32_t cr, uint32_t f, float v, const float *Z,
+                                            const WsFix &fx, bool f32_scale, float scalef,
+                                            double scale)
 {
-    const uint32_t f[4] = {B.f.x, B.f.y, B.f.z, B.f.w};
-    const uint32_t cr[4] = {B.cr.x, B.cr.y, B.cr.z, B.cr.w};
-    const float v[4] = {B.v.x, B.v.y, B.v.z, B.v.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        if (f[e] != kSent) {
-            const float z = Z[cr[e] & (kWsCells - 1)] * v[e];
-            const long long qv = f32_scale ? __float2ll_rn(z * scalef)
-                                           : __double2ll_rn((double)z * scale);
-            atomicAdd(fx.wfix + f[e], static_cast<unsigned long long>(qv));
-        }
+    if (cr & kPadBit) return;
+    const float z = Z[cr & kCellMask] * v;
+    const long long qv = f32_scale ? __float2ll_rn(z * scalef) : __double2ll_rn((double)z * scale);
+    red_keep(fx.wfix + f, static_cast<unsigned long long>(qv), policy_keep());
+}
+
+// ---- WC producers: 4 warps, each scattering two adjacent tiles per step ----
+// The per-tile segments of tiles 2p and 2p+1 are adjacent in the layout, so a
+// WC producer warp stages one contiguous range [p0, p1) with the boundary
+// between its tiles at q0 (reusing Seg; the rank split is irrelevant to WC).
+constexpr int kWcProd = 4;
+constexpr int kWcWarps = kWsCons + kWcProd;
+constexpr int kWcThreads = kWcWarps * 32;
+constexpr int kWcSlot = 2 * kWsSlot;
+static_assert(kWsProd == 8, "WC pairs up the per-tile segments of the 8-producer layout");
+
+__device__ __forceinline__ Seg wc_seg_of(const WsArgs &A, int ct, int c, int p)
+{
+    const size_t t = ((size_t)ct * A.nch + c) * kWsProd + 2 * p;
+    Seg S;
+    S.p0 = __ldg(A.tptr + t);
+    S.q0 = __ldg(A.tptr + t + 1);
+    S.p1 = __ldg(A.tptr + t + 2);
+    return S;
+}
+
+__device__ __forceinline__ View wc_slot_view(float *slots, int p, int s)
+{
+    uint32_t *base = reinterpret_cast<uint32_t *>(slots) + (size_t)(p * 2 + s) * 3 * kWcSlot;
+    return View{base, base + kWcSlot, reinterpret_cast<const float *>(base + 2 * kWcSlot)};
+}
+
+__device__ __forceinline__ void wc_stage_issue(const WsArgs &A, const Seg &S, float *slots, int p,
+                                               int s, uint64_t *bar)
+{
+    const unsigned n = S.p1 - S.p0, bytes = n * 4u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    bar_arrive_tx(bar, 3u * bytes);
+    if (n) {
+        const View D = wc_slot_view(slots, p, s);
+        bulk_g2s_stream((void *)D.cr, A.cr + S.p0, bytes, bar);
+        bulk_g2s_stream((void *)D.f, A.fiber + S.p0, bytes, bar);
+        bulk_g2s_stream((void *)D.v, A.val + S.p0, bytes, bar);
     }
 }
 
 template <int DPL, bool STAGED>
-__global__ void __launch_bounds__(kWsThreads, 1)
+__global__ void __launch_bounds__(kWcThreads, 1)
     k_wc_ws(const WsArgs A, const float *__restrict__ y, const WsFix fx, const CallHooks hooks)
 {
     extern __shared__ __align__(128) float sm[];
-    __shared__ __align__(8) uint64_t dfull[2], dempty[2], zfull[2], zempty[2], slotbar[kWsProd][2];
+    __shared__ __align__(8) uint64_t dfull[2], dempty[2], zfull[2], zempty[2], slotbar[kWcProd][2];
     if (hooks.done && *hooks.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
@@ -690,8 +900,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             bar_init(&dfull[s], 1);
             bar_init(&dempty[s], kWsCons);
             bar_init(&zfull[s], kWsCons);
-            bar_init(&zempty[s], kWsProd);
-            for (int p = 0; p < kWsProd; ++p) bar_init(&slotbar[p][s], 1);
+            bar_init(&zempty[s], kWcProd);
+            for (int p = 0; p < kWcProd; ++p) bar_init(&slotbar[p][s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -734,17 +944,20 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 if (tile_ok && c_ws_isolate != 1) {
                     float *Z = Zbuf + (s * kWsCons + warp) * kWsCells + vg * 8 + dg;
                     const float *D = Dbuf + s * chunk_floats + dg * DPL;
-#pragma unroll 2
-                    for (int a0 = 0; a0 < kWsCA; a0 += 2) {
-                        unsigned long long pp[2][4];
+#pragma unroll 1
+                    for (int a0 = 0; a0 < kWsCA; a0 += kWcAtoms) {
+                        // kWcAtoms independent accumulator sets keep the FMA
+                        // pipe fed while earlier butterflies are in flight
+                        unsigned long long pp[kWcAtoms][4];
 #pragma unroll
-                        for (int aa = 0; aa < 2; ++aa) {
-                            const float4 *d4 = reinterpret_cast<const float4 *>(D + (a0 + aa) * A.nt_pad);
+                        for (int aa = 0; aa < kWcAtoms; ++aa)
 #pragma unroll
                             for (int vp = 0; vp < 4; ++vp) pp[aa][vp] = 0ull;
 #pragma unroll
-                            for (int i = 0; i < DPL / 4; ++i) {
-                                const float4 t = d4[i];
+                        for (int i = 0; i < DPL / 4; ++i) {
+#pragma unroll
+                            for (int aa = 0; aa < kWcAtoms; ++aa) {
+                                const float4 t = reinterpret_cast<const float4 *>(D + (a0 + aa) * A.nt_pad)[i];
                                 const float dv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
                                 for (int e = 0; e < 4; ++e) {
@@ -755,7 +968,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                             }
                         }
 #pragma unroll
-                        for (int aa = 0; aa < 2; ++aa) {
+                        for (int aa = 0; aa < kWcAtoms; ++aa) {
                             float q[8];
 #pragma unroll
                             for (int vp = 0; vp < 4; ++vp) wupk(pp[aa][vp], q[2 * vp], q[2 * vp + 1]);
@@ -785,69 +998,75 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         const bool f32_scale = ex >= -120 && ex <= 120;
         const float scalef = f32_scale ? ldexpf(1.f, ex) : 1.f;
         if (p == 0 && lane == 0 && total > 0) tma_chunk(Dbuf, A.D, chunk_bytes, &dfull[0]);
-        Seg2 cur{}, nxt{};
-        uint32_t off_cur = 0u, off_nxt = 0u;
+        int ct0 = blockIdx.x, c0 = 0, ct1 = ct0, c1 = 0, ct2, c2;
+        step_next(ct1, c1, A.nch);
+        ct2 = ct1; c2 = c1;
+        step_next(ct2, c2, A.nch);
+        Seg cur{}, nxt{};
         if (total > 0) {
-            int ct, c;
-            step_of(0, A.nch, ct, c);
-            cur = seg2_of(A, ct, c, p);
-            if (STAGED && lane == 0) stage_issue(A, cur, slot_at(slots, p, 0u), &slotbar[p][0]);
-            off_nxt = ring_wrap(cur.e - cur.a);
+            cur = wc_seg_of(A, ct0, c0, p);
+            if (STAGED && lane == 0) wc_stage_issue(A, cur, slots, p, 0, &slotbar[p][0]);
         }
         if (total > 1) {
-            int ct, c;
-            step_of(1, A.nch, ct, c);
-            nxt = seg2_of(A, ct, c, p);
-            prefetch_range(A, nxt, lane);
+            nxt = wc_seg_of(A, ct1, c1, p);
+            prefetch_seg(A, nxt, lane);
         }
         for (int k = 0; k < total; ++k) {
             const int s = k & 1;
-            int ct, c;
-            step_of(k, A.nch, ct, c);
             if (p == 0 && lane == 0 && k + 1 < total) {
                 const int s1 = (k + 1) & 1;
                 if (k + 1 >= 2) bar_wait(&dempty[s1], ((k - 1) >> 1) & 1);
-                const int c1 = (c + 1) % A.nch;
                 tma_chunk(Dbuf + s1 * chunk_floats, A.D + (size_t)c1 * chunk_floats, chunk_bytes,
                           &dfull[s1]);
             }
             __syncwarp();
-            Seg2 nn{};
-            if (k + 2 < total) {
-                int ct2, c2;
-                step_of(k + 2, A.nch, ct2, c2);
-                nn = seg2_of(A, ct2, c2, p);
-            }
+            Seg nn{};
+            if (k + 2 < total) nn = wc_seg_of(A, ct2, c2, p);
             if (STAGED && k + 1 < total && lane == 0)
-                stage_issue(A, nxt, slot_at(slots, p, off_nxt), &slotbar[p][s ^ 1]);
-            if (k + 2 < total) prefetch_range(A, nn, lane);
-            const Slot sl = slot_at(slots, p, off_cur);
+                wc_stage_issue(A, nxt, slots, p, s ^ 1, &slotbar[p][s ^ 1]);
+            if (k + 2 < total) prefetch_seg(A, nn, lane);
             if (STAGED) bar_wait(&slotbar[p][s], (k >> 1) & 1);
             bar_wait(&zfull[s], (k >> 1) & 1);
-            const float *Z0 = Zbuf + (s * kWsCons + kTPP * p) * kWsCells;
-            // the pair's range [a, e) in 128-entry blocks; tile 1 starts at b
-            // (a 4-aligned boundary, so no 4-entry group straddles it)
+            const float *Z = Zbuf + (s * kWsCons + 2 * p) * kWsCells;
+            const View V = STAGED ? wc_slot_view(slots, p, s) : global_view(A, cur);
+            const uint32_t mid = cur.q0 - cur.p0;  // tile 2p+1 starts here
+            const uint32_t n = (c_ws_isolate == 2) ? 0u : cur.p1 - cur.p0;
+            // 4 entries per lane, 4 blocks of 128 per round: loads first
             constexpr int kB = 4;
-            for (uint32_t base = cur.a; base < (c_ws_isolate == 2 ? cur.a : cur.e); base += 128u * kB) {
-                VBlk B[kB];
+            for (uint32_t base = 0; base < n; base += 128u * kB) {
+                uint4 cr[kB], f[kB];
+                float4 v[kB];
 #pragma unroll
                 for (int j = 0; j < kB; ++j) {
                     const uint32_t kk = base + 128u * j + 4u * (uint32_t)lane;
-                    if (STAGED) vb_lds(B[j], sl, kk - cur.a, kk < cur.e);
-                    else vb_ldg(B[j], A, kk, kk < cur.e);
+                    if (kk < n) {
+                        cr[j] = ldv<STAGED>(reinterpret_cast<const uint4 *>(V.cr + kk));
+                        f[j] = ldv<STAGED>(reinterpret_cast<const uint4 *>(V.f + kk));
+                        v[j] = ldv<STAGED>(reinterpret_cast<const float4 *>(V.v + kk));
+                    } else {
+                        cr[j] = make_uint4(kPadBit, kPadBit, kPadBit, kPadBit);
+                        f[j] = make_uint4(0u, 0u, 0u, 0u);
+                        v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < kB; ++j) {
+                    // a 4-entry group never straddles the 4-aligned tile boundary
                     const uint32_t kk = base + 128u * j + 4u * (uint32_t)lane;
-                    wc_scatter4(B[j], kk < cur.b ? Z0 : Z0 + kWsCells, fx, f32_scale, scalef, scale);
+                    const float *Zt = Z + (kk >= mid ? kWsCells : 0);
+                    wc_scatter1(cr[j].x, f[j].x, v[j].x, Zt, fx, f32_scale, scalef, scale);
+                    wc_scatter1(cr[j].y, f[j].y, v[j].y, Zt, fx, f32_scale, scalef, scale);
+                    wc_scatter1(cr[j].z, f[j].z, v[j].z, Zt, fx, f32_scale, scalef, scale);
+                    wc_scatter1(cr[j].w, f[j].w, v[j].w, Zt, fx, f32_scale, scalef, scale);
                 }
             }
             __syncwarp();
             if (lane == 0) bar_arrive(&zempty[s]);
-            off_cur = off_nxt;
-            off_nxt = ring_wrap(off_nxt + (nxt.e - nxt.a));
             cur = nxt;
             nxt = nn;
+            ct0 = ct1; c0 = c1;
+            ct1 = ct2; c1 = c2;
+            step_next(ct2, c2, A.nch);
         }
     }
 }
@@ -875,7 +1094,7 @@ static int ws_wc_t(life_phi *phi, const FixParams &fx, const float *y, const Cal
     LIFE_TRY(ensure_smem(k_wc_ws<DPL, STAGED>, phi->d_smem));
     WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_t1, phi->d_D,
              phi->d_slotv, phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
-    k_wc_ws<DPL, STAGED><<<phi->d_blocks, kWsThreads, phi->d_smem, st>>>(A, y, fx, h);
+    k_wc_ws<DPL, STAGED><<<phi->d_blocks, kWcThreads, phi->d_smem, st>>>(A, y, fx, h);
     LIFE_CHECK_LAUNCH();
     return LIFE_OK;
 }
@@ -922,18 +1141,28 @@ extern "C" LIFE_API int life_debug_ws_isolate(int mode)
     if (cudaMemcpyToSymbol(life::c_ws_isolate, &iso, sizeof(int)) != cudaSuccess) return 20;
     return cudaMemcpyToSymbol(life::c_ws_flags, &fl, sizeof(int)) == cudaSuccess ? 0 : 20;
 }
+
+// read and clear the cycle counters (8 x u64)
+extern "C" LIFE_API int life_debug_ws_counters(unsigned long long *out)
+{
+    if (cudaDeviceSynchronize() != cudaSuccess) return 20;
+    if (cudaMemcpyFromSymbol(out, life::g_ws_cyc, 8 * sizeof(unsigned long long)) != cudaSuccess) return 20;
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    return cudaMemcpyToSymbol(life::g_ws_cyc, z, sizeof(z)) == cudaSuccess ? 0 : 20;
+}
 #endif
 
 namespace life {
 
 int ws_warps() { return kWsWarps; }
 int ws_chunk_atoms() { return kWsCA; }
-int ws_ring_entries() { return kWsRing; }
+int ws_slot_entries() { return kWsSlot; }
+int ws_producers() { return kWsProd; }
 
 size_t ws_smem_bytes(int nt_pad, bool staged)
 {
     size_t b = ((size_t)2 * kWsCA * nt_pad + (size_t)2 * kWsCons * kWsCells) * sizeof(float);
-    if (staged) b += (size_t)kWsProd * 3 * kWsRing * 4;
+    if (staged) b += (size_t)kWsProd * 2 * 3 * kWsSlot * 4;
     return b;
 }
 

@@ -30,4 +30,17 @@ for name, fn in (("dsc", lambda: op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absma
         for _ in range(10): fn()
         e1.record(); torch.cuda.synchronize()
         print(f"mrl={args.mrl} {name} mode {mode:#x} ms {e0.elapsed_time(e1) / 10:.4f}", flush=True)
+# per-phase cycle counters of one DSC (sums over producer / consumer warps)
+nprod, ncons = 148 * int(os.environ.get("WS_PROD", "4")), 148 * 8
+for mode in (0, 1, 1 | (4 << 8)):
+    lib.life_debug_ws_isolate(mode)
+    cyc = (ctypes.c_ulonglong * 8)()
+    lib.life_debug_ws_counters(cyc)
+    op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absmax=ym)
+    lib.life_debug_ws_counters(cyc)
+    c = list(cyc)
+    print(f"mode {mode:#x} per producer warp (Mcyc): slot wait {c[0]/nprod/1e6:.3f} "
+          f"empty wait {c[1]/nprod/1e6:.3f} build {c[2]/nprod/1e6:.3f} (fast {c[6]/nprod/1e6:.3f} "
+          f"slow {c[7]/nprod/1e6:.3f}); per consumer warp: full wait {c[4]/ncons/1e6:.3f} "
+          f"compute {c[5]/ncons/1e6:.3f}", flush=True)
 lib.life_debug_ws_isolate(0)
