@@ -138,15 +138,26 @@ __device__ __forceinline__ void bar_arrive_tx(uint64_t *b, unsigned bytes)
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ bool bar_try(uint64_t *b, unsigned parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smaddr(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// A wait that has not completed after 4 s of device time is a protocol
+// deadlock: trap (the launch fails with an error) instead of hanging the GPU.
 __device__ __forceinline__ void bar_wait(uint64_t *b, unsigned parity)
 {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WSW_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WSW_%=;\n}" ::"r"(smaddr(b)),
-        "r"(parity)
-        : "memory");
+    if (bar_try(b, parity)) return;
+    const unsigned long long t0 = globaltimer();
+    while (!bar_try(b, parity))
+        if (globaltimer() - t0 > 4000000000ull) __trap();
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *b)
 {
@@ -268,12 +279,32 @@ __device__ __forceinline__ Seg seg_of(const WsArgs &A, int ct, int c, int p)
     return S;
 }
 
-// the CTA's steps in order: (ct, c), c fastest
-__device__ __forceinline__ void step_next(int &ct, int &c, int nch)
+// WC's balanced schedule: the n_ct * nch steps (ct, c), c fastest, are cut
+// into gridDim.x contiguous ranges of equal length, so every CTA does the
+// same number of steps (a round robin of whole CTA tiles leaves the last of
+// 5.28 rounds 72% idle at C2).  WC has no state across chunks (Z is per chunk
+// and the fascicle sums are integer), so a CTA tile may be split anywhere.
+__device__ __forceinline__ void step_range(int n_ct, int nch, int &s0, int &s1)
+{
+    const long long total = (long long)n_ct * nch;
+    s0 = (int)(total * blockIdx.x / gridDim.x);
+    s1 = (int)(total * (blockIdx.x + 1) / gridDim.x);
+}
+
+// DSC: whole CTA tiles round robin over the grid
+__device__ __forceinline__ void step_next_rr(int &ct, int &c, int nch)
 {
     if (++c == nch) {
         c = 0;
         ct += gridDim.x;
+    }
+}
+
+__device__ __forceinline__ void step_next(int &ct, int &c, int nch)
+{
+    if (++c == nch) {
+        c = 0;
+        ++ct;
     }
 }
 
@@ -558,6 +589,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     float *Cbuf = sm + 2 * chunk_floats;
     float *slots = Cbuf + 2 * kWsCons * kWsCells;
     const int n_ct = (A.n_tiles + kWsCons - 1) / kWsCons;
+    // DSC keeps whole CTA tiles per CTA (round robin): a voxel's chunks are
+    // then always summed in one FMA chain, so results do not depend on the
+    // grid or on multi-GPU sharding (bitwise)
     const int my_ct = (int)blockIdx.x < n_ct ? (n_ct - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int total = my_ct * A.nch;
     if (threadIdx.x == 0) {
@@ -581,6 +615,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
         int k = 0;
         for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
+            const int cb = 0, ce = A.nch;
             const int wt = ct * kWsCons + warp;
             const bool tile_ok = wt < A.n_tiles;
             // acc[vp][t] = (y[2vp][t], y[2vp+1][t]): pairs across voxels so
@@ -591,7 +626,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             for (int v = 0; v < 4; ++v)
 #pragma unroll
                 for (int j = 0; j < DPL; ++j) acc[v][j] = 0ull;
-            for (int c = 0; c < A.nch; ++c, ++k) {
+            for (int c = cb; c < ce; ++c, ++k) {
                 const int s = k & 1;
                 WS_T0(t_f);
                 bar_wait(&full[s], (k >> 1) & 1);
@@ -624,7 +659,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 if (lane == 0) WS_ACC(5, t_c);
                 if (lane == 0) bar_arrive(&empty[s]);
             }
-            if (tile_ok) {
+            // y epilogue over a value source get(vp, j) -> (voxel 2vp, 2vp+1) pair
+            auto epilogue = [&](auto get) {
 #pragma unroll
                 for (int vp = 0; vp < 4; ++vp) {
 #pragma unroll
@@ -635,7 +671,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 #pragma unroll
                         for (int j = 0; j < DPL; ++j) {
                             float o[2];
-                            wupk(acc[vp][j], o[0], o[1]);
+                            wupk(get(vp, j), o[0], o[1]);
                             const int t = dg * DPL + j;
                             if (t < A.nt) {
                                 float r = o[h];
@@ -648,19 +684,20 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                         }
                     }
                 }
-            }
+            };
+            if (tile_ok) epilogue([&](int vp, int j) { return acc[vp][j]; });
         }
     } else {
         // ===== producers: TMA for D and the coefficient segments, tile build =====
         if constexpr (kSplitRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProd));
         const int p = warp - kWsCons;
         // steps k (current), k+1, k+2, k+3 -- c fastest
-        int ct0 = blockIdx.x, c0 = 0, ct1 = ct0, c1 = 0, ct2, c2, ct3, c3;
-        step_next(ct1, c1, A.nch);
+        int ct0 = blockIdx.x, c0 = 0, ct1 = ct0, c1 = c0, ct2, c2, ct3, c3;
+        step_next_rr(ct1, c1, A.nch);
         ct2 = ct1; c2 = c1;
-        step_next(ct2, c2, A.nch);
+        step_next_rr(ct2, c2, A.nch);
         ct3 = ct2; c3 = c2;
-        step_next(ct3, c3, A.nch);
+        step_next_rr(ct3, c3, A.nch);
         float *Cp = nullptr;
         auto tiles = [&](int s) { return Cbuf + (s * kWsCons + kTPP * p) * kWsCells; };
         auto junk_of = [&](int s) { return (int)(junkbuf + p * 32 + lane - tiles(s)); };
@@ -703,7 +740,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 ct0 = ct1; c0 = c1;
                 ct1 = ct2; c1 = c2;
                 ct2 = ct3; c2 = c3;
-                step_next(ct3, c3, A.nch);
+                step_next_rr(ct3, c3, A.nch);
             }
         } else if constexpr (STAGED) {
             // segment k+1 is staged and its w gathered while step k builds;
@@ -759,7 +796,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 ct0 = ct1; c0 = c1;
                 ct1 = ct2; c1 = c2;
                 ct2 = ct3; c2 = c3;
-                step_next(ct3, c3, A.nch);
+                step_next_rr(ct3, c3, A.nch);
             }
         } else {
             // fallback: segments straight from global memory, gathers in registers
@@ -788,7 +825,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 ct0 = ct1; c0 = c1;
                 ct1 = ct2; c1 = c2;
                 ct2 = ct3; c2 = c3;
-                step_next(ct3, c3, A.nch);
+                step_next_rr(ct3, c3, A.nch);
             }
         }
     }
@@ -893,8 +930,9 @@ __global__ void __launch_bounds__(kWcThreads, 1)
     float *Zbuf = sm + 2 * chunk_floats;
     float *slots = Zbuf + 2 * kWsCons * kWsCells;
     const int n_ct = (A.n_tiles + kWsCons - 1) / kWsCons;
-    const int my_ct = (int)blockIdx.x < n_ct ? (n_ct - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    const int total = my_ct * A.nch;
+    int s_begin, s_end;
+    step_range(n_ct, A.nch, s_begin, s_end);
+    const int total = s_end - s_begin;
     if (threadIdx.x == 0) {
         for (int s = 0; s < 2; ++s) {
             bar_init(&dfull[s], 1);
@@ -916,7 +954,10 @@ __global__ void __launch_bounds__(kWcThreads, 1)
         // voxel vg*8 + dg, summed over all 96 directions.
         const int vg = lane >> 3, dg = lane & 7;
         int k = 0;
-        for (int ct = blockIdx.x; ct < n_ct; ct += gridDim.x) {
+        for (int st = s_begin; st < s_end;) {
+            const int ct = st / A.nch, cb = st % A.nch;
+            const int ce = min(A.nch, cb + (s_end - st));
+            st += ce - cb;
             const int wt = ct * kWsCons + warp;
             const bool tile_ok = wt < A.n_tiles;
             unsigned long long yv[4][DPL];  // (slot 2vp, slot 2vp+1) per direction
@@ -937,7 +978,7 @@ __global__ void __launch_bounds__(kWcThreads, 1)
 #pragma unroll
                 for (int j = 0; j < DPL; ++j) yv[vp][j] = wpk(e[0][j], e[1][j]);
             }
-            for (int c = 0; c < A.nch; ++c, ++k) {
+            for (int c = cb; c < ce; ++c, ++k) {
                 const int s = k & 1;
                 bar_wait(&dfull[s], (k >> 1) & 1);
                 if (k >= 2) bar_wait(&zempty[s], ((k - 2) >> 1) & 1);
@@ -997,8 +1038,9 @@ __global__ void __launch_bounds__(kWcThreads, 1)
         // stays in range, so the fixed-point term needs no fp64 arithmetic
         const bool f32_scale = ex >= -120 && ex <= 120;
         const float scalef = f32_scale ? ldexpf(1.f, ex) : 1.f;
-        if (p == 0 && lane == 0 && total > 0) tma_chunk(Dbuf, A.D, chunk_bytes, &dfull[0]);
-        int ct0 = blockIdx.x, c0 = 0, ct1 = ct0, c1 = 0, ct2, c2;
+        int ct0 = s_begin / A.nch, c0 = s_begin % A.nch, ct1 = ct0, c1 = c0, ct2, c2;
+        if (p == 0 && lane == 0 && total > 0)
+            tma_chunk(Dbuf, A.D + (size_t)c0 * chunk_floats, chunk_bytes, &dfull[0]);
         step_next(ct1, c1, A.nch);
         ct2 = ct1; c2 = c1;
         step_next(ct2, c2, A.nch);
