@@ -143,11 +143,13 @@ def cpu_reference(dims, iters_lo=1, iters_hi=5, threads=None):
     sd = sample_dims(dims)
     p = O.generate(sd, max(1.0, 1.04 * sd[4] / sd[1]), 0.5, 0.1, 0)
     t0 = time.perf_counter()
-    O.solve(p, max_iters=iters_lo, grad_tol=0.0, threads=threads)
+    _, tr1 = O.solve(p, max_iters=iters_lo, grad_tol=0.0, threads=threads)
     t1 = time.perf_counter()
-    O.solve(p, max_iters=iters_hi, grad_tol=0.0, threads=threads)
+    _, tr2 = O.solve(p, max_iters=iters_hi, grad_tol=0.0, threads=threads)
     t2 = time.perf_counter()
-    per_iter = ((t2 - t1) - (t1 - t0)) / (iters_hi - iters_lo)
+    # iterations actually run (a solve may stop early on a degenerate step)
+    n_it = max(1, len(tr2["records"]) - len(tr1["records"]))
+    per_iter = ((t2 - t1) - (t1 - t0)) / n_it
     scale = sd[4] / dims[4]
     return {"value": scale / per_iter, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": (f"oracle port of sbbnnls.solve, Nc={sd[4]} (Na={sd[0]} Nv={sd[1]} "
@@ -168,11 +170,14 @@ def run_reference(args, dims):
     # each step: one oracle SBBNNLS iteration on the sample; differencing
     # solves of W and W+K iterations isolates exactly K iterations
     t0 = time.perf_counter()
-    O.solve(p, max_iters=max(1, args.warmup), grad_tol=0.0, threads=threads)
+    _, tr1 = O.solve(p, max_iters=max(1, args.warmup), grad_tol=0.0, threads=threads)
     t1 = time.perf_counter()
-    O.solve(p, max_iters=max(1, args.warmup) + args.steps, grad_tol=0.0, threads=threads)
+    _, tr2 = O.solve(p, max_iters=max(1, args.warmup) + args.steps, grad_tol=0.0,
+                     threads=threads)
     t2 = time.perf_counter()
-    per_iter = ((t2 - t1) - (t1 - t0)) / args.steps
+    # iterations actually run (a solve may stop early on a degenerate step)
+    n_it = max(1, len(tr2["records"]) - len(tr1["records"]))
+    per_iter = ((t2 - t1) - (t1 - t0)) / n_it
     scale = sd[4] / dims[4]
     value = scale / per_iter
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
@@ -375,8 +380,8 @@ def run_ours(args, dims):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
