@@ -88,6 +88,7 @@ LIFE_API uint64_t life_launch_count(void);
 #define LIFE_PHI_NO_FAST_F32  0x4u  /* skip the fp32 fast layout           */
 #define LIFE_PHI_FORCE_SPARSE 0x8u  /* fp32: voxel-segment kernels only    */
 #define LIFE_PHI_FORCE_DENSE  0x10u /* fp32: register-tiled dense kernels  */
+#define LIFE_PHI_NO_TENSOR    0x20u /* fp32: no tcgen05 (tensor-core) DSC   */
 
 /* Build the device operator from COO arrays (PhiTensor + Dictionary,
  * tensor.py:76-170).  atoms/voxels/fibers: u32[n_coeffs]; values:
@@ -105,7 +106,7 @@ LIFE_API int life_phi_destroy(life_phi *phi);
 
 typedef struct life_phi_info {
     life_dims dims;
-    int32_t atom_groups;        /* sparse kernels: passes over Phi (D slices); 0 = dense */
+    int32_t atom_groups;        /* sparse kernels: passes over Phi (D slices); 0 = dense, -1 = dense + tcgen05 DSC */
     int32_t atoms_per_group;
     int32_t n_warps;            /* persistent warps of the SpMV kernels   */
     int32_t has_exact;          /* fp64 bit-exact layout present          */

@@ -23,6 +23,7 @@ PHI_EXACT_F64 = 0x2
 PHI_NO_FAST_F32 = 0x4
 PHI_FORCE_SPARSE = 0x8
 PHI_FORCE_DENSE = 0x10
+PHI_NO_TENSOR = 0x20
 ACCUMULATE = 0x01
 SKIP_ZERO = 0x02
 SUBTRACT_B = 0x04

@@ -116,6 +116,23 @@ struct life_phi {
     int *d_slotv = nullptr;       // ws layout: voxel of each tile slot, -1 = padding
     size_t d_smem = 0;
 
+    // tensor-core tile layout (life_tc.cu): coefficients sorted by (CTA tile of
+    // 128 voxels, atom chunk of 32, producer warp = 16-voxel row block, rank,
+    // cell); cell = fp32 index of (row, atom) in the K-major SWIZZLE_128B
+    // A tile the tcgen05 MMA reads.
+    bool has_tc = false;
+    uint32_t *t_cr = nullptr;     // mixed << 31 | pad << 30 | rank << 12 | cell
+    uint32_t *t_fiber = nullptr;
+    float *t_val = nullptr;
+    uint32_t *t_tptr = nullptr;   // [n_ct*nch*8 + 1] padded segment starts
+    uint32_t *t_t1 = nullptr;     // start of each segment's rank>=1 region
+    uint32_t *t_vslot = nullptr;  // tile slot of each voxel
+    int *t_slotv = nullptr;       // voxel of each tile slot, -1 = padding
+    float *t_D = nullptr;         // [nch][hi|lo][N rows][32] swizzled tf32 split of D^T
+    int t_nct = 0, t_nch = 0, t_n = 0, t_blocks = 0, t_W = 0;
+    int64_t t_npad = 0, t_maxseg = 0;
+    size_t t_smem = 0;
+
     // fixed-point WC accumulator and its scale inputs
     unsigned long long *wfix = nullptr;  // [nf] two's-complement int64
     double vmax = 0.0;                   // max |value|
@@ -225,4 +242,14 @@ int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
 int prepare_spmv(life_phi *phi);
 int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
                 const double *val, const std::vector<double> &hdict, cudaStream_t st);
+int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
+             const double *val, const std::vector<double> &hdict, cudaStream_t st);
+int launch_dsc_tc(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
+                  const DscOut &o, const CallHooks &h, cudaStream_t st);
+int prepare_tc(life_phi *phi);
+// tcgen05 path geometry (life_tc.cu)
+constexpr int kTcTV = 128;       // voxels per CTA tile (MMA M)
+constexpr int kTcCA = 32;        // atoms per chunk (one 128-byte swizzle row of fp32)
+constexpr int kTcProd = 8;       // producer warps, 16 voxel rows each
+constexpr int kTcCellBits = 12;  // cell = fp32 index in the 128 x 32 A tile
 }  // namespace life

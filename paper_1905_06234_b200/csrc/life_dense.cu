@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "life_common.cuh"
@@ -519,6 +520,30 @@ __global__ void k_ws_key1(const uint32_t *a, const uint32_t *v, const uint32_t *
     }
 }
 
+// tensor-core layout (life_tc.cu): 16-voxel row blocks, 8 per CTA tile of 128
+// voxels; segment = (CTA tile, atom chunk of 32, row block); cell = fp32 index
+// of (row, atom) in the K-major SWIZZLE_128B A tile (8-row groups of 1024 B,
+// 16-byte units XOR-swizzled by row % 8)
+__host__ __device__ __forceinline__ uint32_t tc_cell(uint32_t row, uint32_t k)
+{
+    return (row >> 3) * 256u + (row & 7u) * 32u + ((((k >> 2) ^ row) & 7u) << 2) + (k & 3u);
+}
+
+__global__ void k_tc_key1(const uint32_t *a, const uint32_t *v, const uint32_t *vslot, int64_t n,
+                          int nch, unsigned long long *key, uint32_t *iota)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t at = a[i], slot = vslot[v[i]];
+        const uint32_t blk = slot / 16u;  // row block of 16 voxels
+        const unsigned long long seg =
+            ((unsigned long long)(blk / 8u) * nch + at / (uint32_t)kTcCA) * 8u + blk % 8u;
+        const uint32_t cell = tc_cell(slot % (uint32_t)kTcTV, at % (uint32_t)kTcCA);
+        key[i] = (seg << kTcCellBits) | cell;
+        iota[i] = (uint32_t)i;
+    }
+}
+
 // rank = position within the run of equal keys;
 // key2 = tc<<32 | rank<<cell_bits | cell
 __global__ void k_dense_key2(const unsigned long long *sk, int64_t n, int cell_bits,
@@ -869,6 +894,176 @@ int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint3
         phi->d_W = phi->d_blocks * kDenseWarps;
     }
     phi->has_dense = true;
+    return LIFE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// tensor-core layout (life_tc.cu)
+// ---------------------------------------------------------------------------
+static void tf32_split(float x, float &hi, float &lo)
+{
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u &= 0xFFFFE000u;
+    std::memcpy(&hi, &u, 4);
+    lo = x - hi;
+}
+
+int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
+             const double *val, const std::vector<double> &hdict, cudaStream_t st)
+{
+    const int64_t n = phi->nc;
+    const int N = (phi->nt + 31) / 32 * 32;  // MMA N: directions padded to 32
+    if (n == 0 || N > 128) return LIFE_OK;
+    const int nch = (phi->na + kTcCA - 1) / kTcCA;
+    const int64_t nblk = ((int64_t)phi->nv + 15) / 16;   // 16-voxel row blocks
+    const int64_t n_ct = (nblk + 7) / 8;                 // CTA tiles of 128 voxels
+    const int64_t ntc = n_ct * nch * kTcProd;            // segments
+    if (ntc >= (1ll << 31)) return LIFE_OK;
+    // Load balance: voxels sorted by coefficient count are dealt to the row
+    // blocks in snake order, so every producer warp's segment carries about
+    // the same number of coefficients.
+    std::vector<uint32_t> vslot(phi->nv);
+    const int64_t nslots = n_ct * kTcTV;
+    std::vector<int> slotv(nslots, -1);
+    {
+        unsigned *cnt = nullptr;
+        LIFE_CUDA(cudaMallocAsync(&cnt, (size_t)phi->nv * 4, st));
+        LIFE_CUDA(cudaMemsetAsync(cnt, 0, (size_t)phi->nv * 4, st));
+        k_voxel_hist<<<gridn(n), 256, 0, st>>>(v, n, cnt);
+        LIFE_CHECK_LAUNCH();
+        std::vector<unsigned> hc(phi->nv);
+        LIFE_CUDA(cudaMemcpyAsync(hc.data(), cnt, (size_t)phi->nv * 4, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        LIFE_CUDA(cudaFreeAsync(cnt, st));
+        std::vector<uint32_t> order(phi->nv);
+        for (int i = 0; i < phi->nv; ++i) order[i] = (uint32_t)i;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](uint32_t x, uint32_t y) { return hc[x] > hc[y]; });
+        for (int64_t i = 0; i < phi->nv; ++i) {
+            const int64_t r = i / nblk, q = i % nblk, blk = (r & 1) ? nblk - 1 - q : q;
+            const int64_t slot = blk * 16 + r;
+            vslot[order[i]] = (uint32_t)slot;
+            slotv[slot] = (int)order[i];
+        }
+    }
+    LIFE_TRY(dalloc(phi, &phi->t_vslot, (size_t)phi->nv));
+    LIFE_TRY(dalloc(phi, &phi->t_slotv, (size_t)nslots));
+    LIFE_CUDA(cudaMemcpyAsync(phi->t_vslot, vslot.data(), (size_t)phi->nv * 4, cudaMemcpyHostToDevice, st));
+    LIFE_CUDA(cudaMemcpyAsync(phi->t_slotv, slotv.data(), (size_t)nslots * 4, cudaMemcpyHostToDevice, st));
+    unsigned long long *k1 = nullptr, *sk1 = nullptr, *k2 = nullptr, *sk2 = nullptr;
+    uint32_t *iota = nullptr, *perm1 = nullptr, *perm = nullptr;
+    unsigned *mr = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&k1, n * 8, st));
+    LIFE_CUDA(cudaMallocAsync(&sk1, n * 8, st));
+    LIFE_CUDA(cudaMallocAsync(&iota, n * 4, st));
+    LIFE_CUDA(cudaMallocAsync(&perm1, n * 4, st));
+    LIFE_CUDA(cudaMallocAsync(&mr, 4, st));
+    LIFE_CUDA(cudaMemsetAsync(mr, 0, 4, st));
+    k_tc_key1<<<gridn(n), 256, 0, st>>>(a, v, phi->t_vslot, n, nch, k1, iota);
+    LIFE_CHECK_LAUNCH();
+    LIFE_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    int bits_tc = 1;
+    while (bits_tc < 40 && (ntc >> bits_tc) != 0) ++bits_tc;
+    size_t tb = 0;
+    void *temp = nullptr;
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, sk1, iota, perm1, n, 0, kTcCellBits + bits_tc, st));
+    LIFE_CUDA(cudaMallocAsync(&temp, tb, st));
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, k1, sk1, iota, perm1, n, 0, kTcCellBits + bits_tc, st));
+    LIFE_CUDA(cudaFreeAsync(temp, st));
+    g_launches.fetch_add(4, std::memory_order_relaxed);
+    LIFE_CUDA(cudaFreeAsync(k1, st));
+    LIFE_CUDA(cudaFreeAsync(iota, st));
+    LIFE_CUDA(cudaMallocAsync(&k2, n * 8, st));
+    k_dense_key2<<<gridn(n), 256, 0, st>>>(sk1, n, kTcCellBits, k2, mr);
+    LIFE_CHECK_LAUNCH();
+    unsigned hmr = 0;
+    LIFE_CUDA(cudaMemcpyAsync(&hmr, mr, 4, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    LIFE_CUDA(cudaFreeAsync(sk1, st));
+    if (hmr >= (1u << (30 - kTcCellBits))) {  // pathological duplicate counts
+        cudaFreeAsync(perm1, st); cudaFreeAsync(k2, st); cudaFreeAsync(mr, st);
+        return LIFE_OK;
+    }
+    LIFE_CUDA(cudaMallocAsync(&sk2, n * 8, st));
+    LIFE_CUDA(cudaMallocAsync(&perm, n * 4, st));
+    tb = 0;
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k2, sk2, perm1, perm, n, 0, 32 + bits_tc, st));
+    LIFE_CUDA(cudaMallocAsync(&temp, tb, st));
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, k2, sk2, perm1, perm, n, 0, 32 + bits_tc, st));
+    LIFE_CUDA(cudaFreeAsync(temp, st));
+    g_launches.fetch_add(4, std::memory_order_relaxed);
+    LIFE_CUDA(cudaFreeAsync(k2, st));
+    LIFE_CUDA(cudaFreeAsync(perm1, st));
+    uint32_t *s0 = nullptr, *s1 = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&s0, (ntc + 1) * 4, st));
+    LIFE_CUDA(cudaMallocAsync(&s1, (ntc + 1) * 4, st));
+    k_ws_bounds<<<gridn(ntc + 1), 256, 0, st>>>(sk2, n, ntc, kTcCellBits, s0, s1);
+    LIFE_CHECK_LAUNCH();
+    std::vector<uint32_t> h0(ntc + 1), h1(ntc + 1), hP(ntc + 1), hT(ntc + 1);
+    LIFE_CUDA(cudaMemcpyAsync(h0.data(), s0, (ntc + 1) * 4, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaMemcpyAsync(h1.data(), s1, (ntc + 1) * 4, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    // rank-0 and rank>=1 regions each padded to 4 entries (16-byte vectors)
+    int64_t pos = 0, maxseg = 0;
+    for (int64_t t = 0; t < ntc; ++t) {
+        const int64_t n0 = (int64_t)h1[t] - h0[t], n1 = (int64_t)h0[t + 1] - h1[t];
+        hP[t] = (uint32_t)pos;
+        hT[t] = (uint32_t)(pos + (n0 + 3) / 4 * 4);
+        const int64_t len = (n0 + 3) / 4 * 4 + (n1 + 3) / 4 * 4;
+        maxseg = std::max(maxseg, len);
+        pos += len;
+    }
+    hP[ntc] = hT[ntc] = (uint32_t)pos;
+    if (pos >= 0xFFFFFFFFll) return fail(LIFE_ERR_CONFIG_INVALID, "padded layout exceeds u32");
+    const int64_t npad = std::max<int64_t>(pos, 1);
+    LIFE_TRY(dalloc(phi, &phi->t_cr, npad));
+    LIFE_TRY(dalloc(phi, &phi->t_fiber, npad));
+    LIFE_TRY(dalloc(phi, &phi->t_val, npad));
+    LIFE_TRY(dalloc(phi, &phi->t_tptr, ntc + 1));
+    LIFE_TRY(dalloc(phi, &phi->t_t1, ntc + 1));
+    LIFE_CUDA(cudaMemsetAsync(phi->t_cr, 0x40, npad * 4, st));     // pad bit 30
+    LIFE_CUDA(cudaMemsetAsync(phi->t_fiber, 0xFF, npad * 4, st));  // sentinel fascicle
+    LIFE_CUDA(cudaMemsetAsync(phi->t_val, 0, npad * 4, st));
+    LIFE_CUDA(cudaMemcpyAsync(phi->t_tptr, hP.data(), (ntc + 1) * 4, cudaMemcpyHostToDevice, st));
+    LIFE_CUDA(cudaMemcpyAsync(phi->t_t1, hT.data(), (ntc + 1) * 4, cudaMemcpyHostToDevice, st));
+    k_ws_scatter<<<gridn(n), 256, 0, st>>>(sk2, perm, n, f, val, s0, s1, phi->t_tptr, phi->t_t1,
+                                           kTcCellBits, phi->t_cr, phi->t_fiber, phi->t_val);
+    LIFE_CHECK_LAUNCH();
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    LIFE_CUDA(cudaFreeAsync(s0, st));
+    LIFE_CUDA(cudaFreeAsync(s1, st));
+    LIFE_CUDA(cudaFreeAsync(sk2, st));
+    LIFE_CUDA(cudaFreeAsync(perm, st));
+    LIFE_CUDA(cudaFreeAsync(mr, st));
+    // B operand: per chunk, D^T (N directions x 32 atoms) as the K-major
+    // SWIZZLE_128B tile the MMA reads, split hi = tf32(x), lo = x - hi
+    std::vector<float> hD((size_t)nch * 2 * N * kTcCA, 0.f);
+    for (int c = 0; c < nch; ++c)
+        for (int t = 0; t < N; ++t)
+            for (int k = 0; k < kTcCA; ++k) {
+                const int at = c * kTcCA + k;
+                const float x = (at < phi->na && t < phi->nt) ? (float)hdict[(size_t)at * phi->nt + t] : 0.f;
+                float hi, lo;
+                tf32_split(x, hi, lo);
+                const size_t base = (size_t)c * 2 * N * kTcCA;
+                hD[base + tc_cell(t, k)] = hi;
+                hD[base + (size_t)N * kTcCA + tc_cell(t, k)] = lo;
+            }
+    LIFE_TRY(dalloc(phi, &phi->t_D, hD.size()));
+    LIFE_CUDA(cudaMemcpyAsync(phi->t_D, hD.data(), hD.size() * 4, cudaMemcpyHostToDevice, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    phi->t_nct = (int)n_ct;
+    phi->t_nch = nch;
+    phi->t_n = N;
+    phi->t_npad = pos;
+    phi->t_maxseg = maxseg;
+    phi->t_blocks = phi->sms;
+    LIFE_TRY(prepare_tc(phi));  // sets t_smem, t_W
+    phi->has_tc = true;
+    if (getenv("LIFE_DEBUG"))
+        fprintf(stderr, "[life] tc layout: n_ct=%lld nch=%d N=%d padded=%lld maxseg=%lld maxrank=%u\n",
+                (long long)n_ct, nch, N, (long long)pos, (long long)maxseg, hmr);
     return LIFE_OK;
 }
 

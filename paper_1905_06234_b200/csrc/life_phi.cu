@@ -731,6 +731,10 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         if (flags & LIFE_PHI_FORCE_SPARSE) dense = false;
         if (flags & LIFE_PHI_FORCE_DENSE) dense = n > 0;
         if (dense) LIFE_TRY(build_dense(phi, a, v, f, val, hdict, st));
+        // tcgen05 DSC over its own tile layout (life_tc.cu) next to the dense one
+        const char *tc_env = getenv("LIFE_TC");
+        if (dense && phi->has_dense && !(flags & LIFE_PHI_NO_TENSOR) && !(tc_env && tc_env[0] == '0'))
+            LIFE_TRY(build_tc(phi, a, v, f, val, hdict, st));
         if (!phi->has_dense) LIFE_TRY(build_fast(phi, a, v, f, val, hdict, st));
     }
     std::vector<int64_t> fiber_start;
@@ -741,7 +745,7 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
     // fixed-point WC accumulator (both fp32 kernel families)
     LIFE_TRY(dalloc(phi, &phi->wfix, phi->nf));
     LIFE_CUDA(cudaMemsetAsync(phi->wfix, 0, (size_t)phi->nf * sizeof(unsigned long long), st));
-    phi->red_cap = std::max(std::max(std::max(phi->W, phi->xW), phi->d_W), phi->sms * 8) + 1;
+    phi->red_cap = std::max(std::max(std::max(std::max(phi->W, phi->xW), phi->d_W), phi->t_W), phi->sms * 16) + 1;
     LIFE_TRY(dalloc(phi, &phi->red.part_d, phi->red_cap));
     LIFE_TRY(dalloc(phi, &phi->red.part_u, phi->red_cap));
     LIFE_TRY(dalloc(phi, &phi->red.part_f, phi->red_cap));
@@ -803,7 +807,7 @@ int life_phi_get_info(const life_phi *phi, life_phi_info *info)
 {
     if (!phi || !info) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
     info->dims = phi->dims;
-    info->atom_groups = phi->has_dense ? 0 : phi->G;
+    info->atom_groups = phi->has_tc ? -1 : phi->has_dense ? 0 : phi->G;
     info->atoms_per_group = phi->ag;
     info->n_warps = phi->W;
     info->has_exact = phi->has_exact ? 1 : 0;

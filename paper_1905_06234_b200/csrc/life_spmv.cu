@@ -677,6 +677,7 @@ static int launch_dsc_sparse(life_phi *phi, const float *w, float *y, const floa
 int launch_dsc(life_phi *phi, const float *w, float *y, const float *b,
                uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st)
 {
+    if (phi->has_tc) return launch_dsc_tc(phi, w, y, b, flags, o, h, st);
     if (phi->has_dense) return launch_dsc_dense(phi, w, y, b, flags, o, h, st);
     return launch_dsc_sparse(phi, w, y, b, flags, o, h, st);
 }
@@ -716,6 +717,7 @@ static int prepare_sparse(life_phi *phi) { LIFE_NT_DISPATCH(prepare_t, phi); }
 
 int prepare_spmv(life_phi *phi)
 {
+    if (phi->has_tc) LIFE_TRY(prepare_tc(phi));
     if (phi->has_dense) return prepare_dense(phi);
     return prepare_sparse(phi);
 }

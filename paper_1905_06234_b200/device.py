@@ -32,9 +32,11 @@ _LAYOUT = ["auto"]
 
 def set_layout(name):
     """fp32 kernel family for operators built from now on: "auto" (density
-    heuristic), "sparse" (voxel-segment kernels) or "dense" (register-tiled)."""
-    if name not in ("auto", "sparse", "dense"):
-        raise ConfigInvalid(f"layout must be auto/sparse/dense, got {name!r}")
+    heuristic; dense operators run DSC on the tensor cores), "sparse"
+    (voxel-segment kernels), "dense" (tile kernels, tcgen05 DSC) or "fma"
+    (tile kernels on CUDA cores only)."""
+    if name not in ("auto", "sparse", "dense", "fma"):
+        raise ConfigInvalid(f"layout must be auto/sparse/dense/fma, got {name!r}")
     _LAYOUT[0] = name
 
 
@@ -93,7 +95,8 @@ class DeviceOperator:
 
     def _create(self, d, a, v, f, val, dic, stream):
         flags = (N.PHI_EXACT_F64 if self.exact else 0) | (0 if self.fast else N.PHI_NO_FAST_F32)
-        flags |= {"auto": 0, "sparse": N.PHI_FORCE_SPARSE, "dense": N.PHI_FORCE_DENSE}[_LAYOUT[0]]
+        flags |= {"auto": 0, "sparse": N.PHI_FORCE_SPARSE, "dense": N.PHI_FORCE_DENSE,
+                  "fma": N.PHI_FORCE_DENSE | N.PHI_NO_TENSOR}[_LAYOUT[0]]
         dims = N.Dims(d.n_atoms, d.n_voxels, d.n_fibers, d.n_dirs, d.n_coeffs)
         handle = ctypes.c_void_p()
         bad = ctypes.c_int64(-1)
@@ -111,8 +114,10 @@ class DeviceOperator:
 
     @property
     def kind(self):
-        """"dense" or "sparse": the fp32 kernel family this operator uses."""
-        return "sparse" if self.info.atom_groups > 0 else "dense"
+        """"tensor" (tile kernels, tcgen05 DSC), "dense" or "sparse": the fp32
+        kernel family this operator uses."""
+        g = self.info.atom_groups
+        return "sparse" if g > 0 else "tensor" if g < 0 else "dense"
 
     @property
     def handle(self):

@@ -21,9 +21,14 @@ SEEDS = range(30)
 TOL32 = 1e-5
 
 
-@pytest.fixture(params=["sparse", "dense"])
+# set_layout name -> DeviceOperator.kind it yields (at n_dirs <= 128)
+KIND = {"sparse": "sparse", "fma": "dense", "dense": "tensor"}
+
+
+@pytest.fixture(params=["sparse", "fma", "dense"])
 def layout(request):
-    """Run a test against both fp32 kernel families."""
+    """Run a test against every fp32 kernel family: voxel-segment (sparse),
+    tile kernels on CUDA cores (fma), tile kernels with tcgen05 DSC (dense)."""
     from paper_1905_06234_b200 import device
     device.set_layout(request.param)
     yield request.param
@@ -341,7 +346,7 @@ def test_fp32_repeat_bitwise_and_accumulate(layout):
     t, dic, w_true, _ = datagen.draw_arrays(L.GenConfig(dims=dims, mean_run_length=520.0,
                                                         seed=4))
     op = L.DeviceOperator(t, dic)
-    assert op.kind == layout
+    assert op.kind == KIND[layout]
     if layout == "sparse":
         assert op.info.atom_groups == 2  # 1057 x 96 fp32 exceeds one CTA's shared memory
     w = torch.from_numpy(w_true).float().cuda()
