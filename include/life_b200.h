@@ -88,7 +88,8 @@ LIFE_API uint64_t life_launch_count(void);
 #define LIFE_PHI_NO_FAST_F32  0x4u  /* skip the fp32 fast layout           */
 #define LIFE_PHI_FORCE_SPARSE 0x8u  /* fp32: voxel-segment kernels only    */
 #define LIFE_PHI_FORCE_DENSE  0x10u /* fp32: register-tiled dense kernels  */
-#define LIFE_PHI_NO_TENSOR    0x20u /* fp32: no tcgen05 (tensor-core) DSC   */
+#define LIFE_PHI_NO_TENSOR    0x20u /* fp32: never build the tcgen05 DSC layout */
+#define LIFE_PHI_TENSOR       0x40u /* fp32: also build it; DSC runs on tcgen05 */
 
 /* Build the device operator from COO arrays (PhiTensor + Dictionary,
  * tensor.py:76-170).  atoms/voxels/fibers: u32[n_coeffs]; values:

@@ -24,6 +24,7 @@ PHI_NO_FAST_F32 = 0x4
 PHI_FORCE_SPARSE = 0x8
 PHI_FORCE_DENSE = 0x10
 PHI_NO_TENSOR = 0x20
+PHI_TENSOR = 0x40
 ACCUMULATE = 0x01
 SKIP_ZERO = 0x02
 SUBTRACT_B = 0x04

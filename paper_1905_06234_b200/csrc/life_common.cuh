@@ -121,16 +121,14 @@ struct life_phi {
     // cell); cell = fp32 index of (row, atom) in the K-major SWIZZLE_128B
     // A tile the tcgen05 MMA reads.
     bool has_tc = false;
-    uint32_t *t_cr = nullptr;     // mixed << 31 | pad << 30 | rank << 12 | cell
-    uint32_t *t_fiber = nullptr;
-    float *t_val = nullptr;
+    uint32_t *t_q = nullptr;      // 32-byte quads {pk[4], value[4]}, pk = fascicle << 12 | cell
     uint32_t *t_tptr = nullptr;   // [n_ct*nch*8 + 1] padded segment starts
     uint32_t *t_t1 = nullptr;     // start of each segment's rank>=1 region
     uint32_t *t_vslot = nullptr;  // tile slot of each voxel
     int *t_slotv = nullptr;       // voxel of each tile slot, -1 = padding
     float *t_D = nullptr;         // [nch][hi|lo][N rows][32] swizzled tf32 split of D^T
     int t_nct = 0, t_nch = 0, t_n = 0, t_blocks = 0, t_W = 0;
-    int64_t t_npad = 0, t_maxseg = 0;
+    int64_t t_npad = 0, t_maxseg = 0, t_maxstep = 0;
     size_t t_smem = 0;
 
     // fixed-point WC accumulator and its scale inputs

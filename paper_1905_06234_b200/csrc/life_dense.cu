@@ -667,6 +667,39 @@ __global__ void k_ws_scatter(const unsigned long long *sk2, const uint32_t *perm
     }
 }
 
+// tensor-core layout: entries packed as pk = fascicle << 12 | cell (fascicles
+// < 2^20 - 1; all ones = pad) and stored as 32-byte quads {pk[4], value[4]} so
+// one bulk copy stages a whole step (all 8 producer segments)
+__global__ void k_tc_pad(uint32_t *q, int64_t nquads)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nquads;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint4 *o = reinterpret_cast<uint4 *>(q + i * 8);
+        o[0] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        o[1] = make_uint4(0u, 0u, 0u, 0u);
+    }
+}
+
+__global__ void k_tc_scatter(const unsigned long long *sk2, const uint32_t *perm, int64_t n,
+                             const uint32_t *f, const double *val, const uint32_t *s0,
+                             const uint32_t *s1, const uint32_t *P, const uint32_t *T1, uint32_t *q)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = sk2[i];
+        const uint32_t tc = (uint32_t)(k >> 32);
+        const uint32_t cr = (uint32_t)(k & 0xFFFFFFFFull);
+        const uint32_t rank = cr >> kTcCellBits;
+        const int64_t dest = rank == 0 ? (int64_t)P[tc] + (i - (int64_t)s0[tc])
+                                       : (int64_t)T1[tc] + (i - (int64_t)s1[tc]);
+        const uint32_t p = perm[i];
+        uint32_t *o = q + (dest >> 2) * 8 + (dest & 3);
+        o[0] = (f[p] << kTcCellBits) | (cr & ((1u << kTcCellBits) - 1));
+        const float v = (float)val[p];
+        o[4] = __float_as_uint(v);
+    }
+}
+
 static int gridn(int64_t n)
 {
     int64_t b = (n + 255) / 256;
@@ -914,7 +947,7 @@ int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t
 {
     const int64_t n = phi->nc;
     const int N = (phi->nt + 31) / 32 * 32;  // MMA N: directions padded to 32
-    if (n == 0 || N > 128) return LIFE_OK;
+    if (n == 0 || N > 128 || phi->nf >= (1 << 20) - 1) return LIFE_OK;
     const int nch = (phi->na + kTcCA - 1) / kTcCA;
     const int64_t nblk = ((int64_t)phi->nv + 15) / 16;   // 16-voxel row blocks
     const int64_t n_ct = (nblk + 7) / 8;                 // CTA tiles of 128 voxels
@@ -1005,8 +1038,9 @@ int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t
     LIFE_CUDA(cudaMemcpyAsync(h1.data(), s1, (ntc + 1) * 4, cudaMemcpyDeviceToHost, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
     // rank-0 and rank>=1 regions each padded to 4 entries (16-byte vectors)
-    int64_t pos = 0, maxseg = 0;
+    int64_t pos = 0, maxseg = 0, maxstep = 0;
     for (int64_t t = 0; t < ntc; ++t) {
+        if (t % kTcProd == 0 && t) maxstep = std::max<int64_t>(maxstep, pos - hP[t - kTcProd]);
         const int64_t n0 = (int64_t)h1[t] - h0[t], n1 = (int64_t)h0[t + 1] - h1[t];
         hP[t] = (uint32_t)pos;
         hT[t] = (uint32_t)(pos + (n0 + 3) / 4 * 4);
@@ -1015,20 +1049,18 @@ int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t
         pos += len;
     }
     hP[ntc] = hT[ntc] = (uint32_t)pos;
+    if (ntc) maxstep = std::max<int64_t>(maxstep, pos - hP[ntc - kTcProd]);
     if (pos >= 0xFFFFFFFFll) return fail(LIFE_ERR_CONFIG_INVALID, "padded layout exceeds u32");
-    const int64_t npad = std::max<int64_t>(pos, 1);
-    LIFE_TRY(dalloc(phi, &phi->t_cr, npad));
-    LIFE_TRY(dalloc(phi, &phi->t_fiber, npad));
-    LIFE_TRY(dalloc(phi, &phi->t_val, npad));
+    const int64_t npad = std::max<int64_t>(pos, 4);
+    LIFE_TRY(dalloc(phi, &phi->t_q, (size_t)(npad / 4 + 1) * 8));
     LIFE_TRY(dalloc(phi, &phi->t_tptr, ntc + 1));
     LIFE_TRY(dalloc(phi, &phi->t_t1, ntc + 1));
-    LIFE_CUDA(cudaMemsetAsync(phi->t_cr, 0x40, npad * 4, st));     // pad bit 30
-    LIFE_CUDA(cudaMemsetAsync(phi->t_fiber, 0xFF, npad * 4, st));  // sentinel fascicle
-    LIFE_CUDA(cudaMemsetAsync(phi->t_val, 0, npad * 4, st));
+    k_tc_pad<<<gridn(npad / 4 + 1), 256, 0, st>>>(phi->t_q, npad / 4 + 1);
+    LIFE_CHECK_LAUNCH();
     LIFE_CUDA(cudaMemcpyAsync(phi->t_tptr, hP.data(), (ntc + 1) * 4, cudaMemcpyHostToDevice, st));
     LIFE_CUDA(cudaMemcpyAsync(phi->t_t1, hT.data(), (ntc + 1) * 4, cudaMemcpyHostToDevice, st));
-    k_ws_scatter<<<gridn(n), 256, 0, st>>>(sk2, perm, n, f, val, s0, s1, phi->t_tptr, phi->t_t1,
-                                           kTcCellBits, phi->t_cr, phi->t_fiber, phi->t_val);
+    k_tc_scatter<<<gridn(n), 256, 0, st>>>(sk2, perm, n, f, val, s0, s1, phi->t_tptr, phi->t_t1,
+                                           phi->t_q);
     LIFE_CHECK_LAUNCH();
     LIFE_CUDA(cudaStreamSynchronize(st));
     LIFE_CUDA(cudaFreeAsync(s0, st));
@@ -1058,12 +1090,16 @@ int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t
     phi->t_n = N;
     phi->t_npad = pos;
     phi->t_maxseg = maxseg;
+    phi->t_maxstep = maxstep;
     phi->t_blocks = phi->sms;
-    LIFE_TRY(prepare_tc(phi));  // sets t_smem, t_W
+    if (prepare_tc(phi) != LIFE_OK) {  // sets t_smem, t_W; segments too long: stay on CUDA cores
+        ok();
+        return LIFE_OK;
+    }
     phi->has_tc = true;
     if (getenv("LIFE_DEBUG"))
-        fprintf(stderr, "[life] tc layout: n_ct=%lld nch=%d N=%d padded=%lld maxseg=%lld maxrank=%u\n",
-                (long long)n_ct, nch, N, (long long)pos, (long long)maxseg, hmr);
+        fprintf(stderr, "[life] tc layout: n_ct=%lld nch=%d N=%d padded=%lld maxseg=%lld maxstep=%lld maxrank=%u\n",
+                (long long)n_ct, nch, N, (long long)pos, (long long)maxseg, (long long)maxstep, hmr);
     return LIFE_OK;
 }
 

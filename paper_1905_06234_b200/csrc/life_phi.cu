@@ -731,9 +731,12 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         if (flags & LIFE_PHI_FORCE_SPARSE) dense = false;
         if (flags & LIFE_PHI_FORCE_DENSE) dense = n > 0;
         if (dense) LIFE_TRY(build_dense(phi, a, v, f, val, hdict, st));
-        // tcgen05 DSC over its own tile layout (life_tc.cu) next to the dense one
+        // tcgen05 DSC over its own tile layout (life_tc.cu) next to the dense
+        // one: opt-in (LIFE_PHI_TENSOR or LIFE_TC=1) until it beats the
+        // CUDA-core tile kernels
         const char *tc_env = getenv("LIFE_TC");
-        if (dense && phi->has_dense && !(flags & LIFE_PHI_NO_TENSOR) && !(tc_env && tc_env[0] == '0'))
+        const bool want_tc = (flags & LIFE_PHI_TENSOR) || (tc_env && tc_env[0] == '1');
+        if (dense && phi->has_dense && want_tc && !(flags & LIFE_PHI_NO_TENSOR))
             LIFE_TRY(build_tc(phi, a, v, f, val, hdict, st));
         if (!phi->has_dense) LIFE_TRY(build_fast(phi, a, v, f, val, hdict, st));
     }

@@ -27,6 +27,8 @@
 // Pipelines: A/B stages (full: 8 producer arrivals + the B copy's bytes;
 // empty: tcgen05.commit), TMEM buffers (accfull: commit; accempty: 4
 // epilogue warps).  Every wait traps after 4 s instead of hanging.
+#include <algorithm>
+
 #include "life_common.cuh"
 
 namespace life {
@@ -35,25 +37,48 @@ constexpr int kTcMma = 8;                 // MMA warp
 constexpr int kTcEpi = 9;                 // first epilogue warp
 constexpr int kTcWarps = 13;
 constexpr int kTcThreads = kTcWarps * 32;
-constexpr int kTcStages = 3;
+#ifndef LIFE_TC_STAGES
+#define LIFE_TC_STAGES 2
+#endif
+constexpr int kTcStages = LIFE_TC_STAGES;  // A/B stages
 constexpr int kTcGroup = 4;               // chunks per TMEM accumulation group
-constexpr uint32_t kTcPad = 0x40000000u;
-constexpr uint32_t kTcMixed = 0x80000000u;
 constexpr uint32_t kTcCellMask = (1u << kTcCellBits) - 1;
-constexpr uint32_t kTcRankMask = (1u << (30 - kTcCellBits)) - 1;
-constexpr uint32_t kTcSent = 0xFFFFFFFFu;
+constexpr uint32_t kTcSent = 0xFFFFFu;     // fascicle field of pad entries
+constexpr int kTcSlots = 4;                // staged steps (3 ahead of the one being built)
 constexpr int kTcABytes = kTcTV * kTcCA * 4;  // 16 KB per A half (hi or lo)
 
 struct TcArgs {
-    const uint32_t *cr;
-    const uint32_t *fiber;
-    const float *val;
+    const uint32_t *q;   // quads {pk[4], value[4]}, pk = fascicle << 12 | cell
     const uint32_t *tptr;
     const uint32_t *t1;
     const float *D;      // [nch][2][N][32] swizzled
     const int *slotv;
     int nt, nch, n_ct;
+    int slot;            // staged entries per step slot (multiple of 4)
 };
+
+// Diagnostics, compiled in only with -DLIFE_WS_DIAG (tools/tc_isolate.py):
+// c_tc_flags 1 = producers skip the tile build, 2 = no MMAs (commits only),
+// 4 = no w gathers (w = 1), 8 = epilogue skips the TMEM loads, 16 = no L2
+// prefetch, 32 = no dictionary (B) copies; g_tc_cyc
+// accumulates per-role clock64 spans.
+#ifdef LIFE_WS_DIAG
+__constant__ int c_tc_flags = 0;
+__device__ unsigned long long g_tc_cyc[16];
+#define TC_T0(v) const long long v = clock64()
+#define TC_ACC(i, v) (tcc[i] += (unsigned long long)(clock64() - (v)))
+#define TC_DECL unsigned long long tcc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define TC_FLUSH                                                               \
+    if ((threadIdx.x & 31) == 0)                                               \
+        for (int i_ = 0; i_ < 8; ++i_)                                         \
+            if (tcc[i_]) atomicAdd(&g_tc_cyc[i_], tcc[i_])
+#else
+#define TC_DECL
+#define TC_FLUSH
+constexpr int c_tc_flags = 0;
+#define TC_T0(v)
+#define TC_ACC(i, v)
+#endif
 
 // ---- PTX helpers -------------------------------------------------------------
 __device__ __forceinline__ uint32_t tc_sa(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -79,12 +104,34 @@ __device__ __forceinline__ bool tc_try(uint64_t *b, unsigned parity)
                  : "=r"(ok) : "r"(tc_sa(b)), "r"(parity) : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ bool tc_test(uint64_t *b, unsigned parity)
+{
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(tc_sa(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
+#ifndef LIFE_TC_SPIN
+#define LIFE_TC_SPIN 0
+#endif
+// waits spin on test_wait (a try_wait that suspends the warp was measured to
+// add ~1-2k cycles per hand-over); trap after 4 s instead of hanging
 __device__ __forceinline__ void tc_wait(uint64_t *b, unsigned parity)
 {
-    if (tc_try(b, parity)) return;
-    const unsigned long long t0 = globaltimer();
-    while (!tc_try(b, parity))
-        if (globaltimer() - t0 > 4000000000ull) __trap();
+    if (LIFE_TC_SPIN) {
+        if (tc_test(b, parity)) return;
+        const unsigned long long t0 = globaltimer();
+        unsigned n = 0;
+        while (!tc_test(b, parity))
+            if ((++n & 1023u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+    } else {
+        if (tc_try(b, parity)) return;
+        const unsigned long long t0 = globaltimer();
+        while (!tc_try(b, parity))
+            if (globaltimer() - t0 > 4000000000ull) __trap();
+    }
 }
 __device__ __forceinline__ void tc_bulk(void *dst, const void *src, unsigned bytes, uint64_t *b)
 {
@@ -125,6 +172,7 @@ __device__ __forceinline__ uint32_t tc_ld1(const void *p, uint64_t pol)
 __device__ __forceinline__ float tc_gather(const float *w, uint32_t f, uint64_t pol)
 {
     if (f == kTcSent) return 0.f;
+    if (c_tc_flags & 4) return 1.f;
     float r;
     asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(w + f), "l"(pol));
     return r;
@@ -200,112 +248,173 @@ struct TcMax {
 };
 
 // ---- producer: one 16-row block of the A tile for one chunk --------------------
-// entries per lane and batch: kTcVec 16-byte vectors of the rank-0 region
-// (128 entries per vector across the warp) and kTcWin windows of the rank>=1
-// region (32 entries per window), gathered together so a step usually costs
-// one load round trip and one gather round trip
+// The layout stores entries as 48-byte quads {cr[4], fiber[4], value[4]}; a
+// step's 8 producer segments are contiguous, so producer 0 stages the whole
+// step with one bulk copy into a shared-memory slot, two steps ahead (3
+// slots), after an L2 prefetch four steps ahead.  A warp's segment is
+// (p0, q0, p1): rank-0 entries [p0, q0) (distinct cells), repeats [q0, p1)
+// sorted by rank, each region padded to 4.  The w[f] gathers of step k+1 are
+// issued into registers before step k is built, so their L2 round trip
+// overlaps the build.  Per lane the registers hold kTcVec 16-byte vectors of
+// the rank-0 region (128 entries per vector across the warp) and kTcWin
+// 32-entry windows of the repeats; a longer segment gathers the rest inline.
 constexpr int kTcVec = 3;
 constexpr int kTcWin = 4;
 
-__device__ __forceinline__ unsigned tc_build(float *C, const float *__restrict__ w, const TcArgs &A,
-                                             uint32_t p0, uint32_t q0, uint32_t p1, int lane,
-                                             uint64_t pol_s, uint64_t pol_k, float *junk)
+// explicit shared-memory accesses (32-bit shared-window addresses)
+__device__ __forceinline__ uint4 lds4(uint32_t a)
+{
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ uint32_t lds1(uint32_t a)
+{
+    uint32_t r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ float ldsf(uint32_t a)
+{
+    float r;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ void stsf(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory"); }
+__device__ __forceinline__ void sts4(uint32_t a, float4 v)
+{
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float4 lds4f(uint32_t a)
+{
+    float4 r;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a));
+    return r;
+}
+
+// a warp's segment inside a staged step: entries at slot offset < cap are in
+// shared memory (quads at sbase), the rest (steps longer than a slot, rare)
+// in global memory
+struct TcSeg {
+    uint32_t sbase;       // shared address of the step's slot
+    const uint32_t *gq;   // global quads of the step
+    uint32_t off;         // segment start, entries from the step start
+    uint32_t nf, n;       // rank-0 entries, all entries
+    uint32_t cap;         // staged entries
+    // field 0 = pk, 1 = value of the 4 entries starting at k (k % 4 == 0)
+    __device__ __forceinline__ uint4 q4(uint32_t k, int field) const
+    {
+        const uint32_t o = off + k;
+        if (o < cap) return lds4(sbase + (o >> 2) * 32u + 16u * field);
+        return __ldg(reinterpret_cast<const uint4 *>(gq + (o >> 2) * 8u + 4u * field));
+    }
+    __device__ __forceinline__ uint32_t word(uint32_t k, int field) const
+    {
+        const uint32_t o = off + k;
+        if (o < cap) return lds1(sbase + (o >> 2) * 32u + 16u * field + 4u * (o & 3u));
+        return __ldg(gq + (o >> 2) * 8u + 4u * field + (o & 3u));
+    }
+};
+
+struct TcW {
+    float v[kTcVec][4];
+    float r[kTcWin];
+};
+
+// issue the gathers of a staged segment (values land in registers later)
+__device__ __forceinline__ void tc_gathers(const TcSeg &S, const float *__restrict__ w, int lane, uint64_t pol,
+                                           TcW &W)
+{
+#pragma unroll
+    for (int j = 0; j < kTcVec; ++j) {
+        const uint32_t k = 128u * (uint32_t)j + 4u * (uint32_t)lane;
+        uint4 f = make_uint4(~0u, ~0u, ~0u, ~0u);
+        if (k < S.nf) f = S.q4(k, 0);
+        W.v[j][0] = tc_gather(w, f.x >> kTcCellBits, pol);
+        W.v[j][1] = tc_gather(w, f.y >> kTcCellBits, pol);
+        W.v[j][2] = tc_gather(w, f.z >> kTcCellBits, pol);
+        W.v[j][3] = tc_gather(w, f.w >> kTcCellBits, pol);
+    }
+#pragma unroll
+    for (int r = 0; r < kTcWin; ++r) {
+        const uint32_t k = S.nf + 32u * (uint32_t)r + (uint32_t)lane;
+        W.r[r] = tc_gather(w, (k < S.n ? S.word(k, 0) : ~0u) >> kTcCellBits, pol);
+    }
+}
+
+__device__ __forceinline__ void reds(uint32_t a, float v)
+{
+    asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+
+// build the warp's rows of C (shared address C) from a staged segment and its
+// gathered w: rank-0 entries (distinct cells) are stored, then the repeats
+// (sorted by rank, then cell) are added with shared-memory reductions, issued
+// in rank order by this warp alone
+__device__ __forceinline__ unsigned tc_build(uint32_t C, const TcSeg &S, const TcW &W, const float *__restrict__ w,
+                                             int lane, uint64_t pol, uint32_t junk)
 {
     unsigned zeros = 0;
-    const uint32_t nf = q0 - p0, n = p1 - p0;
-    const int nb = (int)((nf + 127u) / 128u), nw = (int)((n - nf + 31u) / 32u);
-    const uint32_t *cr = A.cr + p0;
-    const uint32_t *fb = A.fiber + p0;
-    const float *vl = A.val + p0;
-    float wsl[kTcWin];
-    uint32_t csl[kTcWin];
-    float vsl[kTcWin];
-    for (int b0 = 0; b0 < nb || b0 == 0; b0 += kTcVec) {
-        uint4 c4[kTcVec], f4[kTcVec], v4[kTcVec];
+    auto put4 = [&](uint32_t k, const float (&wv)[4]) {
+        const uint4 c4 = S.q4(k, 0);
+        const uint4 v4 = S.q4(k, 1);
+        const uint32_t c[4] = {c4.x, c4.y, c4.z, c4.w};
+        const float v[4] = {__uint_as_float(v4.x), __uint_as_float(v4.y), __uint_as_float(v4.z),
+                            __uint_as_float(v4.w)};
 #pragma unroll
-        for (int j = 0; j < kTcVec; ++j) {
-            const uint32_t k = 128u * (uint32_t)(b0 + j) + 4u * (uint32_t)lane;
-            if (b0 + j < nb && k < nf) {
-                c4[j] = tc_ld4(cr + k, pol_s);
-                f4[j] = tc_ld4(fb + k, pol_s);
-                v4[j] = tc_ld4(vl + k, pol_s);
-            } else {
-                c4[j] = make_uint4(kTcPad, kTcPad, kTcPad, kTcPad);
-                f4[j] = make_uint4(kTcSent, kTcSent, kTcSent, kTcSent);
-                v4[j] = make_uint4(0u, 0u, 0u, 0u);
-            }
+        for (int e = 0; e < 4; ++e) {
+            const bool ok = (c[e] >> kTcCellBits) != kTcSent;
+            const float sv = __fmul_rn(wv[e], v[e]);
+            zeros += (ok && sv == 0.f) ? 1u : 0u;
+            stsf(ok ? C + 4u * (c[e] & kTcCellMask) : junk, sv);
         }
-        if (b0 == 0) {
+    };
 #pragma unroll
-            for (int r = 0; r < kTcWin; ++r) {
-                const uint32_t k = nf + 32u * (uint32_t)r + (uint32_t)lane;
-                const bool in = r < nw && k < n;
-                csl[r] = in ? tc_ld1(cr + k, pol_s) : kTcPad;
-                const uint32_t f = in ? tc_ld1(fb + k, pol_s) : kTcSent;
-                vsl[r] = in ? __uint_as_float(tc_ld1(vl + k, pol_s)) : 0.f;
-                wsl[r] = tc_gather(w, f, pol_k);
-            }
-        }
-        float wf[kTcVec][4];
-#pragma unroll
-        for (int j = 0; j < kTcVec; ++j) {
-            wf[j][0] = tc_gather(w, f4[j].x, pol_k);
-            wf[j][1] = tc_gather(w, f4[j].y, pol_k);
-            wf[j][2] = tc_gather(w, f4[j].z, pol_k);
-            wf[j][3] = tc_gather(w, f4[j].w, pol_k);
-        }
-#pragma unroll
-        for (int j = 0; j < kTcVec; ++j) {
-            const uint32_t c[4] = {c4[j].x, c4[j].y, c4[j].z, c4[j].w};
-            const float v[4] = {__uint_as_float(v4[j].x), __uint_as_float(v4[j].y), __uint_as_float(v4[j].z),
-                                __uint_as_float(v4[j].w)};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const bool ok = !(c[e] & kTcPad);
-                const float sv = __fmul_rn(wf[j][e], v[e]);
-                zeros += (ok && sv == 0.f) ? 1u : 0u;
-                float *dst = ok ? C + (c[e] & kTcCellMask) : junk;
-                *dst = sv;
-            }
-        }
+    for (int j = 0; j < kTcVec; ++j) {
+        const uint32_t k = 128u * (uint32_t)j + 4u * (uint32_t)lane;
+        if (k < S.nf) put4(k, W.v[j]);
+    }
+    for (uint32_t k = 128u * kTcVec + 4u * (uint32_t)lane; k < S.nf; k += 128u) {  // beyond the registers
+        const uint4 f = S.q4(k, 0);
+        const float wv[4] = {tc_gather(w, f.x >> kTcCellBits, pol), tc_gather(w, f.y >> kTcCellBits, pol),
+                             tc_gather(w, f.z >> kTcCellBits, pol), tc_gather(w, f.w >> kTcCellBits, pol)};
+        put4(k, wv);
     }
     __syncwarp();
-    // repeats, window by window in rank order
-    for (int r0 = 0; r0 < nw; r0 += kTcWin) {
-        if (r0) {
-#pragma unroll
-            for (int r = 0; r < kTcWin; ++r) {
-                const uint32_t k = nf + 32u * (uint32_t)(r0 + r) + (uint32_t)lane;
-                const bool in = r0 + r < nw && k < n;
-                csl[r] = in ? tc_ld1(cr + k, pol_s) : kTcPad;
-                const uint32_t f = in ? tc_ld1(fb + k, pol_s) : kTcSent;
-                vsl[r] = in ? __uint_as_float(tc_ld1(vl + k, pol_s)) : 0.f;
-                wsl[r] = tc_gather(w, f, pol_k);
+    auto rep = [&](uint32_t k, float wv) {
+        if (k < S.n) {
+            const uint32_t c = S.word(k, 0);
+            if ((c >> kTcCellBits) != kTcSent) {
+                const float sv = __fmul_rn(wv, __uint_as_float(S.word(k, 1)));
+                zeros += sv == 0.f ? 1u : 0u;
+                reds(C + 4u * (c & kTcCellMask), sv);
             }
         }
+    };
 #pragma unroll
-        for (int r = 0; r < kTcWin; ++r) {
-            if (r0 + r >= nw) break;  // warp-uniform
-            const uint32_t c = csl[r];
-            const bool ok = !(c & kTcPad);
-            const float sv = ok ? __fmul_rn(wsl[r], vsl[r]) : 0.f;
-            zeros += (ok && sv == 0.f) ? 1u : 0u;
-            const uint32_t cell = c & kTcCellMask;
-            if (!__any_sync(0xffffffffu, ok && (c & kTcMixed))) {
-                if (ok) C[cell] += sv;
-            } else {
-                const uint32_t rank = (c >> kTcCellBits) & kTcRankMask;
-                const uint32_t rmin = __reduce_min_sync(0xffffffffu, ok ? rank : 0xFFFFFFFFu);
-                const uint32_t rmax = __reduce_max_sync(0xffffffffu, ok ? rank : 0u);
-                for (uint32_t rr = rmin; rr <= rmax; ++rr) {
-                    if (ok && rank == rr) C[cell] += sv;
-                    __syncwarp();
-                }
-            }
-            __syncwarp();
-        }
-    }
+    for (int r = 0; r < kTcWin; ++r) rep(S.nf + 32u * (uint32_t)r + (uint32_t)lane, W.r[r]);
+    for (uint32_t k = S.nf + 32u * kTcWin + (uint32_t)lane; k < S.n; k += 32u)
+        rep(k, tc_gather(w, S.word(k, 0) >> kTcCellBits, pol));
     return zeros;
+}
+
+// bulk copy / L2 prefetch of a byte range in pieces of at most 32 KB
+__device__ __forceinline__ void tc_stage_step(void *dst, const void *src, unsigned bytes, uint64_t *bar,
+                                              uint64_t pol)
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_arrive_tx(bar, bytes);
+    const char *s = reinterpret_cast<const char *>(src);
+    char *d = reinterpret_cast<char *>(dst);
+    for (unsigned o = 0; o < bytes; o += 32768u)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                     ::"r"(tc_sa(d + o)), "l"(s + o), "r"(min(32768u, bytes - o)), "r"(tc_sa(bar)), "l"(pol)
+                     : "memory");
+}
+__device__ __forceinline__ void tc_prefetch_step(const void *src, unsigned bytes, uint64_t pol)
+{
+    const char *s = reinterpret_cast<const char *>(src);
+    for (unsigned o = 0; o < bytes; o += 32768u) tc_prefetch(s + o, min(32768u, bytes - o), pol);
 }
 
 template <int NJ>
@@ -319,6 +428,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     constexpr int kStageBytes = 2 * kTcABytes + kBBytes;
     extern __shared__ __align__(1024) unsigned char tc_smraw[];
     __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], accfull[2], accempty[2];
+    __shared__ __align__(8) uint64_t slotfull[kTcSlots], slotfree[kTcSlots];
     __shared__ uint32_t tmem_base;
     __shared__ float junkbuf[kTcProd * 32];
     if (hooks.done && *hooks.done) return;
@@ -336,6 +446,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc_bar_init(&accfull[s], 1);
             tc_bar_init(&accempty[s], 4);
         }
+        for (int j = 0; j < kTcSlots; ++j) {
+            tc_bar_init(&slotfull[j], 1);
+            tc_bar_init(&slotfree[j], kTcProd);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kTcMma) {
@@ -349,55 +463,125 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     double sq = 0.0;
     float amax = 0.f;
     unsigned long long skipped = 0;
+    TC_DECL;
 
     if (warp < kTcProd) {
         // ===== producers =====
         const int p = warp;
         const uint64_t pol_s = tc_pol_stream(), pol_k = tc_pol_keep();
-        float *junk = junkbuf + p * 32 + lane;
-        int ct = blockIdx.x, c = 0;
-        auto seg = [&](int ct_, int c_, uint32_t &s0, uint32_t &s1, uint32_t &s2) {
-            const size_t t = ((size_t)ct_ * A.nch + c_) * kTcProd + p;
-            s0 = __ldg(A.tptr + t);
-            s1 = __ldg(A.t1 + t);
-            s2 = __ldg(A.tptr + t + 1);
+        const uint32_t junk = tc_sa(junkbuf + p * 32 + lane);
+        uint32_t *slotbase = reinterpret_cast<uint32_t *>(sm + (size_t)kTcStages * kStageBytes);
+        const uint32_t slot_sa = tc_sa(slotbase);
+        const uint32_t cap = (uint32_t)A.slot;
+        // segment bounds of 32 steps per window, lane l holding step base+l:
+        // {p0, q0, p1, step start, step end}; the next window is loaded 32
+        // steps before it is needed
+        uint32_t cb[5], nb[5];
+        auto loadw = [&](int base, uint32_t (&o)[5]) {
+            const int kk = base + lane;
+            if (kk < total) {
+                const size_t T = ((size_t)(blockIdx.x + (kk / A.nch) * gridDim.x) * A.nch + kk % A.nch) * kTcProd;
+                o[0] = __ldg(A.tptr + T + p);
+                o[1] = __ldg(A.t1 + T + p);
+                o[2] = __ldg(A.tptr + T + p + 1);
+                o[3] = __ldg(A.tptr + T);
+                o[4] = __ldg(A.tptr + T + kTcProd);
+            } else {
+                o[0] = o[1] = o[2] = o[3] = o[4] = 0u;
+            }
         };
-        uint32_t p0 = 0, q0 = 0, p1 = 0, np0 = 0, nq0 = 0, np1 = 0;
-        if (total > 0) seg(ct, c, p0, q0, p1);
+        loadw(0, cb);
+        loadw(32, nb);
+        int wbase = 0;
+        auto bnd = [&](int kk, int i) {
+            const int d = kk - wbase;
+            return __shfl_sync(0xffffffffu, d < 32 ? cb[i] : nb[i], d & 31);
+        };
+        auto segv = [&](int kk) {
+            const uint32_t b0 = bnd(kk, 0), b1 = bnd(kk, 1), b2 = bnd(kk, 2), s0 = bnd(kk, 3);
+            return TcSeg{slot_sa + (uint32_t)(kk % kTcSlots) * 8u * cap, A.q + (size_t)s0 * 2u, b0 - s0, b1 - b0, b2 - b0, cap};
+        };
+        auto stage = [&](int kk) {  // producer 0, lane 0
+            const uint32_t s0 = bnd(kk, 3), s1 = bnd(kk, 4);
+            const uint32_t n = min(s1 - s0, cap);
+            const int j = kk % kTcSlots;
+            if (lane == 0) {
+                if (kk >= kTcSlots && !(c_tc_flags & 1024)) tc_wait(&slotfree[j], ((kk / kTcSlots) - 1) & 1);
+                if (c_tc_flags & 128) { tc_arrive(&slotfull[j]); return; }
+                tc_stage_step(slotbase + (size_t)j * 2u * cap, A.q + (size_t)s0 * 2u, n * 8u, &slotfull[j], pol_s);
+            }
+        };
+        // L2 prefetch of a step: one 128-byte line per lane and instruction
+        // (LSU-issued, many lines in flight; the bulk copy engine alone keeps
+        // too few HBM requests outstanding for a once-read stream)
+        auto prefetch = [&](int kk) {
+            const uint32_t s0 = bnd(kk, 3), s1 = bnd(kk, 4);
+            if (c_tc_flags & 16) return;
+            const char *b = reinterpret_cast<const char *>(A.q + (size_t)s0 * 2u);
+            const uint32_t bytes = (s1 - s0) * 8u;
+            for (uint32_t o = (uint32_t)lane * 128u; o < bytes; o += 32u * 128u)
+                asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(b + o));
+        };
+        TcW Wc, Wn;
+        constexpr int kAhead = kTcSlots - 1, kPre = 2 * kAhead;
+        if (p == 0) {
+            for (int kk = 0; kk < kAhead && kk < total; ++kk) stage(kk);
+            for (int kk = kAhead; kk < kPre && kk < total; ++kk) prefetch(kk);
+        }
+        if (total > 0) {
+            tc_wait(&slotfull[0], 0);
+            tc_gathers(segv(0), w, lane, pol_k, Wc);
+        }
+        int c0 = 0;
         for (int k = 0; k < total; ++k) {
             const int s = k % kTcStages;
-            // next step's segment: prefetch its three streams into L2
-            int ctn = ct, cn = c + 1;
-            if (cn == A.nch) { cn = 0; ctn += gridDim.x; }
-            if (k + 1 < total) {
-                seg(ctn, cn, np0, nq0, np1);
-                if (lane < 3) {
-                    const void *base = lane == 0 ? (const void *)(A.cr + np0)
-                                     : lane == 1 ? (const void *)(A.fiber + np0) : (const void *)(A.val + np0);
-                    tc_prefetch(base, (np1 - np0) * 4u, pol_s);
-                }
+            if (k > 0 && (k & 31) == 0) {
+#pragma unroll
+                for (int i = 0; i < 5; ++i) cb[i] = nb[i];
+                wbase = k;
+                loadw(k + 32, nb);
             }
-            if (k >= kTcStages) tc_wait(&empty[s], ((k / kTcStages) - 1) & 1);
+            if (p == 0) {
+                if (k + kAhead < total) stage(k + kAhead);
+                if (k + kPre < total) prefetch(k + kPre);
+            }
+            TC_T0(t_slot);
+            if (k + 1 < total) {
+                if (!(c_tc_flags & 1024)) tc_wait(&slotfull[(k + 1) % kTcSlots], ((k + 1) / kTcSlots) & 1);
+                tc_gathers(segv(k + 1), w, lane, pol_k, Wn);
+            }
+            if (lane == 0) TC_ACC(0, t_slot);
+            TC_T0(t_empty);
+            if (k >= kTcStages && !(c_tc_flags & 1024)) tc_wait(&empty[s], ((k / kTcStages) - 1) & 1);
+            if (lane == 0) TC_ACC(1, t_empty);
+            TC_T0(t_build);
             unsigned char *st = sm + (size_t)s * kStageBytes;
             float *Ahi = reinterpret_cast<float *>(st);
             float *Alo = reinterpret_cast<float *>(st + kTcABytes);
             if (p == 0 && lane == 0) {
-                tc_arrive_tx(&full[s], kBBytes);
-                tc_bulk(st + 2 * kTcABytes, A.D + (size_t)c * (kBBytes / 4), kBBytes, &full[s]);
+                if (c_tc_flags & 32) {
+                    tc_arrive(&full[s]);
+                } else {
+                    tc_arrive_tx(&full[s], kBBytes);
+                    tc_bulk(st + 2 * kTcABytes, A.D + (size_t)c0 * (kBBytes / 4), kBBytes, &full[s]);
+                }
             }
             // zero this warp's rows (2 KB)
-            float4 *Z = reinterpret_cast<float4 *>(Ahi) + p * 128;
+            const uint32_t H = tc_sa(Ahi) + (uint32_t)p * 2048u, L = tc_sa(Alo) + (uint32_t)p * 2048u;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) Z[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = 0; i < 4; ++i) sts4(H + 16u * (lane + 32 * i), make_float4(0.f, 0.f, 0.f, 0.f));
             __syncwarp();
-            skipped += tc_build(Ahi, w, A, p0, q0, p1, lane, pol_s, pol_k, junk);
+            if (!(c_tc_flags & 1)) skipped += tc_build(tc_sa(Ahi), segv(k), Wc, w, lane, pol_k, junk);
             __syncwarp();
+            if (lane == 0) {
+                tc_arrive(&slotfree[k % kTcSlots]);  // this warp is done with the step's slot
+                TC_ACC(2, t_build);
+            }
+            TC_T0(t_split);
             // tf32 split of this warp's rows: hi in place, lo alongside
-            float4 *H = reinterpret_cast<float4 *>(Ahi) + p * 128;
-            float4 *L = reinterpret_cast<float4 *>(Alo) + p * 128;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const float4 x = H[lane + 32 * i];
+                const float4 x = lds4f(H + 16u * (lane + 32 * i));
                 float4 h, l;
                 h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
                 h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
@@ -407,16 +591,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 l.y = x.y - h.y;
                 l.z = x.z - h.z;
                 l.w = x.w - h.w;
-                H[lane + 32 * i] = h;
-                L[lane + 32 * i] = l;
+                sts4(H + 16u * (lane + 32 * i), h);
+                sts4(L + 16u * (lane + 32 * i), l);
             }
             // generic-proxy stores -> visible to the tensor core (async proxy)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (!(c_tc_flags & 256)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
+            if (lane == 0) TC_ACC(3, t_split);
             if (lane == 0) tc_arrive(&full[s]);
-            ct = ctn;
-            c = cn;
-            p0 = np0; q0 = nq0; p1 = np1;
+            TC_T0(t_mv);
+            Wc = Wn;
+            if (lane == 0) TC_ACC(4, t_mv);
+            if (++c0 == A.nch) c0 = 0;
         }
     } else if (warp == kTcMma) {
         // ===== MMA issuer =====
@@ -428,10 +614,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     const int s = k % kTcStages;
                     const int buf = grp & 1;
                     if (c % kTcGroup == 0) {
+                        TC_T0(t_ae);
                         if (grp >= 2) tc_wait(&accempty[buf], ((grp >> 1) - 1) & 1);
+                        TC_ACC(6, t_ae);
                         tc_fence_after();
                     }
+                    TC_T0(t_full);
                     tc_wait(&full[s], (k / kTcStages) & 1);
+                    TC_ACC(5, t_full);
                     tc_fence_after();
                     const uint32_t st = tc_sa(sm + (size_t)s * kStageBytes);
                     const uint64_t ah = tc_sdesc(st), al = tc_sdesc(st + kTcABytes);
@@ -440,13 +630,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                     for (int kk = 0; kk < kTcCA / 8; ++kk) {
                         const uint64_t o = (uint64_t)((kk * 32) >> 4);  // 8 tf32 = 32 bytes per K step
+                        if (c_tc_flags & 2) continue;
                         tc_mma(d, ah + o, bh + o, id, (c % kTcGroup) != 0 || kk != 0);
                         tc_mma(d, al + o, bh + o, id, 1u);
                         tc_mma(d, ah + o, bl + o, id, 1u);
                     }
-                    tc_commit(&empty[s]);
+                    if (c_tc_flags & 512) tc_arrive(&empty[s]);
+                    else tc_commit(&empty[s]);
                     if (c % kTcGroup == kTcGroup - 1 || c == A.nch - 1) {
-                        tc_commit(&accfull[buf]);
+                        if (c_tc_flags & 512) tc_arrive(&accfull[buf]);
+                        else tc_commit(&accfull[buf]);
                         ++grp;
                     }
                 }
@@ -468,10 +661,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int t = 0; t < N; ++t) acc[t] = 0.f;
             for (int g = 0; g < ngroups; ++g, ++grp) {
                 const int buf = grp & 1;
+                TC_T0(t_af);
                 tc_wait(&accfull[buf], (grp >> 1) & 1);
+                if (lane == 0) TC_ACC(7, t_af);
                 tc_fence_after();
 #pragma unroll
                 for (int j = 0; j < 2 * NJ; ++j) {
+                    if (c_tc_flags & 8) break;
                     float v[16];
                     tc_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * N + 16 * j), v);
 #pragma unroll
@@ -481,7 +677,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 __syncwarp();
                 if (lane == 0) tc_arrive(&accempty[buf]);
             }
-            const int voxel = __ldg(A.slotv + (size_t)ct * kTcTV + row);
+            const int voxel = (c_tc_flags & 64) ? -1 : __ldg(A.slotv + (size_t)ct * kTcTV + row);
             if (voxel >= 0) {
                 const size_t yo = (size_t)voxel * A.nt;
 #pragma unroll
@@ -500,6 +696,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 
     // ---- teardown and fixed-order completion ------------------------------------
+    TC_FLUSH;
     tc_fence_before();
     __syncthreads();
     if (warp == kTcMma) {
@@ -545,17 +742,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
+static size_t tc_stage_bytes(int N) { return (size_t)kTcStages * (2 * kTcABytes + 2 * N * kTcCA * 4); }
+
+// staged entries per step slot: what fits next to the A/B stages (kTcSlots
+// slots x 8 bytes per entry), a multiple of 32
+static int tc_slot_entries(int N)
+{
+    const long avail = 232448L - 1024 - 4096 - (long)tc_stage_bytes(N);  // dyn limit - align - static
+    return (int)std::max(0L, avail / ((long)kTcSlots * 8) / 32 * 32);
+}
+
 static size_t tc_smem_bytes(int N)
 {
-    return (size_t)kTcStages * (2 * kTcABytes + 2 * N * kTcCA * 4) + 1024;  // + alignment slack
+    return tc_stage_bytes(N) + (size_t)kTcSlots * 8 * tc_slot_entries(N) + 1024;  // + alignment slack
 }
 
 template <int NJ>
 static int tc_dsc_t(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
                     const DscOut &o, const CallHooks &h, cudaStream_t st)
 {
-    TcArgs A{phi->t_cr, phi->t_fiber, phi->t_val, phi->t_tptr, phi->t_t1, phi->t_D, phi->t_slotv,
-             phi->nt, phi->t_nch, phi->t_nct};
+    TcArgs A{phi->t_q, phi->t_tptr, phi->t_t1, phi->t_D, phi->t_slotv,
+             phi->nt, phi->t_nch, phi->t_nct, tc_slot_entries(phi->t_n)};
     k_dsc_tc<NJ><<<phi->t_blocks, kTcThreads, phi->t_smem, st>>>(A, w, y, b, flags, phi->red, o, h);
     LIFE_CHECK_LAUNCH();
     return LIFE_OK;
@@ -564,6 +771,8 @@ static int tc_dsc_t(life_phi *phi, const float *w, float *y, const float *b, uin
 template <int NJ>
 static int tc_prepare_t(life_phi *phi)
 {
+    if (tc_slot_entries(32 * NJ) < 512)
+        return fail(LIFE_ERR_CONFIG_INVALID, "tc layout: staging slots do not fit");
     phi->t_smem = tc_smem_bytes(32 * NJ);
     phi->t_W = phi->t_blocks * kTcWarps;
     return ensure_smem(k_dsc_tc<NJ>, phi->t_smem);
@@ -587,3 +796,16 @@ int launch_dsc_tc(life_phi *phi, const float *w, float *y, const float *b, uint3
 int prepare_tc(life_phi *phi) { LIFE_TC_DISPATCH(tc_prepare_t, phi); }
 
 }  // namespace life
+
+#ifdef LIFE_WS_DIAG
+extern "C" LIFE_API int life_debug_tc(int flags, unsigned long long *cyc_out)
+{
+    if (cyc_out) {
+        if (cudaDeviceSynchronize() != cudaSuccess) return 20;
+        if (cudaMemcpyFromSymbol(cyc_out, life::g_tc_cyc, 16 * sizeof(unsigned long long)) != cudaSuccess) return 20;
+        unsigned long long z[16] = {};
+        if (cudaMemcpyToSymbol(life::g_tc_cyc, z, sizeof(z)) != cudaSuccess) return 20;
+    }
+    return cudaMemcpyToSymbol(life::c_tc_flags, &flags, sizeof(int)) == cudaSuccess ? 0 : 20;
+}
+#endif

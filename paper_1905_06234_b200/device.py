@@ -32,11 +32,11 @@ _LAYOUT = ["auto"]
 
 def set_layout(name):
     """fp32 kernel family for operators built from now on: "auto" (density
-    heuristic; dense operators run DSC on the tensor cores), "sparse"
-    (voxel-segment kernels), "dense" (tile kernels, tcgen05 DSC) or "fma"
-    (tile kernels on CUDA cores only)."""
-    if name not in ("auto", "sparse", "dense", "fma"):
-        raise ConfigInvalid(f"layout must be auto/sparse/dense/fma, got {name!r}")
+    heuristic), "sparse" (voxel-segment kernels), "dense" (register-tiled
+    tile kernels on CUDA cores) or "tensor" (tile kernels with DSC on the
+    tcgen05 tensor cores, 3xTF32)."""
+    if name not in ("auto", "sparse", "dense", "tensor"):
+        raise ConfigInvalid(f"layout must be auto/sparse/dense/tensor, got {name!r}")
     _LAYOUT[0] = name
 
 
@@ -96,7 +96,7 @@ class DeviceOperator:
     def _create(self, d, a, v, f, val, dic, stream):
         flags = (N.PHI_EXACT_F64 if self.exact else 0) | (0 if self.fast else N.PHI_NO_FAST_F32)
         flags |= {"auto": 0, "sparse": N.PHI_FORCE_SPARSE, "dense": N.PHI_FORCE_DENSE,
-                  "fma": N.PHI_FORCE_DENSE | N.PHI_NO_TENSOR}[_LAYOUT[0]]
+                  "tensor": N.PHI_FORCE_DENSE | N.PHI_TENSOR}[_LAYOUT[0]]
         dims = N.Dims(d.n_atoms, d.n_voxels, d.n_fibers, d.n_dirs, d.n_coeffs)
         handle = ctypes.c_void_p()
         bad = ctypes.c_int64(-1)

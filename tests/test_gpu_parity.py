@@ -22,13 +22,13 @@ TOL32 = 1e-5
 
 
 # set_layout name -> DeviceOperator.kind it yields (at n_dirs <= 128)
-KIND = {"sparse": "sparse", "fma": "dense", "dense": "tensor"}
+KIND = {"sparse": "sparse", "dense": "dense", "tensor": "tensor"}
 
 
-@pytest.fixture(params=["sparse", "fma", "dense"])
+@pytest.fixture(params=["sparse", "dense", "tensor"])
 def layout(request):
     """Run a test against every fp32 kernel family: voxel-segment (sparse),
-    tile kernels on CUDA cores (fma), tile kernels with tcgen05 DSC (dense)."""
+    tile kernels on CUDA cores (dense), tile kernels with tcgen05 DSC (tensor)."""
     from paper_1905_06234_b200 import device
     device.set_layout(request.param)
     yield request.param

@@ -1,0 +1,3 @@
+#!/bin/bash
+mkdir -p gpurun_out
+LIFE_B200_LIB=$PWD/build/diag/liblife_b200.so timeout 600 python tools/tc_isolate.py > gpurun_out/tc_iso.log 2>&1

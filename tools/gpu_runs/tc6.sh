@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out
+export LIFE_DEBUG=1
+timeout 120 python tools/tc_check.py --c1 > gpurun_out/tc_c1.log 2>&1
+timeout 300 python tools/tc_check.py > gpurun_out/tc_c2.log 2>&1
+echo "rc=$?" >> gpurun_out/tc_c2.log
+unset LIFE_DEBUG
+LIFE_B200_LIB=$PWD/build/diag/liblife_b200.so timeout 600 python tools/tc_isolate.py > gpurun_out/tc_iso.log 2>&1

@@ -22,10 +22,10 @@ rng = np.random.default_rng(1)
 w64 = w_true.copy()
 w = torch.from_numpy(w64).float().cuda()
 res = {}
-for lay in ("dense", "fma"):
+for lay in ("tensor", "dense"):
     device.set_layout(lay)
     t0 = time.time()
-    op = L.DeviceOperator(t, dic, exact=(lay == "fma"))
+    op = L.DeviceOperator(t, dic, exact=(lay == "dense"))
     torch.cuda.synchronize()
     print(f"{lay}: kind={op.kind} build {time.time() - t0:.2f}s", flush=True)
     y = torch.zeros(dims[1] * dims[3], device="cuda")
@@ -40,7 +40,7 @@ for lay in ("dense", "fma"):
     ms = e0.elapsed_time(e1) / args.reps
     res[lay] = y.double().cpu().numpy()
     print(f"{lay}: dsc {ms:.4f} ms  ({12 * dims[4] / ms / 1e6:.0f} GB/s algorithmic idx+val)", flush=True)
-    if lay == "fma":
+    if lay == "dense":
         y64 = torch.zeros(dims[1] * dims[3], dtype=torch.float64, device="cuda")
         op.dsc_f64(torch.from_numpy(w64).cuda(), y64)
         ref = y64.cpu().numpy()
@@ -48,4 +48,4 @@ for lay in ("dense", "fma"):
     torch.cuda.empty_cache()
 device.set_layout("auto")
 rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
-print(f"rel_l2 tensor vs fp64 exact: {rel(res['dense'], ref):.3e}   fma vs fp64: {rel(res['fma'], ref):.3e}")
+print(f"rel_l2 tensor vs fp64 exact: {rel(res['tensor'], ref):.3e}   dense vs fp64: {rel(res['dense'], ref):.3e}")
