@@ -264,3 +264,40 @@ def wc_accumulate(tensor, dictionary, y, w_out, precision=None):
             _accumulate_into(torch, w_out, wd)
     torch.cuda.synchronize()
     return start.elapsed_time(stop) * 1e-3
+
+
+def autotune_layout(problem, trials=3, candidates=("sparse", "dense", "tensor")):
+    """Pick the fp32 kernel family for a problem by timing one DSC + one WC
+    per candidate on the device (the paper's runtime selection between
+    kernel variants, restructure.py:107-144 for
+    the reference's CPU analogue).  Returns (best name, {name: mean seconds}).
+    A candidate whose layout cannot be built for the problem (e.g. the
+    tensor layout above 128 directions) is skipped."""
+    torch = N.require_cuda()
+    d = problem.dims
+    w = torch.from_numpy(np.asarray(problem.w_true if problem.w_true is not None
+                                    else np.ones(d.n_fibers))).float().cuda()
+    y = torch.zeros(d.signal_len, device="cuda")
+    g = torch.zeros(d.n_fibers, device="cuda")
+    ymax = torch.ones(1, device="cuda")
+    saved, times = _LAYOUT[0], {}
+    try:
+        for name in candidates:
+            set_layout(name)
+            op = DeviceOperator(problem.tensor, problem.dictionary)
+            if name != "sparse" and op.kind != name:
+                continue
+            run = lambda: (op.dsc_f32(w, y), op.wc_f32(y, g, y_absmax=ymax))  # noqa: E731
+            run()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(trials):
+                run()
+            e1.record()
+            torch.cuda.synchronize()
+            times[name] = e0.elapsed_time(e1) / 1e3 / trials
+            op.close()
+    finally:
+        set_layout(saved)
+    best = min(times, key=times.get)
+    return best, times
