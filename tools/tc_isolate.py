@@ -23,7 +23,7 @@ w = torch.from_numpy(w_true).float().cuda()
 y = torch.empty(dims[1] * dims[3], device="cuda")
 names = ["slot wait+gather issue", "empty wait", "build", "split", "w move",
          "mma: full wait", "mma: accempty wait", "epi: accfull wait"]
-for fl in [0xff, 0x4ff, 0x6ff, 0x4fe, 0x4fa]:
+for fl in [int(x, 0) for x in os.environ.get('TC_FLAGS', '0,0xff,0x7e,0x7a,0x4').split(',')]:
     lib.life_debug_tc(fl, None)
     for _ in range(2):
         op.dsc_f32(w, y)
