@@ -386,7 +386,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--layout", default="auto", choices=["auto", "sparse", "dense"])
+    ap.add_argument("--layout", default="auto", choices=["auto", "sparse", "dense", "tensor"])
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
