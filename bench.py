@@ -32,6 +32,15 @@ CONFIGS = {
     "c2": (1057, 200_000, 500_000, 96, 100_000_000),
     "c1": (1057, 10_000, 20_000, 96, 5_000_000),
     "c2s": (1057, 50_000, 125_000, 96, 25_000_000),
+    # BASELINE.json configs[3] (quoted on 8 GPUs; Nv assumed):
+    # N_theta = 150 takes the 160-wide register-tiled kernels
+    "c4": (1057, 250_000, 1_000_000, 150, 400_000_000),
+}
+WORKLOADS = {
+    "c2": "C2 STN96-shaped synthetic LiFE problem (BASELINE.json configs[1])",
+    "c1": "C1 synthetic STD LiFE problem (BASELINE.json configs[0])",
+    "c2s": "C2 at quarter scale",
+    "c4": "C4 probabilistic-tractography scale, N_theta=150 (BASELINE.json configs[3])",
 }
 METRIC = "SBBNNLS iters/sec"
 UNIT = "it/s"
@@ -198,12 +207,11 @@ def run_reference(args, dims):
 
 def workload_config(dims, args, world):
     na, nv, nf, nt, nc = dims
-    return {"workload": f"{args.config.upper()} STN96-shaped synthetic LiFE problem "
-                        f"(BASELINE.json configs[1])" if args.config == "c2" else args.config,
+    return {"workload": WORKLOADS.get(args.config, args.config),
             "n_atoms": na, "n_voxels": nv, "n_fibers": nf, "n_dirs": nt, "n_coeffs": nc,
             "mean_run_length": round(1.04 * nc / nv, 3), "noise_sigma": 0.1, "seed": 0,
             "parallelism": f"voxel-shard x{world}" if world > 1 else "1 GPU",
-            "l2": "inputs larger than L2 (Phi alone 1.2 GB vs 126 MB L2)"}
+            "l2": f"inputs larger than L2 (Phi alone {nc * 12 / 1e9:.1f} GB vs 126 MB L2)"}
 
 
 # ---------------------------------------------------------------------------
@@ -315,7 +323,7 @@ def run_ours(args, dims):
         dom, ach, traffic_key = "wc", wc_gbs, "wc"
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and args.config == "c2" and world == 1:  # captured on C2, 1 GPU
         try:
             with open(prof) as f:
                 traffic = json.load(f).get(traffic_key)
