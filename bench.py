@@ -355,6 +355,7 @@ def run_ours(args, dims):
         h2d = nc * (4 * 3 + 8) + na * nt * 8 + nv * nt * 8
         e2e = {"value": args.steps / e2e_s, "unit": UNIT,
                "setup_s": round(tr.setup_seconds, 3), "loop_s": round(tr.loop_seconds, 4),
+               "other_s": round(e2e_s - tr.setup_seconds - tr.loop_seconds, 3),
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": nf * 8 // args.steps,
                "seconds": round(e2e_s, 3),
                "what": f"one solve() of {args.steps} iterations from host numpy arrays: "
