@@ -263,6 +263,7 @@ def run_ours(args, dims):
     info["restructure_ms"] = round(op.info.sort_ms, 1)
     info["atom_groups"] = op.info.atom_groups
     info["kernels"] = op.kind
+    info["tensor_cores"] = list(op.tensor_ops)
     w = torch.empty(nf, dtype=torch.float32, device="cuda")
     scfg = L.SolverConfig(max_iters=total_iters, grad_tol=0.0)
     sess = L.sbbnnls.SolverSession(op, b, w, scfg, comm=comm)
@@ -395,7 +396,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--layout", default="auto", choices=["auto", "sparse", "dense", "tensor"])
+    ap.add_argument("--layout", default="auto", choices=["auto", "sparse", "dense", "fma", "tensor"])
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -88,8 +88,8 @@ LIFE_API uint64_t life_launch_count(void);
 #define LIFE_PHI_NO_FAST_F32  0x4u  /* skip the fp32 fast layout           */
 #define LIFE_PHI_FORCE_SPARSE 0x8u  /* fp32: voxel-segment kernels only    */
 #define LIFE_PHI_FORCE_DENSE  0x10u /* fp32: register-tiled dense kernels  */
-#define LIFE_PHI_NO_TENSOR    0x20u /* fp32: never build the tcgen05 DSC layout */
-#define LIFE_PHI_TENSOR       0x40u /* fp32: also build it; DSC runs on tcgen05 */
+#define LIFE_PHI_NO_TENSOR    0x20u /* fp32: no tcgen05 products (CUDA cores only) */
+#define LIFE_PHI_TENSOR       0x40u /* fp32: DSC on tcgen05 too (WC is by default) */
 
 /* Build the device operator from COO arrays (PhiTensor + Dictionary,
  * tensor.py:76-170).  atoms/voxels/fibers: u32[n_coeffs]; values:
@@ -117,6 +117,8 @@ typedef struct life_phi_info {
     int64_t max_voxel_run;      /* longest voxel segment                  */
     int64_t device_bytes;       /* bytes owned by the handle              */
     double sort_ms;             /* restructuring time at create           */
+    int32_t tensor_ops;         /* products on tcgen05: bit 0 DSC, bit 1 WC */
+    int32_t reserved;
 } life_phi_info;
 LIFE_API int life_phi_get_info(const life_phi *phi, life_phi_info *info);
 

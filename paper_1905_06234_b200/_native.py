@@ -41,7 +41,8 @@ class PhiInfo(ctypes.Structure):
     _fields_ = [("dims", Dims), ("atom_groups", c_i32), ("atoms_per_group", c_i32),
                 ("n_warps", c_i32), ("has_exact", c_i32), ("n_voxel_runs", c_i64),
                 ("n_fiber_runs", c_i64), ("max_fiber_run", c_i64),
-                ("max_voxel_run", c_i64), ("device_bytes", c_i64), ("sort_ms", c_double)]
+                ("max_voxel_run", c_i64), ("device_bytes", c_i64), ("sort_ms", c_double),
+                ("tensor_ops", c_i32), ("reserved", c_i32)]
 
 
 class SpmvOut(ctypes.Structure):

@@ -104,6 +104,7 @@ struct life_phi {
     float *d_val = nullptr;
     uint32_t *d_tptr = nullptr;   // [n_tiles*n_chunks + 1]
     float *d_D = nullptr;         // [n_chunks][64][nt_pad] zero padded
+    float *d_Bwc = nullptr;       // ws WC on tcgen05: [n_chunks][hi|lo][nt_pad/32][32][32] swizzled
     int n_tiles = 0, n_chunks = 0, nt_pad = 0, d_blocks = 0, d_W = 0;
     int d_kind = 0;       // 1: register-tiled v1 (life_dense.cu), 2: warp-specialized (life_ws.cu)
     int d_tv = 0;         // voxels per tile
@@ -240,6 +241,7 @@ int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
 int prepare_spmv(life_phi *phi);
 int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
                 const double *val, const std::vector<double> &hdict, cudaStream_t st);
+int build_wc_tc(life_phi *phi, const std::vector<double> &hdict, cudaStream_t st);
 int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
              const double *val, const std::vector<double> &hdict, cudaStream_t st);
 int launch_dsc_tc(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,

@@ -942,6 +942,32 @@ static void tf32_split(float x, float &hi, float &lo)
     lo = x - hi;
 }
 
+// B operand of the tensor-core WC (k_wc_tc): per chunk the dictionary rows
+// of its 32 atoms (N) over nt_pad directions (K), K-major SWIZZLE_128B in
+// blocks of 32 directions (4 KB each), split into tf32 hi and lo
+int build_wc_tc(life_phi *phi, const std::vector<double> &hdict, cudaStream_t st)
+{
+    if (phi->d_kind != 2 || phi->nt_pad % 32 != 0 || phi->d_ca != 32) return LIFE_OK;
+    const int nkb = phi->nt_pad / 32, nch = phi->n_chunks;
+    const size_t per = (size_t)2 * nkb * 32 * 32;
+    std::vector<float> hB((size_t)nch * per, 0.f);
+    for (int c = 0; c < nch; ++c)
+        for (int n = 0; n < 32; ++n)
+            for (int t = 0; t < phi->nt_pad; ++t) {
+                const int at = c * 32 + n;
+                const float x = (at < phi->na && t < phi->nt) ? (float)hdict[(size_t)at * phi->nt + t] : 0.f;
+                float hi, lo;
+                tf32_split(x, hi, lo);
+                const size_t o = (size_t)c * per + (size_t)(t / 32) * 1024 + tc_cell(n, t % 32);
+                hB[o] = hi;
+                hB[o + (size_t)nkb * 1024] = lo;
+            }
+    LIFE_TRY(dalloc(phi, &phi->d_Bwc, hB.size()));
+    LIFE_CUDA(cudaMemcpyAsync(phi->d_Bwc, hB.data(), hB.size() * 4, cudaMemcpyHostToDevice, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    return LIFE_OK;
+}
+
 int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
              const double *val, const std::vector<double> &hdict, cudaStream_t st)
 {

@@ -39,6 +39,7 @@
 #include <algorithm>
 
 #include "life_common.cuh"
+#include "life_tcgen05.cuh"
 
 namespace life {
 
@@ -1132,6 +1133,265 @@ __global__ void __launch_bounds__(kWcThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// WC with Z = Y . D^T on the tensor cores (k_wc_tc)
+// ---------------------------------------------------------------------------
+// Same layout, schedule and RED-scatter producers as k_wc_ws; the 8 FFMA
+// consumer warps are replaced by tcgen05:
+//   warps 0-3  RED producers (unchanged code path, segments read from global
+//              memory with an L2 prefetch one step ahead).
+//   warps 4-7  "YZ": at each CTA tile, y rows (thread = voxel = TMEM lane,
+//              two 128-voxel halves) are split into tf32 hi/lo and stored in
+//              TMEM (A operand); per step the Z accumulators are read back
+//              from TMEM and stored to shared memory as the 32 x 32 tiles the
+//              producers expect (cell = atom * 32 + voxel slot).
+//   warp 8     MMA issuer: per half, 3xTF32 over K = directions (M = 128
+//              voxels, N = 32 atoms), A from TMEM, B = the pre-split,
+//              pre-swizzled dictionary chunk (K-major, 3 blocks of 32
+//              directions) staged by producer 0's bulk copy.
+// TMEM (512 columns): Y half h at h*2*ntp (hi) and h*2*ntp + ntp (lo), Z
+// buffers at 4*ntp + s*64 + h*32.  Z accumulates 3*ntp/8 MMAs (36 at 96
+// directions: ~2e-6 relative, tools/ubench/tc_probe.cu).
+constexpr int kWtYZ = 4;
+constexpr int kWtMma = kWcProd + kWtYZ;     // warp 8
+constexpr int kWtWarps = kWtMma + 1;
+constexpr int kWtThreads = kWtWarps * 32;
+
+struct WtArgs {
+    const float *B;   // [nch][hi|lo][nkb][32 atoms][32 dirs] swizzled
+    int nkb;          // direction blocks of 32 (ntp = 32 * nkb <= 96)
+};
+
+// Z is single-buffered in shared memory (the TMEM accumulators are double
+// buffered) so the producers' TMA-staged segment slots still fit.
+template <bool STAGED>
+__global__ void __launch_bounds__(kWtThreads, 1)
+    k_wc_tc(const WsArgs A, const WtArgs T, const float *__restrict__ y, const WsFix fx, const CallHooks hooks)
+{
+    extern __shared__ __align__(1024) unsigned char wt_raw[];
+    __shared__ __align__(8) uint64_t bfull[2], bempty[2], zfull[2], zempty[2], accfull[2], accempty[2];
+    __shared__ __align__(8) uint64_t yready, yfree, slotbar[kWcProd][2];
+    __shared__ uint32_t tmem_base;
+    if (hooks.done && *hooks.done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
+    unsigned char *sm = (unsigned char *)(((uintptr_t)wt_raw + 1023) & ~(uintptr_t)1023);
+    const int ntp = 32 * T.nkb;
+    const unsigned bbytes = 2u * (unsigned)T.nkb * 4096u;  // hi | lo
+    unsigned char *Bbuf = sm;                               // 2 stages
+    float *Zbuf = reinterpret_cast<float *>(sm + 2 * bbytes);  // 1 stage
+    float *slots = Zbuf + kWsCons * kWsCells;
+    const int n_ct = (A.n_tiles + kWsCons - 1) / kWsCons;
+    int s_begin, s_end;
+    step_range(n_ct, A.nch, s_begin, s_end);
+    const int total = s_end - s_begin;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            bar_init(&bfull[s], 1);
+            bar_init(&bempty[s], 1);
+            bar_init(&zfull[s], kWtYZ);
+            bar_init(&zempty[s], kWcProd);
+            bar_init(&accfull[s], 1);
+            bar_init(&accempty[s], kWtYZ);
+        }
+        bar_init(&yready, kWtYZ);
+        bar_init(&yfree, 1);
+        for (int p = 0; p < kWcProd; ++p)
+            for (int s = 0; s < 2; ++s) bar_init(&slotbar[p][s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == kWtMma) tcg::alloc(&tmem_base, 512);
+    tcg::fence_before();
+    __syncthreads();
+    tcg::fence_after();
+    const uint32_t tmem = tmem_base;
+
+    if (warp < kWcProd) {
+        // ===== producers: dictionary chunks (bulk copy), RED scatter =====
+        const int p = warp;
+        const int ex = fix_exponent(fx, A.nt);
+        const double scale = ldexp(1.0, ex);
+        const bool f32_scale = ex >= -120 && ex <= 120;
+        const float scalef = f32_scale ? ldexpf(1.f, ex) : 1.f;
+        int ct0 = s_begin / A.nch, c0 = s_begin % A.nch, ct1 = ct0, c1 = c0, ct2, c2;
+        if (p == 0 && lane == 0 && total > 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_arrive_tx(&bfull[0], bbytes);
+            bulk_g2s(Bbuf, T.B + (size_t)c0 * (bbytes / 4), bbytes, &bfull[0]);
+        }
+        step_next(ct1, c1, A.nch);
+        ct2 = ct1; c2 = c1;
+        step_next(ct2, c2, A.nch);
+        Seg cur{}, nxt{};
+        if (total > 0) {
+            cur = wc_seg_of(A, ct0, c0, p);
+            if (STAGED && lane == 0) wc_stage_issue(A, cur, slots, p, 0, &slotbar[p][0]);
+        }
+        if (total > 1) {
+            nxt = wc_seg_of(A, ct1, c1, p);
+            prefetch_seg(A, nxt, lane);
+        }
+        for (int k = 0; k < total; ++k) {
+            const int s = k & 1;
+            if (p == 0 && lane == 0 && k + 1 < total) {
+                const int s1 = (k + 1) & 1;
+                if (k + 1 >= 2) bar_wait(&bempty[s1], ((k - 1) >> 1) & 1);
+                bar_arrive_tx(&bfull[s1], bbytes);
+                bulk_g2s(Bbuf + (size_t)s1 * bbytes, T.B + (size_t)c1 * (bbytes / 4), bbytes, &bfull[s1]);
+            }
+            __syncwarp();
+            Seg nn{};
+            if (k + 2 < total) nn = wc_seg_of(A, ct2, c2, p);
+            if (STAGED && k + 1 < total && lane == 0)
+                wc_stage_issue(A, nxt, slots, p, s ^ 1, &slotbar[p][s ^ 1]);
+            if (k + 2 < total) prefetch_seg(A, nn, lane);
+            if (STAGED) bar_wait(&slotbar[p][s], (k >> 1) & 1);
+            bar_wait(&zfull[0], k & 1);
+            const float *Z = Zbuf + (2 * p) * kWsCells;
+            const View V = STAGED ? wc_slot_view(slots, p, s) : global_view(A, cur);
+            const uint32_t mid = cur.q0 - cur.p0;
+            const uint32_t n = cur.p1 - cur.p0;
+            constexpr int kB = 4;
+            for (uint32_t base = 0; base < n; base += 128u * kB) {
+                uint4 cr[kB], f[kB];
+                float4 v[kB];
+#pragma unroll
+                for (int j = 0; j < kB; ++j) {
+                    const uint32_t kk = base + 128u * j + 4u * (uint32_t)lane;
+                    if (kk < n) {
+                        cr[j] = ldv<STAGED>(reinterpret_cast<const uint4 *>(V.cr + kk));
+                        f[j] = ldv<STAGED>(reinterpret_cast<const uint4 *>(V.f + kk));
+                        v[j] = ldv<STAGED>(reinterpret_cast<const float4 *>(V.v + kk));
+                    } else {
+                        cr[j] = make_uint4(kPadBit, kPadBit, kPadBit, kPadBit);
+                        f[j] = make_uint4(0u, 0u, 0u, 0u);
+                        v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kB; ++j) {
+                    const uint32_t kk = base + 128u * j + 4u * (uint32_t)lane;
+                    const float *Zt = Z + (kk >= mid ? kWsCells : 0);
+                    wc_scatter1(cr[j].x, f[j].x, v[j].x, Zt, fx, f32_scale, scalef, scale);
+                    wc_scatter1(cr[j].y, f[j].y, v[j].y, Zt, fx, f32_scale, scalef, scale);
+                    wc_scatter1(cr[j].z, f[j].z, v[j].z, Zt, fx, f32_scale, scalef, scale);
+                    wc_scatter1(cr[j].w, f[j].w, v[j].w, Zt, fx, f32_scale, scalef, scale);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(&zempty[0]);
+            cur = nxt;
+            nxt = nn;
+            ct0 = ct1; c0 = c1;
+            ct1 = ct2; c1 = c2;
+            step_next(ct2, c2, A.nch);
+        }
+    } else if (warp < kWtMma) {
+        // ===== YZ warps: y -> TMEM (A operand), Z TMEM -> shared =====
+        const int q = warp & 3;  // TMEM lane quarter
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        int k = 0, tiles = 0;
+        for (int st = s_begin; st < s_end;) {
+            const int ct = st / A.nch, cb = st % A.nch;
+            const int ce = min(A.nch, cb + (s_end - st));
+            st += ce - cb;
+            if (tiles > 0) bar_wait(&yfree, (tiles - 1) & 1);
+            tcg::fence_after();
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int row = h * 128 + q * 32 + lane;
+                const int tile = ct * kWsCons + row / kWsTV;
+                const int voxel = tile < A.n_tiles ? __ldg(A.slotv + (size_t)ct * (kWsCons * kWsTV) + row) : -1;
+                const float *yr = y + (size_t)(voxel < 0 ? 0 : voxel) * A.nt;
+#pragma unroll 1
+                for (int kb = 0; kb < T.nkb; ++kb) {
+                    uint32_t hv[32], lv[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int t = kb * 32 + i;
+                        const float x = (voxel >= 0 && t < A.nt) ? __ldg(yr + t) : 0.f;
+                        const uint32_t hb = tcg::hi_bits(__float_as_uint(x));
+                        hv[i] = hb;
+                        lv[i] = __float_as_uint(x - __uint_as_float(hb));
+                    }
+                    tcg::st32(tmem + lane_base + (uint32_t)(h * 2 * ntp + kb * 32), hv);
+                    tcg::st32(tmem + lane_base + (uint32_t)(h * 2 * ntp + ntp + kb * 32), lv);
+                }
+            }
+            tcg::wait_st();
+            tcg::fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&yready);
+            ++tiles;
+            for (int c = cb; c < ce; ++c, ++k) {
+                const int s = k & 1;
+                bar_wait(&accfull[s], (k >> 1) & 1);
+                if (k >= 1) bar_wait(&zempty[0], (k - 1) & 1);
+                tcg::fence_after();
+                float *Zs = Zbuf;
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t zr[32];
+                    tcg::ld32(tmem + lane_base + (uint32_t)(4 * ntp + s * 64 + h * 32), zr);
+                    // tile h*4 + q, cell = atom * 32 + voxel slot (= lane)
+                    float *Zt = Zs + (h * 4 + q) * kWsCells + lane;
+#pragma unroll
+                    for (int a = 0; a < 32; ++a) Zt[a * kWsTV] = __uint_as_float(zr[a]);
+                }
+                tcg::fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    bar_arrive(&accempty[s]);
+                    bar_arrive(&zfull[0]);
+                }
+            }
+        }
+    } else {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            const uint32_t id = tcg::idesc_tf32(128, 32);
+            int k = 0, tiles = 0;
+            for (int st = s_begin; st < s_end;) {
+                const int cb = st % A.nch;
+                const int ce = min(A.nch, cb + (s_end - st));
+                st += ce - cb;
+                bar_wait(&yready, tiles & 1);
+                ++tiles;
+                for (int c = cb; c < ce; ++c, ++k) {
+                    const int s = k & 1;
+                    bar_wait(&bfull[s], (k >> 1) & 1);
+                    if (k >= 2) bar_wait(&accempty[s], ((k - 2) >> 1) & 1);
+                    tcg::fence_after();
+                    const uint32_t bs = tcg::sa(Bbuf + (size_t)s * bbytes);
+                    const uint64_t bh = tcg::sdesc(bs), bl = tcg::sdesc(bs + (uint32_t)T.nkb * 4096u);
+#pragma unroll 1
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t d = tmem + (uint32_t)(4 * ntp + s * 64 + h * 32);
+                        const uint32_t ay = tmem + (uint32_t)(h * 2 * ntp);
+#pragma unroll 1
+                        for (int kk = 0; kk < ntp / 8; ++kk) {
+                            const uint64_t o = (uint64_t)((((kk >> 2) * 4096) + (kk & 3) * 32) >> 4);
+                            tcg::mma_ts(d, ay + 8u * kk, bh + o, id, kk != 0);
+                            tcg::mma_ts(d, ay + (uint32_t)ntp + 8u * kk, bh + o, id, 1u);
+                            tcg::mma_ts(d, ay + 8u * kk, bl + o, id, 1u);
+                        }
+                    }
+                    tcg::commit(&bempty[s]);
+                    tcg::commit(&accfull[s]);
+                    if (c == ce - 1) tcg::commit(&yfree);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    tcg::fence_before();
+    __syncthreads();
+    if (warp == kWtMma) {
+        tcg::fence_after();
+        tcg::dealloc(tmem, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 template <int DPL, bool STAGED>
@@ -1184,9 +1444,31 @@ int launch_dsc_ws(life_phi *phi, const float *w, float *y, const float *b, uint3
     LIFE_WS_DISPATCH(ws_dsc_t, phi, w, y, b, flags, o, h, st);
 }
 
+size_t wc_tc_smem_bytes(int nkb, bool staged)
+{
+    return 1024 + 2 * (size_t)2 * nkb * 4096 + (size_t)kWsCons * kWsCells * 4 +
+           (staged ? (size_t)kWcProd * 2 * 3 * kWcSlot * 4 : 0);
+}
+
 int launch_wc_ws(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
                  cudaStream_t st)
 {
+    if (phi->d_Bwc) {
+        const bool staged = phi->d_staged && wc_tc_smem_bytes(phi->nt_pad / 32, true) <= 232448 - 2048;
+        const size_t smem = wc_tc_smem_bytes(phi->nt_pad / 32, staged);
+        WsArgs A{phi->d_cr, phi->d_fiber, phi->d_val, phi->d_tptr, phi->d_t1, phi->d_D,
+                 phi->d_slotv, phi->nv, phi->nt, phi->nt_pad, phi->n_chunks, phi->n_tiles, phi->na};
+        WtArgs T{phi->d_Bwc, phi->nt_pad / 32};
+        if (staged) {
+            LIFE_TRY(ensure_smem(k_wc_tc<true>, smem));
+            k_wc_tc<true><<<phi->d_blocks, kWtThreads, smem, st>>>(A, T, y, fx, h);
+        } else {
+            LIFE_TRY(ensure_smem(k_wc_tc<false>, smem));
+            k_wc_tc<false><<<phi->d_blocks, kWtThreads, smem, st>>>(A, T, y, fx, h);
+        }
+        LIFE_CHECK_LAUNCH();
+        return LIFE_OK;
+    }
     LIFE_WS_DISPATCH(ws_wc_t, phi, fx, y, h, st);
 }
 

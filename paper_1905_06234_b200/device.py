@@ -32,11 +32,11 @@ _LAYOUT = ["auto"]
 
 def set_layout(name):
     """fp32 kernel family for operators built from now on: "auto" (density
-    heuristic), "sparse" (voxel-segment kernels), "dense" (register-tiled
-    tile kernels on CUDA cores) or "tensor" (tile kernels with DSC on the
-    tcgen05 tensor cores, 3xTF32)."""
-    if name not in ("auto", "sparse", "dense", "tensor"):
-        raise ConfigInvalid(f"layout must be auto/sparse/dense/tensor, got {name!r}")
+    heuristic), "sparse" (voxel-segment kernels), "dense" (tile kernels: DSC
+    on CUDA cores, WC's Z = Y.D^T on the tcgen05 tensor cores), "fma" (tile
+    kernels on CUDA cores only) or "tensor" (DSC on the tensor cores too)."""
+    if name not in ("auto", "sparse", "dense", "fma", "tensor"):
+        raise ConfigInvalid(f"layout must be auto/sparse/dense/fma/tensor, got {name!r}")
     _LAYOUT[0] = name
 
 
@@ -96,6 +96,7 @@ class DeviceOperator:
     def _create(self, d, a, v, f, val, dic, stream):
         flags = (N.PHI_EXACT_F64 if self.exact else 0) | (0 if self.fast else N.PHI_NO_FAST_F32)
         flags |= {"auto": 0, "sparse": N.PHI_FORCE_SPARSE, "dense": N.PHI_FORCE_DENSE,
+                  "fma": N.PHI_FORCE_DENSE | N.PHI_NO_TENSOR,
                   "tensor": N.PHI_FORCE_DENSE | N.PHI_TENSOR}[_LAYOUT[0]]
         dims = N.Dims(d.n_atoms, d.n_voxels, d.n_fibers, d.n_dirs, d.n_coeffs)
         handle = ctypes.c_void_p()
@@ -118,6 +119,12 @@ class DeviceOperator:
         kernel family this operator uses."""
         g = self.info.atom_groups
         return "sparse" if g > 0 else "tensor" if g < 0 else "dense"
+
+    @property
+    def tensor_ops(self):
+        """Products running on the tcgen05 tensor cores: subset of {"dsc", "wc"}."""
+        t = self.info.tensor_ops
+        return tuple(n for b, n in ((1, "dsc"), (2, "wc")) if t & b)
 
     @property
     def handle(self):
@@ -266,7 +273,7 @@ def wc_accumulate(tensor, dictionary, y, w_out, precision=None):
     return start.elapsed_time(stop) * 1e-3
 
 
-def autotune_layout(problem, trials=3, candidates=("sparse", "dense", "tensor")):
+def autotune_layout(problem, trials=3, candidates=("sparse", "dense", "fma", "tensor")):
     """Pick the fp32 kernel family for a problem by timing one DSC + one WC
     per candidate on the device (the paper's runtime selection between
     kernel variants, restructure.py:107-144 for
@@ -285,7 +292,7 @@ def autotune_layout(problem, trials=3, candidates=("sparse", "dense", "tensor"))
         for name in candidates:
             set_layout(name)
             op = DeviceOperator(problem.tensor, problem.dictionary)
-            if name != "sparse" and op.kind != name:
+            if name != "sparse" and op.kind != {"fma": "dense"}.get(name, name):
                 continue
             run = lambda: (op.dsc_f32(w, y), op.wc_f32(y, g, y_absmax=ymax))  # noqa: E731
             run()

@@ -22,13 +22,15 @@ TOL32 = 1e-5
 
 
 # set_layout name -> DeviceOperator.kind it yields (at n_dirs <= 128)
-KIND = {"sparse": "sparse", "dense": "dense", "tensor": "tensor"}
+KIND = {"sparse": "sparse", "dense": "dense", "fma": "dense", "tensor": "tensor"}
+TENSOR_OPS = {"sparse": (), "dense": ("wc",), "fma": (), "tensor": ("dsc", "wc")}
 
 
-@pytest.fixture(params=["sparse", "dense", "tensor"])
+@pytest.fixture(params=["sparse", "dense", "fma", "tensor"])
 def layout(request):
     """Run a test against every fp32 kernel family: voxel-segment (sparse),
-    tile kernels on CUDA cores (dense), tile kernels with tcgen05 DSC (tensor)."""
+    tile kernels with WC on tcgen05 (dense), tile kernels on CUDA cores only
+    (fma), tile kernels with DSC and WC on tcgen05 (tensor)."""
     from paper_1905_06234_b200 import device
     device.set_layout(request.param)
     yield request.param
@@ -347,6 +349,7 @@ def test_fp32_repeat_bitwise_and_accumulate(layout):
                                                         seed=4))
     op = L.DeviceOperator(t, dic)
     assert op.kind == KIND[layout]
+    assert op.tensor_ops == TENSOR_OPS[layout]
     if layout == "sparse":
         assert op.info.atom_groups == 2  # 1057 x 96 fp32 exceeds one CTA's shared memory
     w = torch.from_numpy(w_true).float().cuda()

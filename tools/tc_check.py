@@ -39,13 +39,31 @@ for lay in ("tensor", "dense"):
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.reps
     res[lay] = y.double().cpu().numpy()
+    g = torch.zeros(dims[2], device="cuda")
+    ymax = torch.ones(1, device="cuda") * float(y.abs().max())
+    op.wc_f32(y, g, y_absmax=ymax)
+    e0.record()
+    for _ in range(args.reps):
+        op.wc_f32(y, g, y_absmax=ymax)
+    e1.record(); torch.cuda.synchronize()
+    print(f"{lay}: wc {e0.elapsed_time(e1) / args.reps:.4f} ms", flush=True)
+    res[lay + "_wc"] = g.double().cpu().numpy()
+    if lay == "tensor":
+        y_in = y.clone()
     print(f"{lay}: dsc {ms:.4f} ms  ({12 * dims[4] / ms / 1e6:.0f} GB/s algorithmic idx+val)", flush=True)
     if lay == "dense":
         y64 = torch.zeros(dims[1] * dims[3], dtype=torch.float64, device="cuda")
         op.dsc_f64(torch.from_numpy(w64).cuda(), y64)
         ref = y64.cpu().numpy()
+        g64 = torch.zeros(dims[2], dtype=torch.float64, device="cuda")
+        op.wc_f64(y_in.double(), g64)
+        ref_wc = g64.cpu().numpy()
+        gd = torch.zeros(dims[2], device="cuda")
+        op.wc_f32(y_in, gd, y_absmax=torch.ones(1, device="cuda") * float(y_in.abs().max()))
+        res["dense_wc_same_y"] = gd.double().cpu().numpy()
     del op
     torch.cuda.empty_cache()
 device.set_layout("auto")
 rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
-print(f"rel_l2 tensor vs fp64 exact: {rel(res['tensor'], ref):.3e}   dense vs fp64: {rel(res['dense'], ref):.3e}")
+print(f"DSC rel_l2 tensor vs fp64 exact: {rel(res['tensor'], ref):.3e}   dense vs fp64: {rel(res['dense'], ref):.3e}")
+print(f"WC  rel_l2 tensor vs fp64 exact: {rel(res['tensor_wc'], ref_wc):.3e}   dense vs fp64: {rel(res['dense_wc_same_y'], ref_wc):.3e}")

@@ -299,8 +299,140 @@ int chain(int nch, bool sparse)
     return 0;
 }
 
+// A operand from TMEM ("ts" form): A (128 x 32 fp32) written to TMEM lanes
+// (row m -> lane m, k -> column a0 + k) with tcgen05.st; B (N x 32) K-major in
+// shared memory; D = A . B^T in TMEM; plain tf32 (1 term) and 3xTF32.
+template <int N>
+__global__ void k_ts(const float *A, const float *B, float *out, float *out3)
+{
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    unsigned char *sm = (unsigned char *)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+    unsigned char *Bhi = sm, *Blo = sm + N * 128;
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < N * K; i += blockDim.x) {
+        const int r = i / K, k = i % K;
+        const float x = B[i], h = tf32_hi(x);
+        *(float *)(Bhi + sw128(r, k)) = h;
+        *(float *)(Blo + sw128(r, k)) = x - h;
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(sa(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = tmem_base;
+    // A hi at columns 128.., A lo at columns 160.. ; D1 at 0.., D3 at 64..
+    {
+        const int row = warp * 32 + lane;
+        uint32_t hv[32], lv[32];
+        for (int k = 0; k < 32; ++k) {
+            const float x = A[row * K + k], h = tf32_hi(x);
+            hv[k] = __float_as_uint(h);
+            lv[k] = __float_as_uint(x - h);
+        }
+        const uint32_t ah = tm + ((uint32_t)(warp * 32) << 16) + 128u, al = ah + 32u;
+#define ST32(addr, v) asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" \
+        ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), \
+          "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]) : "memory")
+        ST32(ah, hv);
+        ST32(al, lv);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (threadIdx.x == 0) {
+        constexpr uint32_t id = idesc_tf32(M, N);
+        const uint64_t bh = sdesc(sa(Bhi)), bl = sdesc(sa(Blo));
+        for (int k = 0; k < K / 8; ++k) {
+            const uint64_t o = (uint64_t)(k * 32 >> 4);
+            const uint32_t ah = tm + 128u + 8u * k, al = tm + 160u + 8u * k;
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm), "r"(ah), "l"(bh + o), "r"(id), "r"((uint32_t)(k != 0)));
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + 64u), "r"(ah), "l"(bh + o), "r"(id), "r"((uint32_t)(k != 0)));
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + 64u), "r"(al), "l"(bh + o), "r"(id), "r"(1u));
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + 64u), "r"(ah), "l"(bl + o), "r"(id), "r"(1u));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(&bar)) : "memory");
+    }
+    __syncthreads();
+    {
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n}"
+                         : "=r"(ok) : "r"(sa(&bar)) : "memory");
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = warp * 32 + lane;
+    for (int pass = 0; pass < 2; ++pass) {
+        uint32_t v[32];
+        const uint32_t addr = tm + ((uint32_t)(warp * 32) << 16) + (pass ? 64u : 0u);
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                     "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                       "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                       "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                       "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                     : "r"(addr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float *o = pass ? out3 : out;
+        for (int j = 0; j < N; ++j) o[row * N + j] = __uint_as_float(v[j]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm));
+}
+
+int ts_test()
+{
+    constexpr int N = 32;
+    std::mt19937 g(5);
+    std::normal_distribution<float> nd;
+    std::vector<float> A(M * K), B(N * K), o1(M * N), o3(M * N);
+    for (auto &x : A) x = nd(g);
+    for (auto &x : B) x = nd(g);
+    float *dA, *dB, *d1, *d3;
+    CK(cudaMalloc(&dA, A.size() * 4));
+    CK(cudaMalloc(&dB, B.size() * 4));
+    CK(cudaMalloc(&d1, o1.size() * 4));
+    CK(cudaMalloc(&d3, o3.size() * 4));
+    CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
+    const int smem = 2 * N * 128 + 1024;
+    CK(cudaFuncSetAttribute(k_ts<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_ts<N><<<1, 128, smem>>>(dA, dB, d1, d3);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(o1.data(), d1, o1.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(o3.data(), d3, o3.size() * 4, cudaMemcpyDeviceToHost));
+    double n1 = 0, n3 = 0, den = 0;
+    for (int m = 0; m < M; ++m)
+        for (int n = 0; n < N; ++n) {
+            double r = 0;
+            for (int k = 0; k < K; ++k) r += (double)A[m * K + k] * B[n * K + k];
+            n1 += (o1[m * N + n] - r) * (o1[m * N + n] - r);
+            n3 += (o3[m * N + n] - r) * (o3[m * N + n] - r);
+            den += r * r;
+        }
+    printf("ts (A in TMEM) N=%d: 1xTF32 rel_l2=%.3e  3xTF32 rel_l2=%.3e\n", N, sqrt(n1 / den), sqrt(n3 / den));
+    return 0;
+}
+
 int main()
 {
+    if (ts_test()) return 1;
     if (chain(34, true) || chain(34, false) || chain(136, true)) return 1;
     if (run<96>(1)) return 1;
     if (run<32>(1)) return 1;
