@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (hooks.done && *hooks.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
-    const int chunk_floats = kWsCA * A.nt_pad;
+    const int chunk_floats = kWsCA * 8 * DPL;  // nt_pad == 8 * DPL
     const unsigned chunk_bytes = (unsigned)chunk_floats * 4u;
     float *Dbuf = sm;
     float *Cbuf = sm + 2 * chunk_floats;
@@ -660,7 +660,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                         const float4 c1 = *reinterpret_cast<const float4 *>(C + a * kWsTV + 4);
                         const unsigned long long cp[4] = {wpk(c0.x, c0.y), wpk(c0.z, c0.w),
                                                           wpk(c1.x, c1.y), wpk(c1.z, c1.w)};
-                        const float4 *d4 = reinterpret_cast<const float4 *>(D + a * A.nt_pad);
+                        // nt_pad == 8 * DPL (dispatch): a compile-time stride folds into LDS offsets
+                        const float4 *d4 = reinterpret_cast<const float4 *>(D + a * (8 * DPL));
 #pragma unroll
                         for (int i = 0; i < DPL / 4; ++i) {
                             const float4 t = d4[i];
@@ -1017,7 +1018,7 @@ __global__ void __launch_bounds__(kWcThreads, 1)
                         for (int i = 0; i < DPL / 4; ++i) {
 #pragma unroll
                             for (int aa = 0; aa < kWcAtoms; ++aa) {
-                                const float4 t = reinterpret_cast<const float4 *>(D + (a0 + aa) * A.nt_pad)[i];
+                                const float4 t = reinterpret_cast<const float4 *>(D + (a0 + aa) * (8 * DPL))[i];
                                 const float dv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
                                 for (int e = 0; e < 4; ++e) {
