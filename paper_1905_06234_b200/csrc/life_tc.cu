@@ -6,14 +6,16 @@
 // shared memory from the sorted coefficient stream (life_dense.cu
 // build_tc).  Roles inside one persistent CTA per SM (13 warps):
 //
-//   warps 0-7   producers.  Warp p owns voxel rows 16p..16p+15 of the A tile:
-//               it zeroes them, streams its segment (index / fascicle / value,
-//               16-byte loads, L2 prefetch one step ahead), gathers w[f],
-//               stores C[cell] (rank 0: distinct cells) and adds the repeats
-//               in rank order (deterministic), then splits the rows into
-//               tf32 hi = x & ~0x1FFF and lo = x - hi in place.  Producer 0
-//               also issues the bulk copy of the chunk's pre-split, pre-swizzled
-//               dictionary tile (B operand, hi | lo).
+//   warps 0-7   builders.  Warp p owns voxel rows 16p..16p+15 of the A tile:
+//               it zeroes them, stores C[cell] = s from the staged step
+//               (rank 0: distinct cells), adds the repeats with shared-memory
+//               reductions in rank order, then splits the rows into tf32
+//               hi = x & ~0x1FFF and lo = x - hi in place.  Builder 0 stages
+//               each step (one bulk copy of its packed quads, 3 steps ahead)
+//               and issues the bulk copy of the chunk's pre-split,
+//               pre-swizzled dictionary tile (B operand, hi | lo).
+//   warps 13-16 gatherers: for each staged step, s = w[f] * value written
+//               over the value field, ahead of the builders.
 //   warp 8      MMA issuer (one lane).  3xTF32 per K step of 8 atoms:
 //               hi.hi + lo.hi + hi.lo into an fp32 TMEM accumulator; every
 //               kTcGroup chunks the accumulator is handed to the epilogue and
@@ -35,7 +37,9 @@ namespace life {
 
 constexpr int kTcMma = 8;                 // MMA warp
 constexpr int kTcEpi = 9;                 // first epilogue warp
-constexpr int kTcWarps = 13;
+constexpr int kTcGat0 = 13;               // first gatherer warp
+constexpr int kTcGat = 4;                 // gatherer warps
+constexpr int kTcWarps = kTcGat0 + kTcGat;
 constexpr int kTcThreads = kTcWarps * 32;
 #ifndef LIFE_TC_STAGES
 #define LIFE_TC_STAGES 2
@@ -398,6 +402,41 @@ __device__ __forceinline__ unsigned tc_build(uint32_t C, const TcSeg &S, const T
     return zeros;
 }
 
+// build from a step whose gatherers already replaced value by s = w[f] * value
+// (slot field 1); entries beyond the slot (global) are gathered here
+__device__ __forceinline__ unsigned tc_build_s(uint32_t C, const TcSeg &S, const float *__restrict__ w,
+                                               int lane, uint64_t pol, uint32_t junk)
+{
+    unsigned zeros = 0;
+    for (uint32_t k = 4u * (uint32_t)lane; k < S.nf; k += 128u) {
+        const uint4 c4 = S.q4(k, 0);
+        const uint4 v4 = S.q4(k, 1);
+        const uint32_t c[4] = {c4.x, c4.y, c4.z, c4.w};
+        float sv[4] = {__uint_as_float(v4.x), __uint_as_float(v4.y), __uint_as_float(v4.z), __uint_as_float(v4.w)};
+        if (S.off + k >= S.cap) {  // not staged: the gatherers did not see it
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                sv[e] = __fmul_rn(tc_gather(w, c[e] >> kTcCellBits, pol), sv[e]);
+                zeros += ((c[e] >> kTcCellBits) != kTcSent && sv[e] == 0.f) ? 1u : 0u;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) stsf((c[e] >> kTcCellBits) != kTcSent ? C + 4u * (c[e] & kTcCellMask) : junk, sv[e]);
+    }
+    __syncwarp();
+    for (uint32_t k = S.nf + (uint32_t)lane; k < S.n; k += 32u) {
+        const uint32_t c = S.word(k, 0);
+        if ((c >> kTcCellBits) == kTcSent) continue;
+        float sv = __uint_as_float(S.word(k, 1));
+        if (S.off + k >= S.cap) {
+            sv = __fmul_rn(tc_gather(w, c >> kTcCellBits, pol), sv);
+            zeros += sv == 0.f ? 1u : 0u;
+        }
+        reds(C + 4u * (c & kTcCellMask), sv);
+    }
+    return zeros;
+}
+
 // bulk copy / L2 prefetch of a byte range in pieces of at most 32 KB
 __device__ __forceinline__ void tc_stage_step(void *dst, const void *src, unsigned bytes, uint64_t *bar,
                                               uint64_t pol)
@@ -428,7 +467,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     constexpr int kStageBytes = 2 * kTcABytes + kBBytes;
     extern __shared__ __align__(1024) unsigned char tc_smraw[];
     __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], accfull[2], accempty[2];
-    __shared__ __align__(8) uint64_t slotfull[kTcSlots], slotfree[kTcSlots];
+    __shared__ __align__(8) uint64_t slotfull[kTcSlots], slotfree[kTcSlots], slotready[kTcSlots];
     __shared__ uint32_t tmem_base;
     __shared__ float junkbuf[kTcProd * 32];
     if (hooks.done && *hooks.done) return;
@@ -447,6 +486,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc_bar_init(&accempty[s], 4);
         }
         for (int j = 0; j < kTcSlots; ++j) {
+            tc_bar_init(&slotready[j], kTcGat);
             tc_bar_init(&slotfull[j], 1);
             tc_bar_init(&slotfree[j], kTcProd);
         }
@@ -522,15 +562,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (uint32_t o = (uint32_t)lane * 128u; o < bytes; o += 32u * 128u)
                 asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(b + o));
         };
-        TcW Wc, Wn;
         constexpr int kAhead = kTcSlots - 1, kPre = 2 * kAhead;
         if (p == 0) {
             for (int kk = 0; kk < kAhead && kk < total; ++kk) stage(kk);
             for (int kk = kAhead; kk < kPre && kk < total; ++kk) prefetch(kk);
-        }
-        if (total > 0) {
-            tc_wait(&slotfull[0], 0);
-            tc_gathers(segv(0), w, lane, pol_k, Wc);
         }
         int c0 = 0;
         for (int k = 0; k < total; ++k) {
@@ -546,10 +581,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 if (k + kPre < total) prefetch(k + kPre);
             }
             TC_T0(t_slot);
-            if (k + 1 < total) {
-                if (!(c_tc_flags & 1024)) tc_wait(&slotfull[(k + 1) % kTcSlots], ((k + 1) / kTcSlots) & 1);
-                tc_gathers(segv(k + 1), w, lane, pol_k, Wn);
-            }
+            if (!(c_tc_flags & 1024)) tc_wait(&slotready[k % kTcSlots], (k / kTcSlots) & 1);
             if (lane == 0) TC_ACC(0, t_slot);
             TC_T0(t_empty);
             if (k >= kTcStages && !(c_tc_flags & 1024)) tc_wait(&empty[s], ((k / kTcStages) - 1) & 1);
@@ -571,7 +603,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
             for (int i = 0; i < 4; ++i) sts4(H + 16u * (lane + 32 * i), make_float4(0.f, 0.f, 0.f, 0.f));
             __syncwarp();
-            if (!(c_tc_flags & 1)) skipped += tc_build(tc_sa(Ahi), segv(k), Wc, w, lane, pol_k, junk);
+            if (!(c_tc_flags & 1)) skipped += tc_build_s(tc_sa(Ahi), segv(k), w, lane, pol_k, junk);
             __syncwarp();
             if (lane == 0) {
                 tc_arrive(&slotfree[k % kTcSlots]);  // this warp is done with the step's slot
@@ -599,10 +631,74 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             __syncwarp();
             if (lane == 0) TC_ACC(3, t_split);
             if (lane == 0) tc_arrive(&full[s]);
-            TC_T0(t_mv);
-            Wc = Wn;
-            if (lane == 0) TC_ACC(4, t_mv);
             if (++c0 == A.nch) c0 = 0;
+        }
+    } else if (warp >= kTcGat0) {
+        // ===== gatherers: s = w[f] * value in place, one staged step at a time =====
+        const int g = warp - kTcGat0;
+        const uint64_t pol_k = tc_pol_keep();
+        const uint32_t slot_sa = tc_sa(sm + (size_t)kTcStages * kStageBytes);
+        const uint32_t cap = (uint32_t)A.slot;
+        uint32_t c3 = 0, c4v = 0, n3 = 0, n4 = 0;  // step start / end, windows of 32 steps
+        auto loadw = [&](int base, uint32_t &o3, uint32_t &o4) {
+            const int kk = base + lane;
+            if (kk < total) {
+                const size_t T = ((size_t)(blockIdx.x + (kk / A.nch) * gridDim.x) * A.nch + kk % A.nch) * kTcProd;
+                o3 = __ldg(A.tptr + T);
+                o4 = __ldg(A.tptr + T + kTcProd);
+            } else {
+                o3 = o4 = 0u;
+            }
+        };
+        loadw(0, c3, c4v);
+        loadw(32, n3, n4);
+        constexpr int kU = 4;  // quads per thread and pass (all loads first)
+        for (int kk = 0; kk < total; ++kk) {
+            if (kk > 0 && (kk & 31) == 0) {
+                c3 = n3;
+                c4v = n4;
+                loadw(kk + 32, n3, n4);
+            }
+            const uint32_t s0 = __shfl_sync(0xffffffffu, c3, kk & 31);
+            const uint32_t s1 = __shfl_sync(0xffffffffu, c4v, kk & 31);
+            const int j = kk % kTcSlots;
+            tc_wait(&slotfull[j], (kk / kTcSlots) & 1);
+            const uint32_t n = min(s1 - s0, cap), nq = (n + 3u) / 4u;
+            const uint32_t base = slot_sa + (uint32_t)j * 8u * cap;
+            for (uint32_t q0 = (uint32_t)(g * 32 + lane); q0 < nq; q0 += (uint32_t)(kTcGat * 32 * kU)) {
+                uint4 pk[kU], v4[kU];
+                float wv[kU][4];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const uint32_t q = q0 + (uint32_t)(u * kTcGat * 32);
+                    pk[u] = make_uint4(~0u, ~0u, ~0u, ~0u);
+                    if (q < nq) {
+                        pk[u] = lds4(base + q * 32u);
+                        v4[u] = lds4(base + q * 32u + 16u);
+                    }
+                    wv[u][0] = tc_gather(w, pk[u].x >> kTcCellBits, pol_k);
+                    wv[u][1] = tc_gather(w, pk[u].y >> kTcCellBits, pol_k);
+                    wv[u][2] = tc_gather(w, pk[u].z >> kTcCellBits, pol_k);
+                    wv[u][3] = tc_gather(w, pk[u].w >> kTcCellBits, pol_k);
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const uint32_t q = q0 + (uint32_t)(u * kTcGat * 32);
+                    if (q >= nq) continue;
+                    const uint32_t c[4] = {pk[u].x, pk[u].y, pk[u].z, pk[u].w};
+                    const float v[4] = {__uint_as_float(v4[u].x), __uint_as_float(v4[u].y),
+                                        __uint_as_float(v4[u].z), __uint_as_float(v4[u].w)};
+                    float sv[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        sv[e] = __fmul_rn(wv[u][e], v[e]);
+                        skipped += ((c[e] >> kTcCellBits) != kTcSent && sv[e] == 0.f) ? 1u : 0u;
+                    }
+                    sts4(base + q * 32u + 16u, make_float4(sv[0], sv[1], sv[2], sv[3]));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) tc_arrive(&slotready[j]);
         }
     } else if (warp == kTcMma) {
         // ===== MMA issuer =====
