@@ -251,19 +251,14 @@ struct TcMax {
     __device__ float operator()(float a, float b) const { return fmaxf(a, b); }
 };
 
-// ---- producer: one 16-row block of the A tile for one chunk --------------------
-// The layout stores entries as 48-byte quads {cr[4], fiber[4], value[4]}; a
-// step's 8 producer segments are contiguous, so producer 0 stages the whole
-// step with one bulk copy into a shared-memory slot, two steps ahead (3
-// slots), after an L2 prefetch four steps ahead.  A warp's segment is
-// (p0, q0, p1): rank-0 entries [p0, q0) (distinct cells), repeats [q0, p1)
-// sorted by rank, each region padded to 4.  The w[f] gathers of step k+1 are
-// issued into registers before step k is built, so their L2 round trip
-// overlaps the build.  Per lane the registers hold kTcVec 16-byte vectors of
-// the rank-0 region (128 entries per vector across the warp) and kTcWin
-// 32-entry windows of the repeats; a longer segment gathers the rest inline.
-constexpr int kTcVec = 3;
-constexpr int kTcWin = 4;
+// ---- builder: one 16-row block of the A tile for one chunk ---------------------
+// The layout stores entries as 32-byte quads {pk[4], value[4]}; a step's 8
+// segments are contiguous, so builder 0 stages the whole step with one bulk
+// copy into a shared-memory slot, 3 steps ahead (kTcSlots slots), after an
+// L2 prefetch 6 steps ahead.  A warp's segment is (p0, q0, p1): rank-0
+// entries [p0, q0) (distinct cells), repeats [q0, p1) sorted by rank, each
+// region padded to 4.  The gatherer warps turn value into s = w[f] * value in
+// the slot before the builders read it.
 
 // explicit shared-memory accesses (32-bit shared-window addresses)
 __device__ __forceinline__ uint4 lds4(uint32_t a)
@@ -320,86 +315,9 @@ struct TcSeg {
     }
 };
 
-struct TcW {
-    float v[kTcVec][4];
-    float r[kTcWin];
-};
-
-// issue the gathers of a staged segment (values land in registers later)
-__device__ __forceinline__ void tc_gathers(const TcSeg &S, const float *__restrict__ w, int lane, uint64_t pol,
-                                           TcW &W)
-{
-#pragma unroll
-    for (int j = 0; j < kTcVec; ++j) {
-        const uint32_t k = 128u * (uint32_t)j + 4u * (uint32_t)lane;
-        uint4 f = make_uint4(~0u, ~0u, ~0u, ~0u);
-        if (k < S.nf) f = S.q4(k, 0);
-        W.v[j][0] = tc_gather(w, f.x >> kTcCellBits, pol);
-        W.v[j][1] = tc_gather(w, f.y >> kTcCellBits, pol);
-        W.v[j][2] = tc_gather(w, f.z >> kTcCellBits, pol);
-        W.v[j][3] = tc_gather(w, f.w >> kTcCellBits, pol);
-    }
-#pragma unroll
-    for (int r = 0; r < kTcWin; ++r) {
-        const uint32_t k = S.nf + 32u * (uint32_t)r + (uint32_t)lane;
-        W.r[r] = tc_gather(w, (k < S.n ? S.word(k, 0) : ~0u) >> kTcCellBits, pol);
-    }
-}
-
 __device__ __forceinline__ void reds(uint32_t a, float v)
 {
     asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
-}
-
-// build the warp's rows of C (shared address C) from a staged segment and its
-// gathered w: rank-0 entries (distinct cells) are stored, then the repeats
-// (sorted by rank, then cell) are added with shared-memory reductions, issued
-// in rank order by this warp alone
-__device__ __forceinline__ unsigned tc_build(uint32_t C, const TcSeg &S, const TcW &W, const float *__restrict__ w,
-                                             int lane, uint64_t pol, uint32_t junk)
-{
-    unsigned zeros = 0;
-    auto put4 = [&](uint32_t k, const float (&wv)[4]) {
-        const uint4 c4 = S.q4(k, 0);
-        const uint4 v4 = S.q4(k, 1);
-        const uint32_t c[4] = {c4.x, c4.y, c4.z, c4.w};
-        const float v[4] = {__uint_as_float(v4.x), __uint_as_float(v4.y), __uint_as_float(v4.z),
-                            __uint_as_float(v4.w)};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const bool ok = (c[e] >> kTcCellBits) != kTcSent;
-            const float sv = __fmul_rn(wv[e], v[e]);
-            zeros += (ok && sv == 0.f) ? 1u : 0u;
-            stsf(ok ? C + 4u * (c[e] & kTcCellMask) : junk, sv);
-        }
-    };
-#pragma unroll
-    for (int j = 0; j < kTcVec; ++j) {
-        const uint32_t k = 128u * (uint32_t)j + 4u * (uint32_t)lane;
-        if (k < S.nf) put4(k, W.v[j]);
-    }
-    for (uint32_t k = 128u * kTcVec + 4u * (uint32_t)lane; k < S.nf; k += 128u) {  // beyond the registers
-        const uint4 f = S.q4(k, 0);
-        const float wv[4] = {tc_gather(w, f.x >> kTcCellBits, pol), tc_gather(w, f.y >> kTcCellBits, pol),
-                             tc_gather(w, f.z >> kTcCellBits, pol), tc_gather(w, f.w >> kTcCellBits, pol)};
-        put4(k, wv);
-    }
-    __syncwarp();
-    auto rep = [&](uint32_t k, float wv) {
-        if (k < S.n) {
-            const uint32_t c = S.word(k, 0);
-            if ((c >> kTcCellBits) != kTcSent) {
-                const float sv = __fmul_rn(wv, __uint_as_float(S.word(k, 1)));
-                zeros += sv == 0.f ? 1u : 0u;
-                reds(C + 4u * (c & kTcCellMask), sv);
-            }
-        }
-    };
-#pragma unroll
-    for (int r = 0; r < kTcWin; ++r) rep(S.nf + 32u * (uint32_t)r + (uint32_t)lane, W.r[r]);
-    for (uint32_t k = S.nf + 32u * kTcWin + (uint32_t)lane; k < S.n; k += 32u)
-        rep(k, tc_gather(w, S.word(k, 0) >> kTcCellBits, pol));
-    return zeros;
 }
 
 // build from a step whose gatherers already replaced value by s = w[f] * value
