@@ -178,7 +178,7 @@ __device__ __forceinline__ float tc_gather(const float *w, uint32_t f, uint64_t 
     if (f == kTcSent) return 0.f;
     if (c_tc_flags & 4) return 1.f;
     float r;
-    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(w + f), "l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(w + f), "l"(pol));
     return r;
 }
 
