@@ -22,7 +22,7 @@ y = torch.empty(dims[1] * dims[3], device="cuda"); g = torch.empty(dims[2], devi
 ym = torch.ones(1, device="cuda")
 for name, fn in (("dsc", lambda: op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absmax=ym)),
                  ("wc", lambda: op.wc_f32(y, g, y_absmax=ym))):
-    for mode in [0, 1, 2, 1 | (1 << 8), 1 | (4 << 8)]:
+    for mode in [int(x, 0) for x in os.environ.get("WS_MODES", "0,1,2,0x101,0x401").split(",")]:
         lib.life_debug_ws_isolate(mode)
         for _ in range(2): fn()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
