@@ -223,18 +223,26 @@ __device__ __forceinline__ bool ws_last_block(unsigned *counter)
 // L2 policies: the coefficient stream (read once per SpMV, 1.2 GB at C2) is
 // evict-first so it does not push the gathered / scattered Nf-vectors (w,
 // the fixed-point sums) out of L2; those are evict-last.
-__device__ __forceinline__ uint64_t policy_stream()
+// (A/B: LIFE_WS_POL_STREAM / LIFE_WS_POL_KEEP = 0 evict_normal, 1 evict_first,
+// 2 evict_last, 3 evict_unchanged)
+#ifndef LIFE_WS_POL_STREAM
+#define LIFE_WS_POL_STREAM 1
+#endif
+#ifndef LIFE_WS_POL_KEEP
+#define LIFE_WS_POL_KEEP 2
+#endif
+template <int K>
+__device__ __forceinline__ uint64_t make_policy()
 {
     uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    if (K == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    else if (K == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else if (K == 3) asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ uint64_t policy_keep()
-{
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
+__device__ __forceinline__ uint64_t policy_stream() { return make_policy<LIFE_WS_POL_STREAM>(); }
+__device__ __forceinline__ uint64_t policy_keep() { return make_policy<LIFE_WS_POL_KEEP>(); }
 
 __device__ __forceinline__ void prefetch_l2(const void *ptr, uint32_t bytes)
 {
