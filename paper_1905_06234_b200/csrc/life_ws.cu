@@ -275,12 +275,16 @@ __device__ __forceinline__ void red_keep(unsigned long long *p, unsigned long lo
     asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
 
-// Repeats (rank >= 1, sorted by rank then cell): LIFE_WS_ORDERED=1 (default)
-// adds them rank by rank with read-modify-writes (a fixed summation order);
-// LIFE_WS_ORDERED=0 issues them as shared-memory reductions in rank order
-// instead (measured: same DSC time at C2, 1.437 vs 1.447 ms).
+// Repeats (rank >= 1, sorted by rank then cell), all in a fixed summation
+// order (each cell's repeats added in rank order):
+//   LIFE_WS_ORDERED=2 (default) batches of 8 windows, one round of
+//     read-modify-writes per rank level (cells are distinct within a level);
+//   LIFE_WS_ORDERED=1 window by window, per-rank rounds only in windows that
+//     straddle two levels;
+//   LIFE_WS_ORDERED=0 shared-memory reductions in rank order (not native for
+//     f32 on sm_100: a CAS loop; same time as 1 at C2).
 #ifndef LIFE_WS_ORDERED
-#define LIFE_WS_ORDERED 1
+#define LIFE_WS_ORDERED 2
 #endif
 __device__ __forceinline__ void ws_red_add(float *p, float v)
 {
@@ -473,6 +477,48 @@ __device__ __forceinline__ unsigned build_pair(float *C, const float *__restrict
     WS_T0(t_slow);
     for (int r0 = 0; r0 < nw; r0 += kSlowRounds) {
         if (r0) gather_slow(r0);
+        if (LIFE_WS_ORDERED == 2) {
+            // level-batched, kLevelBatch windows at a time: within one rank
+            // level all cells are distinct, so each level's read-modify-
+            // writes are issued together (loads, then stores) and levels
+            // follow in rank order -- the same per-cell summation order as
+            // the window-by-window pass, bitwise
+            constexpr int kLevelBatch = 4;
+#pragma unroll
+            for (int b = 0; b < kSlowRounds; b += kLevelBatch) {
+                if (r0 + b >= nw) break;  // warp-uniform
+                uint32_t cell[kLevelBatch], rank[kLevelBatch];
+                float sv[kLevelBatch];
+                uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+#pragma unroll
+                for (int r = 0; r < kLevelBatch; ++r) {
+                    const uint32_t k = nf + 32u * (uint32_t)(r0 + b + r) + (uint32_t)lane;
+                    const bool in = r0 + b + r < nw && k < n;
+                    const uint32_t cr = in ? ldv<STAGED>(V.cr + k) : kPadBit;
+                    const bool ok = !(cr & kPadBit);
+                    sv[r] = ok ? __fmul_rn(ws[b + r], ldv<STAGED>(V.v + k)) : 0.f;
+                    zeros += (ok && sv[r] == 0.f) ? 1u : 0u;
+                    cell[r] = cr & kCellMask;
+                    rank[r] = ok ? (cr >> kWsCellBits) & kRankMask : 0xFFFFFFFFu;
+                    if (ok) {
+                        lo = min(lo, rank[r]);
+                        hi = max(hi, rank[r]);
+                    }
+                }
+                lo = __reduce_min_sync(0xffffffffu, lo);
+                hi = __reduce_max_sync(0xffffffffu, hi);
+                for (uint32_t rr = lo; rr <= hi && lo != 0xFFFFFFFFu; ++rr) {
+                    float cv[kLevelBatch];
+#pragma unroll
+                    for (int r = 0; r < kLevelBatch; ++r) cv[r] = rank[r] == rr ? C[cell[r]] : 0.f;
+#pragma unroll
+                    for (int r = 0; r < kLevelBatch; ++r)
+                        if (rank[r] == rr) C[cell[r]] = cv[r] + sv[r];
+                    __syncwarp();
+                }
+            }
+            continue;
+        }
 #pragma unroll
         for (int r = 0; r < kSlowRounds; ++r) {
             if (r0 + r >= nw) break;  // warp-uniform
