@@ -410,12 +410,23 @@ __device__ __forceinline__ float gather_w(const float *__restrict__ w, uint32_t 
 // the rank-0 batch, so a typical step has one gather round trip.  Repeats
 // are added after every rank-0 store, window by window in rank order; a
 // window straddling two rank levels (kMixedBit) is applied rank by rank.
-constexpr int kFastBlocks = kWsProd == 8 ? 4 : 8;
+// Gather batch sizes: one 128-entry block of the rank-0 region and 4 repeat
+// windows per batch.  Smaller batches measured faster than larger ones
+// (C2 DSC 1.30 ms with 4 blocks / 8 windows, 1.19 ms with 1 / 4): fewer
+// gathers in flight per SM queue less in the LSU and L2 while the tile stores
+// of the previous batch proceed.
+#ifndef LIFE_WS_FAST_BLOCKS
+#define LIFE_WS_FAST_BLOCKS 1
+#endif
+constexpr int kFastBlocks = LIFE_WS_FAST_BLOCKS;  // 128-entry blocks per gather batch
 #ifndef LIFE_WC_ATOMS
 #define LIFE_WC_ATOMS 4
 #endif
 constexpr int kWcAtoms = LIFE_WC_ATOMS;  // atoms per WC consumer iteration
-constexpr int kSlowRounds = 8;
+#ifndef LIFE_WS_SLOW_ROUNDS
+#define LIFE_WS_SLOW_ROUNDS 4
+#endif
+constexpr int kSlowRounds = LIFE_WS_SLOW_ROUNDS;  // repeat windows per gather batch
 
 template <bool STAGED>
 __device__ __forceinline__ unsigned build_pair(float *C, const float *__restrict__ w,
