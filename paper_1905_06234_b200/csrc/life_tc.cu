@@ -38,7 +38,10 @@ namespace life {
 constexpr int kTcMma = 8;                 // MMA warp
 constexpr int kTcEpi = 9;                 // first epilogue warp
 constexpr int kTcGat0 = 13;               // first gatherer warp
-constexpr int kTcGat = 4;                 // gatherer warps
+#ifndef LIFE_TC_GATHERERS
+#define LIFE_TC_GATHERERS 4
+#endif
+constexpr int kTcGat = LIFE_TC_GATHERERS;  // gatherer warps
 constexpr int kTcWarps = kTcGat0 + kTcGat;
 constexpr int kTcThreads = kTcWarps * 32;
 #ifndef LIFE_TC_STAGES
@@ -570,7 +573,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         };
         loadw(0, c3, c4v);
         loadw(32, n3, n4);
-        constexpr int kU = 4;  // quads per thread and pass (all loads first)
+#ifndef LIFE_TC_GATHER_U
+#define LIFE_TC_GATHER_U 1
+#endif
+        constexpr int kU = LIFE_TC_GATHER_U;  // quads per thread and pass (all loads first)
         for (int kk = 0; kk < total; ++kk) {
             if (kk > 0 && (kk & 31) == 0) {
                 c3 = n3;
