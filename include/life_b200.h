@@ -89,7 +89,7 @@ LIFE_API uint64_t life_launch_count(void);
 #define LIFE_PHI_FORCE_SPARSE 0x8u  /* fp32: voxel-segment kernels only    */
 #define LIFE_PHI_FORCE_DENSE  0x10u /* fp32: register-tiled dense kernels  */
 #define LIFE_PHI_NO_TENSOR    0x20u /* fp32: no tcgen05 products (CUDA cores only) */
-#define LIFE_PHI_TENSOR       0x40u /* fp32: DSC on tcgen05 too (WC is by default) */
+#define LIFE_PHI_TENSOR       0x40u /* fp32: tcgen05 products (the default for tile layouts) */
 
 /* Build the device operator from COO arrays (PhiTensor + Dictionary,
  * tensor.py:76-170).  atoms/voxels/fibers: u32[n_coeffs]; values:

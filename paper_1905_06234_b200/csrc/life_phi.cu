@@ -732,10 +732,10 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         if (flags & LIFE_PHI_FORCE_DENSE) dense = n > 0;
         if (dense) LIFE_TRY(build_dense(phi, a, v, f, val, hdict, st));
         // tcgen05 DSC over its own tile layout (life_tc.cu) next to the dense
-        // one: opt-in (LIFE_PHI_TENSOR or LIFE_TC=1) until it beats the
-        // CUDA-core tile kernels
+        // one: default since it beats the CUDA-core tile DSC (1.08 vs 1.19 ms
+        // at C2); LIFE_PHI_NO_TENSOR or LIFE_TC=0 opt out
         const char *tc_env = getenv("LIFE_TC");
-        const bool want_tc = (flags & LIFE_PHI_TENSOR) || (tc_env && tc_env[0] == '1');
+        const bool want_tc = (flags & LIFE_PHI_TENSOR) || !(tc_env && tc_env[0] == '0');
         // WC on tcgen05 over the same tile layout (k_wc_tc): default, it is
         // faster than the CUDA-core WC (0.97 vs 1.19 ms at C2)
         const char *wc_env = getenv("LIFE_WC_TC");

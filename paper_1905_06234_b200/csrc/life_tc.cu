@@ -39,7 +39,7 @@ constexpr int kTcMma = 8;                 // MMA warp
 constexpr int kTcEpi = 9;                 // first epilogue warp
 constexpr int kTcGat0 = 13;               // first gatherer warp
 #ifndef LIFE_TC_GATHERERS
-#define LIFE_TC_GATHERERS 4
+#define LIFE_TC_GATHERERS 3
 #endif
 constexpr int kTcGat = LIFE_TC_GATHERERS;  // gatherer warps
 constexpr int kTcWarps = kTcGat0 + kTcGat;

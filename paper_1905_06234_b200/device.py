@@ -32,9 +32,10 @@ _LAYOUT = ["auto"]
 
 def set_layout(name):
     """fp32 kernel family for operators built from now on: "auto" (density
-    heuristic), "sparse" (voxel-segment kernels), "dense" (tile kernels: DSC
-    on CUDA cores, WC's Z = Y.D^T on the tcgen05 tensor cores), "fma" (tile
-    kernels on CUDA cores only) or "tensor" (DSC on the tensor cores too)."""
+    heuristic), "sparse" (voxel-segment kernels), "dense" (tile kernels with
+    DSC and WC on the tcgen05 tensor cores where the shape allows: n_dirs <=
+    128 for DSC, <= 96 for WC), "fma" (tile kernels on CUDA cores only) or
+    "tensor" (same as "dense")."""
     if name not in ("auto", "sparse", "dense", "fma", "tensor"):
         raise ConfigInvalid(f"layout must be auto/sparse/dense/fma/tensor, got {name!r}")
     _LAYOUT[0] = name
@@ -273,7 +274,7 @@ def wc_accumulate(tensor, dictionary, y, w_out, precision=None):
     return start.elapsed_time(stop) * 1e-3
 
 
-def autotune_layout(problem, trials=3, candidates=("sparse", "dense", "fma", "tensor")):
+def autotune_layout(problem, trials=3, candidates=("sparse", "dense", "fma")):
     """Pick the fp32 kernel family for a problem by timing one DSC + one WC
     per candidate on the device (the paper's runtime selection between
     kernel variants, restructure.py:107-144 for
@@ -292,8 +293,8 @@ def autotune_layout(problem, trials=3, candidates=("sparse", "dense", "fma", "te
         for name in candidates:
             set_layout(name)
             op = DeviceOperator(problem.tensor, problem.dictionary)
-            if name != "sparse" and op.kind != {"fma": "dense"}.get(name, name):
-                continue
+            if name != "sparse" and op.kind == "sparse":
+                continue  # no tile layout for this problem
             run = lambda: (op.dsc_f32(w, y), op.wc_f32(y, g, y_absmax=ymax))  # noqa: E731
             run()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
