@@ -294,6 +294,10 @@ def run_ours(args, dims):
     # ---- kernel-level timing (DSC / WC) for the roofline -------------------
     # (this rank's shard when N > 1: local bytes over local kernel time)
     dsc_b, wc_b = spmv_bytes(local_dims)
+    if "dsc" in op.tensor_ops:
+        # the tensor-core DSC streams 8-byte packed entries (fascicle << 12 |
+        # cell, value): SURVEY 8(d) counts the actual sizes under compression
+        dsc_b, _ = spmv_bytes(local_dims, idx_bytes=2)
     y = torch.empty(local_dims[1] * nt, dtype=torch.float32, device="cuda")
     g = torch.empty(nf, dtype=torch.float32, device="cuda")
     ymax = torch.zeros(1, dtype=torch.float32, device="cuda")

@@ -96,6 +96,8 @@ def main():
         dsc_ms = timed(lambda: op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absmax=ymax), args.reps)
         wc_ms = timed(lambda: op.wc_f32(y, g, y_absmax=ymax), args.reps)
         bd, bw = bench.spmv_bytes((dims.n_atoms, dims.n_voxels, dims.n_fibers, dims.n_dirs, nc))
+        if "dsc" in op.tensor_ops:  # 8-byte packed entries (actual sizes)
+            bd, _ = bench.spmv_bytes((dims.n_atoms, dims.n_voxels, dims.n_fibers, dims.n_dirs, nc), idx_bytes=2)
         parity = None
         if exact:
             y64 = torch.zeros(dims.signal_len, dtype=torch.float64, device="cuda")
@@ -106,7 +108,7 @@ def main():
             parity = {"dsc_rel_l2": rel(y, y64), "wc_rel_l2": rel(g, g64), "tol": 1e-5}
         base = {"config": "C5", "nnz": nc, "n_voxels": dims.n_voxels, "n_fibers": dims.n_fibers,
                 "n_atoms": dims.n_atoms, "n_dirs": dims.n_dirs, "skew": args.skew,
-                "max_fascicle_len": fmax, "kernels": op.kind, "build_s": round(build_s, 3),
+                "max_fascicle_len": fmax, "kernels": op.kind, "tensor_cores": list(op.tensor_ops), "build_s": round(build_s, 3),
                 "peak_gbs": peak, "peak_source": src}
         for name, ms, b in (("dsc", dsc_ms, bd), ("wc", wc_ms, bw)):
             gbs = b / ms / 1e6
