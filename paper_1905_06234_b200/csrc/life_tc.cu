@@ -48,10 +48,16 @@ constexpr int kTcThreads = kTcWarps * 32;
 #define LIFE_TC_STAGES 2
 #endif
 constexpr int kTcStages = LIFE_TC_STAGES;  // A/B stages
-constexpr int kTcGroup = 4;               // chunks per TMEM accumulation group
+#ifndef LIFE_TC_GROUP
+#define LIFE_TC_GROUP 4
+#endif
+constexpr int kTcGroup = LIFE_TC_GROUP;    // chunks per TMEM accumulation group
 constexpr uint32_t kTcCellMask = (1u << kTcCellBits) - 1;
 constexpr uint32_t kTcSent = 0xFFFFFu;     // fascicle field of pad entries
-constexpr int kTcSlots = 4;                // staged steps (3 ahead of the one being built)
+#ifndef LIFE_TC_SLOTS
+#define LIFE_TC_SLOTS 4
+#endif
+constexpr int kTcSlots = LIFE_TC_SLOTS;    // staged steps (kTcSlots-1 ahead of the one being built)
 constexpr int kTcABytes = kTcTV * kTcCA * 4;  // 16 KB per A half (hi or lo)
 
 struct TcArgs {
