@@ -5,8 +5,10 @@
 C ABI on either host arrays (numpy: copied in and out) or CUDA tensors
 (used in place).  Two precisions:
 
-* ``"fp32"`` -- the fast path (fp32 values, FFMA, fixed-point WC
-  accumulation); within ~1e-7 relative of the reference.
+* ``"fp32"`` -- the fast path (fp32 values, fixed-point WC accumulation);
+  tile operators run both products on the tcgen05 tensor cores (3xTF32,
+  ~1e-6 relative of the reference), ``set_layout("fma")`` keeps them on CUDA
+  cores (~3e-7), sparse operators use voxel-segment kernels.
 * ``"fp64"`` -- the bit-exact path: same rounding and per-output order as
   the reference loops (_kernels.py:14-68), equal to
   ``dsc_sequential``/``wc_sequential`` bit for bit.
