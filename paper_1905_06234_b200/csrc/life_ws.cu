@@ -1378,22 +1378,51 @@ __global__ void __launch_bounds__(kWtThreads, 1)
             st += ce - cb;
             if (tiles > 0) bar_wait(&yfree, (tiles - 1) & 1);
             tcg::fence_after();
-#pragma unroll 1
+            // this thread's two voxel rows (one per 128-voxel half)
+            const float *yr[2];
+            bool yok[2];
+#pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int row = h * 128 + q * 32 + lane;
                 const int tile = ct * kWsCons + row / kWsTV;
                 const int voxel = tile < A.n_tiles ? __ldg(A.slotv + (size_t)ct * (kWsCons * kWsTV) + row) : -1;
-                const float *yr = y + (size_t)(voxel < 0 ? 0 : voxel) * A.nt;
+                yok[h] = voxel >= 0;
+                yr[h] = y + (size_t)(voxel < 0 ? 0 : voxel) * A.nt;
+            }
+            const bool vec = (A.nt & 3) == 0;  // rows 16-byte aligned
 #pragma unroll 1
-                for (int kb = 0; kb < T.nkb; ++kb) {
+            for (int kb = 0; kb < T.nkb; ++kb) {
+                // both halves' 32 directions in flight together
+                float x[2][32];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (vec) {
+#pragma unroll
+                        for (int i4 = 0; i4 < 8; ++i4) {
+                            const int t = kb * 32 + 4 * i4;
+                            const float4 v = (yok[h] && t < A.nt) ? __ldg(reinterpret_cast<const float4 *>(yr[h] + t))
+                                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+                            x[h][4 * i4] = v.x;
+                            x[h][4 * i4 + 1] = v.y;
+                            x[h][4 * i4 + 2] = v.z;
+                            x[h][4 * i4 + 3] = v.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int t = kb * 32 + i;
+                            x[h][i] = (yok[h] && t < A.nt) ? __ldg(yr[h] + t) : 0.f;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
                     uint32_t hv[32], lv[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
-                        const int t = kb * 32 + i;
-                        const float x = (voxel >= 0 && t < A.nt) ? __ldg(yr + t) : 0.f;
-                        const uint32_t hb = tcg::hi_bits(__float_as_uint(x));
+                        const uint32_t hb = tcg::hi_bits(__float_as_uint(x[h][i]));
                         hv[i] = hb;
-                        lv[i] = __float_as_uint(x - __uint_as_float(hb));
+                        lv[i] = __float_as_uint(x[h][i] - __uint_as_float(hb));
                     }
                     tcg::st32(tmem + lane_base + (uint32_t)(h * 2 * ntp + kb * 32), hv);
                     tcg::st32(tmem + lane_base + (uint32_t)(h * 2 * ntp + ntp + kb * 32), lv);
