@@ -704,7 +704,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 if (lane == 0) tc_arrive(&accempty[buf]);
             }
             const int voxel = (c_tc_flags & 64) ? -1 : __ldg(A.slotv + (size_t)ct * kTcTV + row);
-            if (voxel >= 0) {
+            if (voxel >= 0 && (A.nt & 3) == 0) {
+                // 16-byte row accesses (rows are 16-byte aligned when nt % 4 == 0)
+                const size_t yo = (size_t)voxel * A.nt;
+                float4 *y4 = reinterpret_cast<float4 *>(y + yo);
+                const float4 *b4 = reinterpret_cast<const float4 *>(subtract ? b + yo : y + yo);
+#pragma unroll
+                for (int t4 = 0; t4 < N / 4; ++t4) {
+                    if (4 * t4 < A.nt) {
+                        float r[4] = {acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]};
+                        if (accumulate) {
+                            const float4 o = y4[t4];
+                            r[0] += o.x; r[1] += o.y; r[2] += o.z; r[3] += o.w;
+                        }
+                        if (subtract) {
+                            const float4 o = __ldg(b4 + t4);
+                            r[0] -= o.x; r[1] -= o.y; r[2] -= o.z; r[3] -= o.w;
+                        }
+                        y4[t4] = make_float4(r[0], r[1], r[2], r[3]);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            sq += (double)r[e] * (double)r[e];
+                            amax = fmaxf(amax, fabsf(r[e]));
+                        }
+                    }
+                }
+            } else if (voxel >= 0) {
                 const size_t yo = (size_t)voxel * A.nt;
 #pragma unroll
                 for (int t = 0; t < N; ++t) {
