@@ -161,6 +161,10 @@ typedef struct life_spmv_out {
     float *absmax;               /* max |output element| (WC fixed-point bound input)  */
 } life_spmv_out;
 
+/* The fp32 products stream vectors in 16-byte units: w, y, b and w_ref must
+ * be 16-byte aligned (every cudaMalloc / torch allocation is); a misaligned
+ * pointer returns LIFE_ERR_INVALID_ARGUMENT before any launch. */
+
 /* y = M w (fp32, fast layout).  w: f32[Nf], y: f32[Nv*Nd], b: f32[Nv*Nd]
  * (LIFE_SUBTRACT_B only).  Replaces dsc_sequential / dsc_parallel
  * (engine.py:218,247) and the dsc_range kernel ABI (_kernels.py:14). */

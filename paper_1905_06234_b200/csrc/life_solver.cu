@@ -80,7 +80,7 @@ template <typename T>
 __global__ void k_project_nonneg(T *w, int n)
 {
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x)
-        w[f] = w[f] > T(0) ? w[f] : T(0);  // max(v, 0); -0 and NaN -> ... see below
+        w[f] = (w[f] >= T(0) || w[f] != w[f]) ? w[f] : T(0);  // np.maximum(v, 0): NaN propagates
 }
 
 template <int BT>
@@ -111,8 +111,7 @@ __global__ void __launch_bounds__(BT)
     T mn = T(INFINITY);
     for (int f = blockIdx.x * BT + threadIdx.x; f < nf; f += gridDim.x * BT) {
         T v = w[f] - alpha * gt[f];
-        v = fmax(v, T(0));  // np.maximum(v, 0.0): negatives become +0
-        if (v == T(0)) v = T(0);
+        v = (v >= T(0) || v != v) ? v : T(0);  // np.maximum(v, 0.0): NaN propagates, -0 stays
         w[f] = v;
         z += (v == T(0)) ? 1ull : 0ull;
         mn = fmin(mn, v);

@@ -674,12 +674,32 @@ static int launch_dsc_sparse(life_phi *phi, const float *w, float *y, const floa
     LIFE_NT_DISPATCH(launch_dsc_t, phi, w, y, b, flags, o, h, st);
 }
 
-int launch_dsc(life_phi *phi, const float *w, float *y, const float *b,
-               uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st)
+static int launch_dsc_kernel(life_phi *phi, const float *w, float *y, const float *b,
+                             uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st)
 {
     if (phi->has_tc) return launch_dsc_tc(phi, w, y, b, flags, o, h, st);
     if (phi->has_dense) return launch_dsc_dense(phi, w, y, b, flags, o, h, st);
     return launch_dsc_sparse(phi, w, y, b, flags, o, h, st);
+}
+
+__global__ void k_zero_skips(unsigned long long *sk, double *skd, const int *done)
+{
+    if (done && *done) return;
+    if (sk) *sk = 0ull;
+    if (skd) *skd = 0.0;
+}
+
+int launch_dsc(life_phi *phi, const float *w, float *y, const float *b,
+               uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st)
+{
+    LIFE_TRY(launch_dsc_kernel(phi, w, y, b, flags, o, h, st));
+    if (!(flags & LIFE_SKIP_ZERO) && (o.skipped || o.skipped_d)) {
+        // KernelStats.skipped_coefficients is 0 when skip_zero is off
+        // (_kernels.dsc_range counts only skipped products, _kernels.py:25-28)
+        k_zero_skips<<<1, 1, 0, st>>>(o.skipped, o.skipped_d, h.done);
+        LIFE_CHECK_LAUNCH();
+    }
+    return LIFE_OK;
 }
 
 static int launch_wc_sparse(life_phi *phi, const float *y, const WcFix &fx,
@@ -760,6 +780,9 @@ int life_dsc_f32(life_phi *phi, const float *w, float *y, const float *b,
     if (!phi->has_fast && !phi->has_dense)
         return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     if ((flags & LIFE_SUBTRACT_B) && !b) return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_SUBTRACT_B needs b");
+    if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(y) |
+         reinterpret_cast<uintptr_t>(b)) & 15u)
+        return fail(LIFE_ERR_INVALID_ARGUMENT, "w, y and b must be 16-byte aligned");
     DscOut o{nullptr, nullptr, nullptr, nullptr};
     if (out) o = DscOut{out->skipped, out->sumsq, out->absmax, nullptr};
     CallHooks h{nullptr, nullptr, nullptr};
@@ -776,6 +799,9 @@ int life_wc_f32(life_phi *phi, const float *y, float *w, const float *w_ref,
         return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     if ((flags & LIFE_PROJECT_GRAD) && !w_ref)
         return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_PROJECT_GRAD needs w_ref");
+    if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(y) |
+         reinterpret_cast<uintptr_t>(w_ref)) & 15u)
+        return fail(LIFE_ERR_INVALID_ARGUMENT, "y, w and w_ref must be 16-byte aligned");
     CallHooks h{nullptr, nullptr, nullptr};
     LIFE_TRY(launch_wc(phi, y, w, w_ref, y_absmax_dev, nullptr, flags,
                        out ? out->sumsq : nullptr, h, nullptr, static_cast<cudaStream_t>(stream)));

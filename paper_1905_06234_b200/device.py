@@ -161,29 +161,48 @@ def _p(t):
 
 
 def operator_for(tensor, dictionary, exact=False):
-    """Cached DeviceOperator for (tensor, dictionary); rebuilt when the exact
-    layout is requested but missing."""
+    """Cached DeviceOperator for (tensor, dictionary) on the current device.
+
+    The cache entry is keyed on the dictionary object, the fp32 layout
+    selected by set_layout() and the CUDA device; a change of any of them,
+    or a request for the exact layout the cached operator lacks, rebuilds
+    it (the old handle is released)."""
+    import torch
     phi = _phi(tensor)
     cache = phi.__dict__.setdefault("_device_cache", {})
+    key = (id(dictionary), _LAYOUT[0], torch.cuda.current_device())
     entry = cache.get("op")
     if entry is not None:
-        op, dic = entry
-        if dic is dictionary and (op.exact or not exact):
+        op, dic, k = entry
+        if dic is dictionary and k == key and (op.exact or not exact):
             return op
         op.close()
+        del cache["op"]
     op = DeviceOperator(phi, dictionary, exact=exact, fast=True)
-    cache["op"] = (op, dictionary)
+    cache["op"] = (op, dictionary, key)
     return op
 
 
 # ---- reference-shaped products (accumulate into caller buffers) ------------
 
 
+def _aligned(t):
+    """The fp32 kernels move vectors in 16-byte units (life_b200.h): views
+    at odd offsets (e.g. ``buf[1:]``) are copied to a fresh allocation."""
+    return t if t.data_ptr() % 16 == 0 else t.clone()
+
+
+def _in_place_ok(torch, t, dtype):
+    return (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype
+            and t.is_contiguous() and t.data_ptr() % 16 == 0
+            and t.device.index == torch.cuda.current_device())
+
+
 def _as_device(torch, x, dtype):
     if isinstance(x, torch.Tensor):
         if not x.is_cuda:
             return x.to(device="cuda", dtype=dtype).contiguous()
-        return x.to(dtype=dtype).contiguous()
+        return _aligned(x.to(device="cuda", dtype=dtype).contiguous())
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(
         device="cuda", dtype=dtype)
 
@@ -207,8 +226,7 @@ def dsc_accumulate(tensor, dictionary, w, y_out, skip_zero=True, precision=None)
     flags = N.SKIP_ZERO if skip_zero else 0
     if precision == "fp64":
         wd = _as_device(torch, w, torch.float64)
-        if isinstance(y_out, torch.Tensor) and y_out.is_cuda and y_out.dtype == torch.float64 \
-                and y_out.is_contiguous():
+        if _in_place_ok(torch, y_out, torch.float64):
             yd = y_out
         else:
             yd = _as_device(torch, y_out, torch.float64)
@@ -222,8 +240,7 @@ def dsc_accumulate(tensor, dictionary, w, y_out, skip_zero=True, precision=None)
                 y_out[...] = yd.cpu().numpy()
     else:
         wd = _as_device(torch, w, torch.float32)
-        if isinstance(y_out, torch.Tensor) and y_out.is_cuda and y_out.dtype == torch.float32 \
-                and y_out.is_contiguous():
+        if _in_place_ok(torch, y_out, torch.float32):
             start.record()
             op.dsc_f32(wd, y_out, None, flags | N.ACCUMULATE, skipped)
             stop.record()
@@ -246,8 +263,7 @@ def wc_accumulate(tensor, dictionary, y, w_out, precision=None):
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if precision == "fp64":
         yd = _as_device(torch, y, torch.float64)
-        if isinstance(w_out, torch.Tensor) and w_out.is_cuda and w_out.dtype == torch.float64 \
-                and w_out.is_contiguous():
+        if _in_place_ok(torch, w_out, torch.float64):
             wd = w_out
         else:
             wd = _as_device(torch, w_out, torch.float64)
@@ -261,8 +277,7 @@ def wc_accumulate(tensor, dictionary, y, w_out, precision=None):
                 w_out[...] = wd.cpu().numpy()
     else:
         yd = _as_device(torch, y, torch.float32)
-        if isinstance(w_out, torch.Tensor) and w_out.is_cuda and w_out.dtype == torch.float32 \
-                and w_out.is_contiguous():
+        if _in_place_ok(torch, w_out, torch.float32):
             start.record()
             op.wc_f32(yd, w_out, flags=N.ACCUMULATE)
             stop.record()

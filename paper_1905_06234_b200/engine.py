@@ -96,26 +96,35 @@ def _whole_runs(keys, nc, threads):
     return [int(starts[min(i * per, n_runs)]) for i in range(threads + 1)]
 
 
+def check_strategy_ordering(strategy, ordering):
+    """The ordering requirements build_plan enforces (engine.py:166-180),
+    raised in the same order with the same messages; usable without a
+    tensor (the solver validates its restructure/strategy pairs up front)."""
+    if strategy.kind == "coefficient":
+        if strategy.sync_free and ordering != "by_voxel":
+            raise StrategyRequiresSorted("sync_free requires a voxel-sorted tensor")
+        return
+    want = _NEEDS[strategy.kind]
+    if ordering != want:
+        raise StrategyRequiresSorted(
+            f"{strategy.kind} partitioning requires ordering {want!r}, "
+            f"tensor is {ordering!r}")
+    if strategy.sync_free and strategy.kind != "voxel":
+        raise StrategyRequiresSorted("sync_free applies to voxel-run splits")
+
+
 def build_plan(tensor, strategy, threads):
     """Chunk boundaries for a strategy on this tensor (engine.py:155-184)."""
     if threads < 1:
         raise ConfigInvalid("threads must be >= 1")
     phi = _phi(tensor)
     nc = phi.dims.n_coeffs
+    check_strategy_ordering(strategy, phi.ordering)
     if strategy.kind == "coefficient":
         bounds = _equal_split(nc, threads)
         if strategy.sync_free:
-            if phi.ordering != "by_voxel":
-                raise StrategyRequiresSorted("sync_free requires a voxel-sorted tensor")
             bounds = snap_to_run_boundaries(phi.voxels, bounds)
     else:
-        want = _NEEDS[strategy.kind]
-        if phi.ordering != want:
-            raise StrategyRequiresSorted(
-                f"{strategy.kind} partitioning requires ordering {want!r}, "
-                f"tensor is {phi.ordering!r}")
-        if strategy.sync_free and strategy.kind != "voxel":
-            raise StrategyRequiresSorted("sync_free applies to voxel-run splits")
         bounds = _whole_runs(phi.key_array(strategy.kind), nc, threads)
     chunks = tuple((bounds[i], bounds[i + 1]) for i in range(threads))
     return ExecutionPlan(strategy=strategy, threads=threads, chunks=chunks)

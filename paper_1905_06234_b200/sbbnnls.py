@@ -25,9 +25,12 @@ DEFAULT_MAX_ITERS = 500
 class SolverConfig:
     """Solver controls (sbbnnls.py:34-62) plus device options.
 
-    ``threads``, the restructure keys and strategies are accepted and
-    validated for compatibility; the device always uses its own voxel-major
-    layout.  ``precision``: "fp32" (fast) or "fp64" (bit-exact kernels)."""
+    ``threads``, the restructure keys and strategies are validated exactly
+    as the reference's ``_runners`` would (``solve`` raises
+    StrategyRequiresSorted / ConfigInvalid for incompatible pairs before any
+    device work); the device then uses its own voxel-major tile layout for
+    both products.  ``precision``: "fp32" (fast) or "fp64" (bit-exact
+    kernels)."""
 
     max_iters: int = DEFAULT_MAX_ITERS
     grad_tol: float = 1e-12
@@ -141,6 +144,22 @@ def step_size(iter_index, g_tilde, problem, *, precision=None):
     return num / den
 
 
+def check_restructure_pairs(ordering, config):
+    """Validate (op, restructure key, strategy) the way the reference's
+    ``_runners`` do (sbbnnls.py:119-167): the strategy defaults to
+    ``best_partition(op, key)`` and must suit the ordering of the copy the
+    key produces (``sort_by`` tags ``by_<key>``; "none" keeps the tensor's
+    own).  Only metadata is involved, no sort runs."""
+    from .restructure import best_partition
+    if config.threads < 1:
+        raise ConfigInvalid("threads must be >= 1")
+    for op, key, strategy in (("dsc", config.dsc_restructure, config.dsc_strategy),
+                              ("wc", config.wc_restructure, config.wc_strategy)):
+        if strategy is None:
+            strategy = best_partition(op, key)
+        engine.check_strategy_ordering(strategy, ordering if key == "none" else f"by_{key}")
+
+
 def solve_device(op, b, w, config, stream=None):
     """Run ``life_solve`` on device tensors: b (signal) and w (in: w0 when
     ``w`` is given initialised, out: final weights).  Returns the raw C result
@@ -237,6 +256,7 @@ def solve(problem, w0=None, config=None):
         config = SolverConfig()
     if problem.y is None:
         raise ConfigInvalid("problem has no signal vector to fit")
+    check_restructure_pairs(problem.tensor.ordering, config)
     torch = N.require_cuda()
     t_setup = time.perf_counter()
     exact = config.precision == "fp64"

@@ -1,5 +1,6 @@
-"""CLI surface (cli.py of the reference): flags, CSV schemas and the exit
-codes of the host-side error paths (no GPU needed for these)."""
+"""CLI surface: the reference's flags for spmv / solve /
+bench, its CSV schemas and the exit codes of the host-side error paths (no
+GPU needed for these)."""
 
 import os
 
@@ -17,11 +18,19 @@ def test_parser_mirrors_reference_flags():
     assert (a.op, a.restructure, a.partition, a.sync_free, a.threads, a.repeat) == \
         ("wc", "auto", "voxel", True, 4, 3)
     a = p.parse_args(["solve", "--in", "x"])
-    assert a.iters == 500 and a.grad_tol == 1e-12
-    a = p.parse_args(["gen", "--out", "o"])
-    assert (a.voxels, a.fibers, a.atoms, a.dirs, a.coeffs, a.run_len) == (128, 64, 32, 96, 4096, 4.0)
+    assert a.iters == 500 and a.grad_tol == 1e-12 and a.precision is None
     a = p.parse_args(["bench", "--in", "x", "--report", "r"])
     assert a.threads_list == "1,2,4,8" and a.iters == 10
+    assert cli.TRACE_COLUMNS == ("iteration", "objective", "alpha", "grad_norm", "zeros",
+                                 "dsc_s", "wc_s")
+    assert cli.BENCH_COLUMNS == ("threads", "iters", "elapsed_s", "speedup_vs_1thread")
+
+
+def test_threads_default_from_env(monkeypatch):
+    monkeypatch.setenv("LIFE_THREADS", "6")
+    assert cli.host_threads(None) == 6 and cli.host_threads(2) == 2
+    monkeypatch.setenv("LIFE_THREADS", "x")
+    assert cli.host_threads(None) == 1
 
 
 def test_exit_codes(tmp_path, capsys):

@@ -161,3 +161,31 @@ def test_generator_draws_c1_hashes(golden_hashes):
     for name in ("atoms", "voxels", "fibers", "values"):
         assert sha(getattr(t, name)) == rec["sha_" + name]
     assert sha(dic.data) == rec["sha_dict"] and sha(w_true) == rec["sha_w_true"]
+
+
+def test_solve_validates_strategy_pairs_like_the_reference():
+    """sbbnnls._runners builds a plan per op (sbbnnls.py:119-167); the drop-in
+    raises the same errors before touching the device."""
+    from paper_1905_06234_b200.errors import StrategyRequiresSorted
+    from paper_1905_06234_b200.sbbnnls import check_restructure_pairs
+    ok = L.SolverConfig()
+    check_restructure_pairs("unsorted", ok)   # voxel/atom defaults pass
+    bad = [
+        L.SolverConfig(dsc_strategy=L.PartitionStrategy("fiber")),               # by_voxel copy
+        L.SolverConfig(wc_strategy=L.PartitionStrategy("coefficient", sync_free=True)),  # by_atom
+        L.SolverConfig(dsc_restructure="none"),   # best_partition: coefficient, no sync-free
+    ]
+    check_restructure_pairs("unsorted", bad[2])
+    for cfg in bad[:2]:
+        with pytest.raises(StrategyRequiresSorted):
+            check_restructure_pairs("unsorted", cfg)
+    cfg = L.SolverConfig(dsc_restructure="none",
+                         dsc_strategy=L.PartitionStrategy("coefficient", sync_free=True))
+    with pytest.raises(StrategyRequiresSorted):
+        check_restructure_pairs("unsorted", cfg)
+    check_restructure_pairs("by_voxel", cfg)   # the tensor itself is voxel-sorted
+    d = L.Dims(1, 1, 1, 1, 1)
+    t = L.PhiTensor(atoms=[0], voxels=[0], fibers=[0], values=[1.0], dims=d)
+    p = L.Problem(tensor=t, dictionary=L.Dictionary(data=[1.0], dims=d), y=np.array([1.0]))
+    with pytest.raises(StrategyRequiresSorted):   # raised before any CUDA work
+        L.solve(p, config=bad[0])

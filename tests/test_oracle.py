@@ -191,3 +191,23 @@ def test_hashed_medium(oracle, golden_hashes):
 @pytest.mark.slow
 def test_hashed_c1(oracle, golden_hashes):
     _check_hashed(oracle, golden_hashes["c1"], solve=False)
+
+
+def test_fp32_input_rounding_drift_of_solver_cases(oracle, golden):
+    """How far the reference's own 30-iteration trajectories move when only
+    the INPUTS (values, D, y) are rounded to fp32: the floor any fp32 path
+    inherits.  All solver cases stay below the north_star 1e-4 bound, so the
+    fp32 device solver is held to 1e-4 on every one of them
+    (tests/test_gpu_parity.py::test_solver_matches_reference)."""
+    for name in [str(n) for n in golden["solver_case_names"]]:
+        pre = f"solp_{name}_"
+        p = dict(atoms=golden[pre + "atoms"], voxels=golden[pre + "voxels"],
+                 fibers=golden[pre + "fibers"], values=golden[pre + "values"],
+                 dict=golden[pre + "dict"], y=golden[pre + "y"], ordering="unsorted",
+                 dims=tuple(int(x) for x in golden[pre + "dims"]))
+        for k in ("values", "dict", "y"):
+            p[k] = p[k].astype(np.float32).astype(np.float64)
+        w, _ = oracle.solve(p, max_iters=30, grad_tol=0.0)
+        ref = golden[f"sol_{name}_t1_w"]
+        drift = np.linalg.norm(w - ref) / np.linalg.norm(ref)
+        assert drift < 5e-5, (name, drift)
