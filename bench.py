@@ -9,8 +9,9 @@ algorithm, seed 0, noise 0.1).  ``value`` times exactly K iterations with
 the problem resident in HBM (CUDA events, max over ranks); ``e2e`` times a
 public ``solve()`` of K iterations from host numpy arrays (H2D of Phi/D/b,
 device restructuring, the iterations, D2H of w).  The reference arm
-(``--impl reference``) times the CPU oracle port of the reference on a
-bounded sample of the same workload on this host's cores.
+(``--impl reference``) times the CPU oracle port of the reference's
+sbbnnls.solve on the full C2 workload on this host's cores: W untimed
+iterations, then exactly K timed ones of the same solve.
 """
 
 import argparse
@@ -130,41 +131,54 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# reference arm: CPU oracle port on a bounded sample
+# reference arm: CPU oracle port on the full workload
 # ---------------------------------------------------------------------------
 
 
-def sample_dims(dims, target_nc=5_000_000):
-    """Same per-voxel / per-fascicle densities, ~target_nc coefficients."""
-    na, nv, nf, nt, nc = dims
-    f = min(1.0, target_nc / nc)
-    return (na, max(1, int(round(nv * f))), max(1, int(round(nf * f))), nt,
-            max(1, int(round(nc * f))))
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
-def cpu_reference(dims, iters_lo=1, iters_hi=5, threads=None):
-    """Per-iteration cost of the oracle port of sbbnnls.solve on a sample,
-    scaled to the full workload (linear in Nc).  (t(k2) - t(k1)) / (k2 - k1)
-    removes the per-solve sorting, as BASELINE.md prescribes."""
+def oracle_problem(problem):
+    """The oracle's dict view of a generated Problem (same arrays, no copy)."""
+    t = problem.tensor
+    d = t.dims
+    return dict(atoms=t.atoms, voxels=t.voxels, fibers=t.fibers, values=t.values,
+                dict=problem.dictionary.data, y=problem.y, ordering="unsorted",
+                dims=(d.n_atoms, d.n_voxels, d.n_fibers, d.n_dirs, d.n_coeffs))
+
+
+def time_oracle_iterations(p, warm, steps, threads):
+    """Seconds for exactly `steps` SBBNNLS iterations of the oracle port of
+    sbbnnls.solve at full size, after `warm` untimed iterations, read from
+    the per-iteration timestamps of ONE solve (its sorting setup and the w0
+    DSC fall before iteration 1 ends and are excluded)."""
     from oracle import oracle as O
-    threads = threads or os.cpu_count()
     O.set_threads(threads)
-    sd = sample_dims(dims)
-    p = O.generate(sd, max(1.0, 1.04 * sd[4] / sd[1]), 0.5, 0.1, 0)
-    t0 = time.perf_counter()
-    _, tr1 = O.solve(p, max_iters=iters_lo, grad_tol=0.0, threads=threads)
-    t1 = time.perf_counter()
-    _, tr2 = O.solve(p, max_iters=iters_hi, grad_tol=0.0, threads=threads)
-    t2 = time.perf_counter()
-    # iterations actually run (a solve may stop early on a degenerate step)
-    n_it = max(1, len(tr2["records"]) - len(tr1["records"]))
-    per_iter = ((t2 - t1) - (t1 - t0)) / n_it
-    scale = sd[4] / dims[4]
-    return {"value": scale / per_iter, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": (f"oracle port of sbbnnls.solve, Nc={sd[4]} (Na={sd[0]} Nv={sd[1]} "
-                       f"Nf={sd[2]} Nt={sd[3]}), (t({iters_hi})-t({iters_lo}))/"
-                       f"{iters_hi - iters_lo} per iteration, scaled by Nc ratio {scale:.4g}"),
-            "sample_seconds_per_iter": per_iter}
+    _, tr = O.solve(p, max_iters=warm + steps, grad_tol=0.0, threads=threads)
+    recs = tr["records"]
+    if len(recs) < warm + steps:
+        raise RuntimeError(f"oracle solve stopped after {len(recs)} iterations ({tr['termination']})")
+    return recs[warm + steps - 1]["t"] - recs[warm - 1]["t"]
+
+
+def cpu_reference(problem, dims, warm=1, steps=2, threads=None):
+    """Per-iteration rate of the oracle port of sbbnnls.solve on the FULL
+    workload (iterations warm+1 .. warm+steps of one solve)."""
+    threads = threads or os.cpu_count()
+    sec = time_oracle_iterations(oracle_problem(problem), warm, steps, threads)
+    return {"value": steps / sec, "unit": UNIT, "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
+            "sample": (f"oracle port (C + numpy, OpenMP) of sbbnnls.solve on the full workload "
+                       f"Nc={dims[4]}: iterations {warm + 1}..{warm + steps} of one solve "
+                       f"({steps} iterations, {sec:.1f} s), sorting setup excluded")}
 
 
 def run_reference(args, dims):
@@ -174,32 +188,26 @@ def run_reference(args, dims):
     from oracle import oracle as O
     threads = os.cpu_count()
     O.set_threads(threads)
-    sd = sample_dims(dims)
-    p = O.generate(sd, max(1.0, 1.04 * sd[4] / sd[1]), 0.5, 0.1, 0)
-    # each step: one oracle SBBNNLS iteration on the sample; differencing
-    # solves of W and W+K iterations isolates exactly K iterations
+    na, nv, nf, nt, nc = dims
     t0 = time.perf_counter()
-    _, tr1 = O.solve(p, max_iters=max(1, args.warmup), grad_tol=0.0, threads=threads)
-    t1 = time.perf_counter()
-    _, tr2 = O.solve(p, max_iters=max(1, args.warmup) + args.steps, grad_tol=0.0,
-                     threads=threads)
-    t2 = time.perf_counter()
-    # iterations actually run (a solve may stop early on a degenerate step)
-    n_it = max(1, len(tr2["records"]) - len(tr1["records"]))
-    per_iter = ((t2 - t1) - (t1 - t0)) / n_it
-    scale = sd[4] / dims[4]
-    value = scale / per_iter
+    p = O.generate(dims, 1.04 * nc / nv, 0.5, 0.1, 0)
+    t_gen = time.perf_counter() - t0
+    # a step is one SBBNNLS iteration of the reference algorithm on the full
+    # workload: W untimed iterations, then exactly K timed ones
+    sec = time_oracle_iterations(p, args.warmup, args.steps, threads)
+    value = args.steps / sec
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(dims, args, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "cpu_model": cpu_model(),
                              "sample": f"oracle port (C + numpy, OpenMP) of sbbnnls.solve on "
-                                       f"Nc={sd[4]} of the same density; per-iteration time "
-                                       f"by differencing solves of {max(1, args.warmup)} and "
-                                       f"{max(1, args.warmup) + args.steps} iterations, scaled "
-                                       f"by the Nc ratio {scale:.4g}"},
+                                       f"the full workload Nc={nc}: iterations "
+                                       f"{args.warmup + 1}..{args.warmup + args.steps} of one "
+                                       f"solve timed from its per-iteration timestamps "
+                                       f"(generation {t_gen:.0f} s and sorting setup excluded)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -369,7 +377,7 @@ def run_ours(args, dims):
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        cpu = cpu_reference(dims)
+        cpu = cpu_reference(problem, dims)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

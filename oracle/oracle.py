@@ -28,6 +28,7 @@ import ctypes
 import math
 import os
 import subprocess
+import time
 
 import numpy as np
 
@@ -381,7 +382,8 @@ def solve(p, w0=None, max_iters=500, grad_tol=1e-12, threads=1,
                          grad_norm=gnorm, zeros=int(np.count_nonzero(w == 0.0)),
                          dsc_calls=calls["dsc"] - c0[0],
                          wc_calls=calls["wc"] - c0[1], dsc_skipped=skipped,
-                         w_min=float(w.min()) if len(w) else 0.0))
+                         w_min=float(w.min()) if len(w) else 0.0,
+                         t=time.perf_counter()))
     else:
         term = "max_iters"
         r = mv(w) - b

@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(256)
                     sc = __dmul_rn(w[fiber[k]], val[k]);
                 }
                 const unsigned zm = __ballot_sync(0xffffffffu, valid && sc == 0.0);
-                if (t0 == 0) skipped += __popc(zm);
+                if (t0 == 0 && skip_zero) skipped += __popc(zm);  // counted only when skipping (_kernels.py:25-28)
                 unsigned m = __ballot_sync(0xffffffffu, valid);
                 if (skip_zero) m &= ~zm;
                 while (m) {

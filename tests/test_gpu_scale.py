@@ -11,7 +11,8 @@ Chain of evidence at C2 (Nc = 100M):
   * a 5-iteration fp32 SBBNNLS matches the reference's weights (full vector)
     and per-iteration objectives within 1e-4.
 At C1 a 50-iteration fp32 SBBNNLS matches the reference's full weight vector
-and every per-iteration objective and step within 1e-4.
+and every per-iteration objective within 1e-4, and the step sizes of the
+iterations before convergence (after it alpha is roundoff, see _determined).
 """
 
 import hashlib
@@ -56,7 +57,20 @@ def c2(scale):
     return _generate(recs["c2"])
 
 
-def _check_trace(tr, rec, tol):
+def _determined(ref_o, floor):
+    """Iterations whose step size is determined by the problem rather than by
+    roundoff: while the reference objective still falls by more than `floor`
+    (relative) into the next iteration.  Once the fit has converged (C1: by
+    iteration ~9 at fp32 resolution, ~16 at fp64) alpha is a ratio of
+    gradient norms at rounding level and differs even between two fp64 runs
+    (SURVEY.md 8(c) fact 4)."""
+    n = 0
+    while n + 1 < len(ref_o) and (ref_o[n] - ref_o[n + 1]) > floor * abs(ref_o[n + 1]):
+        n += 1
+    return n + 1
+
+
+def _check_trace(tr, rec, tol, alpha_floor=1e-5):
     objs = np.array([r.objective for r in tr.records])
     alphas = np.array([r.alpha for r in tr.records])
     ref_o = np.array(rec["solve_objective"])
@@ -64,7 +78,8 @@ def _check_trace(tr, rec, tol):
     assert tr.termination == rec["solve_termination"]
     assert len(objs) == len(ref_o)
     worst_o = float(np.max(np.abs(objs - ref_o) / np.abs(ref_o)))
-    worst_a = float(np.max(np.abs(alphas - ref_a) / np.abs(ref_a)))
+    n = _determined(ref_o, alpha_floor)
+    worst_a = float(np.max(np.abs(alphas[:n] - ref_a[:n]) / np.abs(ref_a[:n])))
     assert worst_o <= tol, ("objective", worst_o)
     assert worst_a <= tol, ("alpha", worst_a)
     fo = rec["solve_final_objective"]
@@ -96,7 +111,7 @@ def test_c1_solve_fp64_bitwise_trajectory(scale):
     p = _generate(rec)
     w, tr = L.solve(p, config=L.SolverConfig(max_iters=50, grad_tol=0.0, precision="fp64"))
     assert rel_l2(w, arrays["c1_solve50_w"]) <= 1e-9
-    _check_trace(tr, rec, 1e-9)
+    _check_trace(tr, rec, 1e-9, alpha_floor=1e-12)
     assert [r.zeros for r in tr.records] == rec["solve_zeros"]
 
 

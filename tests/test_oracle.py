@@ -10,7 +10,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from conftest import golden_problem
+from conftest import fp32_product_floor, golden_problem, rel_l2, solver_case
 
 
 def sha(a):
@@ -195,19 +195,26 @@ def test_hashed_c1(oracle, golden_hashes):
 
 def test_fp32_input_rounding_drift_of_solver_cases(oracle, golden):
     """How far the reference's own 30-iteration trajectories move when only
-    the INPUTS (values, D, y) are rounded to fp32: the floor any fp32 path
-    inherits.  All solver cases stay below the north_star 1e-4 bound, so the
-    fp32 device solver is held to 1e-4 on every one of them
-    (tests/test_gpu_parity.py::test_solver_matches_reference)."""
+    the INPUTS (values, D, y) are rounded to fp32: well-conditioned cases stay
+    far below the north_star 1e-4 bound."""
     for name in [str(n) for n in golden["solver_case_names"]]:
-        pre = f"solp_{name}_"
-        p = dict(atoms=golden[pre + "atoms"], voxels=golden[pre + "voxels"],
-                 fibers=golden[pre + "fibers"], values=golden[pre + "values"],
-                 dict=golden[pre + "dict"], y=golden[pre + "y"], ordering="unsorted",
-                 dims=tuple(int(x) for x in golden[pre + "dims"]))
+        p = solver_case(golden, name)
         for k in ("values", "dict", "y"):
             p[k] = p[k].astype(np.float32).astype(np.float64)
         w, _ = oracle.solve(p, max_iters=30, grad_tol=0.0)
-        ref = golden[f"sol_{name}_t1_w"]
-        drift = np.linalg.norm(w - ref) / np.linalg.norm(ref)
+        drift = rel_l2(w, golden[f"sol_{name}_t1_w"])
         assert drift < 5e-5, (name, drift)
+
+
+def test_fp32_product_rounding_floor_of_solver_cases(oracle, golden):
+    """The floor an fp32 solver inherits: inputs AND every product correctly
+    rounded to fp32.  Measured: small11 6.8e-4 and small3 8.4e-5 (the BB
+    iteration amplifies one-ulp product errors ~1e4x on these ill-conditioned
+    cases), every other case < 1e-7.  The fp32 device solver is therefore held
+    to max(1e-4, 10 x floor) per case, and the fp64 path to 1e-9 on all
+    (tests/test_gpu_parity.py::test_solver_matches_reference)."""
+    floors = {str(n): fp32_product_floor(golden, str(n))[0] for n in golden["solver_case_names"]}
+    assert floors["small11"] > 1e-4, floors       # infeasible at 1e-4 for any fp32 path
+    for name, f in floors.items():
+        if name not in ("small11", "small3"):
+            assert f < 1e-6, (name, f)
