@@ -89,7 +89,8 @@ LIFE_API uint64_t life_launch_count(void);
 #define LIFE_PHI_FORCE_SPARSE 0x8u  /* fp32: voxel-segment kernels only    */
 #define LIFE_PHI_FORCE_DENSE  0x10u /* fp32: register-tiled dense kernels  */
 #define LIFE_PHI_NO_TENSOR    0x20u /* fp32: no tcgen05 products (CUDA cores only) */
-#define LIFE_PHI_TENSOR       0x40u /* fp32: tcgen05 products (the default for tile layouts) */
+#define LIFE_PHI_TENSOR       0x40u /* fp32: single-pass tcgen05 tile products (with LIFE_PHI_NO_BIN) */
+#define LIFE_PHI_NO_BIN       0x80u /* fp32: not the binned two-phase products (life_bin.cu)   */
 
 /* Build the device operator from COO arrays (PhiTensor + Dictionary,
  * tensor.py:76-170).  atoms/voxels/fibers: u32[n_coeffs]; values:
@@ -107,7 +108,7 @@ LIFE_API int life_phi_destroy(life_phi *phi);
 
 typedef struct life_phi_info {
     life_dims dims;
-    int32_t atom_groups;        /* sparse kernels: passes over Phi (D slices); 0 = dense, -1 = dense + tcgen05 DSC */
+    int32_t atom_groups;        /* sparse kernels: passes over Phi (D slices); 0 = dense, -1 = dense + tcgen05 DSC, -2 = binned two-phase (tcgen05) */
     int32_t atoms_per_group;
     int32_t n_warps;            /* persistent warps of the SpMV kernels   */
     int32_t has_exact;          /* fp64 bit-exact layout present          */

@@ -25,6 +25,7 @@ PHI_FORCE_SPARSE = 0x8
 PHI_FORCE_DENSE = 0x10
 PHI_NO_TENSOR = 0x20
 PHI_TENSOR = 0x40
+PHI_NO_BIN = 0x80
 ACCUMULATE = 0x01
 SKIP_ZERO = 0x02
 SUBTRACT_B = 0x04

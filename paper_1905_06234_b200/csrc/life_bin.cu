@@ -1,0 +1,1981 @@
+// life_bin.cu -- the binned two-phase DSC / WC products (default fp32 path).
+//
+// Every product of M = Phi x_1 D pairs two orders of the coefficients:
+//
+//   tile side  coefficients grouped by (tile of 128 voxel rows, chunk of KA
+//              atoms): the dense contraction runs on tcgen05 (DSC:
+//              Y += C . D_chunk with C[row, atom] = sum s; WC: Z = Y . D_chunk^T);
+//   bin side   coefficients grouped by fascicle bin (a range of at most
+//              kSB virtual fascicle slots): the per-coefficient random
+//              access (DSC: w[f]; WC: the fascicle sum) hits a bin-sized
+//              slice in shared memory instead of L2.
+//
+// The sides exchange one value per coefficient through a tile-major scratch
+// vector: the DSC bin side writes s = w[f] * value there and the tile side
+// reads it; the WC tile side writes z = Z[row, atom] there and the bin side
+// reads it.  Both orders are stable sorts of the same coefficient list, so a
+// segment (tile, chunk, bin) is contiguous in both: the bin side streams its
+// bin-major arrays and reads/writes the scratch in runs.  Random accesses per
+// coefficient are shared-memory only; global memory is streamed.
+//
+// Determinism without ordering constraints: DSC repeats of a (row, atom) cell
+// are added in rank order (rank-level passes); WC fascicle sums are exact
+// integers (64-bit fixed point, accumulated as two 32-bit limbs with native
+// shared-memory atomics; a virtual fascicle slot holds at most kSlotCap
+// coefficients so the limbs cannot overflow), so any summation order gives
+// the same bits, across CTAs, slots, and ranks.
+//
+// Reference: _kernels.dsc_range / wc_range (/root/reference/pkg/src/
+// lifespmv/_kernels.py:14-33, 57-68) under the owned regimes of
+// engine.dsc_parallel / wc_parallel (engine.py:247-289, 372-413).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "life_common.cuh"
+#include "life_tcgen05.cuh"
+
+namespace life {
+namespace bin {
+
+constexpr int kTV = 128;            // tile rows (tcgen05 M)
+constexpr int kRanks = 7;           // duplicate ranks per tile row (rank field value 7 = pad)
+constexpr uint16_t kPad = 0xFFFFu;  // tile-major pad entry
+constexpr int kSlotCap = 256;       // coefficients per virtual fascicle slot (2-limb fixed point)
+constexpr int kSB = 16384;          // virtual slots per bin: 64 KB (DSC w) / 128 KB (WC limbs)
+constexpr int kBuild = 8;           // builder / gatherer warps of the tile kernels
+constexpr int kSideWarps = 32;      // bin-side CTA
+constexpr int kSideU = 4;           // 32-entry chunks per warp batch on the bin side
+constexpr int kSlots = 3;           // staged steps per tile kernel
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t sa(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t *b, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(count));
+}
+__device__ __forceinline__ void bar_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(uint64_t *b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool bar_try(uint64_t *b, unsigned parity)
+{
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(sa(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
+// trap after 4 s instead of hanging the GPU
+__device__ __forceinline__ void bar_wait(uint64_t *b, unsigned parity)
+{
+    if (bar_try(b, parity)) return;
+    const unsigned long long t0 = globaltimer();
+    while (!bar_try(b, parity))
+        if (globaltimer() - t0 > 4000000000ull) __trap();
+}
+// bulk copy global -> shared in pieces of at most 32 KB, completing on bar
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *b, uint64_t pol)
+{
+    const char *s = reinterpret_cast<const char *>(src);
+    char *d = reinterpret_cast<char *>(dst);
+    for (unsigned o = 0; o < bytes; o += 32768u)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                     ::"r"(sa(d + o)), "l"(s + o), "r"(min(32768u, bytes - o)), "r"(sa(b)), "l"(pol)
+                     : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void *src, unsigned bytes)
+{
+    const char *s = reinterpret_cast<const char *>(src);
+    for (unsigned o = 0; o < bytes; o += 32768u)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s + o), "r"(min(32768u, bytes - o)) : "memory");
+}
+__device__ __forceinline__ uint64_t pol_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void named_bar(int id, int threads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a)
+{
+    uint16_t r;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ float lds_f(uint32_t a)
+{
+    float r;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ void sts_f(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory"); }
+__device__ __forceinline__ float4 lds_f4(uint32_t a)
+{
+    float4 r;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ void sts_f4(uint32_t a, float4 v)
+{
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+// TMEM stores / loads of 16 consecutive 32-bit columns of this thread's lane
+__device__ __forceinline__ void tm_st16(uint32_t addr, const uint32_t (&v)[16])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                 "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld16(uint32_t addr, uint32_t (&r)[16])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// 64-bit fixed-point exponent of the WC bin side: every term |val * z| is at
+// most vmax * dmax * ||y_v|| <= vmax * dmax * ynorm; scaled terms stay below
+// 2^45 (two limbs: 24 low bits summed in u32 over <= 256 terms, the signed
+// rest in i32), and a fascicle total (fmax_nnz terms, all ranks) below 2^62.
+__host__ __device__ inline int bin_exponent(double vmax, double dmax, double ynorm, double fmax_nnz)
+{
+    const double bound = vmax * dmax * ynorm * (1.0 + 1.0 / 1024.0);
+    if (!(bound > 0.0) || !(bound < 1e300)) return 0;
+    int eb;
+    frexp(bound, &eb);  // bound < 2^eb
+    int ef;
+    frexp(fmax_nnz > 1.0 ? fmax_nnz : 1.0, &ef);  // fmax_nnz < 2^ef
+    int cap = 62 - ef;
+    if (cap > 45) cap = 45;
+    int ex = cap - eb;
+    if (ex > 1000) ex = 1000;
+    if (ex < -1000) ex = -1000;
+    return ex;
+}
+__device__ inline int bin_exponent_dev(const FixParams &fx, int nt)
+{
+    const double yn = fx.ysumsq ? sqrt(*fx.ysumsq) : sqrt((double)nt) * (double)*fx.ymax;
+    return bin_exponent(fx.vmax, fx.dmax, yn, fx.fmax_nnz);
+}
+
+// fixed-order reductions of per-warp partials (last CTA)
+template <typename T, typename Op>
+__device__ T block_reduce(const T *part, int n, T init, Op op, int nthreads)
+{
+    __shared__ T s[32];
+    T acc = init;
+    for (int i = threadIdx.x; i < n; i += nthreads) acc = op(acc, __ldcg(part + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = op(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    T r = init;
+    if (threadIdx.x < 32) {
+        r = threadIdx.x < (nthreads >> 5) ? s[threadIdx.x] : init;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r = op(r, __shfl_xor_sync(0xffffffffu, r, o));
+        if (threadIdx.x == 0) s[0] = r;
+    }
+    __syncthreads();
+    r = s[0];
+    __syncthreads();
+    return r;
+}
+struct OpSum {
+    template <typename T>
+    __device__ T operator()(T a, T b) const { return a + b; }
+};
+struct OpMaxF {
+    __device__ float operator()(float a, float b) const { return fmaxf(a, b); }
+};
+
+__device__ __forceinline__ bool last_cta(unsigned *counter)
+{
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
+// DSC outputs from the tile/fixup partials and the bin side's skip partials
+__device__ void dsc_finish(const ReduceSlots &red, int nparts, const unsigned long long *skip, int nskip,
+                           const DscOut &out, unsigned *counter, const CallHooks &hooks, int nthreads)
+{
+    const double tsq = block_reduce<double>(red.part_d, nparts, 0.0, OpSum{}, nthreads);
+    const float tmax = block_reduce<float>(red.part_f, nparts, 0.f, OpMaxF{}, nthreads);
+    const unsigned long long tsk = block_reduce<unsigned long long>(skip, nskip, 0ull, OpSum{}, nthreads);
+    if (threadIdx.x == 0) {
+        if (out.sumsq) *out.sumsq = tsq;
+        if (out.absmax) *out.absmax = tmax;
+        if (out.skipped) *out.skipped = tsk;
+        if (out.skipped_d) *out.skipped_d = (double)tsk;
+        *counter = 0;
+        if (hooks.t_accum && hooks.t_begin) *hooks.t_accum += globaltimer() - *hooks.t_begin;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// construction kernels
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t gtid() { return blockIdx.x * (int64_t)blockDim.x + threadIdx.x; }
+__device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
+
+__global__ void k_iota(uint32_t *o, int64_t n)
+{
+    for (int64_t i = gtid(); i < n; i += gstride()) o[i] = (uint32_t)i;
+}
+__global__ void k_key_va(const uint32_t *a, const uint32_t *v, int64_t n, uint32_t na, unsigned long long *key)
+{
+    for (int64_t i = gtid(); i < n; i += gstride()) key[i] = (unsigned long long)v[i] * na + a[i];
+}
+// run heads of a sorted u64 key: head[p] = p at a run start, else 0
+__global__ void k_heads64(const unsigned long long *k, int64_t n, uint32_t *head)
+{
+    for (int64_t p = gtid(); p < n; p += gstride()) head[p] = (p == 0 || k[p] != k[p - 1]) ? (uint32_t)p : 0u;
+}
+__global__ void k_heads32(const uint32_t *k, int64_t n, uint32_t *head)
+{
+    for (int64_t p = gtid(); p < n; p += gstride()) head[p] = (p == 0 || k[p] != k[p - 1]) ? (uint32_t)p : 0u;
+}
+// rank of each coefficient among the equal (voxel, atom) pairs in stable
+// order, and the largest rank per voxel
+__global__ void k_rank_va(const unsigned long long *sk, const uint32_t *perm, const uint32_t *rstart, int64_t n,
+                          uint32_t na, uint32_t *rank_o, uint32_t *vmaxr)
+{
+    for (int64_t p = gtid(); p < n; p += gstride()) {
+        const uint32_t r = (uint32_t)p - rstart[p];
+        rank_o[perm[p]] = r;
+        if (p == n - 1 || sk[p + 1] != sk[p]) atomicMax(&vmaxr[(uint32_t)(sk[p] / na)], r);
+    }
+}
+__global__ void k_rows_per_voxel(const uint32_t *vmaxr, int nv, uint32_t *nr)
+{
+    for (int64_t v = gtid(); v < nv; v += gstride()) nr[v] = vmaxr[v] / kRanks + 1u;
+}
+__global__ void k_row_of(const uint32_t *v, const uint32_t *rank_o, const uint32_t *rowbase, int64_t n,
+                         uint32_t *row_o, unsigned *rcnt)
+{
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        const uint32_t r = rowbase[v[i]] + rank_o[i] / kRanks;
+        row_o[i] = r;
+        atomicAdd(&rcnt[r], 1u);
+    }
+}
+__global__ void k_hist(const uint32_t *x, int64_t n, unsigned *cnt)
+{
+    for (int64_t i = gtid(); i < n; i += gstride()) atomicAdd(&cnt[x[i]], 1u);
+}
+__global__ void k_slots_per_fiber(const unsigned *cnt, int nf, uint32_t *ns)
+{
+    for (int64_t f = gtid(); f < nf; f += gstride()) ns[f] = cnt[f] <= (unsigned)kSlotCap ? 1u : (cnt[f] + kSlotCap - 1) / kSlotCap;
+}
+__global__ void k_vf2f(const uint32_t *f2vf, int nf, uint32_t *vf2f)
+{
+    for (int64_t f = gtid(); f < nf; f += gstride())
+        for (uint32_t s = f2vf[f]; s < f2vf[f + 1]; ++s) vf2f[s] = (uint32_t)f;
+}
+// virtual slot of each coefficient: the fascicle's occurrence index (stable
+// order) in blocks of kSlotCap
+__global__ void k_vf_split(const uint32_t *perm, const uint32_t *sf, const uint32_t *rstart, const uint32_t *f2vf,
+                           int64_t n, uint32_t *vf_o)
+{
+    for (int64_t p = gtid(); p < n; p += gstride())
+        vf_o[perm[p]] = f2vf[sf[p]] + ((uint32_t)p - rstart[p]) / kSlotCap;
+}
+__global__ void k_vf_identity(const uint32_t *f, const uint32_t *f2vf, int64_t n, uint32_t *vf_o)
+{
+    for (int64_t i = gtid(); i < n; i += gstride()) vf_o[i] = f2vf[f[i]];
+}
+// bin-major key (bin, tile, chunk) of each coefficient
+__global__ void k_key_bm(const uint32_t *a, const uint32_t *row_o, const uint32_t *vf_o, const uint32_t *slot_of_row,
+                         const uint32_t *rank_o, int64_t n, int ka_shift, uint32_t nch, uint32_t ntiles,
+                         unsigned long long *kbm)
+{
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        const uint32_t t = slot_of_row[row_o[i]] / kTV;
+        const uint32_t c = a[i] >> ka_shift;
+        const uint32_t b = vf_o[i] / kSB;
+        kbm[i] = ((unsigned long long)b * ntiles + t) * nch + c;
+    }
+}
+__global__ void k_head_flags(const unsigned long long *k, int64_t n, uint8_t *head, uint32_t *head32)
+{
+    for (int64_t p = gtid(); p < n; p += gstride()) {
+        const bool h = p == 0 || k[p] != k[p - 1];
+        head[p] = h ? 1 : 0;
+        head32[p] = h ? 1u : 0u;
+    }
+}
+// per segment (bin-major order): key, length in 4-entry units, and the
+// tile-major sort key (tile, chunk, bin)
+__global__ void k_seg_info(const unsigned long long *kbm_sorted, const uint32_t *first, int64_t nseg, int64_t n,
+                           unsigned long long per_bin, uint32_t nbins, uint32_t *len4, unsigned long long *segkey,
+                           unsigned long long *tmkey, uint32_t *step)
+{
+    for (int64_t s = gtid(); s < nseg; s += gstride()) {
+        const uint32_t f0 = first[s], f1 = s + 1 < nseg ? first[s + 1] : (uint32_t)n;
+        const unsigned long long k = kbm_sorted[f0];
+        len4[s] = (f1 - f0 + 3u) / 4u;
+        segkey[s] = k;
+        const unsigned long long b = k / per_bin, tc = k % per_bin;
+        tmkey[s] = tc * nbins + b;
+        step[s] = (uint32_t)tc;
+    }
+}
+__global__ void k_pad8(const unsigned *cnt, int64_t n, unsigned *pcnt)
+{
+    for (int64_t s = gtid(); s < n; s += gstride()) pcnt[s] = (cnt[s] + 7u) & ~7u;
+}
+__global__ void k_step_units(const uint32_t *step, const uint32_t *len4, int64_t nseg, unsigned *units)
+{
+    for (int64_t s = gtid(); s < nseg; s += gstride()) atomicAdd(&units[step[s]], len4[s]);
+}
+__global__ void k_step_pad(const unsigned *units, int64_t nsteps, unsigned *padded)
+{
+    for (int64_t s = gtid(); s < nsteps; s += gstride()) padded[s] = (4u * units[s] + 7u) & ~7u;
+}
+// tile-major exclusive unit prefix at the first segment of each step
+__global__ void k_step_first(const uint32_t *perm_seg, const uint32_t *tm_excl, const uint32_t *step, int64_t nseg,
+                             uint32_t *stepx)
+{
+    for (int64_t i = gtid(); i < nseg; i += gstride()) {
+        const uint32_t st = step[perm_seg[i]];
+        if (i == 0 || step[perm_seg[i - 1]] != st) stepx[st] = tm_excl[i];
+    }
+}
+// tile-major start of each segment: its step's start + the 4-padded lengths
+// of the step's earlier segments (lower rank, then lower bin)
+__global__ void k_seg_tm(const uint32_t *perm_seg, const uint32_t *tm_excl, const uint32_t *step, int64_t nseg,
+                         const uint32_t *step_ptr, const uint32_t *stepx, uint32_t *dst4)
+{
+    for (int64_t i = gtid(); i < nseg; i += gstride()) {
+        const uint32_t s = perm_seg[i], st = step[s];
+        dst4[s] = step_ptr[st] / 4u + (tm_excl[i] - stepx[st]);
+    }
+}
+// place every coefficient in both orders
+__global__ void k_place(const uint32_t *perm_bm, const uint32_t *segid, const uint32_t *first, const uint32_t *src4,
+                        const uint32_t *dst4, int64_t n, const uint32_t *vf_o, const double *val, const uint32_t *a,
+                        const uint32_t *rank_o, const uint32_t *row_o, const uint32_t *slot_of_row, int ka, int cellbits,
+                        uint16_t *vid, float *val32, uint16_t *cellr)
+{
+    for (int64_t p = gtid(); p < n; p += gstride()) {
+        const uint32_t i = perm_bm[p], s = segid[p] - 1u;
+        const uint32_t idx = (uint32_t)p - first[s];
+        const uint32_t bp = 4u * src4[s] + idx, tp = 4u * dst4[s] + idx;
+        vid[bp] = (uint16_t)(vf_o[i] % kSB);
+        val32[bp] = (float)val[i];
+        const uint32_t lane = slot_of_row[row_o[i]] % kTV;
+        const uint32_t cell = lane * (uint32_t)ka + (a[i] & (uint32_t)(ka - 1));
+        cellr[tp] = (uint16_t)(((rank_o[i] % kRanks) << cellbits) | cell);
+    }
+}
+// lower bound of key b * per_bin over the bin-major segment keys
+__global__ void k_bin_seg(const unsigned long long *segkey, int64_t nseg, int nbins, unsigned long long per_bin,
+                          uint32_t *binseg)
+{
+    for (int64_t b = gtid(); b <= nbins; b += gstride()) {
+        const unsigned long long key = (unsigned long long)b * per_bin;
+        int64_t lo = 0, hi = nseg;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (segkey[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        binseg[b] = (uint32_t)lo;
+    }
+}
+// bin-side CTA c takes the segments whose start lies in units [c*U/g, (c+1)*U/g)
+__global__ void k_cta_seg(const uint32_t *src4, int64_t nseg, int grid, uint32_t *ctaseg)
+{
+    for (int64_t c = gtid(); c <= grid; c += gstride()) {
+        const unsigned long long target = (unsigned long long)src4[nseg] * (unsigned long long)c / (unsigned long long)grid;
+        int64_t lo = 0, hi = nseg;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((unsigned long long)src4[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        ctaseg[c] = (uint32_t)(c == grid ? nseg : lo);
+    }
+}
+__global__ void k_gather_u32(const uint32_t *idx, const uint32_t *in, int64_t n, uint32_t *out)
+{
+    for (int64_t i = gtid(); i < n; i += gstride()) out[i] = in[idx[i]];
+}
+__global__ void k_fill_u16(uint16_t *x, int64_t n, uint16_t v)
+{
+    for (int64_t i = gtid(); i < n; i += gstride()) x[i] = v;
+}
+
+static int gridn(int64_t n)
+{
+    int64_t b = (n + 255) / 256;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, 65535 * 8));
+}
+static int bits64(unsigned long long x)
+{
+    int b = 0;
+    while (b < 64 && (x >> b) != 0) ++b;
+    return std::max(b, 1);
+}
+
+template <typename K>
+static int sort_pairs(const K *kin, K *kout, const uint32_t *vin, uint32_t *vout, int64_t n, int bits,
+                      cudaStream_t st)
+{
+    size_t tb = 0;
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0, bits, st));
+    void *temp = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&temp, tb, st));
+    LIFE_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, kin, kout, vin, vout, n, 0, bits, st));
+    LIFE_CUDA(cudaFreeAsync(temp, st));
+    g_launches.fetch_add(4, std::memory_order_relaxed);
+    return LIFE_OK;
+}
+static int scan_max(const uint32_t *in, uint32_t *out, int64_t n, cudaStream_t st)
+{
+    size_t tb = 0;
+    LIFE_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, in, out, cub::Max(), n, st));
+    void *temp = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&temp, tb, st));
+    LIFE_CUDA(cub::DeviceScan::InclusiveScan(temp, tb, in, out, cub::Max(), n, st));
+    LIFE_CUDA(cudaFreeAsync(temp, st));
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return LIFE_OK;
+}
+// exclusive sum of n counts into out[0..n] (out[n] = total)
+static int scan_excl(const uint32_t *in, uint32_t *out, int64_t n, cudaStream_t st)
+{
+    LIFE_CUDA(cudaMemsetAsync(out, 0, sizeof(uint32_t), st));
+    if (n == 0) return LIFE_OK;
+    size_t tb = 0;
+    LIFE_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out + 1, n, st));
+    void *temp = nullptr;
+    LIFE_CUDA(cudaMallocAsync(&temp, tb, st));
+    LIFE_CUDA(cub::DeviceScan::InclusiveSum(temp, tb, in, out + 1, n, st));
+    LIFE_CUDA(cudaFreeAsync(temp, st));
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return LIFE_OK;
+}
+
+// tf32 split on the host (same bits as the device split)
+static void tf32_split_h(float x, float &hi, float &lo)
+{
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u &= 0xFFFFE000u;
+    std::memcpy(&hi, &u, 4);
+    lo = x - hi;
+}
+// float index of (row, k) in a K-major SWIZZLE_128B tile of 32 fp32 per row
+static inline size_t sw_cell(uint32_t row, uint32_t k)
+{
+    return (size_t)(row >> 3) * 256u + (row & 7u) * 32u + ((((k >> 2) ^ row) & 7u) << 2) + (k & 3u);
+}
+
+}  // namespace bin
+
+// ---------------------------------------------------------------------------
+// build
+// ---------------------------------------------------------------------------
+int prepare_bin(life_phi *phi);
+
+int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f, const double *val,
+              const std::vector<double> &hdict, cudaStream_t st)
+{
+    using namespace bin;
+    const int64_t n = phi->nc;
+    const int N = (phi->nt + 31) / 32 * 32;
+    if (n == 0 || N > 192 || n >= 0xF0000000ll) return LIFE_OK;
+    const int ka = N <= 128 ? 64 : 32;
+    const int ka_shift = ka == 64 ? 6 : 5;
+    const int cellbits = ka == 64 ? 13 : 12;
+    const int nch = (phi->na + ka - 1) / ka;
+    const uint32_t na = (uint32_t)phi->na;
+    const int nv = phi->nv, nf = phi->nf;
+
+    // temporaries (stream-ordered)
+    std::vector<void *> tmp;
+    auto talloc = [&](void **p, size_t bytes) -> int {
+        LIFE_CUDA(cudaMallocAsync(p, std::max<size_t>(bytes, 16), st));
+        tmp.push_back(*p);
+        return LIFE_OK;
+    };
+    struct Free {
+        std::vector<void *> &t;
+        cudaStream_t s;
+        ~Free()
+        {
+            for (void *p : t) cudaFreeAsync(p, s);
+        }
+    } freer{tmp, st};
+
+    // 1. rank of each coefficient within its (voxel, atom) pair
+    unsigned long long *kva, *skva;
+    uint32_t *iota, *perm, *head, *rstart, *rank_o, *vmaxr;
+    LIFE_TRY(talloc((void **)&kva, n * 8));
+    LIFE_TRY(talloc((void **)&skva, n * 8));
+    LIFE_TRY(talloc((void **)&iota, n * 4));
+    LIFE_TRY(talloc((void **)&perm, n * 4));
+    LIFE_TRY(talloc((void **)&head, n * 4));
+    LIFE_TRY(talloc((void **)&rstart, n * 4));
+    LIFE_TRY(talloc((void **)&rank_o, n * 4));
+    LIFE_TRY(talloc((void **)&vmaxr, (size_t)nv * 4));
+    k_iota<<<gridn(n), 256, 0, st>>>(iota, n);
+    LIFE_CHECK_LAUNCH();
+    k_key_va<<<gridn(n), 256, 0, st>>>(a, v, n, na, kva);
+    LIFE_CHECK_LAUNCH();
+    LIFE_TRY(sort_pairs<unsigned long long>(kva, skva, iota, perm, n, bits64((unsigned long long)nv * na), st));
+    k_heads64<<<gridn(n), 256, 0, st>>>(skva, n, head);
+    LIFE_CHECK_LAUNCH();
+    LIFE_TRY(scan_max(head, rstart, n, st));
+    LIFE_CUDA(cudaMemsetAsync(vmaxr, 0, (size_t)nv * 4, st));
+    k_rank_va<<<gridn(n), 256, 0, st>>>(skva, perm, rstart, n, na, rank_o, vmaxr);
+    LIFE_CHECK_LAUNCH();
+
+    // 2. tile rows: a voxel gets one row per kRanks duplicate ranks
+    uint32_t *nr, *rowbase, *row_o;
+    unsigned *rcnt;
+    LIFE_TRY(talloc((void **)&nr, (size_t)nv * 4));
+    LIFE_TRY(talloc((void **)&rowbase, ((size_t)nv + 1) * 4));
+    LIFE_TRY(talloc((void **)&row_o, n * 4));
+    k_rows_per_voxel<<<gridn(nv), 256, 0, st>>>(vmaxr, nv, nr);
+    LIFE_CHECK_LAUNCH();
+    LIFE_TRY(scan_excl(nr, rowbase, nv, st));
+    uint32_t R = 0;
+    LIFE_CUDA(cudaMemcpyAsync(&R, rowbase + nv, 4, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    LIFE_TRY(talloc((void **)&rcnt, (size_t)R * 4));
+    LIFE_CUDA(cudaMemsetAsync(rcnt, 0, (size_t)R * 4, st));
+    k_row_of<<<gridn(n), 256, 0, st>>>(v, rank_o, rowbase, n, row_o, rcnt);
+    LIFE_CHECK_LAUNCH();
+    std::vector<uint32_t> hcnt(R), hbase(nv + 1);
+    LIFE_CUDA(cudaMemcpyAsync(hcnt.data(), rcnt, (size_t)R * 4, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaMemcpyAsync(hbase.data(), rowbase, ((size_t)nv + 1) * 4, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+
+    // 3. deal rows to tiles: counting sort by coefficient count (descending,
+    // stable), snake order over the tiles so every tile carries about the
+    // same number of coefficients
+    const int64_t ntiles = ((int64_t)R + kTV - 1) / kTV;
+    std::vector<uint32_t> slot_of_row(R);
+    std::vector<int> rowvox((size_t)ntiles * kTV, -1), rowpart((size_t)ntiles * kTV, -1);
+    {
+        uint32_t cmax = 0;
+        for (uint32_t c : hcnt) cmax = std::max(cmax, c);
+        std::vector<uint32_t> start((size_t)cmax + 2, 0);
+        for (uint32_t c : hcnt) ++start[cmax - c + 1];
+        for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
+        std::vector<uint32_t> order(R);
+        for (uint32_t r = 0; r < R; ++r) order[start[cmax - hcnt[r]]++] = r;
+        for (int64_t i = 0; i < (int64_t)R; ++i) {
+            const int64_t lane = i / ntiles, q = i % ntiles;
+            const int64_t t = (lane & 1) ? ntiles - 1 - q : q;
+            slot_of_row[order[i]] = (uint32_t)(t * kTV + lane);
+        }
+    }
+    std::vector<uint32_t> fixptr(1, 0);
+    std::vector<int> fixvox;
+    int nprow = 0;
+    for (int vx = 0; vx < nv; ++vx) {
+        const uint32_t r0 = hbase[vx], r1 = hbase[vx + 1];
+        for (uint32_t r = r0; r < r1; ++r) rowvox[slot_of_row[r]] = vx;
+        if (r1 - r0 > 1) {
+            for (uint32_t r = r0; r < r1; ++r) rowpart[slot_of_row[r]] = nprow++;
+            fixptr.push_back((uint32_t)nprow);
+            fixvox.push_back(vx);
+        }
+    }
+    uint32_t *d_slot;
+    LIFE_TRY(talloc((void **)&d_slot, (size_t)R * 4));
+    LIFE_CUDA(cudaMemcpyAsync(d_slot, slot_of_row.data(), (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    LIFE_TRY(dalloc(phi, &phi->b_rowvox, rowvox.size()));
+    LIFE_TRY(dalloc(phi, &phi->b_rowpart, rowpart.size()));
+    LIFE_CUDA(cudaMemcpyAsync(phi->b_rowvox, rowvox.data(), rowvox.size() * 4, cudaMemcpyHostToDevice, st));
+    LIFE_CUDA(cudaMemcpyAsync(phi->b_rowpart, rowpart.data(), rowpart.size() * 4, cudaMemcpyHostToDevice, st));
+    phi->b_nfix = (int)fixvox.size();
+    phi->b_nprow = nprow;
+    if (phi->b_nfix) {
+        LIFE_TRY(dalloc(phi, &phi->b_fixptr, fixptr.size()));
+        LIFE_TRY(dalloc(phi, &phi->b_fixvox, fixvox.size()));
+        LIFE_TRY(dalloc(phi, &phi->b_ypart, (size_t)nprow * N));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_fixptr, fixptr.data(), fixptr.size() * 4, cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_fixvox, fixvox.data(), fixvox.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+
+    // 4. virtual fascicle slots (at most kSlotCap coefficients each) and bins
+    unsigned *fcnt;
+    uint32_t *nslot, *vf_o;
+    LIFE_TRY(talloc((void **)&fcnt, (size_t)nf * 4));
+    LIFE_TRY(talloc((void **)&nslot, (size_t)nf * 4));
+    LIFE_TRY(talloc((void **)&vf_o, n * 4));
+    LIFE_TRY(dalloc(phi, &phi->b_f2vf, (size_t)nf + 1));
+    LIFE_CUDA(cudaMemsetAsync(fcnt, 0, (size_t)nf * 4, st));
+    k_hist<<<gridn(n), 256, 0, st>>>(f, n, fcnt);
+    LIFE_CHECK_LAUNCH();
+    k_slots_per_fiber<<<gridn(nf), 256, 0, st>>>(fcnt, nf, nslot);
+    LIFE_CHECK_LAUNCH();
+    LIFE_TRY(scan_excl(nslot, phi->b_f2vf, nf, st));
+    uint32_t nvf = 0;
+    LIFE_CUDA(cudaMemcpyAsync(&nvf, phi->b_f2vf + nf, 4, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    LIFE_TRY(dalloc(phi, &phi->b_vf2f, (size_t)nvf));
+    k_vf2f<<<gridn(nf), 256, 0, st>>>(phi->b_f2vf, nf, phi->b_vf2f);
+    LIFE_CHECK_LAUNCH();
+    if (nvf == (uint32_t)nf) {
+        k_vf_identity<<<gridn(n), 256, 0, st>>>(f, phi->b_f2vf, n, vf_o);
+        LIFE_CHECK_LAUNCH();
+    } else {
+        // occurrence index within each fascicle (stable order)
+        uint32_t *sf;
+        LIFE_TRY(talloc((void **)&sf, n * 4));
+        LIFE_TRY(sort_pairs<uint32_t>(f, sf, iota, perm, n, bits64((unsigned long long)nf), st));
+        k_heads32<<<gridn(n), 256, 0, st>>>(sf, n, head);
+        LIFE_CHECK_LAUNCH();
+        LIFE_TRY(scan_max(head, rstart, n, st));
+        k_vf_split<<<gridn(n), 256, 0, st>>>(perm, sf, rstart, phi->b_f2vf, n, vf_o);
+        LIFE_CHECK_LAUNCH();
+    }
+    const int nbins = (int)((nvf + kSB - 1) / kSB);
+
+    // 5. bin-major order (bin, tile, chunk), stable; its runs are the
+    // segments, each padded to 4 entries in both orders
+    unsigned long long *kbm = kva, *skbm = skva;
+    uint32_t *perm_bm = perm;
+    k_key_bm<<<gridn(n), 256, 0, st>>>(a, row_o, vf_o, d_slot, rank_o, n, ka_shift, (uint32_t)nch, (uint32_t)ntiles,
+                                       kbm);
+    LIFE_CHECK_LAUNCH();
+    const int64_t nsteps = ntiles * nch;
+    const unsigned long long per_bin = (unsigned long long)ntiles * nch;
+    LIFE_TRY(sort_pairs<unsigned long long>(kbm, skbm, iota, perm_bm, n, bits64(per_bin * nbins), st));
+    uint8_t *seghead;
+    uint32_t *head32 = head, *segid = rstart, *first;
+    int64_t *nsel;
+    LIFE_TRY(talloc((void **)&seghead, n));
+    LIFE_TRY(talloc((void **)&nsel, 8));
+    LIFE_TRY(talloc((void **)&first, n * 4));
+    k_head_flags<<<gridn(n), 256, 0, st>>>(skbm, n, seghead, head32);
+    LIFE_CHECK_LAUNCH();
+    {
+        cub::CountingInputIterator<uint32_t> pos(0);
+        size_t t1 = 0, t2 = 0;
+        LIFE_CUDA(cub::DeviceSelect::Flagged(nullptr, t1, pos, seghead, first, nsel, n, st));
+        LIFE_CUDA(cub::DeviceScan::InclusiveSum(nullptr, t2, head32, segid, n, st));
+        void *temp = nullptr;
+        LIFE_CUDA(cudaMallocAsync(&temp, std::max(t1, t2), st));
+        LIFE_CUDA(cub::DeviceSelect::Flagged(temp, t1, pos, seghead, first, nsel, n, st));
+        LIFE_CUDA(cub::DeviceScan::InclusiveSum(temp, t2, head32, segid, n, st));
+        LIFE_CUDA(cudaFreeAsync(temp, st));
+        g_launches.fetch_add(4, std::memory_order_relaxed);
+    }
+    int64_t nseg = 0;
+    LIFE_CUDA(cudaMemcpyAsync(&nseg, nsel, 8, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    uint32_t *len4, *sstep, *seg_iota, *perm_seg, *tm_excl;
+    unsigned long long *segkey, *tmkey, *stmkey;
+    unsigned *units, *spad;
+    LIFE_TRY(talloc((void **)&len4, (nseg + 1) * 4));
+    LIFE_TRY(talloc((void **)&sstep, nseg * 4));
+    LIFE_TRY(talloc((void **)&seg_iota, nseg * 4));
+    LIFE_TRY(talloc((void **)&perm_seg, nseg * 4));
+    LIFE_TRY(talloc((void **)&tm_excl, (nseg + 1) * 4));
+    LIFE_TRY(talloc((void **)&segkey, nseg * 8));
+    LIFE_TRY(talloc((void **)&tmkey, nseg * 8));
+    LIFE_TRY(talloc((void **)&stmkey, nseg * 8));
+    LIFE_TRY(talloc((void **)&units, nsteps * 4));
+    LIFE_TRY(talloc((void **)&spad, nsteps * 4));
+    k_seg_info<<<gridn(nseg), 256, 0, st>>>(skbm, first, nseg, n, per_bin, (uint32_t)nbins, len4, segkey, tmkey, sstep);
+    LIFE_CHECK_LAUNCH();
+    // bin-major unit starts
+    LIFE_TRY(dalloc(phi, &phi->b_segsrc, (size_t)nseg + 1));
+    LIFE_TRY(scan_excl(len4, phi->b_segsrc, nseg, st));
+    // tile-major: steps padded to 8 entries, segments in bin order inside
+    LIFE_CUDA(cudaMemsetAsync(units, 0, nsteps * 4, st));
+    k_step_units<<<gridn(nseg), 256, 0, st>>>(sstep, len4, nseg, units);
+    LIFE_CHECK_LAUNCH();
+    k_step_pad<<<gridn(nsteps), 256, 0, st>>>(units, nsteps, spad);
+    LIFE_CHECK_LAUNCH();
+    LIFE_TRY(dalloc(phi, &phi->b_step, (size_t)nsteps + 1));
+    LIFE_TRY(scan_excl(spad, phi->b_step, nsteps, st));
+    k_iota<<<gridn(nseg), 256, 0, st>>>(seg_iota, nseg);
+    LIFE_CHECK_LAUNCH();
+    LIFE_TRY(sort_pairs<unsigned long long>(tmkey, stmkey, seg_iota, perm_seg, nseg, bits64(per_bin * nbins), st));
+    {   // tile-major exclusive scan of the segment lengths (in units)
+        uint32_t *len_tm = seg_iota;  // reuse
+        k_gather_u32<<<gridn(nseg), 256, 0, st>>>(perm_seg, len4, nseg, len_tm);
+        LIFE_CHECK_LAUNCH();
+        LIFE_TRY(scan_excl(len_tm, tm_excl, nseg, st));
+    }
+    LIFE_TRY(dalloc(phi, &phi->b_segdst, (size_t)nseg + 1));
+    uint32_t *stepx = (uint32_t *)spad;  // reuse: padded sizes are scanned already
+    k_step_first<<<gridn(nseg), 256, 0, st>>>(perm_seg, tm_excl, sstep, nseg, stepx);
+    LIFE_CHECK_LAUNCH();
+    k_seg_tm<<<gridn(nseg), 256, 0, st>>>(perm_seg, tm_excl, sstep, nseg, phi->b_step, stepx, phi->b_segdst);
+    LIFE_CHECK_LAUNCH();
+    uint32_t npad = 0, nbm4 = 0;
+    LIFE_CUDA(cudaMemcpyAsync(&npad, phi->b_step + nsteps, 4, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaMemcpyAsync(&nbm4, phi->b_segsrc + nseg, 4, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+
+    // 6. placement (pads: cellr kPad, vid kPad, value 0)
+    const int64_t nbm = (int64_t)nbm4 * 4;
+    LIFE_TRY(dalloc(phi, &phi->b_cellr, (size_t)npad + 8));
+    LIFE_TRY(dalloc(phi, &phi->b_scr, (size_t)npad + 8));
+    LIFE_TRY(dalloc(phi, &phi->b_vid, (size_t)nbm + 8));
+    LIFE_TRY(dalloc(phi, &phi->b_val, (size_t)nbm + 8));
+    k_fill_u16<<<gridn(npad + 8), 256, 0, st>>>(phi->b_cellr, (int64_t)npad + 8, kPad);
+    LIFE_CHECK_LAUNCH();
+    k_fill_u16<<<gridn(nbm + 8), 256, 0, st>>>(phi->b_vid, nbm + 8, kPad);
+    LIFE_CHECK_LAUNCH();
+    LIFE_CUDA(cudaMemsetAsync(phi->b_val, 0, ((size_t)nbm + 8) * 4, st));
+    LIFE_CUDA(cudaMemsetAsync(phi->b_scr, 0, ((size_t)npad + 8) * 4, st));
+    k_place<<<gridn(n), 256, 0, st>>>(perm_bm, segid, first, phi->b_segsrc, phi->b_segdst, n, vf_o, val, a, rank_o,
+                                      row_o, d_slot, ka, cellbits, phi->b_vid, phi->b_val, phi->b_cellr);
+    LIFE_CHECK_LAUNCH();
+
+    // 7. bin and CTA segment ranges of the bin side
+    LIFE_TRY(dalloc(phi, &phi->b_binptr, (size_t)nbins + 1));
+    k_bin_seg<<<gridn(nbins + 1), 256, 0, st>>>(segkey, nseg, nbins, per_bin, phi->b_binptr);
+    LIFE_CHECK_LAUNCH();
+    const int side_grid = phi->sms;
+    LIFE_TRY(dalloc(phi, &phi->b_ctaseg, (size_t)side_grid + 1));
+    k_cta_seg<<<gridn(side_grid + 1), 256, 0, st>>>(phi->b_segsrc, nseg, side_grid, phi->b_ctaseg);
+    LIFE_CHECK_LAUNCH();
+
+    // 8. dictionary chunks as the two B operands (tf32 hi | lo, swizzled)
+    {
+        const size_t per = (size_t)2 * N * ka;
+        std::vector<float> hd((size_t)nch * per, 0.f), hw((size_t)nch * per, 0.f);
+        for (int c = 0; c < nch; ++c)
+            for (int k = 0; k < ka; ++k) {
+                const int at = c * ka + k;
+                for (int t = 0; t < N; ++t) {
+                    const float x = (at < phi->na && t < phi->nt) ? (float)hdict[(size_t)at * phi->nt + t] : 0.f;
+                    float hi, lo;
+                    tf32_split_h(x, hi, lo);
+                    // DSC: rows = directions, K = atoms (blocks of 32 atoms)
+                    const size_t od = (size_t)c * per + (size_t)(k / 32) * N * 32 + sw_cell(t, k % 32);
+                    hd[od] = hi;
+                    hd[od + (size_t)N * ka] = lo;
+                    // WC: rows = atoms, K = directions (blocks of 32 directions)
+                    const size_t ow = (size_t)c * per + (size_t)(t / 32) * ka * 32 + sw_cell(k, t % 32);
+                    hw[ow] = hi;
+                    hw[ow + (size_t)N * ka] = lo;
+                }
+            }
+        LIFE_TRY(dalloc(phi, &phi->b_Ddsc, hd.size()));
+        LIFE_TRY(dalloc(phi, &phi->b_Dwc, hw.size()));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_Ddsc, hd.data(), hd.size() * 4, cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_Dwc, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+    }
+
+    LIFE_TRY(dalloc(phi, &phi->b_wfix, (size_t)nvf));
+    LIFE_TRY(dalloc(phi, &phi->b_nanf, (size_t)nvf));
+    LIFE_CUDA(cudaMemsetAsync(phi->b_wfix, 0, (size_t)nvf * 8, st));
+    LIFE_CUDA(cudaMemsetAsync(phi->b_nanf, 0, (size_t)nvf, st));
+    phi->b_ka = ka;
+    phi->b_n = N;
+    phi->b_nch = nch;
+    phi->b_ntiles = (int)ntiles;
+    phi->b_nbins = nbins;
+    phi->b_sb = kSB;
+    phi->b_cellbits = cellbits;
+    phi->b_nvf = nvf;
+    phi->b_nsteps = nsteps;
+    phi->b_nseg = nseg;
+    phi->b_npad = npad;
+    phi->b_tile_grid = (int)std::min<int64_t>(phi->sms, ntiles);
+    phi->b_side_grid = side_grid;
+    LIFE_TRY(dalloc(phi, &phi->b_skip, (size_t)phi->b_side_grid));
+    LIFE_TRY(dalloc(phi, &phi->b_smax, (size_t)phi->b_side_grid));
+    LIFE_CUDA(cudaMemsetAsync(phi->b_skip, 0, (size_t)phi->b_side_grid * 8, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    LIFE_TRY(prepare_bin(phi));
+    phi->has_bin = true;
+    if (getenv("LIFE_DEBUG"))
+        fprintf(stderr, "[life] bin layout: N=%d KA=%d rows=%u tiles=%lld nch=%d nbins=%d nvf=%u steps=%lld "
+                        "segs=%lld padded=%u/%lld split voxels=%d\n",
+                N, ka, R, (long long)ntiles, nch, nbins, nvf, (long long)nsteps, (long long)nseg, npad,
+                (long long)nbm, phi->b_nfix);
+    return LIFE_OK;
+}
+
+
+// ===========================================================================
+// bin side (streaming; per-coefficient random access in shared memory)
+// ===========================================================================
+namespace bin {
+
+struct SideArgs {
+    const uint16_t *vid;     // bin-major virtual slot within the bin (kPad = pad)
+    const float *val;        // bin-major values (0 at pads)
+    const uint32_t *src4;    // [nseg + 1] bin-major segment starts, 4-entry units
+    const uint32_t *dst4;    // [nseg] tile-major segment starts, 4-entry units
+    const uint32_t *binseg;  // [nbins + 1] first segment of each bin
+    const uint32_t *ctaseg;  // [grid + 1] first segment of each CTA
+    const uint32_t *vf2f;    // [nvf]
+    int64_t nvf;
+    int nbins;
+};
+
+constexpr int kSideUN = 4;   // 4-entry units per lane in flight
+
+// Segment groups: a warp takes 32 consecutive segments of a bin piece (lane =
+// segment record), an inclusive scan of their unit counts, and walks the
+// group's units 32 * kSideUN at a time; each lane finds its unit's segment
+// with a 5-step shuffle search, so no dependent global loads are on the path.
+struct Group {
+    uint32_t src, dst, P;  // this lane's segment: starts (units), inclusive prefix of unit counts
+    uint32_t tot;          // units in the group
+};
+__device__ __forceinline__ Group load_group(const SideArgs &A, uint32_t gs, uint32_t pe, int lane)
+{
+    const uint32_t si = gs + (uint32_t)lane;
+    Group g;
+    g.src = si < pe ? __ldg(A.src4 + si) : 0u;
+    const uint32_t n4 = si < pe ? __ldg(A.src4 + si + 1) - g.src : 0u;
+    g.dst = si < pe ? __ldg(A.dst4 + si) : 0u;
+    uint32_t P = n4;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, P, o);
+        if (lane >= o) P += x;
+    }
+    g.P = P;
+    g.tot = __shfl_sync(0xffffffffu, P, 31);
+    return g;
+}
+// bin-major and tile-major unit of the group's unit u (all lanes call)
+__device__ __forceinline__ void unit_of(const Group &g, uint32_t u, uint32_t &su, uint32_t &du)
+{
+    int sl = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t pv = __shfl_sync(0xffffffffu, g.P, sl + step - 1);
+        if (pv <= u) sl += step;
+    }
+    sl = min(sl, 31);
+    const uint32_t ex = __shfl_sync(0xffffffffu, g.P, max(sl - 1, 0));
+    const uint32_t off = u - (sl ? ex : 0u);
+    su = __shfl_sync(0xffffffffu, g.src, sl) + off;
+    du = __shfl_sync(0xffffffffu, g.dst, sl) + off;
+}
+__device__ __forceinline__ int find_bin(const uint32_t *binseg, int nbins, uint32_t s)
+{
+    int lo = 0, hi = nbins;  // largest b with binseg[b] <= s
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(binseg + mid) <= s) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// DSC bin side: scr[tile-major] = s = w[f] * value, exact skip count (fp32
+// s == 0, _kernels.py:24-28)
+__global__ void __launch_bounds__(kSideWarps * 32, 1)
+    k_side_dsc(const SideArgs A, const float *__restrict__ w, float *__restrict__ scr, int count_skips,
+               unsigned long long *__restrict__ skip_part, float *__restrict__ smax_part, const CallHooks hooks)
+{
+    extern __shared__ float ws[];  // kSB
+    __shared__ uint32_t s_ctr;
+    if (hooks.done && *hooks.done) return;
+    if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t S0 = __ldg(A.ctaseg + blockIdx.x), S1 = __ldg(A.ctaseg + blockIdx.x + 1);
+    unsigned long long zeros = 0;
+    float smax = 0.f;
+    int b = S0 < S1 ? find_bin(A.binseg, A.nbins, S0) : A.nbins;
+    for (uint32_t s = S0; s < S1; ++b) {
+        const uint32_t pe = min(S1, __ldg(A.binseg + b + 1));
+        if (pe <= s) continue;
+        const int64_t s0 = (int64_t)b * kSB;
+        const int ns = (int)min((int64_t)kSB, A.nvf - s0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < ns; i += blockDim.x) ws[i] = __ldg(w + __ldg(A.vf2f + s0 + i));
+        if (threadIdx.x == 0) s_ctr = 0;
+        __syncthreads();
+        for (;;) {
+            uint32_t gi = 0;
+            if (lane == 0) gi = atomicAdd(&s_ctr, 1u);
+            const uint32_t gs = s + 32u * __shfl_sync(0xffffffffu, gi, 0);
+            if (gs >= pe) break;
+            const Group g = load_group(A, gs, pe, lane);
+            for (uint32_t u0 = 0; u0 < g.tot; u0 += 32u * kSideUN) {
+                uint32_t su[kSideUN], du[kSideUN];
+                uint2 id[kSideUN];
+                float4 vv[kSideUN];
+#pragma unroll
+                for (int k = 0; k < kSideUN; ++k) {
+                    const uint32_t u = u0 + 32u * k + (uint32_t)lane;
+                    unit_of(g, min(u, g.tot - 1), su[k], du[k]);
+                    if (u < g.tot) {
+                        id[k] = __ldcs(reinterpret_cast<const uint2 *>(A.vid) + su[k]);
+                        vv[k] = __ldcs(reinterpret_cast<const float4 *>(A.val) + su[k]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kSideUN; ++k) {
+                    if (u0 + 32u * k + (uint32_t)lane >= g.tot) continue;
+                    const uint32_t ids[4] = {id[k].x & 0xFFFFu, id[k].x >> 16, id[k].y & 0xFFFFu, id[k].y >> 16};
+                    const float vs[4] = {vv[k].x, vv[k].y, vv[k].z, vv[k].w};
+                    float o[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const bool pad = ids[e] == kPad;
+                        o[e] = pad ? 0.f : __fmul_rn(ws[pad ? 0 : ids[e]], vs[e]);
+                        zeros += (!pad && o[e] == 0.f) ? 1ull : 0ull;
+                        if (isfinite(o[e])) smax = fmaxf(smax, fabsf(o[e]));
+                    }
+                    reinterpret_cast<float4 *>(scr)[du[k]] = make_float4(o[0], o[1], o[2], o[3]);
+                }
+            }
+        }
+        s = pe;
+    }
+    // per-CTA skip count (fixed-order total in the tile kernel's last CTA)
+    __shared__ unsigned long long sz[kSideWarps];
+    __shared__ float sm[kSideWarps];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        zeros += __shfl_xor_sync(0xffffffffu, zeros, o);
+        smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    }
+    if (lane == 0) {
+        sz[warp] = zeros;
+        sm[warp] = smax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        float m = 0.f;
+        for (int i = 0; i < kSideWarps; ++i) {
+            t += sz[i];
+            m = fmaxf(m, sm[i]);
+        }
+        skip_part[blockIdx.x] = count_skips ? t : 0ull;
+        smax_part[blockIdx.x] = m;
+    }
+}
+
+// WC bin side: fascicle sums of value * z in 64-bit fixed point, two 32-bit
+// limbs per virtual slot in shared memory (native u32 atomics: order
+// independent, exact), flushed per bin piece into wfix (int64 atomics, also
+// exact).
+__global__ void __launch_bounds__(kSideWarps * 32, 1)
+    k_side_wc(const SideArgs A, const float *__restrict__ scr, const FixParams fx, int nt,
+              unsigned long long *__restrict__ wfix, unsigned char *__restrict__ nanf, const CallHooks hooks)
+{
+    extern __shared__ uint32_t limbs[];  // lo[kSB], hi[kSB]
+    __shared__ uint32_t s_ctr;
+    if (hooks.done && *hooks.done) return;
+    uint32_t *lo = limbs, *hi = limbs + kSB;
+    const int lane = threadIdx.x & 31;
+    const double scale = ldexp(1.0, bin_exponent_dev(fx, nt));
+    const uint32_t S0 = __ldg(A.ctaseg + blockIdx.x), S1 = __ldg(A.ctaseg + blockIdx.x + 1);
+    int b = S0 < S1 ? find_bin(A.binseg, A.nbins, S0) : A.nbins;
+    for (uint32_t s = S0; s < S1; ++b) {
+        const uint32_t pe = min(S1, __ldg(A.binseg + b + 1));
+        if (pe <= s) continue;
+        const int64_t s0 = (int64_t)b * kSB;
+        const int ns = (int)min((int64_t)kSB, A.nvf - s0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+            lo[i] = 0u;
+            hi[i] = 0u;
+        }
+        if (threadIdx.x == 0) s_ctr = 0;
+        __syncthreads();
+        for (;;) {
+            uint32_t gi = 0;
+            if (lane == 0) gi = atomicAdd(&s_ctr, 1u);
+            const uint32_t gs = s + 32u * __shfl_sync(0xffffffffu, gi, 0);
+            if (gs >= pe) break;
+            const Group g = load_group(A, gs, pe, lane);
+            for (uint32_t u0 = 0; u0 < g.tot; u0 += 32u * kSideUN) {
+                uint32_t su[kSideUN], du[kSideUN];
+                uint2 id[kSideUN];
+                float4 vv[kSideUN], zz[kSideUN];
+#pragma unroll
+                for (int k = 0; k < kSideUN; ++k) {
+                    const uint32_t u = u0 + 32u * k + (uint32_t)lane;
+                    unit_of(g, min(u, g.tot - 1), su[k], du[k]);
+                    if (u < g.tot) {
+                        id[k] = __ldcs(reinterpret_cast<const uint2 *>(A.vid) + su[k]);
+                        vv[k] = __ldcs(reinterpret_cast<const float4 *>(A.val) + su[k]);
+                        zz[k] = __ldcs(reinterpret_cast<const float4 *>(scr) + du[k]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kSideUN; ++k) {
+                    if (u0 + 32u * k + (uint32_t)lane >= g.tot) continue;
+                    const uint32_t ids[4] = {id[k].x & 0xFFFFu, id[k].x >> 16, id[k].y & 0xFFFFu, id[k].y >> 16};
+                    const float vs[4] = {vv[k].x, vv[k].y, vv[k].z, vv[k].w};
+                    const float zs[4] = {zz[k].x, zz[k].y, zz[k].z, zz[k].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if (ids[e] == kPad) continue;
+                        const float t = __fmul_rn(zs[e], vs[e]);  // acc * value (_kernels.py:67)
+                        if (!isfinite(t)) {
+                            nanf[s0 + ids[e]] = 1;
+                            continue;
+                        }
+                        const long long q = __double2ll_rn((double)t * scale);
+                        atomicAdd(lo + ids[e], (uint32_t)q & 0xFFFFFFu);
+                        atomicAdd(hi + ids[e], (uint32_t)(int32_t)(q >> 24));
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+            const long long v = (long long)(int32_t)hi[i] * 16777216ll + (long long)lo[i];
+            if (v) atomicAdd(wfix + s0 + i, (unsigned long long)v);
+        }
+        s = pe;
+    }
+}
+
+// WC finish: mode 0 = single GPU (fold virtual slots, convert, flags, sum of
+// squares); mode 1 = fold into per-fascicle int64 sums (multi-GPU, before the
+// all-reduce); mode 2 = convert all-reduced sums.
+template <int BT>
+__global__ void __launch_bounds__(BT)
+    k_wc_fin(unsigned long long *__restrict__ wfix, unsigned char *__restrict__ nanf, const uint32_t *__restrict__ f2vf,
+             unsigned long long *__restrict__ wsum, int nf, float *__restrict__ w_out, const float *__restrict__ w_ref,
+             uint32_t flags, const FixParams fx, int nt, int mode, double *part, unsigned *counter, double *sumsq_out,
+             const CallHooks hooks)
+{
+    if (hooks.done && *hooks.done) return;
+    const double inv = ldexp(1.0, -bin_exponent_dev(fx, nt));
+    const bool accumulate = flags & LIFE_ACCUMULATE;
+    const bool project = (flags & LIFE_PROJECT_GRAD) && w_ref != nullptr;
+    double sq = 0.0;
+    for (int f = blockIdx.x * BT + threadIdx.x; f < nf; f += gridDim.x * BT) {
+        long long q = 0;
+        bool bad = false;
+        if (mode == 2) {
+            q = (long long)wsum[f];
+        } else {
+            for (uint32_t s = __ldg(f2vf + f); s < __ldg(f2vf + f + 1); ++s) {
+                q += (long long)wfix[s];
+                wfix[s] = 0ull;
+                if (nanf[s]) {
+                    bad = true;
+                    nanf[s] = 0;
+                }
+            }
+            if (mode == 1) {
+                wsum[f] = (unsigned long long)q;
+                continue;
+            }
+        }
+        float o = bad ? __int_as_float(0x7fc00000) : (float)((double)q * inv);
+        if (accumulate) o = w_out[f] + o;
+        if (project && w_ref[f] == 0.f && o > 0.f) o = 0.f;
+        w_out[f] = o;
+        sq += (double)o * (double)o;
+    }
+    if (mode == 1) return;
+    __shared__ double s[BT];
+    s[threadIdx.x] = sq;
+    __syncthreads();
+    for (int h = BT / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) s[threadIdx.x] += s[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+    if (last_cta(counter)) {
+        const double tot = block_reduce<double>(part, gridDim.x, 0.0, OpSum{}, BT);
+        if (threadIdx.x == 0) {
+            if (sumsq_out) *sumsq_out = tot;
+            *counter = 0;
+            if (hooks.t_accum && hooks.t_begin) *hooks.t_accum += globaltimer() - *hooks.t_begin;
+        }
+    }
+}
+
+// ===========================================================================
+// tile side (tcgen05)
+// ===========================================================================
+struct TileArgs {
+    const uint16_t *cellr;  // tile-major
+    const uint32_t *step;   // [nsteps + 1]
+    const float *D;         // dictionary chunks (product-specific B layout)
+    const int *rowvox;      // [ntiles * 128]
+    const int *rowpart;     // [ntiles * 128]
+    float *ypart;           // [nprow * N]
+    int ntiles, nch, nt, cap;
+};
+
+template <int N, int KA>
+struct DscCfg {
+    static constexpr int EQ = (N + 63) / 64;   // epilogue warps per TMEM lane quarter
+    static constexpr int kProdS = kBuild;      // step staging (bulk copies)
+    static constexpr int kProdD = kBuild + 1;  // dictionary chunks
+    static constexpr int kMma = kBuild + 2;
+    static constexpr int kEpi = kBuild + 3;
+    static constexpr int kWarps = kEpi + 4 * EQ;
+    static constexpr int kThreads = kWarps * 32;
+    static constexpr int DB = 2 * N * KA * 4;  // one chunk, hi | lo
+    static constexpr int CS = KA + 4;          // C tile row stride (floats): conflict-free row reads
+    static constexpr int CBytes = kTV * CS * 4;
+    static constexpr int FOLD = 128 / KA;      // steps per TMEM accumulation group (128 atoms)
+    static constexpr int NBLK = N / 16;
+    static constexpr int MB = (NBLK + EQ - 1) / EQ;
+    static constexpr int TACC = 4 * KA;        // TMEM: A stages at st * 2KA, accumulators at TACC + g * N
+    static constexpr int CB = KA == 64 ? 13 : 12;  // cell bits
+    static constexpr int KSH = KA == 64 ? 6 : 5;
+    static_assert(4 * KA + 2 * N <= 512, "TMEM budget");
+};
+
+template <int N, int KA>
+struct WcCfg {
+    static constexpr int kProdS = kBuild;
+    static constexpr int kProdD = kBuild + 1;
+    static constexpr int kMma = kBuild + 2;
+    static constexpr int kYZ = kBuild + 3;     // 8 warps: two per TMEM lane quarter
+    static constexpr int kWarps = kYZ + 8;
+    static constexpr int kThreads = kWarps * 32;
+    static constexpr int DB = 2 * N * KA * 4;
+    static constexpr int ZS = KA + 4;
+    static constexpr int ZBytes = kTV * ZS * 4;
+    static constexpr int TZ = 2 * N;           // TMEM: Y hi at 0, lo at N, Z buffers at TZ + zb * KA
+    static constexpr int CB = KA == 64 ? 13 : 12;
+    static constexpr int KSH = KA == 64 ? 6 : 5;
+    static_assert(2 * N + 2 * KA <= 512, "TMEM budget");
+};
+
+__device__ __forceinline__ unsigned char *align1024(unsigned char *p)
+{
+    return (unsigned char *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+}
+
+// DSC tile side.  Roles (warps):
+//   0-7   builders: per step, C[row, atom] = sum of s over the step's entries
+//         in shared memory (rank 0: plain stores; ranks 1..: one pass per
+//         rank, so repeats of a cell are added in a fixed order), then split
+//         into tf32 hi/lo and stored to a TMEM A stage (warp w: lanes
+//         32*(w%4).., atoms (w/4)*KA/2..), zeroing the C tile behind them
+//   8     step staging: bulk copies of the step's (cellr, s) into a slot
+//   9     dictionary chunks (pre-split, pre-swizzled B operand) into 2 stages
+//   10    MMA issuer: 3xTF32 Y += A_hi.D_hi + A_lo.D_hi + A_hi.D_lo, A from TMEM
+//   11..  epilogue: fold each group of FOLD steps (128 atoms) from TMEM into
+//         fp32 registers (the tensor core's accumulation truncates), write y
+//         (accumulate / subtract b), sum of squares and max |r|
+template <int N, int KA>
+__global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
+    k_tile_dsc(const TileArgs A, const float *__restrict__ scr, float *__restrict__ y, const float *__restrict__ b,
+               const uint32_t flags, const ReduceSlots red, const DscOut out, const CallHooks hooks,
+               const unsigned long long *__restrict__ skip_part, int nskip, const float *__restrict__ smax, int nsmax,
+               int finalize)
+{
+    using C = DscCfg<N, KA>;
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    __shared__ __align__(8) uint64_t slot_full[kSlots], slot_empty[kSlots], d_full[2], d_empty[2], a_full[2],
+        a_empty[2], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(16) uint32_t s_hdr[kSlots][2];  // per staged step: start, count
+    __shared__ uint32_t s_rowbad[2][4];                    // rows with a non-finite s (per step parity)
+    __shared__ float s_scale[2];
+    if (hooks.done && *hooks.done) return;
+    unsigned char *sm = align1024(smraw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int my_tiles = (int)blockIdx.x < A.ntiles ? (A.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int total = my_tiles * A.nch;
+    unsigned char *Dbuf = sm;
+    float *Ct = reinterpret_cast<float *>(sm + 2 * C::DB);
+    unsigned char *slots = sm + 2 * C::DB + C::CBytes;
+    const uint32_t cap = (uint32_t)A.cap;  // staged entries per slot
+    const uint32_t slot_bytes = cap * 6u;
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < kSlots; ++j) {
+            bar_init(&slot_full[j], 1);
+            bar_init(&slot_empty[j], kBuild);
+        }
+        for (int s = 0; s < 2; ++s) {
+            bar_init(&d_full[s], 1);
+            bar_init(&d_empty[s], 1);
+            bar_init(&a_full[s], kBuild);
+            bar_init(&a_empty[s], 1);
+            bar_init(&acc_full[s], 1);
+            bar_init(&acc_empty[s], 4 * C::EQ);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == C::kMma) tcg::alloc(&tmem_base, 512);
+    tcg::fence_before();
+    __syncthreads();
+    tcg::fence_after();
+    const uint32_t tmem = tmem_base;
+    double sq = 0.0;
+    float amax = 0.f;
+    auto step_of = [&](int k) -> size_t {
+        return (size_t)((int)blockIdx.x + (k / A.nch) * (int)gridDim.x) * A.nch + (k % A.nch);
+    };
+
+    if (warp < kBuild) {
+        // ===== builders =====
+        const int tid = threadIdx.x;
+        const uint32_t Cs = sa(Ct);
+        const int q = warp & 3, hh = warp >> 2;
+        const uint32_t rowaddr = Cs + 4u * (uint32_t)((q * 32 + lane) * C::CS + hh * (KA / 2));
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        // the C tile starts zeroed; each step's convert pass zeroes it behind
+        for (int i = tid; i < kTV * C::CS / 4; i += 256) sts_f4(Cs + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
+        if (tid < 8) s_rowbad[tid >> 2][tid & 3] = 0u;
+        // fixed-point scale of this call: |s| * scale < 2^27, so a cell's
+        // kRanks terms stay below 2^30
+        if (warp == 0) {
+            float m = 0.f;
+            for (int i = lane; i < nsmax; i += 32) m = fmaxf(m, __ldcg(smax + i));
+            m = __reduce_max_sync(0xffffffffu, __float_as_uint(m)) == 0u ? 0.f
+                : __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
+            if (lane == 0) {
+                int ex = 0;
+                if (m > 0.f) {
+                    frexpf(m, &ex);  // m < 2^ex
+                    ex = 27 - ex;
+                }
+                s_scale[0] = ldexpf(1.f, ex);
+                s_scale[1] = ldexpf(1.f, -ex);
+            }
+        }
+        named_bar(1, 256);
+        const float scale = s_scale[0], inv = s_scale[1];
+        for (int k = 0; k < total; ++k) {
+            const int j = k % kSlots;
+            bar_wait(&slot_full[j], (k / kSlots) & 1);
+            const uint32_t p0 = s_hdr[j][0], n = s_hdr[j][1];
+            const uint32_t nst4 = min(n, cap) / 4u;
+            const uint32_t sc = sa(slots + (size_t)j * slot_bytes), ss = sc + cap * 2;
+            if (tid == 0) {
+                s_rowbad[(k + 1) & 1][0] = s_rowbad[(k + 1) & 1][1] = 0u;
+                s_rowbad[(k + 1) & 1][2] = s_rowbad[(k + 1) & 1][3] = 0u;
+            }
+            // C[row, atom] = sum of s in 32-bit fixed point: integer adds are
+            // order independent, so repeats need no ordering (deterministic)
+            for (uint32_t u = tid; u < n / 4u; u += 256u) {
+                uint2 cr;
+                float4 sv;
+                if (u < nst4) {
+                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(cr.x), "=r"(cr.y) : "r"(sc + 8u * u));
+                    sv = lds_f4(ss + 16u * u);
+                } else {
+                    cr = __ldg(reinterpret_cast<const uint2 *>(A.cellr + p0) + u);
+                    sv = __ldcg(reinterpret_cast<const float4 *>(scr + p0) + u);
+                }
+                const uint32_t cs4[4] = {cr.x & 0xFFFFu, cr.x >> 16, cr.y & 0xFFFFu, cr.y >> 16};
+                const float vs4[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (cs4[e] == kPad) continue;
+                    const uint32_t cell = cs4[e] & ((1u << C::CB) - 1);
+                    if (!isfinite(vs4[e])) {
+                        atomicOr(&s_rowbad[k & 1][(cell >> C::KSH) >> 5], 1u << ((cell >> C::KSH) & 31));
+                        continue;
+                    }
+                    const int qv = __float2int_rn(vs4[e] * scale);
+                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(Cs + 4u * ((cell >> C::KSH) * C::CS + (cell & (KA - 1)))),
+                                 "r"((uint32_t)qv) : "memory");
+                }
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(&slot_empty[j]);
+            named_bar(1, 256);  // the C tile is complete
+            // convert this warp's rows/atoms into the TMEM A stage, zero behind
+            const int st = k & 1;
+            if (k >= 2) bar_wait(&a_empty[st], ((k >> 1) - 1) & 1);
+            tcg::fence_after();
+            const uint32_t ta = tmem + lane_base + (uint32_t)(st * 2 * KA + hh * (KA / 2));
+            const bool bad = (s_rowbad[k & 1][q] >> lane) & 1u;
+#pragma unroll
+            for (int h16 = 0; h16 < KA / 32; ++h16) {
+                uint32_t hv[16], lv2[16];
+#pragma unroll
+                for (int i4 = 0; i4 < 4; ++i4) {
+                    const uint32_t ad = rowaddr + 64u * h16 + 16u * i4;
+                    const float4 x = lds_f4(ad);
+                    sts_f4(ad, make_float4(0.f, 0.f, 0.f, 0.f));
+                    float xs[4] = {__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
+                                   __int_as_float(0x7fc00000)};
+                    if (!bad) {
+                        xs[0] = (float)__float_as_int(x.x) * inv;
+                        xs[1] = (float)__float_as_int(x.y) * inv;
+                        xs[2] = (float)__float_as_int(x.z) * inv;
+                        xs[3] = (float)__float_as_int(x.w) * inv;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t hb = tcg::hi_bits(__float_as_uint(xs[e]));
+                        hv[4 * i4 + e] = hb;
+                        lv2[4 * i4 + e] = __float_as_uint(xs[e] - __uint_as_float(hb));
+                    }
+                }
+                tm_st16(ta + 16u * h16, hv);
+                tm_st16(ta + (uint32_t)KA + 16u * h16, lv2);
+            }
+            tcg::wait_st();
+            tcg::fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&a_full[st]);
+            named_bar(1, 256);  // C tile zeroed before the next step's stores
+        }
+    } else if (warp == C::kProdS) {
+        // ===== step staging =====
+        if (lane == 0) {
+            const uint64_t pol = pol_first();
+            for (int k = 0; k < total; ++k) {
+                const size_t gs = step_of(k);
+                const uint32_t p0 = __ldg(A.step + gs), n = __ldg(A.step + gs + 1) - p0;
+                const int j = k % kSlots;
+                if (k >= kSlots) bar_wait(&slot_empty[j], ((k / kSlots) - 1) & 1);
+                const uint32_t nst = min(n, cap);
+                s_hdr[j][0] = p0;
+                s_hdr[j][1] = n;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bar_arrive_tx(&slot_full[j], nst * 6u);
+                unsigned char *dst = slots + (size_t)j * slot_bytes;
+                if (nst) {
+                    bulk_g2s(dst, A.cellr + p0, nst * 2u, &slot_full[j], pol);
+                    bulk_g2s(dst + cap * 2, scr + p0, nst * 4u, &slot_full[j], pol);
+                }
+                if (k + kSlots < total) {
+                    const size_t g2 = step_of(k + kSlots);
+                    const uint32_t q0 = __ldg(A.step + g2), n2 = min(__ldg(A.step + g2 + 1) - q0, cap);
+                    if (n2) {
+                        prefetch_l2(A.cellr + q0, n2 * 2u);
+                        prefetch_l2(scr + q0, n2 * 4u);
+                    }
+                }
+            }
+        }
+    } else if (warp == C::kProdD) {
+        // ===== dictionary chunks =====
+        if (lane == 0) {
+            const uint64_t pol = pol_last();
+            for (int k = 0; k < total; ++k) {
+                const int st = k & 1, c = k % A.nch;
+                if (k >= 2) bar_wait(&d_empty[st], ((k >> 1) - 1) & 1);
+                bar_arrive_tx(&d_full[st], (unsigned)C::DB);
+                bulk_g2s(Dbuf + (size_t)st * C::DB, A.D + (size_t)c * (C::DB / 4), (unsigned)C::DB, &d_full[st], pol);
+            }
+        }
+    } else if (warp == C::kMma) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            constexpr uint32_t id = tcg::idesc_tf32(kTV, N);
+            int k = 0, G = 0;
+            for (int i = 0; i < my_tiles; ++i) {
+                for (int c = 0; c < A.nch; ++c, ++k) {
+                    const int st = k & 1, buf = G & 1;
+                    const bool first = (c % C::FOLD) == 0;
+                    const bool last = (c % C::FOLD) == C::FOLD - 1 || c == A.nch - 1;
+                    if (first) {
+                        if (G >= 2) bar_wait(&acc_empty[buf], ((G >> 1) - 1) & 1);
+                        tcg::fence_after();
+                    }
+                    bar_wait(&a_full[st], (k >> 1) & 1);
+                    bar_wait(&d_full[st], (k >> 1) & 1);
+                    tcg::fence_after();
+                    const uint32_t db = sa(Dbuf + (size_t)st * C::DB);
+                    const uint64_t bh = tcg::sdesc(db), bl = tcg::sdesc(db + (uint32_t)(N * KA * 4));
+                    const uint32_t d = tmem + (uint32_t)(C::TACC + buf * N);
+                    const uint32_t ah = tmem + (uint32_t)(st * 2 * KA), al = ah + (uint32_t)KA;
+#pragma unroll
+                    for (int kk = 0; kk < KA / 8; ++kk) {
+                        const uint64_t o = (uint64_t)((((kk >> 2) * N * 128) + (kk & 3) * 32) >> 4);
+                        tcg::mma_ts(d, ah + 8u * kk, bh + o, id, (first && kk == 0) ? 0u : 1u);
+                        tcg::mma_ts(d, al + 8u * kk, bh + o, id, 1u);
+                        tcg::mma_ts(d, ah + 8u * kk, bl + o, id, 1u);
+                    }
+                    tcg::commit(&a_empty[st]);
+                    tcg::commit(&d_empty[st]);
+                    if (last) {
+                        tcg::commit(&acc_full[buf]);
+                        ++G;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===== epilogue: thread = tile row (TMEM lane), a slice of columns =====
+        const int ew = warp - C::kEpi, q = warp & 3, cs = ew >> 2;
+        const int row = q * 32 + lane;
+        const int b0 = cs * C::NBLK / C::EQ, b1 = (cs + 1) * C::NBLK / C::EQ;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const bool accumulate = flags & LIFE_ACCUMULATE;
+        const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
+        const int ngroups = (A.nch + C::FOLD - 1) / C::FOLD;
+        int G = 0;
+        for (int i = 0; i < my_tiles; ++i) {
+            const int t = (int)blockIdx.x + i * (int)gridDim.x;
+            float acc[C::MB * 16];
+#pragma unroll
+            for (int e = 0; e < C::MB * 16; ++e) acc[e] = 0.f;
+            for (int g = 0; g < ngroups; ++g, ++G) {
+                const int buf = G & 1;
+                bar_wait(&acc_full[buf], (G >> 1) & 1);
+                tcg::fence_after();
+#pragma unroll
+                for (int bb = 0; bb < C::MB; ++bb) {
+                    if (b0 + bb < b1) {
+                        uint32_t r[16];
+                        tm_ld16(tmem + lane_base + (uint32_t)(C::TACC + buf * N + 16 * (b0 + bb)), r);
+                        tm_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) acc[16 * bb + e] += __uint_as_float(r[e]);
+                    }
+                }
+                tcg::fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(&acc_empty[buf]);
+            }
+            const int rv = __ldg(A.rowvox + (size_t)t * kTV + row);
+            const int rp = __ldg(A.rowpart + (size_t)t * kTV + row);
+            if (rv < 0) continue;
+            if (rp >= 0) {
+                float *yp = A.ypart + (size_t)rp * N;
+#pragma unroll
+                for (int bb = 0; bb < C::MB; ++bb)
+                    if (b0 + bb < b1)
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) yp[16 * (b0 + bb) + e] = acc[16 * bb + e];
+                continue;
+            }
+            const size_t yo = (size_t)rv * A.nt;
+            if ((A.nt & 3) == 0) {
+#pragma unroll
+                for (int bb = 0; bb < C::MB; ++bb) {
+#pragma unroll
+                    for (int e4 = 0; e4 < 4; ++e4) {
+                        const int col = 16 * (b0 + bb) + 4 * e4;
+                        if (b0 + bb < b1 && col < A.nt) {
+                            float r[4] = {acc[16 * bb + 4 * e4], acc[16 * bb + 4 * e4 + 1], acc[16 * bb + 4 * e4 + 2],
+                                          acc[16 * bb + 4 * e4 + 3]};
+                            float4 *y4 = reinterpret_cast<float4 *>(y + yo + col);
+                            if (accumulate) {
+                                const float4 o = *y4;
+                                r[0] += o.x; r[1] += o.y; r[2] += o.z; r[3] += o.w;
+                            }
+                            if (subtract) {
+                                const float4 o = __ldg(reinterpret_cast<const float4 *>(b + yo + col));
+                                r[0] -= o.x; r[1] -= o.y; r[2] -= o.z; r[3] -= o.w;
+                            }
+                            *y4 = make_float4(r[0], r[1], r[2], r[3]);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                sq += (double)r[e] * (double)r[e];
+                                amax = fmaxf(amax, fabsf(r[e]));
+                            }
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int bb = 0; bb < C::MB; ++bb) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int col = 16 * (b0 + bb) + e;
+                        if (b0 + bb < b1 && col < A.nt) {
+                            float r = acc[16 * bb + e];
+                            if (accumulate) r += y[yo + col];
+                            if (subtract) r -= b[yo + col];
+                            y[yo + col] = r;
+                            sq += (double)r * (double)r;
+                            amax = fmaxf(amax, fabsf(r));
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    // ---- teardown, fixed-order completion --------------------------------------
+    tcg::fence_before();
+    __syncthreads();
+    if (warp == C::kMma) {
+        tcg::fence_after();
+        tcg::dealloc(tmem, 512);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    const int gw = (int)blockIdx.x * C::kWarps + warp;
+    if (lane == 0) {
+        red.part_d[gw] = sq;
+        red.part_f[gw] = amax;
+    }
+    if (finalize && last_cta(red.counter))
+        dsc_finish(red, (int)gridDim.x * C::kWarps, skip_part, nskip, out, red.counter, hooks, C::kThreads);
+}
+
+// voxels split over several tile rows: sum their partial rows in row order
+// and apply the epilogue; then the DSC outputs over all partials
+template <int N>
+__global__ void __launch_bounds__(256)
+    k_tile_dsc_fix(const uint32_t *__restrict__ fixptr, const int *__restrict__ fixvox, int nfix,
+                   const float *__restrict__ ypart, int nt, float *__restrict__ y, const float *__restrict__ b,
+                   uint32_t flags, const ReduceSlots red, int part0, const DscOut out, const CallHooks hooks,
+                   const unsigned long long *__restrict__ skip_part, int nskip)
+{
+    if (hooks.done && *hooks.done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool accumulate = flags & LIFE_ACCUMULATE;
+    const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
+    double sq = 0.0;
+    float amax = 0.f;
+    for (int m = blockIdx.x * 8 + warp; m < nfix; m += gridDim.x * 8) {
+        const int vx = fixvox[m];
+        const uint32_t r0 = fixptr[m], r1 = fixptr[m + 1];
+        for (int col = lane; col < nt; col += 32) {
+            float r = 0.f;
+            for (uint32_t p = r0; p < r1; ++p) r += ypart[(size_t)p * N + col];
+            const size_t o = (size_t)vx * nt + col;
+            if (accumulate) r += y[o];
+            if (subtract) r -= b[o];
+            y[o] = r;
+            sq += (double)r * (double)r;
+            amax = fmaxf(amax, fabsf(r));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    if (lane == 0) {
+        red.part_d[part0 + blockIdx.x * 8 + warp] = sq;
+        red.part_f[part0 + blockIdx.x * 8 + warp] = amax;
+    }
+    if (last_cta(red.counter)) dsc_finish(red, part0 + (int)gridDim.x * 8, skip_part, nskip, out, red.counter, hooks, 256);
+}
+
+// WC tile side.  Roles (warps):
+//   0-7   gatherers: per step, z = Z[row, atom] of every entry from the
+//         shared-memory Z tile into the tile-major scratch (coalesced)
+//   8     step staging (cellr), 9 dictionary chunks (WC B operand)
+//   10    MMA issuer: Z = Y_hi.D_hi + Y_lo.D_hi + Y_hi.D_lo (M = 128 rows,
+//         N = KA atoms, K = directions), Y from TMEM
+//   11-18 YZ: per tile, y rows (thread = row) split into tf32 hi/lo and stored
+//         to TMEM (next tile's rows prefetched into registers); per step,
+//         Z read back from TMEM into a double-buffered shared-memory tile
+template <int N, int KA>
+__global__ void __launch_bounds__(WcCfg<N, KA>::kThreads, 1)
+    k_tile_wc(const TileArgs A, const float *__restrict__ y, float *__restrict__ scr, const CallHooks hooks)
+{
+    using C = WcCfg<N, KA>;
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    __shared__ __align__(8) uint64_t slot_full[kSlots], slot_empty[kSlots], d_full[2], d_empty[2], acc_full[2],
+        acc_empty[2], z_full[2], z_empty[2], y_ready, y_free;
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(16) uint32_t s_hdr[kSlots][2];  // per staged step: start, count
+    if (hooks.done && *hooks.done) return;
+    if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
+    unsigned char *sm = align1024(smraw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int my_tiles = (int)blockIdx.x < A.ntiles ? (A.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int total = my_tiles * A.nch;
+    unsigned char *Dbuf = sm;
+    float *Zt = reinterpret_cast<float *>(sm + 2 * C::DB);
+    unsigned char *slots = sm + 2 * C::DB + 2 * C::ZBytes;
+    const uint32_t cap = (uint32_t)A.cap;
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < kSlots; ++j) {
+            bar_init(&slot_full[j], 1);
+            bar_init(&slot_empty[j], kBuild);
+        }
+        for (int s = 0; s < 2; ++s) {
+            bar_init(&d_full[s], 1);
+            bar_init(&d_empty[s], 1);
+            bar_init(&acc_full[s], 1);
+            bar_init(&acc_empty[s], 8);
+            bar_init(&z_full[s], 8);
+            bar_init(&z_empty[s], kBuild);
+        }
+        bar_init(&y_ready, 8);
+        bar_init(&y_free, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == C::kMma) tcg::alloc(&tmem_base, 512);
+    tcg::fence_before();
+    __syncthreads();
+    tcg::fence_after();
+    const uint32_t tmem = tmem_base;
+    auto step_of = [&](int k) -> size_t {
+        return (size_t)((int)blockIdx.x + (k / A.nch) * (int)gridDim.x) * A.nch + (k % A.nch);
+    };
+
+    if (warp < kBuild) {
+        // ===== gatherers =====
+        const int tid = threadIdx.x;
+        for (int k = 0; k < total; ++k) {
+            const int j = k % kSlots, zb = k & 1;
+            bar_wait(&slot_full[j], (k / kSlots) & 1);
+            bar_wait(&z_full[zb], (k >> 1) & 1);
+            const uint32_t p0 = s_hdr[j][0], n = s_hdr[j][1];
+            const uint32_t nst4 = min(n, cap) / 4u;
+            const uint32_t sc = sa(slots + (size_t)j * cap * 2);
+            const uint32_t Z = sa(Zt) + (uint32_t)(zb * C::ZBytes);
+            float4 *dst = reinterpret_cast<float4 *>(scr + p0);
+            for (uint32_t u = tid; u < n / 4u; u += 256u) {
+                uint2 cr;
+                if (u < nst4)
+                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(cr.x), "=r"(cr.y) : "r"(sc + 8u * u));
+                else
+                    cr = __ldg(reinterpret_cast<const uint2 *>(A.cellr + p0) + u);
+                const uint32_t cs4[4] = {cr.x & 0xFFFFu, cr.x >> 16, cr.y & 0xFFFFu, cr.y >> 16};
+                float z[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t cell = cs4[e] & ((1u << C::CB) - 1);
+                    z[e] = cs4[e] != kPad ? lds_f(Z + 4u * ((cell >> C::KSH) * C::ZS + (cell & (KA - 1)))) : 0.f;
+                }
+                dst[u] = make_float4(z[0], z[1], z[2], z[3]);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                bar_arrive(&slot_empty[j]);
+                bar_arrive(&z_empty[zb]);
+            }
+        }
+    } else if (warp == C::kProdS) {
+        if (lane == 0) {
+            const uint64_t pol = pol_first();
+            for (int k = 0; k < total; ++k) {
+                const size_t gs = step_of(k);
+                const uint32_t p0 = __ldg(A.step + gs), n = __ldg(A.step + gs + 1) - p0;
+                const int j = k % kSlots;
+                if (k >= kSlots) bar_wait(&slot_empty[j], ((k / kSlots) - 1) & 1);
+                const uint32_t nst = min(n, cap);
+                s_hdr[j][0] = p0;
+                s_hdr[j][1] = n;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bar_arrive_tx(&slot_full[j], nst * 2u);
+                if (nst) bulk_g2s(slots + (size_t)j * cap * 2, A.cellr + p0, nst * 2u, &slot_full[j], pol);
+                if (k + kSlots < total) {
+                    const size_t g2 = step_of(k + kSlots);
+                    const uint32_t q0 = __ldg(A.step + g2), n2 = min(__ldg(A.step + g2 + 1) - q0, cap);
+                    if (n2) prefetch_l2(A.cellr + q0, n2 * 2u);
+                }
+            }
+        }
+    } else if (warp == C::kProdD) {
+        if (lane == 0) {
+            const uint64_t pol = pol_last();
+            for (int k = 0; k < total; ++k) {
+                const int st = k & 1, c = k % A.nch;
+                if (k >= 2) bar_wait(&d_empty[st], ((k >> 1) - 1) & 1);
+                bar_arrive_tx(&d_full[st], (unsigned)C::DB);
+                bulk_g2s(Dbuf + (size_t)st * C::DB, A.D + (size_t)c * (C::DB / 4), (unsigned)C::DB, &d_full[st], pol);
+            }
+        }
+    } else if (warp == C::kMma) {
+        if (lane == 0) {
+            constexpr uint32_t id = tcg::idesc_tf32(kTV, KA);
+            int k = 0;
+            for (int i = 0; i < my_tiles; ++i) {
+                bar_wait(&y_ready, i & 1);
+                tcg::fence_after();
+                for (int c = 0; c < A.nch; ++c, ++k) {
+                    const int zb = k & 1;
+                    bar_wait(&d_full[zb], (k >> 1) & 1);
+                    if (k >= 2) bar_wait(&acc_empty[zb], ((k >> 1) - 1) & 1);
+                    tcg::fence_after();
+                    const uint32_t db = sa(Dbuf + (size_t)zb * C::DB);
+                    const uint64_t bh = tcg::sdesc(db), bl = tcg::sdesc(db + (uint32_t)(N * KA * 4));
+                    const uint32_t d = tmem + (uint32_t)(C::TZ + zb * KA);
+#pragma unroll 4
+                    for (int kk = 0; kk < N / 8; ++kk) {
+                        const uint64_t o = (uint64_t)((((kk >> 2) * KA * 128) + (kk & 3) * 32) >> 4);
+                        tcg::mma_ts(d, tmem + 8u * kk, bh + o, id, kk != 0 ? 1u : 0u);
+                        tcg::mma_ts(d, tmem + (uint32_t)N + 8u * kk, bh + o, id, 1u);
+                        tcg::mma_ts(d, tmem + 8u * kk, bl + o, id, 1u);
+                    }
+                    tcg::commit(&d_empty[zb]);
+                    tcg::commit(&acc_full[zb]);
+                    if (c == A.nch - 1) tcg::commit(&y_free);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===== YZ =====
+        const int ew = warp - C::kYZ, q = warp & 3, cs = ew >> 2;
+        const int row = q * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        constexpr int YH = N / 2;          // y columns per thread
+        constexpr int ZH = KA / 2;         // Z columns per thread
+        const bool vec = (A.nt & 3) == 0;
+        // y rows: prefetched one tile ahead into registers when they fit
+        // (N <= 96), else loaded at the tile start in 16-column blocks
+        constexpr bool kPre = YH <= 48;
+        constexpr int YR = kPre ? YH : 16;
+        float yr[YR];
+        auto load_y = [&](int t, int c0, int ncol) {
+            const int rv = __ldg(A.rowvox + (size_t)t * kTV + row);
+            const float *src = y + (size_t)(rv < 0 ? 0 : rv) * A.nt;
+#pragma unroll
+            for (int i4 = 0; i4 < YR / 4; ++i4) {
+                if (4 * i4 >= ncol) break;
+                const int col = c0 + 4 * i4;
+                if (rv >= 0 && vec && col < A.nt) {
+                    const float4 v = __ldg(reinterpret_cast<const float4 *>(src + col));
+                    yr[4 * i4] = v.x; yr[4 * i4 + 1] = v.y; yr[4 * i4 + 2] = v.z; yr[4 * i4 + 3] = v.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        yr[4 * i4 + e] = (rv >= 0 && col + e < A.nt) ? __ldg(src + col + e) : 0.f;
+                }
+            }
+        };
+        auto store_y = [&](int h16, int roff) {  // 16 columns from yr[roff..]
+            uint32_t hv[16], lv[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const float x = yr[roff + e];
+                const uint32_t hb = tcg::hi_bits(__float_as_uint(x));
+                hv[e] = hb;
+                lv[e] = __float_as_uint(x - __uint_as_float(hb));
+            }
+            tm_st16(tmem + lane_base + (uint32_t)(cs * YH + 16 * h16), hv);
+            tm_st16(tmem + lane_base + (uint32_t)(N + cs * YH + 16 * h16), lv);
+        };
+        if (kPre && my_tiles > 0) load_y((int)blockIdx.x, cs * YH, YH);
+        int k = 0;
+        for (int i = 0; i < my_tiles; ++i) {
+            const int t = (int)blockIdx.x + i * (int)gridDim.x;
+            if (i >= 1) bar_wait(&y_free, (i - 1) & 1);
+            tcg::fence_after();
+            if (kPre) {
+#pragma unroll
+                for (int h16 = 0; h16 < YH / 16; ++h16) store_y(h16, 16 * h16);
+            } else {
+#pragma unroll 1
+                for (int h16 = 0; h16 < YH / 16; ++h16) {
+                    load_y(t, cs * YH + 16 * h16, 16);
+                    store_y(h16, 0);
+                }
+            }
+            tcg::wait_st();
+            tcg::fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&y_ready);
+            if (kPre && i + 1 < my_tiles) load_y(t + (int)gridDim.x, cs * YH, YH);  // in flight meanwhile
+            for (int c = 0; c < A.nch; ++c, ++k) {
+                const int zb = k & 1;
+                bar_wait(&acc_full[zb], (k >> 1) & 1);
+                tcg::fence_after();
+                uint32_t zr[ZH];
+#pragma unroll
+                for (int h16 = 0; h16 < ZH / 16; ++h16) {
+                    uint32_t r[16];
+                    tm_ld16(tmem + lane_base + (uint32_t)(C::TZ + zb * KA + cs * ZH + 16 * h16), r);
+                    tm_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) zr[16 * h16 + e] = r[e];
+                }
+                tcg::fence_before();
+                if (k >= 2) bar_wait(&z_empty[zb], ((k >> 1) - 1) & 1);
+                const uint32_t za = sa(Zt) + (uint32_t)(zb * C::ZBytes) + 4u * (uint32_t)(row * C::ZS + cs * ZH);
+#pragma unroll
+                for (int i4 = 0; i4 < ZH / 4; ++i4)
+                    sts_f4(za + 16u * i4, make_float4(__uint_as_float(zr[4 * i4]), __uint_as_float(zr[4 * i4 + 1]),
+                                                      __uint_as_float(zr[4 * i4 + 2]), __uint_as_float(zr[4 * i4 + 3])));
+                __syncwarp();
+                if (lane == 0) {
+                    bar_arrive(&acc_empty[zb]);
+                    bar_arrive(&z_full[zb]);
+                }
+            }
+        }
+    }
+    tcg::fence_before();
+    __syncthreads();
+    if (warp == C::kMma) {
+        tcg::fence_after();
+        tcg::dealloc(tmem, 512);
+    }
+}
+
+}  // namespace bin
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+namespace {
+using namespace bin;
+
+constexpr int kSmemMax = 232448 - 2048;  // opt-in dynamic limit minus static + alignment slack
+
+template <int N, int KA>
+int dsc_slot_cap()
+{
+    using C = DscCfg<N, KA>;
+    const long avail = (long)kSmemMax - 2L * C::DB - C::CBytes;
+    return (int)std::min(16384L, std::max(0L, avail / (kSlots * 6L) / 32 * 32));
+}
+template <int N, int KA>
+int wc_slot_cap()
+{
+    using C = WcCfg<N, KA>;
+    const long avail = (long)kSmemMax - 2L * C::DB - 2L * C::ZBytes;
+    return (int)std::min(32768L, std::max(0L, avail / (kSlots * 2L) / 8 * 8));
+}
+
+SideArgs side_args(const life_phi *phi)
+{
+    return SideArgs{phi->b_vid, phi->b_val, phi->b_segsrc, phi->b_segdst, phi->b_binptr, phi->b_ctaseg,
+                    phi->b_vf2f, phi->b_nvf, phi->b_nbins};
+}
+
+template <int N, int KA>
+int prep_t(life_phi *phi)
+{
+    using CD = DscCfg<N, KA>;
+    using CW = WcCfg<N, KA>;
+    phi->b_slot_dsc = dsc_slot_cap<N, KA>();
+    phi->b_slot_wc = wc_slot_cap<N, KA>();
+    if (phi->b_slot_dsc < 1024 || phi->b_slot_wc < 1024)
+        return fail(LIFE_ERR_CONFIG_INVALID, "bin layout: staging slots do not fit");
+    phi->b_dsc_smem = 1024 + 2 * (size_t)CD::DB + CD::CBytes + (size_t)kSlots * 6 * phi->b_slot_dsc;
+    phi->b_wc_smem = 1024 + 2 * (size_t)CW::DB + 2 * (size_t)CW::ZBytes + (size_t)kSlots * 2 * phi->b_slot_wc;
+    phi->b_side_smem = (size_t)kSB * 4;
+    phi->b_wcs_smem = (size_t)kSB * 8;
+    LIFE_TRY(ensure_smem(k_tile_dsc<N, KA>, phi->b_dsc_smem));
+    LIFE_TRY(ensure_smem(k_tile_wc<N, KA>, phi->b_wc_smem));
+    LIFE_TRY(ensure_smem(k_side_dsc, phi->b_side_smem));
+    LIFE_TRY(ensure_smem(k_side_wc, phi->b_wcs_smem));
+    return LIFE_OK;
+}
+
+template <int N, int KA>
+int dsc_t(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags, const DscOut &o,
+          const CallHooks &h, cudaStream_t st)
+{
+    using CD = DscCfg<N, KA>;
+    k_side_dsc<<<phi->b_side_grid, kSideWarps * 32, phi->b_side_smem, st>>>(
+        side_args(phi), w, phi->b_scr, (flags & LIFE_SKIP_ZERO) ? 1 : 0, phi->b_skip, phi->b_smax, h);
+    LIFE_CHECK_LAUNCH();
+    const TileArgs A{phi->b_cellr, phi->b_step, phi->b_Ddsc, phi->b_rowvox, phi->b_rowpart, phi->b_ypart,
+                     phi->b_ntiles, phi->b_nch, phi->nt, phi->b_slot_dsc};
+    const int fin = phi->b_nfix == 0 ? 1 : 0;
+    k_tile_dsc<N, KA><<<phi->b_tile_grid, CD::kThreads, phi->b_dsc_smem, st>>>(
+        A, phi->b_scr, y, b, flags, phi->red, o, h, phi->b_skip, phi->b_side_grid, phi->b_smax, phi->b_side_grid, fin);
+    LIFE_CHECK_LAUNCH();
+    if (!fin) {
+        const int blocks = std::max(1, std::min(phi->sms, (phi->b_nfix + 7) / 8));
+        k_tile_dsc_fix<N><<<blocks, 256, 0, st>>>(phi->b_fixptr, phi->b_fixvox, phi->b_nfix, phi->b_ypart, phi->nt,
+                                                  y, b, flags, phi->red, phi->b_tile_grid * CD::kWarps, o, h,
+                                                  phi->b_skip, phi->b_side_grid);
+        LIFE_CHECK_LAUNCH();
+    }
+    return LIFE_OK;
+}
+
+template <int N, int KA>
+int wc_tile_t(life_phi *phi, const float *y, const CallHooks &h, cudaStream_t st)
+{
+    using CW = WcCfg<N, KA>;
+    const TileArgs A{phi->b_cellr, phi->b_step, phi->b_Dwc, phi->b_rowvox, phi->b_rowpart, phi->b_ypart,
+                     phi->b_ntiles, phi->b_nch, phi->nt, phi->b_slot_wc};
+    k_tile_wc<N, KA><<<phi->b_tile_grid, CW::kThreads, phi->b_wc_smem, st>>>(A, y, phi->b_scr, h);
+    LIFE_CHECK_LAUNCH();
+    return LIFE_OK;
+}
+
+#define LIFE_BIN_DISPATCH(FN, ...)                                             \
+    switch (phi->b_n) {                                                        \
+    case 32: return FN<32, 64>(__VA_ARGS__);                                   \
+    case 64: return FN<64, 64>(__VA_ARGS__);                                   \
+    case 96: return FN<96, 64>(__VA_ARGS__);                                   \
+    case 128: return FN<128, 64>(__VA_ARGS__);                                 \
+    case 160: return FN<160, 32>(__VA_ARGS__);                                 \
+    case 192: return FN<192, 32>(__VA_ARGS__);                                 \
+    default: return fail(LIFE_ERR_CONFIG_INVALID, "bin layout: unsupported n_dirs"); \
+    }
+
+}  // namespace
+
+int prepare_bin(life_phi *phi) { LIFE_BIN_DISPATCH(prep_t, phi); }
+
+int bin_tile_warps(const life_phi *phi)
+{
+    switch (phi->b_n) {
+    case 32: case 64: return DscCfg<64, 64>::kWarps;
+    case 96: case 128: return DscCfg<128, 64>::kWarps;
+    default: return DscCfg<192, 32>::kWarps;
+    }
+}
+
+int launch_dsc_bin(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags, const DscOut &o,
+                   const CallHooks &h, cudaStream_t st)
+{
+    LIFE_BIN_DISPATCH(dsc_t, phi, w, y, b, flags, o, h, st);
+}
+
+static int wc_tile(life_phi *phi, const float *y, const CallHooks &h, cudaStream_t st)
+{
+    LIFE_BIN_DISPATCH(wc_tile_t, phi, y, h, st);
+}
+
+int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, const FixParams &fx, uint32_t flags,
+                  double *sumsq, const CallHooks &h, const life_comm *comm, cudaStream_t st)
+{
+    LIFE_TRY(wc_tile(phi, y, h, st));
+    k_side_wc<<<phi->b_side_grid, kSideWarps * 32, phi->b_wcs_smem, st>>>(side_args(phi), phi->b_scr, fx, phi->nt,
+                                                                          phi->b_wfix, phi->b_nanf, h);
+    LIFE_CHECK_LAUNCH();
+    const int blocks = std::max(1, std::min(phi->sms * 4, (phi->nf + 255) / 256));
+    if (comm && comm->nranks > 1) {
+        if (!phi->b_wsum) LIFE_TRY(dalloc(phi, &phi->b_wsum, (size_t)phi->nf));
+        k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->b_f2vf, phi->b_wsum, phi->nf, w, w_ref,
+                                              flags, fx, phi->nt, 1, phi->part_d2, phi->counter2, sumsq, h);
+        LIFE_CHECK_LAUNCH();
+        if (comm->allreduce(phi->b_wsum, phi->nf, LIFE_DT_I64, LIFE_OP_SUM, st, comm->ctx) != 0)
+            return fail(LIFE_ERR_NCCL, "allreduce(wsum) failed");
+        k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->b_f2vf, phi->b_wsum, phi->nf, w, w_ref,
+                                              flags, fx, phi->nt, 2, phi->part_d2, phi->counter2, sumsq, h);
+        LIFE_CHECK_LAUNCH();
+    } else {
+        k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->b_f2vf, nullptr, phi->nf, w, w_ref,
+                                              flags, fx, phi->nt, 0, phi->part_d2, phi->counter2, sumsq, h);
+        LIFE_CHECK_LAUNCH();
+    }
+    return LIFE_OK;
+}
+
+}  // namespace life

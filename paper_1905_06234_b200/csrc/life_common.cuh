@@ -132,6 +132,41 @@ struct life_phi {
     int64_t t_npad = 0, t_maxseg = 0, t_maxstep = 0;
     size_t t_smem = 0;
 
+    // binned two-phase layout (life_bin.cu, the default fp32 products):
+    // "tile side" = 128-row voxel tiles x atom chunks on tcgen05, "bin
+    // side" = fascicle bins held in shared memory; the two meet in a
+    // tile-major scratch vector (s = w[f]*value for DSC, z = (Y D^T)[cell]
+    // for WC) through contiguous segments (tile, chunk, bin).
+    bool has_bin = false;
+    int b_ka = 0, b_n = 0, b_nch = 0, b_ntiles = 0, b_nbins = 0, b_sb = 0, b_cellbits = 0;
+    int64_t b_nvf = 0, b_nsteps = 0, b_nseg = 0, b_npad = 0;
+    uint16_t *b_cellr = nullptr;   // tile-major [npad]: rank << cellbits | row*KA + atom%KA
+    uint16_t *b_vid = nullptr;     // bin-major [nc]: virtual fascicle slot within its bin
+    float *b_val = nullptr;        // bin-major [nc]
+    float *b_scr = nullptr;        // tile-major scratch [npad]
+    uint32_t *b_step = nullptr;    // [nsteps + 1] tile-major start of each (tile, chunk)
+    uint32_t *b_segsrc = nullptr;  // [nseg + 1] bin-major start of each (bin, tile, chunk), 4-entry units
+    uint32_t *b_segdst = nullptr;  // [nseg] its tile-major start, 4-entry units
+    uint32_t *b_binptr = nullptr;  // [nbins + 1] first segment of each bin
+    uint32_t *b_ctaseg = nullptr;  // [side grid + 1] first segment of each bin-side CTA
+    uint32_t *b_vf2f = nullptr;    // [nvf] fascicle of each virtual slot
+    uint32_t *b_f2vf = nullptr;    // [nf + 1] first virtual slot of each fascicle
+    int *b_rowvox = nullptr;       // [ntiles*128] voxel of each tile row, -1 = empty
+    int *b_rowpart = nullptr;      // [ntiles*128] partial-row index, -1 = the voxel's only row
+    float *b_Ddsc = nullptr;       // per chunk: [hi|lo][KA/32][N][32] swizzled D^T (DSC B operand)
+    float *b_Dwc = nullptr;        // per chunk: [hi|lo][N/32][KA][32] swizzled D (WC B operand)
+    float *b_ypart = nullptr;      // [nprow * N] rows of voxels split over several rows
+    uint32_t *b_fixptr = nullptr;  // [nfix + 1] partial rows of each split voxel
+    int *b_fixvox = nullptr;       // [nfix]
+    int b_nfix = 0, b_nprow = 0;
+    unsigned long long *b_wfix = nullptr;  // [nvf] int64 fixed-point sums (zero between calls)
+    unsigned char *b_nanf = nullptr;       // [nvf] non-finite term seen
+    unsigned long long *b_wsum = nullptr;  // [nf] per-fascicle sums for multi-GPU reduction
+    unsigned long long *b_skip = nullptr;  // [side grid] skip-count partials of the bin side
+    float *b_smax = nullptr;               // [side grid] max |s| partials (DSC fixed-point scale)
+    int b_tile_grid = 0, b_side_grid = 0, b_slot_dsc = 0, b_slot_wc = 0;
+    size_t b_dsc_smem = 0, b_wc_smem = 0, b_side_smem = 0, b_wcs_smem = 0;
+
     // fixed-point WC accumulator and its scale inputs
     unsigned long long *wfix = nullptr;  // [nf] two's-complement int64
     double vmax = 0.0;                   // max |value|
@@ -247,6 +282,15 @@ int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t
 int launch_dsc_tc(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
                   const DscOut &o, const CallHooks &h, cudaStream_t st);
 int prepare_tc(life_phi *phi);
+// binned two-phase products (life_bin.cu)
+int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
+              const double *val, const std::vector<double> &hdict, cudaStream_t st);
+int launch_dsc_bin(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
+                   const DscOut &o, const CallHooks &h, cudaStream_t st);
+int bin_tile_warps(const life_phi *phi);
+int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, const FixParams &fx,
+                  uint32_t flags, double *sumsq, const CallHooks &h, const life_comm *comm,
+                  cudaStream_t st);
 // tcgen05 path geometry (life_tc.cu)
 constexpr int kTcTV = 128;       // voxels per CTA tile (MMA M)
 constexpr int kTcCA = 32;        // atoms per chunk (one 128-byte swizzle row of fp32)

@@ -677,6 +677,7 @@ static int launch_dsc_sparse(life_phi *phi, const float *w, float *y, const floa
 static int launch_dsc_kernel(life_phi *phi, const float *w, float *y, const float *b,
                              uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st)
 {
+    if (phi->has_bin) return launch_dsc_bin(phi, w, y, b, flags, o, h, st);
     if (phi->has_tc) return launch_dsc_tc(phi, w, y, b, flags, o, h, st);
     if (phi->has_dense) return launch_dsc_dense(phi, w, y, b, flags, o, h, st);
     return launch_dsc_sparse(phi, w, y, b, flags, o, h, st);
@@ -751,6 +752,7 @@ int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
         ymax_dev = phi->ybound;
     }
     WcFix fx{phi->wfix, ymax_dev, ysumsq_dev, phi->vmax, phi->dmax, (double)phi->fmax_nnz};
+    if (phi->has_bin) return launch_wc_bin(phi, y, w, w_ref, fx, flags, sumsq, h, comm, st);
     LIFE_TRY(launch_wc_main(phi, y, fx, h, st));
     if (comm && comm->nranks > 1) {
         // fascicle partial sums of all voxel shards: integer sum, so every
@@ -777,7 +779,7 @@ int life_dsc_f32(life_phi *phi, const float *w, float *y, const float *b,
                  uint32_t flags, const life_spmv_out *out, void *stream)
 {
     if (!phi || !w || !y) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
-    if (!phi->has_fast && !phi->has_dense)
+    if (!phi->has_fast && !phi->has_dense && !phi->has_bin)
         return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     if ((flags & LIFE_SUBTRACT_B) && !b) return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_SUBTRACT_B needs b");
     if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(y) |
@@ -795,7 +797,7 @@ int life_wc_f32(life_phi *phi, const float *y, float *w, const float *w_ref,
                 const life_spmv_out *out, void *stream)
 {
     if (!phi || !w || !y) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
-    if (!phi->has_fast && !phi->has_dense)
+    if (!phi->has_fast && !phi->has_dense && !phi->has_bin)
         return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     if ((flags & LIFE_PROJECT_GRAD) && !w_ref)
         return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_PROJECT_GRAD needs w_ref");

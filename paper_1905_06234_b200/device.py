@@ -32,14 +32,18 @@ warnings.filterwarnings("ignore", message="The given NumPy array is not writable
 _LAYOUT = ["auto"]
 
 
+_LAYOUTS = ("auto", "sparse", "dense", "bin", "fma", "tensor")
+
+
 def set_layout(name):
     """fp32 kernel family for operators built from now on: "auto" (density
-    heuristic), "sparse" (voxel-segment kernels), "dense" (tile kernels with
-    DSC and WC on the tcgen05 tensor cores where the shape allows: n_dirs <=
-    128 for DSC, <= 96 for WC), "fma" (tile kernels on CUDA cores only) or
-    "tensor" (same as "dense")."""
-    if name not in ("auto", "sparse", "dense", "fma", "tensor"):
-        raise ConfigInvalid(f"layout must be auto/sparse/dense/fma/tensor, got {name!r}")
+    heuristic: "bin" for tile-shaped operators, else "sparse"), "sparse"
+    (voxel-segment kernels), "bin" or "dense" (binned two-phase products:
+    tcgen05 tile side + shared-memory fascicle bins, n_dirs <= 192), "tensor"
+    (single-pass tcgen05 tile kernels) or "fma" (single-pass tile kernels on
+    CUDA cores)."""
+    if name not in _LAYOUTS:
+        raise ConfigInvalid(f"layout must be one of {'/'.join(_LAYOUTS)}, got {name!r}")
     _LAYOUT[0] = name
 
 
@@ -99,8 +103,9 @@ class DeviceOperator:
     def _create(self, d, a, v, f, val, dic, stream):
         flags = (N.PHI_EXACT_F64 if self.exact else 0) | (0 if self.fast else N.PHI_NO_FAST_F32)
         flags |= {"auto": 0, "sparse": N.PHI_FORCE_SPARSE, "dense": N.PHI_FORCE_DENSE,
-                  "fma": N.PHI_FORCE_DENSE | N.PHI_NO_TENSOR,
-                  "tensor": N.PHI_FORCE_DENSE | N.PHI_TENSOR}[_LAYOUT[0]]
+                  "bin": N.PHI_FORCE_DENSE,
+                  "fma": N.PHI_FORCE_DENSE | N.PHI_NO_TENSOR | N.PHI_NO_BIN,
+                  "tensor": N.PHI_FORCE_DENSE | N.PHI_TENSOR | N.PHI_NO_BIN}[_LAYOUT[0]]
         dims = N.Dims(d.n_atoms, d.n_voxels, d.n_fibers, d.n_dirs, d.n_coeffs)
         handle = ctypes.c_void_p()
         bad = ctypes.c_int64(-1)
@@ -118,10 +123,11 @@ class DeviceOperator:
 
     @property
     def kind(self):
-        """"tensor" (tile kernels, tcgen05 DSC), "dense" or "sparse": the fp32
-        kernel family this operator uses."""
+        """"bin" (binned two-phase products), "tensor" (single-pass tcgen05
+        tile kernels), "dense" (single-pass CUDA-core tile kernels) or
+        "sparse": the fp32 kernel family this operator uses."""
         g = self.info.atom_groups
-        return "sparse" if g > 0 else "tensor" if g < 0 else "dense"
+        return "sparse" if g > 0 else "bin" if g == -2 else "tensor" if g < 0 else "dense"
 
     @property
     def tensor_ops(self):
