@@ -29,6 +29,7 @@
 // lifespmv/_kernels.py:14-33, 57-68) under the owned regimes of
 // engine.dsc_parallel / wc_parallel (engine.py:247-289, 372-413).
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cmath>
@@ -52,6 +53,30 @@ constexpr int kBuild = 8;           // builder / gatherer warps of the tile kern
 constexpr int kSideWarps = 32;      // bin-side CTA
 constexpr int kSideU = 4;           // 32-entry chunks per warp batch on the bin side
 constexpr int kSlots = 3;           // staged steps per tile kernel
+
+// Role timing, compiled in only with -DLIFE_BIN_DIAG (tools/bin_roles.py):
+// clock64 spans per category summed over warps (lane 0) into g_bin_cyc.
+#ifdef LIFE_BIN_DIAG
+__device__ unsigned long long g_bin_cyc[32];
+#define BD_T0(v) const long long v = clock64()
+#define BD_ACC(i, v) (bdc[i] += (unsigned long long)(clock64() - (v)))
+#define BD_DECL unsigned long long bdc[32] = {}
+#define BD_FLUSH                                                               \
+    if ((threadIdx.x & 31) == 0)                                               \
+        for (int i_ = 0; i_ < 32; ++i_)                                        \
+            if (bdc[i_]) atomicAdd(&g_bin_cyc[i_], bdc[i_])
+#else
+#define BD_T0(v)
+#define BD_ACC(i, v)
+#define BD_DECL
+#define BD_FLUSH
+#endif
+#define BD_WAIT(i, expr) \
+    do {                 \
+        BD_T0(bt_);      \
+        expr;            \
+        BD_ACC(i, bt_);  \
+    } while (0)
 
 // ---------------------------------------------------------------------------
 // device helpers
@@ -78,13 +103,24 @@ __device__ __forceinline__ bool bar_try(uint64_t *b, unsigned parity)
                  : "=r"(ok) : "r"(sa(b)), "r"(parity) : "memory");
     return ok != 0;
 }
+// host-mapped debug record of the first timed-out wait (life_debug_timeout)
+__device__ unsigned *g_timeout_rec = nullptr;
 // trap after 4 s instead of hanging the GPU
 __device__ __forceinline__ void bar_wait(uint64_t *b, unsigned parity)
 {
     if (bar_try(b, parity)) return;
     const unsigned long long t0 = globaltimer();
     while (!bar_try(b, parity))
-        if (globaltimer() - t0 > 4000000000ull) __trap();
+        if (globaltimer() - t0 > 4000000000ull) {
+            if (g_timeout_rec && atomicCAS(g_timeout_rec, 0u, 1u) == 0u) {
+                g_timeout_rec[1] = blockIdx.x;
+                g_timeout_rec[2] = threadIdx.x >> 5;
+                g_timeout_rec[3] = sa(b);
+                g_timeout_rec[4] = parity;
+                __threadfence_system();
+            }
+            __trap();
+        }
 }
 // bulk copy global -> shared in pieces of at most 32 KB, completing on bar
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *b, uint64_t pol)
@@ -230,7 +266,8 @@ __device__ __forceinline__ bool last_cta(unsigned *counter)
 
 // DSC outputs from the tile/fixup partials and the bin side's skip partials
 __device__ void dsc_finish(const ReduceSlots &red, int nparts, const unsigned long long *skip, int nskip,
-                           const DscOut &out, unsigned *counter, const CallHooks &hooks, int nthreads)
+                           const DscOut &out, unsigned *counter, const CallHooks &hooks, int nthreads,
+                           unsigned *nonfinite)
 {
     const double tsq = block_reduce<double>(red.part_d, nparts, 0.0, OpSum{}, nthreads);
     const float tmax = block_reduce<float>(red.part_f, nparts, 0.f, OpMaxF{}, nthreads);
@@ -241,6 +278,7 @@ __device__ void dsc_finish(const ReduceSlots &red, int nparts, const unsigned lo
         if (out.skipped) *out.skipped = tsk;
         if (out.skipped_d) *out.skipped_d = (double)tsk;
         *counter = 0;
+        if (nonfinite) *nonfinite = 0u;
         if (hooks.t_accum && hooks.t_begin) *hooks.t_accum += globaltimer() - *hooks.t_begin;
     }
 }
@@ -387,8 +425,8 @@ __global__ void k_seg_tm(const uint32_t *perm_seg, const uint32_t *tm_excl, cons
 // place every coefficient in both orders
 __global__ void k_place(const uint32_t *perm_bm, const uint32_t *segid, const uint32_t *first, const uint32_t *src4,
                         const uint32_t *dst4, int64_t n, const uint32_t *vf_o, const double *val, const uint32_t *a,
-                        const uint32_t *rank_o, const uint32_t *row_o, const uint32_t *slot_of_row, int ka, int cellbits,
-                        uint16_t *vid, float *val32, uint16_t *cellr)
+                        const uint32_t *row_o, const uint32_t *slot_of_row, int ka, uint16_t *vid, float *val32,
+                        uint16_t *cellr)
 {
     for (int64_t p = gtid(); p < n; p += gstride()) {
         const uint32_t i = perm_bm[p], s = segid[p] - 1u;
@@ -397,8 +435,7 @@ __global__ void k_place(const uint32_t *perm_bm, const uint32_t *segid, const ui
         vid[bp] = (uint16_t)(vf_o[i] % kSB);
         val32[bp] = (float)val[i];
         const uint32_t lane = slot_of_row[row_o[i]] % kTV;
-        const uint32_t cell = lane * (uint32_t)ka + (a[i] & (uint32_t)(ka - 1));
-        cellr[tp] = (uint16_t)(((rank_o[i] % kRanks) << cellbits) | cell);
+        cellr[tp] = (uint16_t)(lane * (uint32_t)(ka + 4) + (a[i] & (uint32_t)(ka - 1)));
     }
 }
 // lower bound of key b * per_bin over the bin-major segment keys
@@ -497,10 +534,10 @@ static void tf32_split_h(float x, float &hi, float &lo)
     std::memcpy(&hi, &u, 4);
     lo = x - hi;
 }
-// float index of (row, k) in a K-major SWIZZLE_128B tile of 32 fp32 per row
-static inline size_t sw_cell(uint32_t row, uint32_t k)
+// byte offset of f16 element (row, k) in a K-major SWIZZLE_128B tile (64 per row)
+static inline size_t sw16(uint32_t row, uint32_t k)
 {
-    return (size_t)(row >> 3) * 256u + (row & 7u) * 32u + ((((k >> 2) ^ row) & 7u) << 2) + (k & 3u);
+    return (size_t)(row >> 3) * 1024u + (row & 7u) * 128u + ((((k >> 3) ^ row) & 7u) << 4) + (k & 7u) * 2u;
 }
 
 }  // namespace bin
@@ -517,9 +554,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     const int64_t n = phi->nc;
     const int N = (phi->nt + 31) / 32 * 32;
     if (n == 0 || N > 192 || n >= 0xF0000000ll) return LIFE_OK;
-    const int ka = N <= 128 ? 64 : 32;
-    const int ka_shift = ka == 64 ? 6 : 5;
-    const int cellbits = ka == 64 ? 13 : 12;
+    const int ka = 64, ka_shift = 6;
     const int nch = (phi->na + ka - 1) / ka;
     const uint32_t na = (uint32_t)phi->na;
     const int nv = phi->nv, nf = phi->nf;
@@ -753,14 +788,14 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     LIFE_TRY(dalloc(phi, &phi->b_scr, (size_t)npad + 8));
     LIFE_TRY(dalloc(phi, &phi->b_vid, (size_t)nbm + 8));
     LIFE_TRY(dalloc(phi, &phi->b_val, (size_t)nbm + 8));
-    k_fill_u16<<<gridn(npad + 8), 256, 0, st>>>(phi->b_cellr, (int64_t)npad + 8, kPad);
+    k_fill_u16<<<gridn(npad + 8), 256, 0, st>>>(phi->b_cellr, (int64_t)npad + 8, (uint16_t)ka);
     LIFE_CHECK_LAUNCH();
     k_fill_u16<<<gridn(nbm + 8), 256, 0, st>>>(phi->b_vid, nbm + 8, kPad);
     LIFE_CHECK_LAUNCH();
     LIFE_CUDA(cudaMemsetAsync(phi->b_val, 0, ((size_t)nbm + 8) * 4, st));
     LIFE_CUDA(cudaMemsetAsync(phi->b_scr, 0, ((size_t)npad + 8) * 4, st));
-    k_place<<<gridn(n), 256, 0, st>>>(perm_bm, segid, first, phi->b_segsrc, phi->b_segdst, n, vf_o, val, a, rank_o,
-                                      row_o, d_slot, ka, cellbits, phi->b_vid, phi->b_val, phi->b_cellr);
+    k_place<<<gridn(n), 256, 0, st>>>(perm_bm, segid, first, phi->b_segsrc, phi->b_segdst, n, vf_o, val, a, row_o,
+                                      d_slot, ka, phi->b_vid, phi->b_val, phi->b_cellr);
     LIFE_CHECK_LAUNCH();
 
     // 7. bin and CTA segment ranges of the bin side
@@ -772,31 +807,33 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     k_cta_seg<<<gridn(side_grid + 1), 256, 0, st>>>(phi->b_segsrc, nseg, side_grid, phi->b_ctaseg);
     LIFE_CHECK_LAUNCH();
 
-    // 8. dictionary chunks as the two B operands (tf32 hi | lo, swizzled)
+    // 8. dictionary chunks as the two B operands: f16 hi | lo of D * kDScale,
+    // K-major SWIZZLE_128B (64 f16 per 128-byte row)
     {
-        const size_t per = (size_t)2 * N * ka;
-        std::vector<float> hd((size_t)nch * per, 0.f), hw((size_t)nch * per, 0.f);
+        const int nkb = (N + 63) / 64;
+        const size_t pd = (size_t)2 * N * ka, pw = (size_t)2 * nkb * ka * 64;  // halves per chunk
+        std::vector<uint16_t> hd((size_t)nch * pd, 0), hw((size_t)nch * pw, 0);
         for (int c = 0; c < nch; ++c)
             for (int k = 0; k < ka; ++k) {
                 const int at = c * ka + k;
                 for (int t = 0; t < N; ++t) {
-                    const float x = (at < phi->na && t < phi->nt) ? (float)hdict[(size_t)at * phi->nt + t] : 0.f;
-                    float hi, lo;
-                    tf32_split_h(x, hi, lo);
-                    // DSC: rows = directions, K = atoms (blocks of 32 atoms)
-                    const size_t od = (size_t)c * per + (size_t)(k / 32) * N * 32 + sw_cell(t, k % 32);
-                    hd[od] = hi;
-                    hd[od + (size_t)N * ka] = lo;
-                    // WC: rows = atoms, K = directions (blocks of 32 directions)
-                    const size_t ow = (size_t)c * per + (size_t)(t / 32) * ka * 32 + sw_cell(k, t % 32);
-                    hw[ow] = hi;
-                    hw[ow + (size_t)N * ka] = lo;
+                    const float x = (at < phi->na && t < phi->nt) ? (float)hdict[(size_t)at * phi->nt + t] * 256.f : 0.f;
+                    const __half h = __float2half_rn(x), l = __float2half_rn(x - __half2float(h));
+                    const uint16_t hb = __half_as_ushort(h), lb = __half_as_ushort(l);
+                    // DSC: rows = directions, K = the chunk's 64 atoms
+                    const size_t od = (size_t)c * pd + sw16(t, k) / 2;
+                    hd[od] = hb;
+                    hd[od + (size_t)N * ka] = lb;
+                    // WC: rows = atoms, K = directions in blocks of 64
+                    const size_t ow = (size_t)c * pw + (size_t)(t / 64) * ka * 64 + sw16(k, t % 64) / 2;
+                    hw[ow] = hb;
+                    hw[ow + (size_t)nkb * ka * 64] = lb;
                 }
             }
         LIFE_TRY(dalloc(phi, &phi->b_Ddsc, hd.size()));
         LIFE_TRY(dalloc(phi, &phi->b_Dwc, hw.size()));
-        LIFE_CUDA(cudaMemcpyAsync(phi->b_Ddsc, hd.data(), hd.size() * 4, cudaMemcpyHostToDevice, st));
-        LIFE_CUDA(cudaMemcpyAsync(phi->b_Dwc, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_Ddsc, hd.data(), hd.size() * 2, cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_Dwc, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice, st));
         LIFE_CUDA(cudaStreamSynchronize(st));
     }
 
@@ -810,7 +847,6 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     phi->b_ntiles = (int)ntiles;
     phi->b_nbins = nbins;
     phi->b_sb = kSB;
-    phi->b_cellbits = cellbits;
     phi->b_nvf = nvf;
     phi->b_nsteps = nsteps;
     phi->b_nseg = nseg;
@@ -819,6 +855,8 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     phi->b_side_grid = side_grid;
     LIFE_TRY(dalloc(phi, &phi->b_skip, (size_t)phi->b_side_grid));
     LIFE_TRY(dalloc(phi, &phi->b_smax, (size_t)phi->b_side_grid));
+    LIFE_TRY(dalloc(phi, &phi->b_nonfin, 1));
+    LIFE_CUDA(cudaMemsetAsync(phi->b_nonfin, 0, 4, st));
     LIFE_CUDA(cudaMemsetAsync(phi->b_skip, 0, (size_t)phi->b_side_grid * 8, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
     LIFE_TRY(prepare_bin(phi));
@@ -905,7 +943,8 @@ __device__ __forceinline__ int find_bin(const uint32_t *binseg, int nbins, uint3
 // s == 0, _kernels.py:24-28)
 __global__ void __launch_bounds__(kSideWarps * 32, 1)
     k_side_dsc(const SideArgs A, const float *__restrict__ w, float *__restrict__ scr, int count_skips,
-               unsigned long long *__restrict__ skip_part, float *__restrict__ smax_part, const CallHooks hooks)
+               unsigned long long *__restrict__ skip_part, float *__restrict__ smax_part, unsigned *__restrict__ nonfinite,
+               const CallHooks hooks)
 {
     extern __shared__ float ws[];  // kSB
     __shared__ uint32_t s_ctr;
@@ -915,6 +954,7 @@ __global__ void __launch_bounds__(kSideWarps * 32, 1)
     const uint32_t S0 = __ldg(A.ctaseg + blockIdx.x), S1 = __ldg(A.ctaseg + blockIdx.x + 1);
     unsigned long long zeros = 0;
     float smax = 0.f;
+    bool nonfin = false;
     int b = S0 < S1 ? find_bin(A.binseg, A.nbins, S0) : A.nbins;
     for (uint32_t s = S0; s < S1; ++b) {
         const uint32_t pe = min(S1, __ldg(A.binseg + b + 1));
@@ -956,6 +996,7 @@ __global__ void __launch_bounds__(kSideWarps * 32, 1)
                         o[e] = pad ? 0.f : __fmul_rn(ws[pad ? 0 : ids[e]], vs[e]);
                         zeros += (!pad && o[e] == 0.f) ? 1ull : 0ull;
                         if (isfinite(o[e])) smax = fmaxf(smax, fabsf(o[e]));
+                        else nonfin = true;
                     }
                     reinterpret_cast<float4 *>(scr)[du[k]] = make_float4(o[0], o[1], o[2], o[3]);
                 }
@@ -964,6 +1005,9 @@ __global__ void __launch_bounds__(kSideWarps * 32, 1)
         s = pe;
     }
     // per-CTA skip count (fixed-order total in the tile kernel's last CTA)
+    // this call's non-finite flag (read by the tile kernel, cleared by the
+    // CTA that finishes the call)
+    if (__any_sync(0xffffffffu, nonfin) && lane == 0) atomicAdd(nonfinite, 1u);
     __shared__ unsigned long long sz[kSideWarps];
     __shared__ float sm[kSideWarps];
 #pragma unroll
@@ -1129,51 +1173,81 @@ __global__ void __launch_bounds__(BT)
 // tile side (tcgen05)
 // ===========================================================================
 struct TileArgs {
-    const uint16_t *cellr;  // tile-major
+    const uint16_t *cellr;  // tile-major: C/Z tile word offset row * kCS + atom % kKA (pads: kKA)
     const uint32_t *step;   // [nsteps + 1]
-    const float *D;         // dictionary chunks (product-specific B layout)
+    const uint16_t *D;      // dictionary chunks: product-specific B operand, f16 hi | lo, x kDScale
     const int *rowvox;      // [ntiles * 128]
     const int *rowpart;     // [ntiles * 128]
     float *ypart;           // [nprow * N]
-    int ntiles, nch, nt, cap;
+    int ntiles, nch, nt;
 };
 
-template <int N, int KA>
+constexpr int kKA = 64;            // atoms per step: one 128-byte row of f16
+constexpr int kCS = kKA + 4;       // C / Z tile row stride (words): conflict-free row reads
+constexpr int kUMax = 4;           // 4-entry units per thread prefetched one step ahead
+constexpr float kDScale = 256.f;   // dictionary pre-scale (keeps the f16 lo parts normal)
+
+__device__ __forceinline__ uint64_t idesc_f16(int m, int n)
+{
+    return (uint64_t)((1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24));
+}
+__device__ __forceinline__ void mma_f16(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                 "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void tm_st8(uint32_t addr, const uint32_t (&v)[8])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+// x = hi + lo in f16 (2 x 11 significant bits); returns the packed pair words
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t &hi, uint32_t &lo)
+{
+    const __half2 h = __floats2half2_rn(x0, x1);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+    hi = *reinterpret_cast<const uint32_t *>(&h);
+    lo = *reinterpret_cast<const uint32_t *>(&l);
+}
+
+template <int N>
 struct DscCfg {
     static constexpr int EQ = (N + 63) / 64;   // epilogue warps per TMEM lane quarter
-    static constexpr int kProdS = kBuild;      // step staging (bulk copies)
-    static constexpr int kProdD = kBuild + 1;  // dictionary chunks
-    static constexpr int kMma = kBuild + 2;
-    static constexpr int kEpi = kBuild + 3;
+    static constexpr int kProdD = kBuild;      // warpgroup 2: dictionary chunks, two MMA issuers, spare
+    static constexpr int kMma = kBuild + 1;    // two issuers: even / odd steps
+    static constexpr int kEpi = kBuild + 4;
     static constexpr int kWarps = kEpi + 4 * EQ;
     static constexpr int kThreads = kWarps * 32;
-    static constexpr int DB = 2 * N * KA * 4;  // one chunk, hi | lo
-    static constexpr int CS = KA + 4;          // C tile row stride (floats): conflict-free row reads
-    static constexpr int CBytes = kTV * CS * 4;
-    static constexpr int FOLD = 128 / KA;      // steps per TMEM accumulation group (128 atoms)
+    // registers: warpgroup 2 hands what it releases to the two builder
+    // warpgroups (setmaxnreg; only released registers can be claimed)
+    static constexpr int kRegBase = (65536 / kThreads) / 8 * 8;
+    static constexpr int kRegLow = 56;
+    static constexpr int kRegBuild = kRegBase + (128 * (kRegBase - kRegLow) / 256) / 8 * 8 > 232
+                                         ? 232
+                                         : kRegBase + (128 * (kRegBase - kRegLow) / 256) / 8 * 8;
+    static constexpr int DB = 2 * N * 128;     // one chunk: N rows x 64 f16, hi | lo
+    static constexpr int CBytes = kTV * kCS * 4;
     static constexpr int NBLK = N / 16;
     static constexpr int MB = (NBLK + EQ - 1) / EQ;
-    static constexpr int TACC = 4 * KA;        // TMEM: A stages at st * 2KA, accumulators at TACC + g * N
-    static constexpr int CB = KA == 64 ? 13 : 12;  // cell bits
-    static constexpr int KSH = KA == 64 ? 6 : 5;
-    static_assert(4 * KA + 2 * N <= 512, "TMEM budget");
+    static constexpr int TACC = 128;           // TMEM: A stage e at 64 e (hi 32 cols | lo 32), accumulator e at TACC + e N
+    static_assert(TACC + 2 * N <= 512, "TMEM budget");
 };
 
-template <int N, int KA>
+template <int N>
 struct WcCfg {
-    static constexpr int kProdS = kBuild;
-    static constexpr int kProdD = kBuild + 1;
-    static constexpr int kMma = kBuild + 2;
+    static constexpr int NKB = (N + 63) / 64;  // 64-direction K blocks of the B operand
+    static constexpr int kProdD = kBuild;
+    static constexpr int kMma = kBuild + 1;    // two issuers
     static constexpr int kYZ = kBuild + 3;     // 8 warps: two per TMEM lane quarter
     static constexpr int kWarps = kYZ + 8;
     static constexpr int kThreads = kWarps * 32;
-    static constexpr int DB = 2 * N * KA * 4;
-    static constexpr int ZS = KA + 4;
-    static constexpr int ZBytes = kTV * ZS * 4;
-    static constexpr int TZ = 2 * N;           // TMEM: Y hi at 0, lo at N, Z buffers at TZ + zb * KA
-    static constexpr int CB = KA == 64 ? 13 : 12;
-    static constexpr int KSH = KA == 64 ? 6 : 5;
-    static_assert(2 * N + 2 * KA <= 512, "TMEM budget");
+    static constexpr int DB = 2 * NKB * kKA * 128;
+    static constexpr int ZBytes = kTV * kCS * 4;
+    static constexpr int TZ = N;               // TMEM: Y hi at 0 (N/2 cols), lo at N/2, Z buffer e at TZ + e kKA
+    static_assert(N + 2 * kKA <= 512, "TMEM budget");
 };
 
 __device__ __forceinline__ unsigned char *align1024(unsigned char *p)
@@ -1181,59 +1255,95 @@ __device__ __forceinline__ unsigned char *align1024(unsigned char *p)
     return (unsigned char *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
 }
 
+// (tile, chunk) walk of a CTA's steps without divisions: step k is chunk
+// k % nch of tile blockIdx.x + (k / nch) * gridDim.x
+struct StepIter {
+    int c, nch;
+    size_t gs, tile_stride;
+    __device__ StepIter(int k, int nch_) : c(k % nch_), nch(nch_)
+    {
+        gs = ((size_t)blockIdx.x + (size_t)(k / nch_) * gridDim.x) * nch_ + c;
+        tile_stride = (size_t)gridDim.x * nch_;
+    }
+    __device__ __forceinline__ void next()
+    {
+        ++gs;
+        if (++c == nch) {
+            c = 0;
+            gs += tile_stride - nch;
+        }
+    }
+};
+
+// One step's entries, prefetched into registers one step ahead (4 per unit)
+struct StepRegs {
+    uint32_t p0, n;
+    uint2 c[kUMax];
+    float4 s[kUMax];
+};
+
 // DSC tile side.  Roles (warps):
-//   0-7   builders: per step, C[row, atom] = sum of s over the step's entries
-//         in shared memory (rank 0: plain stores; ranks 1..: one pass per
-//         rank, so repeats of a cell are added in a fixed order), then split
-//         into tf32 hi/lo and stored to a TMEM A stage (warp w: lanes
-//         32*(w%4).., atoms (w/4)*KA/2..), zeroing the C tile behind them
-//   8     step staging: bulk copies of the step's (cellr, s) into a slot
-//   9     dictionary chunks (pre-split, pre-swizzled B operand) into 2 stages
-//   10    MMA issuer: 3xTF32 Y += A_hi.D_hi + A_lo.D_hi + A_hi.D_lo, A from TMEM
-//   11..  epilogue: fold each group of FOLD steps (128 atoms) from TMEM into
-//         fp32 registers (the tensor core's accumulation truncates), write y
-//         (accumulate / subtract b), sum of squares and max |r|
-template <int N, int KA>
-__global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
+//   0-7   builders: per step, C[row, atom] = sum of s as 32-bit fixed point
+//         (red.shared.add.u32: order independent, deterministic) from entries
+//         prefetched into registers one step ahead (L2-prefetched three
+//         ahead); then each thread converts its (row, 32 atoms) to f16 hi/lo
+//         into the step's TMEM A stage.  The C tile is never cleared: each
+//         thread keeps its cells' previous totals and converts differences.
+//   8     dictionary chunks (pre-split, pre-scaled f16 B operand), 2 stages
+//   9-10  MMA issuers for even / odd steps (one issuing thread cannot keep
+//         the tensor core busy at these shapes): Y_e = A_hi.D_hi + A_lo.D_hi +
+//         A_hi.D_lo, kind::f16, A from TMEM, fp32 accumulator per step
+//   11..  epilogue: fold every step's accumulator into fp32 registers (the
+//         tensor core's accumulation truncates), write y (accumulate /
+//         subtract b), sum of squares and max |r|
+template <int N>
+__global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
     k_tile_dsc(const TileArgs A, const float *__restrict__ scr, float *__restrict__ y, const float *__restrict__ b,
                const uint32_t flags, const ReduceSlots red, const DscOut out, const CallHooks hooks,
                const unsigned long long *__restrict__ skip_part, int nskip, const float *__restrict__ smax, int nsmax,
-               int finalize)
+               unsigned *__restrict__ nonfinite, int finalize)
 {
-    using C = DscCfg<N, KA>;
+    using C = DscCfg<N>;
     extern __shared__ __align__(1024) unsigned char smraw[];
-    __shared__ __align__(8) uint64_t slot_full[kSlots], slot_empty[kSlots], d_full[2], d_empty[2], a_full[2],
-        a_empty[2], acc_full[2], acc_empty[2];
+    __shared__ __align__(8) uint64_t d_full[2], d_empty[2], a_full[2], a_empty[2], acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_base;
-    __shared__ __align__(16) uint32_t s_hdr[kSlots][2];  // per staged step: start, count
-    __shared__ uint32_t s_rowbad[2][4];                    // rows with a non-finite s (per step parity)
+    __shared__ uint32_t s_rowbad[2][4];  // rows with a non-finite s (slow path; per step parity)
     __shared__ float s_scale[2];
     if (hooks.done && *hooks.done) return;
+    BD_DECL;
     unsigned char *sm = align1024(smraw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int my_tiles = (int)blockIdx.x < A.ntiles ? (A.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int total = my_tiles * A.nch;
     unsigned char *Dbuf = sm;
-    float *Ct = reinterpret_cast<float *>(sm + 2 * C::DB);
-    unsigned char *slots = sm + 2 * C::DB + C::CBytes;
-    const uint32_t cap = (uint32_t)A.cap;  // staged entries per slot
-    const uint32_t slot_bytes = cap * 6u;
+    const uint32_t Cs = sa(sm + 2 * C::DB);
     if (threadIdx.x == 0) {
-        for (int j = 0; j < kSlots; ++j) {
-            bar_init(&slot_full[j], 1);
-            bar_init(&slot_empty[j], kBuild);
-        }
-        for (int s = 0; s < 2; ++s) {
-            bar_init(&d_full[s], 1);
-            bar_init(&d_empty[s], 1);
-            bar_init(&a_full[s], kBuild);
-            bar_init(&a_empty[s], 1);
-            bar_init(&acc_full[s], 1);
-            bar_init(&acc_empty[s], 4 * C::EQ);
+        for (int e = 0; e < 2; ++e) {
+            bar_init(&d_full[e], 1);
+            bar_init(&d_empty[e], 1);
+            bar_init(&a_full[e], kBuild);
+            bar_init(&a_empty[e], 1);
+            bar_init(&acc_full[e], 1);
+            bar_init(&acc_empty[e], 4 * C::EQ);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == C::kMma) tcg::alloc(&tmem_base, 512);
+    if (warp == 0) {
+        // fixed-point scale: |s| * scale < 2^27, so a cell's kRanks terms stay below 2^30
+        float m = 0.f;
+        for (int i = lane; i < nsmax; i += 32) m = fmaxf(m, __ldcg(smax + i));
+        m = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
+        if (lane == 0) {
+            int ex = 0;
+            if (m > 0.f) {
+                frexpf(m, &ex);  // m < 2^ex
+                ex = 27 - ex;
+            }
+            s_scale[0] = ldexpf(1.f, ex);
+            s_scale[1] = ldexpf(1.f, -ex) * (32768.f / kDScale);  // y = acc * inv_q * 2^15 / kDScale
+        }
+    }
     tcg::fence_before();
     __syncthreads();
     tcg::fence_after();
@@ -1246,189 +1356,181 @@ __global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
 
     if (warp < kBuild) {
         // ===== builders =====
+#ifndef LIFE_BIN_NOREGSPLIT
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kRegBuild));
+#endif
         const int tid = threadIdx.x;
-        const uint32_t Cs = sa(Ct);
         const int q = warp & 3, hh = warp >> 2;
-        const uint32_t rowaddr = Cs + 4u * (uint32_t)((q * 32 + lane) * C::CS + hh * (KA / 2));
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-        // the C tile starts zeroed; each step's convert pass zeroes it behind
-        for (int i = tid; i < kTV * C::CS / 4; i += 256) sts_f4(Cs + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
+        const uint32_t rowaddr = Cs + 4u * (uint32_t)((q * 32 + lane) * kCS + hh * 32);
+        const float scale = s_scale[0];
+        const bool slow = *nonfinite != 0u;  // non-finite s somewhere: check every entry
+        for (int i = tid; i < kTV * kCS / 4; i += 256) sts_f4(Cs + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
         if (tid < 8) s_rowbad[tid >> 2][tid & 3] = 0u;
-        // fixed-point scale of this call: |s| * scale < 2^27, so a cell's
-        // kRanks terms stay below 2^30
-        if (warp == 0) {
-            float m = 0.f;
-            for (int i = lane; i < nsmax; i += 32) m = fmaxf(m, __ldcg(smax + i));
-            m = __reduce_max_sync(0xffffffffu, __float_as_uint(m)) == 0u ? 0.f
-                : __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
-            if (lane == 0) {
-                int ex = 0;
-                if (m > 0.f) {
-                    frexpf(m, &ex);  // m < 2^ex
-                    ex = 27 - ex;
-                }
-                s_scale[0] = ldexpf(1.f, ex);
-                s_scale[1] = ldexpf(1.f, -ex);
+        int prev[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) prev[i] = 0;
+        StepRegs R;
+        uint32_t np0 = 0, nn = 0;  // pointers of the step after the prefetched one
+        StepIter it2(0, A.nch);    // walks two steps ahead of the current one
+        auto ptrs = [&](int k, uint32_t &p0, uint32_t &n) {
+            if (k < total) {
+                p0 = __ldg(A.step + it2.gs);
+                n = __ldg(A.step + it2.gs + 1) - p0;
+                it2.next();
+            } else {
+                p0 = n = 0;
             }
-        }
+        };
+        auto fetch = [&](StepRegs &S) {
+#pragma unroll
+            for (int i = 0; i < kUMax; ++i) {
+                const uint32_t u = (uint32_t)tid + 256u * i;
+                if (u < S.n / 4u) {
+                    S.c[i] = __ldg(reinterpret_cast<const uint2 *>(A.cellr + S.p0) + u);
+                    S.s[i] = __ldcg(reinterpret_cast<const float4 *>(scr + S.p0) + u);
+                }
+            }
+        };
+        // fixed-point adds of 4 entries (pads hold s = 0 at a padding column)
+        auto add4 = [&](uint2 c, float4 v) {
+            const uint32_t o[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
+            const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(Cs + 4u * o[e]),
+                             "r"((uint32_t)__float2int_rn(x[e] * scale)) : "memory");
+        };
+        // slow path (a non-finite s in this call): rows that see one become NaN
+        auto add4_checked = [&](uint2 c, float4 v, int k) {
+            const uint32_t o[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
+            const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (o[e] != (uint32_t)kKA && !isfinite(x[e])) {
+                    const uint32_t row = o[e] / kCS;
+                    atomicOr(&s_rowbad[k & 1][row >> 5], 1u << (row & 31));
+                    continue;
+                }
+                asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(Cs + 4u * o[e]),
+                             "r"((uint32_t)__float2int_rn(x[e] * scale)) : "memory");
+            }
+        };
+        ptrs(0, R.p0, R.n);
+        fetch(R);
+        ptrs(1, np0, nn);
         named_bar(1, 256);
-        const float scale = s_scale[0], inv = s_scale[1];
         for (int k = 0; k < total; ++k) {
-            const int j = k % kSlots;
-            bar_wait(&slot_full[j], (k / kSlots) & 1);
-            const uint32_t p0 = s_hdr[j][0], n = s_hdr[j][1];
-            const uint32_t nst4 = min(n, cap) / 4u;
-            const uint32_t sc = sa(slots + (size_t)j * slot_bytes), ss = sc + cap * 2;
-            if (tid == 0) {
-                s_rowbad[(k + 1) & 1][0] = s_rowbad[(k + 1) & 1][1] = 0u;
-                s_rowbad[(k + 1) & 1][2] = s_rowbad[(k + 1) & 1][3] = 0u;
-            }
-            // C[row, atom] = sum of s in 32-bit fixed point: integer adds are
-            // order independent, so repeats need no ordering (deterministic)
-            for (uint32_t u = tid; u < n / 4u; u += 256u) {
-                uint2 cr;
-                float4 sv;
-                if (u < nst4) {
-                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(cr.x), "=r"(cr.y) : "r"(sc + 8u * u));
-                    sv = lds_f4(ss + 16u * u);
-                } else {
-                    cr = __ldg(reinterpret_cast<const uint2 *>(A.cellr + p0) + u);
-                    sv = __ldcg(reinterpret_cast<const float4 *>(scr + p0) + u);
-                }
-                const uint32_t cs4[4] = {cr.x & 0xFFFFu, cr.x >> 16, cr.y & 0xFFFFu, cr.y >> 16};
-                const float vs4[4] = {sv.x, sv.y, sv.z, sv.w};
+            BD_T0(t_sc);
+            StepRegs S = R;  // this step (loaded during the previous one)
+            R.p0 = np0;
+            R.n = nn;
+            fetch(R);        // next step, in flight during this one
+            ptrs(k + 2, np0, nn);
+            const uint32_t nu = S.n / 4u;
+            if (!slow) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if (cs4[e] == kPad) continue;
-                    const uint32_t cell = cs4[e] & ((1u << C::CB) - 1);
-                    if (!isfinite(vs4[e])) {
-                        atomicOr(&s_rowbad[k & 1][(cell >> C::KSH) >> 5], 1u << ((cell >> C::KSH) & 31));
-                        continue;
-                    }
-                    const int qv = __float2int_rn(vs4[e] * scale);
-                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(Cs + 4u * ((cell >> C::KSH) * C::CS + (cell & (KA - 1)))),
-                                 "r"((uint32_t)qv) : "memory");
+                for (int i = 0; i < kUMax; ++i)
+                    if ((uint32_t)tid + 256u * i < nu) add4(S.c[i], S.s[i]);
+                for (uint32_t u = (uint32_t)tid + 256u * kUMax; u < nu; u += 256u)
+                    add4(__ldg(reinterpret_cast<const uint2 *>(A.cellr + S.p0) + u),
+                         __ldcg(reinterpret_cast<const float4 *>(scr + S.p0) + u));
+            } else {
+                if (tid == 0) {
+                    s_rowbad[(k + 1) & 1][0] = s_rowbad[(k + 1) & 1][1] = 0u;
+                    s_rowbad[(k + 1) & 1][2] = s_rowbad[(k + 1) & 1][3] = 0u;
                 }
+#pragma unroll
+                for (int i = 0; i < kUMax; ++i)
+                    if ((uint32_t)tid + 256u * i < nu) add4_checked(S.c[i], S.s[i], k);
+                for (uint32_t u = (uint32_t)tid + 256u * kUMax; u < nu; u += 256u)
+                    add4_checked(__ldg(reinterpret_cast<const uint2 *>(A.cellr + S.p0) + u),
+                                 __ldcg(reinterpret_cast<const float4 *>(scr + S.p0) + u), k);
             }
-            __syncwarp();
-            if (lane == 0) bar_arrive(&slot_empty[j]);
-            named_bar(1, 256);  // the C tile is complete
-            // convert this warp's rows/atoms into the TMEM A stage, zero behind
-            const int st = k & 1;
-            if (k >= 2) bar_wait(&a_empty[st], ((k >> 1) - 1) & 1);
+            BD_ACC(1, t_sc);
+            BD_WAIT(2, named_bar(1, 256));  // the step's sums are complete
+            const int e = k & 1;
+            if (k >= 2) BD_WAIT(3, bar_wait(&a_empty[e], ((k >> 1) - 1) & 1));
             tcg::fence_after();
-            const uint32_t ta = tmem + lane_base + (uint32_t)(st * 2 * KA + hh * (KA / 2));
-            const bool bad = (s_rowbad[k & 1][q] >> lane) & 1u;
+            BD_T0(t_cv);
+            const bool bad = slow && ((s_rowbad[k & 1][q] >> lane) & 1u);
+            uint32_t hv[16], lv[16];
 #pragma unroll
-            for (int h16 = 0; h16 < KA / 32; ++h16) {
-                uint32_t hv[16], lv2[16];
+            for (int i4 = 0; i4 < 8; ++i4) {
+                const float4 x = lds_f4(rowaddr + 16u * i4);
+                const int cur[4] = {__float_as_int(x.x), __float_as_int(x.y), __float_as_int(x.z), __float_as_int(x.w)};
+                float f[4];
 #pragma unroll
-                for (int i4 = 0; i4 < 4; ++i4) {
-                    const uint32_t ad = rowaddr + 64u * h16 + 16u * i4;
-                    const float4 x = lds_f4(ad);
-                    sts_f4(ad, make_float4(0.f, 0.f, 0.f, 0.f));
-                    float xs[4] = {__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
-                                   __int_as_float(0x7fc00000)};
-                    if (!bad) {
-                        xs[0] = (float)__float_as_int(x.x) * inv;
-                        xs[1] = (float)__float_as_int(x.y) * inv;
-                        xs[2] = (float)__float_as_int(x.z) * inv;
-                        xs[3] = (float)__float_as_int(x.w) * inv;
-                    }
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const uint32_t hb = tcg::hi_bits(__float_as_uint(xs[e]));
-                        hv[4 * i4 + e] = hb;
-                        lv2[4 * i4 + e] = __float_as_uint(xs[e] - __uint_as_float(hb));
-                    }
+                for (int t = 0; t < 4; ++t) {
+                    const int dlt = (int)((uint32_t)cur[t] - (uint32_t)prev[4 * i4 + t]);
+                    prev[4 * i4 + t] = cur[t];
+                    f[t] = bad ? __int_as_float(0x7fc00000) : (float)dlt * (1.f / 32768.f);
                 }
-                tm_st16(ta + 16u * h16, hv);
-                tm_st16(ta + (uint32_t)KA + 16u * h16, lv2);
+                split2(f[0], f[1], hv[2 * i4], lv[2 * i4]);
+                split2(f[2], f[3], hv[2 * i4 + 1], lv[2 * i4 + 1]);
             }
+            const uint32_t ta = tmem + lane_base + (uint32_t)(e * 64 + hh * 16);
+            tm_st16(ta, hv);
+            tm_st16(ta + 32u, lv);
             tcg::wait_st();
             tcg::fence_before();
             __syncwarp();
-            if (lane == 0) bar_arrive(&a_full[st]);
-            named_bar(1, 256);  // C tile zeroed before the next step's stores
+            BD_ACC(4, t_cv);
+            if (lane == 0) bar_arrive(&a_full[e]);
+            BD_WAIT(5, named_bar(1, 256));  // every cell read before the next step's adds
         }
-    } else if (warp == C::kProdS) {
-        // ===== step staging =====
-        if (lane == 0) {
-            const uint64_t pol = pol_first();
-            for (int k = 0; k < total; ++k) {
-                const size_t gs = step_of(k);
-                const uint32_t p0 = __ldg(A.step + gs), n = __ldg(A.step + gs + 1) - p0;
-                const int j = k % kSlots;
-                if (k >= kSlots) bar_wait(&slot_empty[j], ((k / kSlots) - 1) & 1);
-                const uint32_t nst = min(n, cap);
-                s_hdr[j][0] = p0;
-                s_hdr[j][1] = n;
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                bar_arrive_tx(&slot_full[j], nst * 6u);
-                unsigned char *dst = slots + (size_t)j * slot_bytes;
-                if (nst) {
-                    bulk_g2s(dst, A.cellr + p0, nst * 2u, &slot_full[j], pol);
-                    bulk_g2s(dst + cap * 2, scr + p0, nst * 4u, &slot_full[j], pol);
-                }
-                if (k + kSlots < total) {
-                    const size_t g2 = step_of(k + kSlots);
-                    const uint32_t q0 = __ldg(A.step + g2), n2 = min(__ldg(A.step + g2 + 1) - q0, cap);
-                    if (n2) {
-                        prefetch_l2(A.cellr + q0, n2 * 2u);
-                        prefetch_l2(scr + q0, n2 * 4u);
-                    }
-                }
-            }
-        }
-    } else if (warp == C::kProdD) {
+    } else if (warp < C::kEpi) {
+#ifndef LIFE_BIN_NOREGSPLIT
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::kRegLow));
+#endif
+      if (warp == C::kProdD) {
         // ===== dictionary chunks =====
         if (lane == 0) {
             const uint64_t pol = pol_last();
-            for (int k = 0; k < total; ++k) {
-                const int st = k & 1, c = k % A.nch;
-                if (k >= 2) bar_wait(&d_empty[st], ((k >> 1) - 1) & 1);
-                bar_arrive_tx(&d_full[st], (unsigned)C::DB);
-                bulk_g2s(Dbuf + (size_t)st * C::DB, A.D + (size_t)c * (C::DB / 4), (unsigned)C::DB, &d_full[st], pol);
-            }
-        }
-    } else if (warp == C::kMma) {
-        // ===== MMA issuer =====
-        if (lane == 0) {
-            constexpr uint32_t id = tcg::idesc_tf32(kTV, N);
-            int k = 0, G = 0;
-            for (int i = 0; i < my_tiles; ++i) {
-                for (int c = 0; c < A.nch; ++c, ++k) {
-                    const int st = k & 1, buf = G & 1;
-                    const bool first = (c % C::FOLD) == 0;
-                    const bool last = (c % C::FOLD) == C::FOLD - 1 || c == A.nch - 1;
-                    if (first) {
-                        if (G >= 2) bar_wait(&acc_empty[buf], ((G >> 1) - 1) & 1);
-                        tcg::fence_after();
-                    }
-                    bar_wait(&a_full[st], (k >> 1) & 1);
-                    bar_wait(&d_full[st], (k >> 1) & 1);
-                    tcg::fence_after();
-                    const uint32_t db = sa(Dbuf + (size_t)st * C::DB);
-                    const uint64_t bh = tcg::sdesc(db), bl = tcg::sdesc(db + (uint32_t)(N * KA * 4));
-                    const uint32_t d = tmem + (uint32_t)(C::TACC + buf * N);
-                    const uint32_t ah = tmem + (uint32_t)(st * 2 * KA), al = ah + (uint32_t)KA;
-#pragma unroll
-                    for (int kk = 0; kk < KA / 8; ++kk) {
-                        const uint64_t o = (uint64_t)((((kk >> 2) * N * 128) + (kk & 3) * 32) >> 4);
-                        tcg::mma_ts(d, ah + 8u * kk, bh + o, id, (first && kk == 0) ? 0u : 1u);
-                        tcg::mma_ts(d, al + 8u * kk, bh + o, id, 1u);
-                        tcg::mma_ts(d, ah + 8u * kk, bl + o, id, 1u);
-                    }
-                    tcg::commit(&a_empty[st]);
-                    tcg::commit(&d_empty[st]);
-                    if (last) {
-                        tcg::commit(&acc_full[buf]);
-                        ++G;
+            StepIter it(0, A.nch), it3(3, A.nch);
+            for (int k = 0; k < total; ++k, it.next(), it3.next()) {
+                const int e = k & 1, c = it.c;
+                if (k >= 2) BD_WAIT(10, bar_wait(&d_empty[e], ((k >> 1) - 1) & 1));
+                bar_arrive_tx(&d_full[e], (unsigned)C::DB);
+                bulk_g2s(Dbuf + (size_t)e * C::DB, reinterpret_cast<const unsigned char *>(A.D) + (size_t)c * C::DB,
+                         (unsigned)C::DB, &d_full[e], pol);
+                if (k + 3 < total) {  // the builders' entries, three steps ahead
+                    const size_t g3 = it3.gs;
+                    const uint32_t p3 = __ldg(A.step + g3), n3 = __ldg(A.step + g3 + 1) - p3;
+                    if (n3) {
+                        prefetch_l2(A.cellr + p3, n3 * 2u);
+                        prefetch_l2(scr + p3, n3 * 4u);
                     }
                 }
             }
         }
+      } else if (warp < C::kMma + 2) {
+        // ===== MMA issuers: warp kMma + e takes the steps k = e (mod 2) =====
+        const int e = warp - C::kMma;
+        if (lane == 0) {
+            const uint32_t id = (uint32_t)idesc_f16(kTV, N);
+            const uint32_t db = sa(Dbuf + (size_t)e * C::DB);
+            const uint64_t bh = tcg::sdesc(db), bl = tcg::sdesc(db + (uint32_t)(N * 128));
+            const uint32_t d = tmem + (uint32_t)(C::TACC + e * N), ah = tmem + (uint32_t)(e * 64), al = ah + 32u;
+            for (int k = e, j = 0; k < total; k += 2, ++j) {
+                if (j >= 1) BD_WAIT(6, bar_wait(&acc_empty[e], (j - 1) & 1));
+                BD_WAIT(7, bar_wait(&a_full[e], j & 1));
+                BD_WAIT(8, bar_wait(&d_full[e], j & 1));
+                tcg::fence_after();
+#pragma unroll
+                for (int kk = 0; kk < kKA / 16; ++kk) {
+                    const uint64_t o = (uint64_t)((kk * 32) >> 4);
+                    mma_f16(d, ah + 8u * kk, bh + o, id, kk ? 1u : 0u);
+                    mma_f16(d, al + 8u * kk, bh + o, id, 1u);
+                    mma_f16(d, ah + 8u * kk, bl + o, id, 1u);
+                }
+                tcg::commit(&a_empty[e]);
+                tcg::commit(&d_empty[e]);
+                tcg::commit(&acc_full[e]);
+            }
+        }
         __syncwarp();
+      }
     } else {
         // ===== epilogue: thread = tile row (TMEM lane), a slice of columns =====
         const int ew = warp - C::kEpi, q = warp & 3, cs = ew >> 2;
@@ -1437,30 +1539,32 @@ __global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const bool accumulate = flags & LIFE_ACCUMULATE;
         const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
-        const int ngroups = (A.nch + C::FOLD - 1) / C::FOLD;
-        int G = 0;
+        const float oscale = s_scale[1];
+        int k = 0;
         for (int i = 0; i < my_tiles; ++i) {
             const int t = (int)blockIdx.x + i * (int)gridDim.x;
             float acc[C::MB * 16];
 #pragma unroll
-            for (int e = 0; e < C::MB * 16; ++e) acc[e] = 0.f;
-            for (int g = 0; g < ngroups; ++g, ++G) {
-                const int buf = G & 1;
-                bar_wait(&acc_full[buf], (G >> 1) & 1);
+            for (int x = 0; x < C::MB * 16; ++x) acc[x] = 0.f;
+            for (int c = 0; c < A.nch; ++c, ++k) {
+                const int e = k & 1;
+                BD_WAIT(11, bar_wait(&acc_full[e], (k >> 1) & 1));
                 tcg::fence_after();
+                BD_T0(t_fd);
 #pragma unroll
                 for (int bb = 0; bb < C::MB; ++bb) {
                     if (b0 + bb < b1) {
                         uint32_t r[16];
-                        tm_ld16(tmem + lane_base + (uint32_t)(C::TACC + buf * N + 16 * (b0 + bb)), r);
+                        tm_ld16(tmem + lane_base + (uint32_t)(C::TACC + e * N + 16 * (b0 + bb)), r);
                         tm_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) acc[16 * bb + e] += __uint_as_float(r[e]);
+                        for (int x = 0; x < 16; ++x) acc[16 * bb + x] += __uint_as_float(r[x]);
                     }
                 }
+                BD_ACC(12, t_fd);
                 tcg::fence_before();
                 __syncwarp();
-                if (lane == 0) bar_arrive(&acc_empty[buf]);
+                if (lane == 0) bar_arrive(&acc_empty[e]);
             }
             const int rv = __ldg(A.rowvox + (size_t)t * kTV + row);
             const int rp = __ldg(A.rowpart + (size_t)t * kTV + row);
@@ -1471,7 +1575,7 @@ __global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
                 for (int bb = 0; bb < C::MB; ++bb)
                     if (b0 + bb < b1)
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) yp[16 * (b0 + bb) + e] = acc[16 * bb + e];
+                        for (int x = 0; x < 16; ++x) yp[16 * (b0 + bb) + x] = acc[16 * bb + x] * oscale;
                 continue;
             }
             const size_t yo = (size_t)rv * A.nt;
@@ -1482,8 +1586,8 @@ __global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
                     for (int e4 = 0; e4 < 4; ++e4) {
                         const int col = 16 * (b0 + bb) + 4 * e4;
                         if (b0 + bb < b1 && col < A.nt) {
-                            float r[4] = {acc[16 * bb + 4 * e4], acc[16 * bb + 4 * e4 + 1], acc[16 * bb + 4 * e4 + 2],
-                                          acc[16 * bb + 4 * e4 + 3]};
+                            float r[4] = {acc[16 * bb + 4 * e4] * oscale, acc[16 * bb + 4 * e4 + 1] * oscale,
+                                          acc[16 * bb + 4 * e4 + 2] * oscale, acc[16 * bb + 4 * e4 + 3] * oscale};
                             float4 *y4 = reinterpret_cast<float4 *>(y + yo + col);
                             if (accumulate) {
                                 const float4 o = *y4;
@@ -1495,9 +1599,9 @@ __global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
                             }
                             *y4 = make_float4(r[0], r[1], r[2], r[3]);
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                sq += (double)r[e] * (double)r[e];
-                                amax = fmaxf(amax, fabsf(r[e]));
+                            for (int x = 0; x < 4; ++x) {
+                                sq += (double)r[x] * (double)r[x];
+                                amax = fmaxf(amax, fabsf(r[x]));
                             }
                         }
                     }
@@ -1506,10 +1610,10 @@ __global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
 #pragma unroll
                 for (int bb = 0; bb < C::MB; ++bb) {
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int col = 16 * (b0 + bb) + e;
+                    for (int x = 0; x < 16; ++x) {
+                        const int col = 16 * (b0 + bb) + x;
                         if (b0 + bb < b1 && col < A.nt) {
-                            float r = acc[16 * bb + e];
+                            float r = acc[16 * bb + x] * oscale;
                             if (accumulate) r += y[yo + col];
                             if (subtract) r -= b[yo + col];
                             y[yo + col] = r;
@@ -1523,6 +1627,7 @@ __global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
     }
 
     // ---- teardown, fixed-order completion --------------------------------------
+    BD_FLUSH;
     tcg::fence_before();
     __syncthreads();
     if (warp == C::kMma) {
@@ -1540,7 +1645,8 @@ __global__ void __launch_bounds__(DscCfg<N, KA>::kThreads, 1)
         red.part_f[gw] = amax;
     }
     if (finalize && last_cta(red.counter))
-        dsc_finish(red, (int)gridDim.x * C::kWarps, skip_part, nskip, out, red.counter, hooks, C::kThreads);
+        dsc_finish(red, (int)gridDim.x * C::kWarps, skip_part, nskip, out, red.counter, hooks, C::kThreads,
+                   nonfinite);
 }
 
 // voxels split over several tile rows: sum their partial rows in row order
@@ -1550,7 +1656,7 @@ __global__ void __launch_bounds__(256)
     k_tile_dsc_fix(const uint32_t *__restrict__ fixptr, const int *__restrict__ fixvox, int nfix,
                    const float *__restrict__ ypart, int nt, float *__restrict__ y, const float *__restrict__ b,
                    uint32_t flags, const ReduceSlots red, int part0, const DscOut out, const CallHooks hooks,
-                   const unsigned long long *__restrict__ skip_part, int nskip)
+                   const unsigned long long *__restrict__ skip_part, int nskip, unsigned *__restrict__ nonfinite)
 {
     if (hooks.done && *hooks.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1581,53 +1687,50 @@ __global__ void __launch_bounds__(256)
         red.part_d[part0 + blockIdx.x * 8 + warp] = sq;
         red.part_f[part0 + blockIdx.x * 8 + warp] = amax;
     }
-    if (last_cta(red.counter)) dsc_finish(red, part0 + (int)gridDim.x * 8, skip_part, nskip, out, red.counter, hooks, 256);
+    if (last_cta(red.counter))
+        dsc_finish(red, part0 + (int)gridDim.x * 8, skip_part, nskip, out, red.counter, hooks, 256, nonfinite);
 }
 
 // WC tile side.  Roles (warps):
-//   0-7   gatherers: per step, z = Z[row, atom] of every entry from the
-//         shared-memory Z tile into the tile-major scratch (coalesced)
-//   8     step staging (cellr), 9 dictionary chunks (WC B operand)
-//   10    MMA issuer: Z = Y_hi.D_hi + Y_lo.D_hi + Y_hi.D_lo (M = 128 rows,
-//         N = KA atoms, K = directions), Y from TMEM
-//   11-18 YZ: per tile, y rows (thread = row) split into tf32 hi/lo and stored
-//         to TMEM (next tile's rows prefetched into registers); per step,
-//         Z read back from TMEM into a double-buffered shared-memory tile
-template <int N, int KA>
-__global__ void __launch_bounds__(WcCfg<N, KA>::kThreads, 1)
-    k_tile_wc(const TileArgs A, const float *__restrict__ y, float *__restrict__ scr, const CallHooks hooks)
+//   0-7   gatherers: per step, z = Z[row, atom] of every entry (cell offsets
+//         prefetched into registers one step ahead) from the shared-memory Z
+//         tile into the tile-major scratch (16-byte stores)
+//   8     dictionary chunks (WC B operand: atoms x directions, f16 hi | lo)
+//   9-10  MMA issuers for even / odd steps: Z_e = Y_hi.D_hi + Y_lo.D_hi +
+//         Y_hi.D_lo (M = 128 rows, N = 64 atoms, K = directions), Y from TMEM
+//   11-18 YZ: per tile, y rows (thread = row, scaled into the f16 range) split
+//         into f16 hi/lo and stored to TMEM; per step, Z read back from TMEM,
+//         rescaled, into a double-buffered shared-memory tile
+template <int N>
+__global__ void __launch_bounds__(WcCfg<N>::kThreads, 1)
+    k_tile_wc(const TileArgs A, const float *__restrict__ y, float *__restrict__ scr, const float *__restrict__ ymax,
+              const double *__restrict__ ysumsq, const CallHooks hooks)
 {
-    using C = WcCfg<N, KA>;
+    using C = WcCfg<N>;
     extern __shared__ __align__(1024) unsigned char smraw[];
-    __shared__ __align__(8) uint64_t slot_full[kSlots], slot_empty[kSlots], d_full[2], d_empty[2], acc_full[2],
-        acc_empty[2], z_full[2], z_empty[2], y_ready, y_free;
+    __shared__ __align__(8) uint64_t d_full[2], d_empty[2], acc_full[2], acc_empty[2], z_full[2], z_empty[2],
+        y_ready, y_free;
     __shared__ uint32_t tmem_base;
-    __shared__ __align__(16) uint32_t s_hdr[kSlots][2];  // per staged step: start, count
     if (hooks.done && *hooks.done) return;
     if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
+    BD_DECL;
     unsigned char *sm = align1024(smraw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int my_tiles = (int)blockIdx.x < A.ntiles ? (A.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int total = my_tiles * A.nch;
     unsigned char *Dbuf = sm;
-    float *Zt = reinterpret_cast<float *>(sm + 2 * C::DB);
-    unsigned char *slots = sm + 2 * C::DB + 2 * C::ZBytes;
-    const uint32_t cap = (uint32_t)A.cap;
+    const uint32_t Zs = sa(sm + 2 * C::DB);
     if (threadIdx.x == 0) {
-        for (int j = 0; j < kSlots; ++j) {
-            bar_init(&slot_full[j], 1);
-            bar_init(&slot_empty[j], kBuild);
-        }
-        for (int s = 0; s < 2; ++s) {
-            bar_init(&d_full[s], 1);
-            bar_init(&d_empty[s], 1);
-            bar_init(&acc_full[s], 1);
-            bar_init(&acc_empty[s], 8);
-            bar_init(&z_full[s], 8);
-            bar_init(&z_empty[s], kBuild);
+        for (int e = 0; e < 2; ++e) {
+            bar_init(&d_full[e], 1);
+            bar_init(&d_empty[e], 1);
+            bar_init(&acc_full[e], 1);
+            bar_init(&acc_empty[e], 8);
+            bar_init(&z_full[e], 8);
+            bar_init(&z_empty[e], kBuild);
         }
         bar_init(&y_ready, 8);
-        bar_init(&y_free, 1);
+        bar_init(&y_free, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == C::kMma) tcg::alloc(&tmem_base, 512);
@@ -1642,93 +1745,105 @@ __global__ void __launch_bounds__(WcCfg<N, KA>::kThreads, 1)
     if (warp < kBuild) {
         // ===== gatherers =====
         const int tid = threadIdx.x;
-        for (int k = 0; k < total; ++k) {
-            const int j = k % kSlots, zb = k & 1;
-            bar_wait(&slot_full[j], (k / kSlots) & 1);
-            bar_wait(&z_full[zb], (k >> 1) & 1);
-            const uint32_t p0 = s_hdr[j][0], n = s_hdr[j][1];
-            const uint32_t nst4 = min(n, cap) / 4u;
-            const uint32_t sc = sa(slots + (size_t)j * cap * 2);
-            const uint32_t Z = sa(Zt) + (uint32_t)(zb * C::ZBytes);
-            float4 *dst = reinterpret_cast<float4 *>(scr + p0);
-            for (uint32_t u = tid; u < n / 4u; u += 256u) {
-                uint2 cr;
-                if (u < nst4)
-                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(cr.x), "=r"(cr.y) : "r"(sc + 8u * u));
-                else
-                    cr = __ldg(reinterpret_cast<const uint2 *>(A.cellr + p0) + u);
-                const uint32_t cs4[4] = {cr.x & 0xFFFFu, cr.x >> 16, cr.y & 0xFFFFu, cr.y >> 16};
-                float z[4];
+        StepIter it2(0, A.nch);
+        auto ptrs = [&](int k, uint32_t &p0, uint32_t &n) {
+            if (k < total) {
+                p0 = __ldg(A.step + it2.gs);
+                n = __ldg(A.step + it2.gs + 1) - p0;
+                it2.next();
+            } else {
+                p0 = n = 0;
+            }
+        };
+        uint32_t cp0, cn, np0, nn;
+        uint2 cc[kUMax], nc[kUMax];
+        auto fetch = [&](uint32_t p0, uint32_t n, uint2 (&c)[kUMax]) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const uint32_t cell = cs4[e] & ((1u << C::CB) - 1);
-                    z[e] = cs4[e] != kPad ? lds_f(Z + 4u * ((cell >> C::KSH) * C::ZS + (cell & (KA - 1)))) : 0.f;
-                }
-                dst[u] = make_float4(z[0], z[1], z[2], z[3]);
+            for (int i = 0; i < kUMax; ++i) {
+                const uint32_t u = (uint32_t)tid + 256u * i;
+                if (u < n / 4u) c[i] = __ldg(reinterpret_cast<const uint2 *>(A.cellr + p0) + u);
             }
+        };
+        ptrs(0, np0, nn);
+        fetch(np0, nn, nc);
+        uint32_t p2, n2;
+        ptrs(1, p2, n2);
+        for (int k = 0; k < total; ++k) {
+            const int e = k & 1;
+            cp0 = np0;  // this step: registers loaded during the previous one
+            cn = nn;
+#pragma unroll
+            for (int i = 0; i < kUMax; ++i) cc[i] = nc[i];
+            np0 = p2;
+            nn = n2;
+            fetch(np0, nn, nc);  // next step, in flight during this one
+            ptrs(k + 2, p2, n2);
+            BD_WAIT(17, bar_wait(&z_full[e], (k >> 1) & 1));
+            BD_T0(t_g);
+            const uint32_t Z = Zs + (uint32_t)(e * C::ZBytes);
+            float4 *dst = reinterpret_cast<float4 *>(scr + cp0);
+            auto gat = [&](uint2 c, uint32_t u) {
+                const uint32_t o[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
+                dst[u] = make_float4(lds_f(Z + 4u * o[0]), lds_f(Z + 4u * o[1]), lds_f(Z + 4u * o[2]),
+                                     lds_f(Z + 4u * o[3]));
+            };
+#pragma unroll
+            for (int i = 0; i < kUMax; ++i) {
+                const uint32_t u = (uint32_t)tid + 256u * i;
+                if (u < cn / 4u) gat(cc[i], u);
+            }
+            for (uint32_t u = (uint32_t)tid + 256u * kUMax; u < cn / 4u; u += 256u)
+                gat(__ldg(reinterpret_cast<const uint2 *>(A.cellr + cp0) + u), u);
+            BD_ACC(18, t_g);
             __syncwarp();
-            if (lane == 0) {
-                bar_arrive(&slot_empty[j]);
-                bar_arrive(&z_empty[zb]);
-            }
-        }
-    } else if (warp == C::kProdS) {
-        if (lane == 0) {
-            const uint64_t pol = pol_first();
-            for (int k = 0; k < total; ++k) {
-                const size_t gs = step_of(k);
-                const uint32_t p0 = __ldg(A.step + gs), n = __ldg(A.step + gs + 1) - p0;
-                const int j = k % kSlots;
-                if (k >= kSlots) bar_wait(&slot_empty[j], ((k / kSlots) - 1) & 1);
-                const uint32_t nst = min(n, cap);
-                s_hdr[j][0] = p0;
-                s_hdr[j][1] = n;
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                bar_arrive_tx(&slot_full[j], nst * 2u);
-                if (nst) bulk_g2s(slots + (size_t)j * cap * 2, A.cellr + p0, nst * 2u, &slot_full[j], pol);
-                if (k + kSlots < total) {
-                    const size_t g2 = step_of(k + kSlots);
-                    const uint32_t q0 = __ldg(A.step + g2), n2 = min(__ldg(A.step + g2 + 1) - q0, cap);
-                    if (n2) prefetch_l2(A.cellr + q0, n2 * 2u);
-                }
-            }
+            if (lane == 0) bar_arrive(&z_empty[e]);
         }
     } else if (warp == C::kProdD) {
         if (lane == 0) {
             const uint64_t pol = pol_last();
-            for (int k = 0; k < total; ++k) {
-                const int st = k & 1, c = k % A.nch;
-                if (k >= 2) bar_wait(&d_empty[st], ((k >> 1) - 1) & 1);
-                bar_arrive_tx(&d_full[st], (unsigned)C::DB);
-                bulk_g2s(Dbuf + (size_t)st * C::DB, A.D + (size_t)c * (C::DB / 4), (unsigned)C::DB, &d_full[st], pol);
+            StepIter it(0, A.nch), it3(3, A.nch);
+            for (int k = 0; k < total; ++k, it.next(), it3.next()) {
+                const int e = k & 1, c = it.c;
+                if (k >= 2) BD_WAIT(23, bar_wait(&d_empty[e], ((k >> 1) - 1) & 1));
+                bar_arrive_tx(&d_full[e], (unsigned)C::DB);
+                bulk_g2s(Dbuf + (size_t)e * C::DB, reinterpret_cast<const unsigned char *>(A.D) + (size_t)c * C::DB,
+                         (unsigned)C::DB, &d_full[e], pol);
+                if (k + 3 < total) {  // the gatherers' cell offsets, three steps ahead
+                    const size_t g3 = it3.gs;
+                    const uint32_t p3 = __ldg(A.step + g3), n3 = __ldg(A.step + g3 + 1) - p3;
+                    if (n3) prefetch_l2(A.cellr + p3, n3 * 2u);
+                }
             }
         }
-    } else if (warp == C::kMma) {
+    } else if (warp < C::kYZ) {
+        // ===== MMA issuers =====
+        const int e = warp - C::kMma;
         if (lane == 0) {
-            constexpr uint32_t id = tcg::idesc_tf32(kTV, KA);
-            int k = 0;
+            const uint32_t id = (uint32_t)idesc_f16(kTV, kKA);
+            const uint32_t db = sa(Dbuf + (size_t)e * C::DB);
+            const uint64_t bh = tcg::sdesc(db), bl = tcg::sdesc(db + (uint32_t)(C::NKB * kKA * 128));
+            const uint32_t d = tmem + (uint32_t)(C::TZ + e * kKA);
+            int k = 0, j = 0;
             for (int i = 0; i < my_tiles; ++i) {
-                bar_wait(&y_ready, i & 1);
+                BD_WAIT(19, bar_wait(&y_ready, i & 1));
                 tcg::fence_after();
                 for (int c = 0; c < A.nch; ++c, ++k) {
-                    const int zb = k & 1;
-                    bar_wait(&d_full[zb], (k >> 1) & 1);
-                    if (k >= 2) bar_wait(&acc_empty[zb], ((k >> 1) - 1) & 1);
+                    if ((k & 1) != e) continue;
+                    if (j >= 1) BD_WAIT(21, bar_wait(&acc_empty[e], (j - 1) & 1));
+                    BD_WAIT(20, bar_wait(&d_full[e], j & 1));
                     tcg::fence_after();
-                    const uint32_t db = sa(Dbuf + (size_t)zb * C::DB);
-                    const uint64_t bh = tcg::sdesc(db), bl = tcg::sdesc(db + (uint32_t)(N * KA * 4));
-                    const uint32_t d = tmem + (uint32_t)(C::TZ + zb * KA);
-#pragma unroll 4
-                    for (int kk = 0; kk < N / 8; ++kk) {
-                        const uint64_t o = (uint64_t)((((kk >> 2) * KA * 128) + (kk & 3) * 32) >> 4);
-                        tcg::mma_ts(d, tmem + 8u * kk, bh + o, id, kk != 0 ? 1u : 0u);
-                        tcg::mma_ts(d, tmem + (uint32_t)N + 8u * kk, bh + o, id, 1u);
-                        tcg::mma_ts(d, tmem + 8u * kk, bl + o, id, 1u);
+#pragma unroll
+                    for (int kk = 0; kk < N / 16; ++kk) {
+                        const uint64_t o = (uint64_t)((((kk >> 2) * kKA * 128) + (kk & 3) * 32) >> 4);
+                        mma_f16(d, tmem + 8u * kk, bh + o, id, kk ? 1u : 0u);
+                        mma_f16(d, tmem + (uint32_t)(N / 2) + 8u * kk, bh + o, id, 1u);
+                        mma_f16(d, tmem + 8u * kk, bl + o, id, 1u);
                     }
-                    tcg::commit(&d_empty[zb]);
-                    tcg::commit(&acc_full[zb]);
-                    if (c == A.nch - 1) tcg::commit(&y_free);
+                    tcg::commit(&d_empty[e]);
+                    tcg::commit(&acc_full[e]);
+                    ++j;
                 }
+                tcg::commit(&y_free);  // this issuer's MMAs of the tile (arrives at once if none)
             }
         }
         __syncwarp();
@@ -1737,92 +1852,118 @@ __global__ void __launch_bounds__(WcCfg<N, KA>::kThreads, 1)
         const int ew = warp - C::kYZ, q = warp & 3, cs = ew >> 2;
         const int row = q * 32 + lane;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-        constexpr int YH = N / 2;          // y columns per thread
-        constexpr int ZH = KA / 2;         // Z columns per thread
+        constexpr int NB8 = N / 16;                 // 16-direction blocks (8 TMEM columns of f16 pairs)
+        constexpr int BPS = (NB8 + 1) / 2;          // blocks per slice (max)
+        const int bb0 = cs * NB8 / 2, bb1 = (cs + 1) * NB8 / 2;
         const bool vec = (A.nt & 3) == 0;
-        // y rows: prefetched one tile ahead into registers when they fit
-        // (N <= 96), else loaded at the tile start in 16-column blocks
-        constexpr bool kPre = YH <= 48;
-        constexpr int YR = kPre ? YH : 16;
-        float yr[YR];
-        auto load_y = [&](int t, int c0, int ncol) {
-            const int rv = __ldg(A.rowvox + (size_t)t * kTV + row);
-            const float *src = y + (size_t)(rv < 0 ? 0 : rv) * A.nt;
+        // y scale into the f16 range: |y| * ys < 2^14; z = Z / (ys * kDScale)
+        const float yb = ysumsq ? (float)sqrt(*ysumsq) : *ymax;
+        int ex = 0;
+        if (yb > 0.f && isfinite(yb)) {
+            frexpf(yb, &ex);
+            ex = 14 - ex;
+        }
+        const float ys = ldexpf(1.f, ex), zinv = ldexpf(1.f, -ex) / kDScale;
+        constexpr bool kPre = N <= 96;
+        float yr[kPre ? BPS * 16 : 16];
+        auto load_blk = [&](const float *src, bool ok, int blk, float *dstv) {
 #pragma unroll
-            for (int i4 = 0; i4 < YR / 4; ++i4) {
-                if (4 * i4 >= ncol) break;
-                const int col = c0 + 4 * i4;
-                if (rv >= 0 && vec && col < A.nt) {
+            for (int i4 = 0; i4 < 4; ++i4) {
+                const int col = 16 * blk + 4 * i4;
+                if (ok && vec && col < A.nt) {
                     const float4 v = __ldg(reinterpret_cast<const float4 *>(src + col));
-                    yr[4 * i4] = v.x; yr[4 * i4 + 1] = v.y; yr[4 * i4 + 2] = v.z; yr[4 * i4 + 3] = v.w;
+                    dstv[4 * i4] = v.x; dstv[4 * i4 + 1] = v.y; dstv[4 * i4 + 2] = v.z; dstv[4 * i4 + 3] = v.w;
                 } else {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        yr[4 * i4 + e] = (rv >= 0 && col + e < A.nt) ? __ldg(src + col + e) : 0.f;
+                    for (int x = 0; x < 4; ++x) dstv[4 * i4 + x] = (ok && col + x < A.nt) ? __ldg(src + col + x) : 0.f;
                 }
             }
         };
-        auto store_y = [&](int h16, int roff) {  // 16 columns from yr[roff..]
-            uint32_t hv[16], lv[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const float x = yr[roff + e];
-                const uint32_t hb = tcg::hi_bits(__float_as_uint(x));
-                hv[e] = hb;
-                lv[e] = __float_as_uint(x - __uint_as_float(hb));
-            }
-            tm_st16(tmem + lane_base + (uint32_t)(cs * YH + 16 * h16), hv);
-            tm_st16(tmem + lane_base + (uint32_t)(N + cs * YH + 16 * h16), lv);
+        auto row_src = [&](int t, bool &ok) {
+            const int rv = __ldg(A.rowvox + (size_t)t * kTV + row);
+            ok = rv >= 0;
+            return y + (size_t)(rv < 0 ? 0 : rv) * A.nt;
         };
-        if (kPre && my_tiles > 0) load_y((int)blockIdx.x, cs * YH, YH);
+        auto store_blk = [&](int blk, const float *v) {
+            uint32_t hv[8], lv[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) split2(v[2 * x] * ys, v[2 * x + 1] * ys, hv[x], lv[x]);
+            tm_st8(tmem + lane_base + (uint32_t)(8 * blk), hv);
+            tm_st8(tmem + lane_base + (uint32_t)(N / 2 + 8 * blk), lv);
+        };
+        if (kPre && my_tiles > 0) {
+            bool ok;
+            const float *src = row_src((int)blockIdx.x, ok);
+#pragma unroll
+            for (int bb = 0; bb < BPS; ++bb)
+                if (bb0 + bb < bb1) load_blk(src, ok, bb0 + bb, yr + 16 * bb);
+        }
         int k = 0;
         for (int i = 0; i < my_tiles; ++i) {
             const int t = (int)blockIdx.x + i * (int)gridDim.x;
-            if (i >= 1) bar_wait(&y_free, (i - 1) & 1);
+            if (i >= 1) BD_WAIT(24, bar_wait(&y_free, (i - 1) & 1));
             tcg::fence_after();
+            BD_T0(t_y);
             if (kPre) {
 #pragma unroll
-                for (int h16 = 0; h16 < YH / 16; ++h16) store_y(h16, 16 * h16);
+                for (int bb = 0; bb < BPS; ++bb)
+                    if (bb0 + bb < bb1) store_blk(bb0 + bb, yr + 16 * bb);
             } else {
+                bool ok;
+                const float *src = row_src(t, ok);
 #pragma unroll 1
-                for (int h16 = 0; h16 < YH / 16; ++h16) {
-                    load_y(t, cs * YH + 16 * h16, 16);
-                    store_y(h16, 0);
+                for (int blk = bb0; blk < bb1; ++blk) {
+                    load_blk(src, ok, blk, yr);
+                    store_blk(blk, yr);
                 }
             }
             tcg::wait_st();
             tcg::fence_before();
             __syncwarp();
+            BD_ACC(25, t_y);
             if (lane == 0) bar_arrive(&y_ready);
-            if (kPre && i + 1 < my_tiles) load_y(t + (int)gridDim.x, cs * YH, YH);  // in flight meanwhile
-            for (int c = 0; c < A.nch; ++c, ++k) {
-                const int zb = k & 1;
-                bar_wait(&acc_full[zb], (k >> 1) & 1);
-                tcg::fence_after();
-                uint32_t zr[ZH];
+            if (kPre && i + 1 < my_tiles) {  // next tile's rows, in flight meanwhile
+                bool ok;
+                const float *src = row_src(t + (int)gridDim.x, ok);
 #pragma unroll
-                for (int h16 = 0; h16 < ZH / 16; ++h16) {
+                for (int bb = 0; bb < BPS; ++bb)
+                    if (bb0 + bb < bb1) load_blk(src, ok, bb0 + bb, yr + 16 * bb);
+            }
+            for (int c = 0; c < A.nch; ++c, ++k) {
+                const int e = k & 1;
+                BD_WAIT(26, bar_wait(&acc_full[e], (k >> 1) & 1));
+                tcg::fence_after();
+                BD_T0(t_z);
+                uint32_t zr[32];
+#pragma unroll
+                for (int h16 = 0; h16 < 2; ++h16) {
                     uint32_t r[16];
-                    tm_ld16(tmem + lane_base + (uint32_t)(C::TZ + zb * KA + cs * ZH + 16 * h16), r);
+                    tm_ld16(tmem + lane_base + (uint32_t)(C::TZ + e * kKA + cs * 32 + 16 * h16), r);
                     tm_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) zr[16 * h16 + e] = r[e];
+                    for (int x = 0; x < 16; ++x) zr[16 * h16 + x] = r[x];
                 }
+                BD_ACC(27, t_z);
                 tcg::fence_before();
-                if (k >= 2) bar_wait(&z_empty[zb], ((k >> 1) - 1) & 1);
-                const uint32_t za = sa(Zt) + (uint32_t)(zb * C::ZBytes) + 4u * (uint32_t)(row * C::ZS + cs * ZH);
+                if (k >= 2) BD_WAIT(28, bar_wait(&z_empty[e], ((k >> 1) - 1) & 1));
+                BD_T0(t_zs);
+                const uint32_t za = Zs + (uint32_t)(e * C::ZBytes) + 4u * (uint32_t)(row * kCS + cs * 32);
 #pragma unroll
-                for (int i4 = 0; i4 < ZH / 4; ++i4)
-                    sts_f4(za + 16u * i4, make_float4(__uint_as_float(zr[4 * i4]), __uint_as_float(zr[4 * i4 + 1]),
-                                                      __uint_as_float(zr[4 * i4 + 2]), __uint_as_float(zr[4 * i4 + 3])));
+                for (int i4 = 0; i4 < 8; ++i4)
+                    sts_f4(za + 16u * i4, make_float4(__uint_as_float(zr[4 * i4]) * zinv,
+                                                      __uint_as_float(zr[4 * i4 + 1]) * zinv,
+                                                      __uint_as_float(zr[4 * i4 + 2]) * zinv,
+                                                      __uint_as_float(zr[4 * i4 + 3]) * zinv));
+                BD_ACC(29, t_zs);
                 __syncwarp();
                 if (lane == 0) {
-                    bar_arrive(&acc_empty[zb]);
-                    bar_arrive(&z_full[zb]);
+                    bar_arrive(&acc_empty[e]);
+                    bar_arrive(&z_full[e]);
                 }
             }
         }
     }
+    BD_FLUSH;
     tcg::fence_before();
     __syncthreads();
     if (warp == C::kMma) {
@@ -1841,90 +1982,74 @@ using namespace bin;
 
 constexpr int kSmemMax = 232448 - 2048;  // opt-in dynamic limit minus static + alignment slack
 
-template <int N, int KA>
-int dsc_slot_cap()
-{
-    using C = DscCfg<N, KA>;
-    const long avail = (long)kSmemMax - 2L * C::DB - C::CBytes;
-    return (int)std::min(16384L, std::max(0L, avail / (kSlots * 6L) / 32 * 32));
-}
-template <int N, int KA>
-int wc_slot_cap()
-{
-    using C = WcCfg<N, KA>;
-    const long avail = (long)kSmemMax - 2L * C::DB - 2L * C::ZBytes;
-    return (int)std::min(32768L, std::max(0L, avail / (kSlots * 2L) / 8 * 8));
-}
-
 SideArgs side_args(const life_phi *phi)
 {
     return SideArgs{phi->b_vid, phi->b_val, phi->b_segsrc, phi->b_segdst, phi->b_binptr, phi->b_ctaseg,
                     phi->b_vf2f, phi->b_nvf, phi->b_nbins};
 }
 
-template <int N, int KA>
+template <int N>
 int prep_t(life_phi *phi)
 {
-    using CD = DscCfg<N, KA>;
-    using CW = WcCfg<N, KA>;
-    phi->b_slot_dsc = dsc_slot_cap<N, KA>();
-    phi->b_slot_wc = wc_slot_cap<N, KA>();
-    if (phi->b_slot_dsc < 1024 || phi->b_slot_wc < 1024)
-        return fail(LIFE_ERR_CONFIG_INVALID, "bin layout: staging slots do not fit");
-    phi->b_dsc_smem = 1024 + 2 * (size_t)CD::DB + CD::CBytes + (size_t)kSlots * 6 * phi->b_slot_dsc;
-    phi->b_wc_smem = 1024 + 2 * (size_t)CW::DB + 2 * (size_t)CW::ZBytes + (size_t)kSlots * 2 * phi->b_slot_wc;
+    using CD = DscCfg<N>;
+    using CW = WcCfg<N>;
+    phi->b_dsc_smem = 1024 + 2 * (size_t)CD::DB + CD::CBytes;
+    phi->b_wc_smem = 1024 + 2 * (size_t)CW::DB + 2 * (size_t)CW::ZBytes;
+    if (phi->b_dsc_smem > (size_t)kSmemMax || phi->b_wc_smem > (size_t)kSmemMax)
+        return fail(LIFE_ERR_CONFIG_INVALID, "bin layout: shared memory does not fit");
     phi->b_side_smem = (size_t)kSB * 4;
     phi->b_wcs_smem = (size_t)kSB * 8;
-    LIFE_TRY(ensure_smem(k_tile_dsc<N, KA>, phi->b_dsc_smem));
-    LIFE_TRY(ensure_smem(k_tile_wc<N, KA>, phi->b_wc_smem));
+    LIFE_TRY(ensure_smem(k_tile_dsc<N>, phi->b_dsc_smem));
+    LIFE_TRY(ensure_smem(k_tile_wc<N>, phi->b_wc_smem));
     LIFE_TRY(ensure_smem(k_side_dsc, phi->b_side_smem));
     LIFE_TRY(ensure_smem(k_side_wc, phi->b_wcs_smem));
     return LIFE_OK;
 }
 
-template <int N, int KA>
+template <int N>
 int dsc_t(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags, const DscOut &o,
           const CallHooks &h, cudaStream_t st)
 {
-    using CD = DscCfg<N, KA>;
+    using CD = DscCfg<N>;
     k_side_dsc<<<phi->b_side_grid, kSideWarps * 32, phi->b_side_smem, st>>>(
-        side_args(phi), w, phi->b_scr, (flags & LIFE_SKIP_ZERO) ? 1 : 0, phi->b_skip, phi->b_smax, h);
+        side_args(phi), w, phi->b_scr, (flags & LIFE_SKIP_ZERO) ? 1 : 0, phi->b_skip, phi->b_smax, phi->b_nonfin, h);
     LIFE_CHECK_LAUNCH();
     const TileArgs A{phi->b_cellr, phi->b_step, phi->b_Ddsc, phi->b_rowvox, phi->b_rowpart, phi->b_ypart,
-                     phi->b_ntiles, phi->b_nch, phi->nt, phi->b_slot_dsc};
+                     phi->b_ntiles, phi->b_nch, phi->nt};
     const int fin = phi->b_nfix == 0 ? 1 : 0;
-    k_tile_dsc<N, KA><<<phi->b_tile_grid, CD::kThreads, phi->b_dsc_smem, st>>>(
-        A, phi->b_scr, y, b, flags, phi->red, o, h, phi->b_skip, phi->b_side_grid, phi->b_smax, phi->b_side_grid, fin);
+    k_tile_dsc<N><<<phi->b_tile_grid, CD::kThreads, phi->b_dsc_smem, st>>>(
+        A, phi->b_scr, y, b, flags, phi->red, o, h, phi->b_skip, phi->b_side_grid, phi->b_smax, phi->b_side_grid,
+        phi->b_nonfin, fin);
     LIFE_CHECK_LAUNCH();
     if (!fin) {
         const int blocks = std::max(1, std::min(phi->sms, (phi->b_nfix + 7) / 8));
         k_tile_dsc_fix<N><<<blocks, 256, 0, st>>>(phi->b_fixptr, phi->b_fixvox, phi->b_nfix, phi->b_ypart, phi->nt,
                                                   y, b, flags, phi->red, phi->b_tile_grid * CD::kWarps, o, h,
-                                                  phi->b_skip, phi->b_side_grid);
+                                                  phi->b_skip, phi->b_side_grid, phi->b_nonfin);
         LIFE_CHECK_LAUNCH();
     }
     return LIFE_OK;
 }
 
-template <int N, int KA>
-int wc_tile_t(life_phi *phi, const float *y, const CallHooks &h, cudaStream_t st)
+template <int N>
+int wc_tile_t(life_phi *phi, const float *y, const FixParams &fx, const CallHooks &h, cudaStream_t st)
 {
-    using CW = WcCfg<N, KA>;
+    using CW = WcCfg<N>;
     const TileArgs A{phi->b_cellr, phi->b_step, phi->b_Dwc, phi->b_rowvox, phi->b_rowpart, phi->b_ypart,
-                     phi->b_ntiles, phi->b_nch, phi->nt, phi->b_slot_wc};
-    k_tile_wc<N, KA><<<phi->b_tile_grid, CW::kThreads, phi->b_wc_smem, st>>>(A, y, phi->b_scr, h);
+                     phi->b_ntiles, phi->b_nch, phi->nt};
+    k_tile_wc<N><<<phi->b_tile_grid, CW::kThreads, phi->b_wc_smem, st>>>(A, y, phi->b_scr, fx.ymax, fx.ysumsq, h);
     LIFE_CHECK_LAUNCH();
     return LIFE_OK;
 }
 
 #define LIFE_BIN_DISPATCH(FN, ...)                                             \
     switch (phi->b_n) {                                                        \
-    case 32: return FN<32, 64>(__VA_ARGS__);                                   \
-    case 64: return FN<64, 64>(__VA_ARGS__);                                   \
-    case 96: return FN<96, 64>(__VA_ARGS__);                                   \
-    case 128: return FN<128, 64>(__VA_ARGS__);                                 \
-    case 160: return FN<160, 32>(__VA_ARGS__);                                 \
-    case 192: return FN<192, 32>(__VA_ARGS__);                                 \
+    case 32: return FN<32>(__VA_ARGS__);                                       \
+    case 64: return FN<64>(__VA_ARGS__);                                       \
+    case 96: return FN<96>(__VA_ARGS__);                                       \
+    case 128: return FN<128>(__VA_ARGS__);                                     \
+    case 160: return FN<160>(__VA_ARGS__);                                     \
+    case 192: return FN<192>(__VA_ARGS__);                                     \
     default: return fail(LIFE_ERR_CONFIG_INVALID, "bin layout: unsupported n_dirs"); \
     }
 
@@ -1935,9 +2060,9 @@ int prepare_bin(life_phi *phi) { LIFE_BIN_DISPATCH(prep_t, phi); }
 int bin_tile_warps(const life_phi *phi)
 {
     switch (phi->b_n) {
-    case 32: case 64: return DscCfg<64, 64>::kWarps;
-    case 96: case 128: return DscCfg<128, 64>::kWarps;
-    default: return DscCfg<192, 32>::kWarps;
+    case 32: case 64: return DscCfg<64>::kWarps;
+    case 96: case 128: return DscCfg<128>::kWarps;
+    default: return DscCfg<192>::kWarps;
     }
 }
 
@@ -1947,15 +2072,15 @@ int launch_dsc_bin(life_phi *phi, const float *w, float *y, const float *b, uint
     LIFE_BIN_DISPATCH(dsc_t, phi, w, y, b, flags, o, h, st);
 }
 
-static int wc_tile(life_phi *phi, const float *y, const CallHooks &h, cudaStream_t st)
+static int wc_tile(life_phi *phi, const float *y, const FixParams &fx, const CallHooks &h, cudaStream_t st)
 {
-    LIFE_BIN_DISPATCH(wc_tile_t, phi, y, h, st);
+    LIFE_BIN_DISPATCH(wc_tile_t, phi, y, fx, h, st);
 }
 
 int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, const FixParams &fx, uint32_t flags,
                   double *sumsq, const CallHooks &h, const life_comm *comm, cudaStream_t st)
 {
-    LIFE_TRY(wc_tile(phi, y, h, st));
+    LIFE_TRY(wc_tile(phi, y, fx, h, st));
     k_side_wc<<<phi->b_side_grid, kSideWarps * 32, phi->b_wcs_smem, st>>>(side_args(phi), phi->b_scr, fx, phi->nt,
                                                                           phi->b_wfix, phi->b_nanf, h);
     LIFE_CHECK_LAUNCH();
@@ -1979,3 +2104,23 @@ int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, c
 }
 
 }  // namespace life
+
+#ifdef LIFE_BIN_DIAG
+extern "C" LIFE_API int life_debug_bin(unsigned long long *cyc_out)
+{
+    if (cudaDeviceSynchronize() != cudaSuccess) return 20;
+    if (cyc_out && cudaMemcpyFromSymbol(cyc_out, life::bin::g_bin_cyc, 32 * sizeof(unsigned long long)) != cudaSuccess)
+        return 20;
+    unsigned long long z[32] = {};
+    return cudaMemcpyToSymbol(life::bin::g_bin_cyc, z, sizeof(z)) == cudaSuccess ? 0 : 20;
+}
+#endif
+
+// Debugging aid: register a host-mapped u32[8] that receives (1, block, warp,
+// shared address, parity) of the first mbarrier wait that times out.
+extern "C" LIFE_API int life_debug_timeout(unsigned *host_mapped)
+{
+    unsigned *dptr = nullptr;
+    if (host_mapped && cudaHostGetDevicePointer((void **)&dptr, host_mapped, 0) != cudaSuccess) return 20;
+    return cudaMemcpyToSymbol(life::bin::g_timeout_rec, &dptr, sizeof(dptr)) == cudaSuccess ? 0 : 20;
+}

@@ -138,7 +138,7 @@ struct life_phi {
     // tile-major scratch vector (s = w[f]*value for DSC, z = (Y D^T)[cell]
     // for WC) through contiguous segments (tile, chunk, bin).
     bool has_bin = false;
-    int b_ka = 0, b_n = 0, b_nch = 0, b_ntiles = 0, b_nbins = 0, b_sb = 0, b_cellbits = 0;
+    int b_ka = 0, b_n = 0, b_nch = 0, b_ntiles = 0, b_nbins = 0, b_sb = 0;
     int64_t b_nvf = 0, b_nsteps = 0, b_nseg = 0, b_npad = 0;
     uint16_t *b_cellr = nullptr;   // tile-major [npad]: rank << cellbits | row*KA + atom%KA
     uint16_t *b_vid = nullptr;     // bin-major [nc]: virtual fascicle slot within its bin
@@ -153,8 +153,8 @@ struct life_phi {
     uint32_t *b_f2vf = nullptr;    // [nf + 1] first virtual slot of each fascicle
     int *b_rowvox = nullptr;       // [ntiles*128] voxel of each tile row, -1 = empty
     int *b_rowpart = nullptr;      // [ntiles*128] partial-row index, -1 = the voxel's only row
-    float *b_Ddsc = nullptr;       // per chunk: [hi|lo][KA/32][N][32] swizzled D^T (DSC B operand)
-    float *b_Dwc = nullptr;        // per chunk: [hi|lo][N/32][KA][32] swizzled D (WC B operand)
+    uint16_t *b_Ddsc = nullptr;    // per chunk: f16 [hi|lo][N][64 atoms] swizzled D^T * 256 (DSC B operand)
+    uint16_t *b_Dwc = nullptr;     // per chunk: f16 [hi|lo][N/64][64 atoms][64] swizzled D * 256 (WC B operand)
     float *b_ypart = nullptr;      // [nprow * N] rows of voxels split over several rows
     uint32_t *b_fixptr = nullptr;  // [nfix + 1] partial rows of each split voxel
     int *b_fixvox = nullptr;       // [nfix]
@@ -164,7 +164,8 @@ struct life_phi {
     unsigned long long *b_wsum = nullptr;  // [nf] per-fascicle sums for multi-GPU reduction
     unsigned long long *b_skip = nullptr;  // [side grid] skip-count partials of the bin side
     float *b_smax = nullptr;               // [side grid] max |s| partials (DSC fixed-point scale)
-    int b_tile_grid = 0, b_side_grid = 0, b_slot_dsc = 0, b_slot_wc = 0;
+    unsigned *b_nonfin = nullptr;          // non-finite s seen by the DSC bin side (this call)
+    int b_tile_grid = 0, b_side_grid = 0;
     size_t b_dsc_smem = 0, b_wc_smem = 0, b_side_smem = 0, b_wcs_smem = 0;
 
     // fixed-point WC accumulator and its scale inputs
