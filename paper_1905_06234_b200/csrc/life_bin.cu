@@ -53,6 +53,7 @@ constexpr int kBuild = 8;           // builder / gatherer warps of the tile kern
 constexpr int kSideWarps = 32;      // bin-side CTA
 constexpr int kSideU = 4;           // 32-entry chunks per warp batch on the bin side
 constexpr int kSlots = 3;           // staged steps per tile kernel
+constexpr int kCH = 1024;           // 4-entry units per bin-side chunk
 
 // Role timing, compiled in only with -DLIFE_BIN_DIAG (tools/bin_roles.py):
 // clock64 spans per category summed over warps (lane 0) into g_bin_cyc.
@@ -803,9 +804,53 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     k_bin_seg<<<gridn(nbins + 1), 256, 0, st>>>(segkey, nseg, nbins, per_bin, phi->b_binptr);
     LIFE_CHECK_LAUNCH();
     const int side_grid = phi->sms;
-    LIFE_TRY(dalloc(phi, &phi->b_ctaseg, (size_t)side_grid + 1));
-    k_cta_seg<<<gridn(side_grid + 1), 256, 0, st>>>(phi->b_segsrc, nseg, side_grid, phi->b_ctaseg);
-    LIFE_CHECK_LAUNCH();
+    {   // bin-side chunks: per CTA (balanced by units, cut at segment ends),
+        // per bin piece, at most kCH units each
+        uint32_t *dcs;
+        LIFE_TRY(talloc((void **)&dcs, ((size_t)side_grid + 1) * 4));
+        k_cta_seg<<<gridn(side_grid + 1), 256, 0, st>>>(phi->b_segsrc, nseg, side_grid, dcs);
+        LIFE_CHECK_LAUNCH();
+        std::vector<uint32_t> hsrc((size_t)nseg + 1), hbin((size_t)nbins + 1), hcta((size_t)side_grid + 1);
+        LIFE_CUDA(cudaMemcpyAsync(hsrc.data(), phi->b_segsrc, hsrc.size() * 4, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaMemcpyAsync(hbin.data(), phi->b_binptr, hbin.size() * 4, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaMemcpyAsync(hcta.data(), dcs, hcta.size() * 4, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        std::vector<uint32_t> chunks, ctachunk(1, 0);
+        int b = 0;
+        for (int c = 0; c < side_grid; ++c) {
+            const uint32_t S0 = hcta[c], S1 = hcta[c + 1];
+            uint32_t s = S0;
+            while (b < nbins && hbin[b + 1] <= S0) ++b;
+            int bb = b;
+            while (s < S1) {
+                while (bb < nbins && hbin[bb + 1] <= s) ++bb;
+                const uint32_t pe = std::min(S1, hbin[bb + 1]);
+                const uint32_t pu0 = hsrc[s], pu1 = hsrc[pe];
+                uint32_t sl = s;  // segment containing the chunk start
+                bool first = true;
+                for (uint32_t u0 = pu0; u0 < pu1; u0 += (uint32_t)kCH) {
+                    const uint32_t u1 = std::min(pu1, u0 + (uint32_t)kCH);
+                    while (hsrc[sl + 1] <= u0) ++sl;
+                    uint32_t sh = sl;  // segment containing u1 - 1
+                    while (hsrc[sh + 1] < u1) ++sh;
+                    const uint32_t ns = sh - sl + 1;
+                    chunks.push_back(u0);
+                    chunks.push_back((u1 - u0) | (first ? 0x80000000u : 0u));
+                    chunks.push_back(sl);
+                    chunks.push_back(ns | ((uint32_t)bb << 16));
+                    first = false;
+                }
+                s = pe;
+            }
+            ctachunk.push_back((uint32_t)(chunks.size() / 4));
+        }
+        if (chunks.empty()) chunks.assign(4, 0u);
+        LIFE_TRY(dalloc(phi, &phi->b_chunks, chunks.size()));
+        LIFE_TRY(dalloc(phi, &phi->b_ctachunk, ctachunk.size()));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_chunks, chunks.data(), chunks.size() * 4, cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_ctachunk, ctachunk.data(), ctachunk.size() * 4, cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+    }
 
     // 8. dictionary chunks as the two B operands: f16 hi | lo of D * kDScale,
     // K-major SWIZZLE_128B (64 f16 per 128-byte row)
@@ -881,7 +926,6 @@ struct SideArgs {
     const uint32_t *src4;    // [nseg + 1] bin-major segment starts, 4-entry units
     const uint32_t *dst4;    // [nseg] tile-major segment starts, 4-entry units
     const uint32_t *binseg;  // [nbins + 1] first segment of each bin
-    const uint32_t *ctaseg;  // [grid + 1] first segment of each CTA
     const uint32_t *vf2f;    // [nvf]
     int64_t nvf;
     int nbins;
@@ -939,77 +983,156 @@ __device__ __forceinline__ int find_bin(const uint32_t *binseg, int nbins, uint3
     return lo;
 }
 
-// DSC bin side: scr[tile-major] = s = w[f] * value, exact skip count (fp32
-// s == 0, _kernels.py:24-28)
-__global__ void __launch_bounds__(kSideWarps * 32, 1)
-    k_side_dsc(const SideArgs A, const float *__restrict__ w, float *__restrict__ scr, int count_skips,
-               unsigned long long *__restrict__ skip_part, float *__restrict__ smax_part, unsigned *__restrict__ nonfinite,
-               const CallHooks hooks)
+// Bin side, streamed: the CTA's bin-major range is cut (at build time) into
+// chunks of at most kCH 4-entry units inside one bin; a producer warp stages
+// each chunk's ids, values and segment records into a shared-memory ring with
+// bulk copies (kNS in flight), so memory traffic is decoupled from the
+// consumers' per-entry work.  Chunk descriptor (uint4): x = first unit, y =
+// units | first-of-piece << 31, z = first segment, w = segments | bin << 16.
+constexpr int kSideThreads = 1024;        // warp 0 produces, warps 1..31 consume
+constexpr int kCons = kSideThreads - 32;
+// slot regions (16-byte aligned bulk-copy destinations; each holds its range
+// plus the alignment slack of an unaligned global start)
+constexpr uint32_t kSlotVid = 0, kSlotVal = (kCH * 8 + 16 + 15) / 16 * 16, kSlotSrc = kSlotVal + kCH * 16,
+                   kSlotDst = kSlotSrc + ((kCH + 2) * 4 + 16 + 15) / 16 * 16,
+                   kSlotBytes = (kSlotDst + (kCH + 1) * 4 + 16 + 127) / 128 * 128;
+constexpr int kNsDsc = 4, kNsWc = 3;
+
+struct ChunkArgs {
+    const uint4 *chunks;      // chunk descriptors
+    const uint32_t *ctachunk; // [grid + 1]
+};
+
+// producer: stage chunk j of the CTA into slot j % NS (header: byte offsets of
+// the unaligned starts)
+template <int NS, int CAT>
+__device__ __forceinline__ void side_produce(const SideArgs &A, const uint4 *tab, int nch, unsigned char *ring,
+                                             uint4 (*hdr)[2], uint64_t *full, uint64_t *empty)
 {
-    extern __shared__ float ws[];  // kSB
-    __shared__ uint32_t s_ctr;
+    BD_DECL;
+    const uint64_t pol = pol_first();
+    uint4 cn = nch > 0 ? __ldg(tab) : make_uint4(0, 0, 0, 0), cnn = nch > 1 ? __ldg(tab + 1) : cn;
+    for (int j = 0; j < nch; ++j) {
+        const int sl = j % NS;
+        const uint4 c = cn;  // descriptors prefetched two chunks ahead
+        cn = cnn;
+        if (j + 2 < nch) cnn = __ldg(tab + j + 2);
+        if (j >= NS) BD_WAIT(CAT, bar_wait(&empty[sl], ((j / NS) - 1) & 1));
+        const uint32_t u0 = c.x, nu = c.y & 0x7FFFFFFFu, s0 = c.z, ns = c.w & 0xFFFFu;
+        unsigned char *slot = ring + (size_t)sl * kSlotBytes;
+        const uint64_t vb0 = 8ull * u0, vb1 = 8ull * (u0 + nu);
+        const uint64_t va = vb0 & ~15ull, vz = (vb1 + 15) & ~15ull;
+        const uint64_t sb0 = 4ull * s0, sb1 = 4ull * (s0 + ns + 1);
+        const uint64_t sa0 = sb0 & ~15ull, sz = (sb1 + 15) & ~15ull;
+        const uint64_t db1 = 4ull * (s0 + ns);
+        const uint64_t dz = (db1 + 15) & ~15ull;
+        hdr[sl][0] = c;  // the descriptor and the byte offsets of the unaligned starts
+        hdr[sl][1] = make_uint4((uint32_t)(vb0 - va), (uint32_t)(sb0 - sa0), 0u, 0u);
+        const unsigned bytes = (unsigned)((vz - va) + 16ull * nu + (sz - sa0) + (dz - sa0));
+        bar_arrive_tx(&full[sl], bytes);
+        bulk_g2s(slot + kSlotVid, reinterpret_cast<const unsigned char *>(A.vid) + va, (unsigned)(vz - va), &full[sl], pol);
+        bulk_g2s(slot + kSlotVal, reinterpret_cast<const unsigned char *>(A.val) + 16ull * u0, 16u * nu, &full[sl], pol);
+        bulk_g2s(slot + kSlotSrc, reinterpret_cast<const unsigned char *>(A.src4) + sa0, (unsigned)(sz - sa0), &full[sl], pol);
+        bulk_g2s(slot + kSlotDst, reinterpret_cast<const unsigned char *>(A.dst4) + sa0, (unsigned)(dz - sa0), &full[sl], pol);
+    }
+    BD_FLUSH;
+}
+
+// consumer: tile-major unit of chunk unit u (staged segment records)
+__device__ __forceinline__ uint32_t side_dst(uint32_t slot_sa, uint32_t hs, uint32_t u0, uint32_t ns, uint32_t u)
+{
+    const uint32_t U = u0 + u;
+    const uint32_t src = slot_sa + kSlotSrc + hs, dst = slot_sa + kSlotDst + hs;
+    uint32_t lo = 0, hi = ns;  // largest i < ns with src4[i] <= U
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(src + 4u * mid));
+        if (v <= U) lo = mid; else hi = mid;
+    }
+    uint32_t s0, d0;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s0) : "r"(src + 4u * lo));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d0) : "r"(dst + 4u * lo));
+    return d0 + (U - s0);
+}
+
+// DSC bin side: scr[tile-major] = s = w[f] * value, exact skip count (fp32
+// s == 0, _kernels.py:24-28), max |s| and a non-finite flag
+__global__ void __launch_bounds__(kSideThreads, 1)
+    k_side_dsc(const SideArgs A, const ChunkArgs CA, const float *__restrict__ w, float *__restrict__ scr,
+               int count_skips, unsigned long long *__restrict__ skip_part, float *__restrict__ smax_part,
+               unsigned *__restrict__ nonfinite, const CallHooks hooks)
+{
+    extern __shared__ __align__(128) unsigned char side_sm[];
+    __shared__ __align__(8) uint64_t full[kNsDsc], empty[kNsDsc];
+    __shared__ uint4 hdr[kNsDsc][2];
     if (hooks.done && *hooks.done) return;
     if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
+    float *ws = reinterpret_cast<float *>(side_sm);  // kSB
+    unsigned char *ring = side_sm + kSB * 4;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t S0 = __ldg(A.ctaseg + blockIdx.x), S1 = __ldg(A.ctaseg + blockIdx.x + 1);
+    const int c0 = (int)__ldg(CA.ctachunk + blockIdx.x), nch = (int)__ldg(CA.ctachunk + blockIdx.x + 1) - c0;
+    const uint4 *tab = CA.chunks + c0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kNsDsc; ++i) {
+            bar_init(&full[i], 1);
+            bar_init(&empty[i], kCons / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     unsigned long long zeros = 0;
     float smax = 0.f;
     bool nonfin = false;
-    int b = S0 < S1 ? find_bin(A.binseg, A.nbins, S0) : A.nbins;
-    for (uint32_t s = S0; s < S1; ++b) {
-        const uint32_t pe = min(S1, __ldg(A.binseg + b + 1));
-        if (pe <= s) continue;
-        const int64_t s0 = (int64_t)b * kSB;
-        const int ns = (int)min((int64_t)kSB, A.nvf - s0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < ns; i += blockDim.x) ws[i] = __ldg(w + __ldg(A.vf2f + s0 + i));
-        if (threadIdx.x == 0) s_ctr = 0;
-        __syncthreads();
-        for (;;) {
-            uint32_t gi = 0;
-            if (lane == 0) gi = atomicAdd(&s_ctr, 1u);
-            const uint32_t gs = s + 32u * __shfl_sync(0xffffffffu, gi, 0);
-            if (gs >= pe) break;
-            const Group g = load_group(A, gs, pe, lane);
-            for (uint32_t u0 = 0; u0 < g.tot; u0 += 32u * kSideUN) {
-                uint32_t su[kSideUN], du[kSideUN];
-                uint2 id[kSideUN];
-                float4 vv[kSideUN];
-#pragma unroll
-                for (int k = 0; k < kSideUN; ++k) {
-                    const uint32_t u = u0 + 32u * k + (uint32_t)lane;
-                    unit_of(g, min(u, g.tot - 1), su[k], du[k]);
-                    if (u < g.tot) {
-                        id[k] = __ldcs(reinterpret_cast<const uint2 *>(A.vid) + su[k]);
-                        vv[k] = __ldcs(reinterpret_cast<const float4 *>(A.val) + su[k]);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < kSideUN; ++k) {
-                    if (u0 + 32u * k + (uint32_t)lane >= g.tot) continue;
-                    const uint32_t ids[4] = {id[k].x & 0xFFFFu, id[k].x >> 16, id[k].y & 0xFFFFu, id[k].y >> 16};
-                    const float vs[4] = {vv[k].x, vv[k].y, vv[k].z, vv[k].w};
-                    float o[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const bool pad = ids[e] == kPad;
-                        o[e] = pad ? 0.f : __fmul_rn(ws[pad ? 0 : ids[e]], vs[e]);
-                        zeros += (!pad && o[e] == 0.f) ? 1ull : 0ull;
-                        if (isfinite(o[e])) smax = fmaxf(smax, fabsf(o[e]));
-                        else nonfin = true;
-                    }
-                    reinterpret_cast<float4 *>(scr)[du[k]] = make_float4(o[0], o[1], o[2], o[3]);
-                }
+    if (warp == 0) {
+        if (lane == 0) side_produce<kNsDsc, 15>(A, tab, nch, ring, hdr, full, empty);
+    } else {
+        const uint32_t ct = threadIdx.x - 32;
+        BD_DECL;
+        for (int j = 0; j < nch; ++j) {
+            const int sl = j % kNsDsc;
+            BD_WAIT(13, bar_wait(&full[sl], (j / kNsDsc) & 1));
+            BD_T0(t_p);
+            const uint4 c = hdr[sl][0];
+            const uint32_t u0 = c.x, nu = c.y & 0x7FFFFFFFu, ns = c.w & 0xFFFFu;
+            if (c.y >> 31) {  // a new bin: its w slice into shared memory
+                const int64_t s0 = (int64_t)(c.w >> 16) * kSB;
+                const int nsl = (int)min((int64_t)kSB, A.nvf - s0);
+                named_bar(1, kCons);
+                for (int i = ct; i < nsl; i += kCons) ws[i] = __ldg(w + __ldg(A.vf2f + s0 + i));
+                named_bar(1, kCons);
             }
+            const uint32_t slot_sa = sa(ring) + (uint32_t)sl * kSlotBytes;
+            const uint32_t hv = hdr[sl][1].x, hs = hdr[sl][1].y;
+            for (uint32_t u = ct; u < nu; u += kCons) {
+                const uint32_t du = side_dst(slot_sa, hs, u0, ns, u);
+                uint2 id;
+                asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(id.x), "=r"(id.y) : "r"(slot_sa + kSlotVid + hv + 8u * u));
+                const float4 vv = lds_f4(slot_sa + kSlotVal + 16u * u);
+                const uint32_t ids[4] = {id.x & 0xFFFFu, id.x >> 16, id.y & 0xFFFFu, id.y >> 16};
+                const float vs[4] = {vv.x, vv.y, vv.z, vv.w};
+                float o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const bool pad = ids[e] == kPad;
+                    o[e] = pad ? 0.f : __fmul_rn(ws[pad ? 0 : ids[e]], vs[e]);
+                    zeros += (!pad && o[e] == 0.f) ? 1ull : 0ull;
+                    if (isfinite(o[e])) smax = fmaxf(smax, fabsf(o[e]));
+                    else nonfin = true;
+                }
+                reinterpret_cast<float4 *>(scr)[du] = make_float4(o[0], o[1], o[2], o[3]);
+            }
+            BD_ACC(14, t_p);
+            __syncwarp();
+            if (lane == 0) bar_arrive(&empty[sl]);
         }
-        s = pe;
+        BD_FLUSH;
     }
-    // per-CTA skip count (fixed-order total in the tile kernel's last CTA)
     // this call's non-finite flag (read by the tile kernel, cleared by the
-    // CTA that finishes the call)
+    // CTA that finishes the call); per-CTA skip count and max |s|
     if (__any_sync(0xffffffffu, nonfin) && lane == 0) atomicAdd(nonfinite, 1u);
-    __shared__ unsigned long long sz[kSideWarps];
-    __shared__ float sm[kSideWarps];
+    __shared__ unsigned long long sz[32];
+    __shared__ float smx[32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         zeros += __shfl_xor_sync(0xffffffffu, zeros, o);
@@ -1017,15 +1140,15 @@ __global__ void __launch_bounds__(kSideWarps * 32, 1)
     }
     if (lane == 0) {
         sz[warp] = zeros;
-        sm[warp] = smax;
+        smx[warp] = smax;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long t = 0;
         float m = 0.f;
-        for (int i = 0; i < kSideWarps; ++i) {
+        for (int i = 0; i < 32; ++i) {
             t += sz[i];
-            m = fmaxf(m, sm[i]);
+            m = fmaxf(m, smx[i]);
         }
         skip_part[blockIdx.x] = count_skips ? t : 0ull;
         smax_part[blockIdx.x] = m;
@@ -1035,79 +1158,113 @@ __global__ void __launch_bounds__(kSideWarps * 32, 1)
 // WC bin side: fascicle sums of value * z in 64-bit fixed point, two 32-bit
 // limbs per virtual slot in shared memory (native u32 atomics: order
 // independent, exact), flushed per bin piece into wfix (int64 atomics, also
-// exact).
-__global__ void __launch_bounds__(kSideWarps * 32, 1)
-    k_side_wc(const SideArgs A, const float *__restrict__ scr, const FixParams fx, int nt,
+// exact).  The consumers load the next chunk's z (tile-major scratch) while
+// accumulating the current one.
+__global__ void __launch_bounds__(kSideThreads, 1)
+    k_side_wc(const SideArgs A, const ChunkArgs CA, const float *__restrict__ scr, const FixParams fx, int nt,
               unsigned long long *__restrict__ wfix, unsigned char *__restrict__ nanf, const CallHooks hooks)
 {
-    extern __shared__ uint32_t limbs[];  // lo[kSB], hi[kSB]
-    __shared__ uint32_t s_ctr;
+    extern __shared__ __align__(128) unsigned char side_sm[];
+    __shared__ __align__(8) uint64_t full[kNsWc], empty[kNsWc];
+    __shared__ uint4 hdr[kNsWc][2];
     if (hooks.done && *hooks.done) return;
-    uint32_t *lo = limbs, *hi = limbs + kSB;
-    const int lane = threadIdx.x & 31;
+    uint32_t *lo = reinterpret_cast<uint32_t *>(side_sm), *hi = lo + kSB;
+    unsigned char *ring = side_sm + kSB * 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c0 = (int)__ldg(CA.ctachunk + blockIdx.x), nch = (int)__ldg(CA.ctachunk + blockIdx.x + 1) - c0;
+    const uint4 *tab = CA.chunks + c0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kNsWc; ++i) {
+            bar_init(&full[i], 1);
+            bar_init(&empty[i], kCons / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) side_produce<kNsWc, 31>(A, tab, nch, ring, hdr, full, empty);
+        return;
+    }
+    const uint32_t ct = threadIdx.x - 32;
     const double scale = ldexp(1.0, bin_exponent_dev(fx, nt));
-    const uint32_t S0 = __ldg(A.ctaseg + blockIdx.x), S1 = __ldg(A.ctaseg + blockIdx.x + 1);
-    int b = S0 < S1 ? find_bin(A.binseg, A.nbins, S0) : A.nbins;
-    for (uint32_t s = S0; s < S1; ++b) {
-        const uint32_t pe = min(S1, __ldg(A.binseg + b + 1));
-        if (pe <= s) continue;
-        const int64_t s0 = (int64_t)b * kSB;
-        const int ns = (int)min((int64_t)kSB, A.nvf - s0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < ns; i += blockDim.x) {
-            lo[i] = 0u;
-            hi[i] = 0u;
+    constexpr int UPT = (kCH + kCons - 1) / kCons;  // units per consumer thread per chunk
+    float4 zc[UPT], zn[UPT];
+    // z of chunk j (its records are staged) into z[]
+    BD_DECL;
+    auto load_z = [&](int j, float4 (&z)[UPT]) {
+        const int sl = j % kNsWc;
+        BD_WAIT(30, bar_wait(&full[sl], (j / kNsWc) & 1));
+        const uint4 c = hdr[sl][0];
+        const uint32_t u0 = c.x, nu = c.y & 0x7FFFFFFFu, ns = c.w & 0xFFFFu;
+        const uint32_t slot_sa = sa(ring) + (uint32_t)sl * kSlotBytes, hs = hdr[sl][1].y;
+#pragma unroll
+        for (int i = 0; i < UPT; ++i) {
+            const uint32_t u = ct + (uint32_t)(kCons * i);
+            if (u < nu) z[i] = __ldcs(reinterpret_cast<const float4 *>(scr) + side_dst(slot_sa, hs, u0, ns, u));
         }
-        if (threadIdx.x == 0) s_ctr = 0;
-        __syncthreads();
-        for (;;) {
-            uint32_t gi = 0;
-            if (lane == 0) gi = atomicAdd(&s_ctr, 1u);
-            const uint32_t gs = s + 32u * __shfl_sync(0xffffffffu, gi, 0);
-            if (gs >= pe) break;
-            const Group g = load_group(A, gs, pe, lane);
-            for (uint32_t u0 = 0; u0 < g.tot; u0 += 32u * kSideUN) {
-                uint32_t su[kSideUN], du[kSideUN];
-                uint2 id[kSideUN];
-                float4 vv[kSideUN], zz[kSideUN];
-#pragma unroll
-                for (int k = 0; k < kSideUN; ++k) {
-                    const uint32_t u = u0 + 32u * k + (uint32_t)lane;
-                    unit_of(g, min(u, g.tot - 1), su[k], du[k]);
-                    if (u < g.tot) {
-                        id[k] = __ldcs(reinterpret_cast<const uint2 *>(A.vid) + su[k]);
-                        vv[k] = __ldcs(reinterpret_cast<const float4 *>(A.val) + su[k]);
-                        zz[k] = __ldcs(reinterpret_cast<const float4 *>(scr) + du[k]);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < kSideUN; ++k) {
-                    if (u0 + 32u * k + (uint32_t)lane >= g.tot) continue;
-                    const uint32_t ids[4] = {id[k].x & 0xFFFFu, id[k].x >> 16, id[k].y & 0xFFFFu, id[k].y >> 16};
-                    const float vs[4] = {vv[k].x, vv[k].y, vv[k].z, vv[k].w};
-                    const float zs[4] = {zz[k].x, zz[k].y, zz[k].z, zz[k].w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        if (ids[e] == kPad) continue;
-                        const float t = __fmul_rn(zs[e], vs[e]);  // acc * value (_kernels.py:67)
-                        if (!isfinite(t)) {
-                            nanf[s0 + ids[e]] = 1;
-                            continue;
-                        }
-                        const long long q = __double2ll_rn((double)t * scale);
-                        atomicAdd(lo + ids[e], (uint32_t)q & 0xFFFFFFu);
-                        atomicAdd(hi + ids[e], (uint32_t)(int32_t)(q >> 24));
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+    };
+    int cur_bin = -1;
+    auto flush = [&]() {
+        const int64_t s0 = (int64_t)cur_bin * kSB;
+        const int nsl = (int)min((int64_t)kSB, A.nvf - s0);
+        for (int i = ct; i < nsl; i += kCons) {
             const long long v = (long long)(int32_t)hi[i] * 16777216ll + (long long)lo[i];
             if (v) atomicAdd(wfix + s0 + i, (unsigned long long)v);
         }
-        s = pe;
+    };
+    if (nch > 0) load_z(0, zn);
+    for (int j = 0; j < nch; ++j) {
+        const int sl = j % kNsWc;
+        const uint4 c = hdr[sl][0];  // chunk j is staged (load_z waited for it)
+        const uint32_t nu = c.y & 0x7FFFFFFFu;
+#pragma unroll
+        for (int i = 0; i < UPT; ++i) zc[i] = zn[i];
+        if (c.y >> 31) {  // a new bin: flush the previous one, clear the limbs
+            named_bar(1, kCons);
+            if (cur_bin >= 0) flush();
+            named_bar(1, kCons);
+            cur_bin = (int)(c.w >> 16);
+            const int nsl = (int)min((int64_t)kSB, A.nvf - (int64_t)cur_bin * kSB);
+            for (int i = ct; i < nsl; i += kCons) {
+                lo[i] = 0u;
+                hi[i] = 0u;
+            }
+            named_bar(1, kCons);
+        }
+        if (j + 1 < nch) load_z(j + 1, zn);  // next chunk's z, in flight meanwhile
+        BD_T0(t_p);
+        const uint32_t slot_sa = sa(ring) + (uint32_t)sl * kSlotBytes, hv = hdr[sl][1].x;
+        const int64_t s0 = (int64_t)cur_bin * kSB;
+#pragma unroll
+        for (int i = 0; i < UPT; ++i) {
+            const uint32_t u = ct + (uint32_t)(kCons * i);
+            if (u >= nu) continue;
+            uint2 id;
+            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(id.x), "=r"(id.y) : "r"(slot_sa + kSlotVid + hv + 8u * u));
+            const float4 vv = lds_f4(slot_sa + kSlotVal + 16u * u);
+            const uint32_t ids[4] = {id.x & 0xFFFFu, id.x >> 16, id.y & 0xFFFFu, id.y >> 16};
+            const float vs[4] = {vv.x, vv.y, vv.z, vv.w};
+            const float zs[4] = {zc[i].x, zc[i].y, zc[i].z, zc[i].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (ids[e] == kPad) continue;
+                const float t = __fmul_rn(zs[e], vs[e]);  // acc * value (_kernels.py:67)
+                if (!isfinite(t)) {
+                    nanf[s0 + ids[e]] = 1;
+                    continue;
+                }
+                const long long q = __double2ll_rn((double)t * scale);
+                atomicAdd(lo + ids[e], (uint32_t)q & 0xFFFFFFu);
+                atomicAdd(hi + ids[e], (uint32_t)(int32_t)(q >> 24));
+            }
+        }
+        BD_ACC(9, t_p);
+        __syncwarp();
+        if (lane == 0) bar_arrive(&empty[sl]);
     }
+    named_bar(1, kCons);
+    if (cur_bin >= 0) flush();
+    BD_FLUSH;
 }
 
 // WC finish: mode 0 = single GPU (fold virtual slots, convert, flags, sum of
@@ -1216,24 +1373,21 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t &hi, uint32_
 template <int N>
 struct DscCfg {
     static constexpr int EQ = (N + 63) / 64;   // epilogue warps per TMEM lane quarter
-    static constexpr int kProdD = kBuild;      // warpgroup 2: dictionary chunks, two MMA issuers, spare
-    static constexpr int kMma = kBuild + 1;    // two issuers: even / odd steps
-    static constexpr int kEpi = kBuild + 4;
+    static constexpr int kNB = 16;             // builder warps: two groups of 8 on alternating steps
+    static constexpr int kProdD = kNB;         // dictionary chunks
+    static constexpr int kMma = kNB + 1;       // two issuers: even / odd steps (= builder groups)
+    static constexpr int kProdS = kNB + 3;     // step entries into the groups' slots
+    static constexpr int kEpi = kNB + 4;
     static constexpr int kWarps = kEpi + 4 * EQ;
     static constexpr int kThreads = kWarps * 32;
-    // registers: warpgroup 2 hands what it releases to the two builder
-    // warpgroups (setmaxnreg; only released registers can be claimed)
-    static constexpr int kRegBase = (65536 / kThreads) / 8 * 8;
-    static constexpr int kRegLow = 56;
-    static constexpr int kRegBuild = kRegBase + (128 * (kRegBase - kRegLow) / 256) / 8 * 8 > 232
-                                         ? 232
-                                         : kRegBase + (128 * (kRegBase - kRegLow) / 256) / 8 * 8;
     static constexpr int DB = 2 * N * 128;     // one chunk: N rows x 64 f16, hi | lo
     static constexpr int CBytes = kTV * kCS * 4;
     static constexpr int NBLK = N / 16;
     static constexpr int MB = (NBLK + EQ - 1) / EQ;
-    static constexpr int TACC = 128;           // TMEM: A stage e at 64 e (hi 32 cols | lo 32), accumulator e at TACC + e N
-    static_assert(TACC + 2 * N <= 512, "TMEM budget");
+    static constexpr int TACC = 128;           // TMEM: A stage e at 64 e (hi 32 cols | lo 32), accumulators from TACC
+    static constexpr int NACC = TACC + 4 * N <= 512 ? 2 : 1;  // accumulator buffers per issuer
+    static constexpr int kSlotsG = 2;          // staged steps per builder group
+    static_assert(TACC + 2 * NACC * N <= 512, "TMEM budget");
 };
 
 template <int N>
@@ -1276,10 +1430,11 @@ struct StepIter {
 };
 
 // One step's entries, prefetched into registers one step ahead (4 per unit)
+constexpr int kUBld = 2;  // units per DSC builder thread prefetched (16 builder warps)
 struct StepRegs {
     uint32_t p0, n;
-    uint2 c[kUMax];
-    float4 s[kUMax];
+    uint2 c[kUBld];
+    float4 s[kUBld];
 };
 
 // DSC tile side.  Roles (warps):
@@ -1301,13 +1456,15 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
     k_tile_dsc(const TileArgs A, const float *__restrict__ scr, float *__restrict__ y, const float *__restrict__ b,
                const uint32_t flags, const ReduceSlots red, const DscOut out, const CallHooks hooks,
                const unsigned long long *__restrict__ skip_part, int nskip, const float *__restrict__ smax, int nsmax,
-               unsigned *__restrict__ nonfinite, int finalize)
+               unsigned *__restrict__ nonfinite, int finalize, int cap)
 {
     using C = DscCfg<N>;
     extern __shared__ __align__(1024) unsigned char smraw[];
-    __shared__ __align__(8) uint64_t d_full[2], d_empty[2], a_full[2], a_empty[2], acc_full[2], acc_empty[2];
+    __shared__ __align__(8) uint64_t d_full[2], d_empty[2], a_full[2], a_empty[2], acc_full[4], acc_empty[4],
+        slot_full[4], slot_empty[4];
+    __shared__ uint32_t s_hdr[4][2];  // staged step: tile-major start, entries
     __shared__ uint32_t tmem_base;
-    __shared__ uint32_t s_rowbad[2][4];  // rows with a non-finite s (slow path; per step parity)
+    __shared__ uint32_t s_rowbad[2][4];  // rows with a non-finite s (slow path; per builder group)
     __shared__ float s_scale[2];
     if (hooks.done && *hooks.done) return;
     BD_DECL;
@@ -1316,15 +1473,22 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
     const int my_tiles = (int)blockIdx.x < A.ntiles ? (A.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int total = my_tiles * A.nch;
     unsigned char *Dbuf = sm;
-    const uint32_t Cs = sa(sm + 2 * C::DB);
+    const uint32_t Cs0 = sa(sm + 2 * C::DB);  // C tile of group g at Cs0 + g CBytes
+    unsigned char *slots = sm + 2 * C::DB + 2 * C::CBytes;  // slot 2g + j: cap cellr, cap s
     if (threadIdx.x == 0) {
         for (int e = 0; e < 2; ++e) {
             bar_init(&d_full[e], 1);
             bar_init(&d_empty[e], 1);
-            bar_init(&a_full[e], kBuild);
+            bar_init(&a_full[e], C::kNB / 2);
             bar_init(&a_empty[e], 1);
-            bar_init(&acc_full[e], 1);
-            bar_init(&acc_empty[e], 4 * C::EQ);
+        }
+        for (int b = 0; b < 4; ++b) {
+            bar_init(&acc_full[b], 1);
+            bar_init(&acc_empty[b], 4 * C::EQ);
+        }
+        for (int i = 0; i < 4; ++i) {
+            bar_init(&slot_full[i], 1);
+            bar_init(&slot_empty[i], C::kNB / 2);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -1354,44 +1518,18 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
         return (size_t)((int)blockIdx.x + (k / A.nch) * (int)gridDim.x) * A.nch + (k % A.nch);
     };
 
-    if (warp < kBuild) {
-        // ===== builders =====
-#ifndef LIFE_BIN_NOREGSPLIT
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kRegBuild));
-#endif
-        const int tid = threadIdx.x;
-        const int q = warp & 3, hh = warp >> 2;
+    if (warp < C::kNB) {
+        // ===== builders: group g (8 warps) takes the steps k = g (mod 2) =====
+        const int g = warp >> 3, tid = threadIdx.x & 255;
+        const int q = warp & 3, hh = (warp >> 2) & 1;  // lane quarter, 32-atom half
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const uint32_t Cs = Cs0 + (uint32_t)(g * C::CBytes);
         const uint32_t rowaddr = Cs + 4u * (uint32_t)((q * 32 + lane) * kCS + hh * 32);
         const float scale = s_scale[0];
-        const bool slow = *nonfinite != 0u;  // non-finite s somewhere: check every entry
+        const bool slow = *nonfinite != 0u;  // a non-finite s in this call: check every entry
         for (int i = tid; i < kTV * kCS / 4; i += 256) sts_f4(Cs + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
-        if (tid < 8) s_rowbad[tid >> 2][tid & 3] = 0u;
-        int prev[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) prev[i] = 0;
-        StepRegs R;
-        uint32_t np0 = 0, nn = 0;  // pointers of the step after the prefetched one
-        StepIter it2(0, A.nch);    // walks two steps ahead of the current one
-        auto ptrs = [&](int k, uint32_t &p0, uint32_t &n) {
-            if (k < total) {
-                p0 = __ldg(A.step + it2.gs);
-                n = __ldg(A.step + it2.gs + 1) - p0;
-                it2.next();
-            } else {
-                p0 = n = 0;
-            }
-        };
-        auto fetch = [&](StepRegs &S) {
-#pragma unroll
-            for (int i = 0; i < kUMax; ++i) {
-                const uint32_t u = (uint32_t)tid + 256u * i;
-                if (u < S.n / 4u) {
-                    S.c[i] = __ldg(reinterpret_cast<const uint2 *>(A.cellr + S.p0) + u);
-                    S.s[i] = __ldcg(reinterpret_cast<const float4 *>(scr + S.p0) + u);
-                }
-            }
-        };
+        if (tid < 4) s_rowbad[g][tid] = 0u;
+        named_bar(1 + g, 256);
         // fixed-point adds of 4 entries (pads hold s = 0 at a padding column)
         auto add4 = [&](uint2 c, float4 v) {
             const uint32_t o[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
@@ -1401,88 +1539,103 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
                 asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(Cs + 4u * o[e]),
                              "r"((uint32_t)__float2int_rn(x[e] * scale)) : "memory");
         };
-        // slow path (a non-finite s in this call): rows that see one become NaN
-        auto add4_checked = [&](uint2 c, float4 v, int k) {
+        // slow path: rows that see a non-finite s become NaN
+        auto add4_checked = [&](uint2 c, float4 v) {
             const uint32_t o[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
             const float x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 if (o[e] != (uint32_t)kKA && !isfinite(x[e])) {
                     const uint32_t row = o[e] / kCS;
-                    atomicOr(&s_rowbad[k & 1][row >> 5], 1u << (row & 31));
+                    atomicOr(&s_rowbad[g][row >> 5], 1u << (row & 31));
                     continue;
                 }
                 asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(Cs + 4u * o[e]),
                              "r"((uint32_t)__float2int_rn(x[e] * scale)) : "memory");
             }
         };
-        ptrs(0, R.p0, R.n);
-        fetch(R);
-        ptrs(1, np0, nn);
-        named_bar(1, 256);
-        for (int k = 0; k < total; ++k) {
+        for (int k = g, j = 0; k < total; k += 2, ++j) {
+            const int sl = 2 * g + (j & 1);
+            BD_WAIT(0, bar_wait(&slot_full[sl], (j >> 1) & 1));
             BD_T0(t_sc);
-            StepRegs S = R;  // this step (loaded during the previous one)
-            R.p0 = np0;
-            R.n = nn;
-            fetch(R);        // next step, in flight during this one
-            ptrs(k + 2, np0, nn);
-            const uint32_t nu = S.n / 4u;
-            if (!slow) {
-#pragma unroll
-                for (int i = 0; i < kUMax; ++i)
-                    if ((uint32_t)tid + 256u * i < nu) add4(S.c[i], S.s[i]);
-                for (uint32_t u = (uint32_t)tid + 256u * kUMax; u < nu; u += 256u)
-                    add4(__ldg(reinterpret_cast<const uint2 *>(A.cellr + S.p0) + u),
-                         __ldcg(reinterpret_cast<const float4 *>(scr + S.p0) + u));
-            } else {
-                if (tid == 0) {
-                    s_rowbad[(k + 1) & 1][0] = s_rowbad[(k + 1) & 1][1] = 0u;
-                    s_rowbad[(k + 1) & 1][2] = s_rowbad[(k + 1) & 1][3] = 0u;
+            const uint32_t p0 = s_hdr[sl][0], n = s_hdr[sl][1];
+            const uint32_t nu = n / 4u, nst4 = min(n, (uint32_t)cap) / 4u;
+            const uint32_t sc = sa(slots + (size_t)sl * cap * 6), ss = sc + (uint32_t)cap * 2u;
+            auto unit = [&](uint32_t u, uint2 &c, float4 &v) {
+                if (u < nst4) {
+                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(c.x), "=r"(c.y) : "r"(sc + 8u * u));
+                    v = lds_f4(ss + 16u * u);
+                } else {
+                    c = __ldg(reinterpret_cast<const uint2 *>(A.cellr + p0) + u);
+                    v = __ldcg(reinterpret_cast<const float4 *>(scr + p0) + u);
                 }
-#pragma unroll
-                for (int i = 0; i < kUMax; ++i)
-                    if ((uint32_t)tid + 256u * i < nu) add4_checked(S.c[i], S.s[i], k);
-                for (uint32_t u = (uint32_t)tid + 256u * kUMax; u < nu; u += 256u)
-                    add4_checked(__ldg(reinterpret_cast<const uint2 *>(A.cellr + S.p0) + u),
-                                 __ldcg(reinterpret_cast<const float4 *>(scr + S.p0) + u), k);
+            };
+            if (!slow) {
+                for (uint32_t u = tid; u < nu; u += 512u) {  // two units in flight per thread
+                    uint2 c0, c1;
+                    float4 v0, v1;
+                    unit(u, c0, v0);
+                    const bool two = u + 256u < nu;
+                    if (two) unit(u + 256u, c1, v1);
+                    add4(c0, v0);
+                    if (two) add4(c1, v1);
+                }
+            } else {
+                for (uint32_t u = tid; u < nu; u += 256u) {
+                    uint2 c0;
+                    float4 v0;
+                    unit(u, c0, v0);
+                    add4_checked(c0, v0);
+                }
             }
             BD_ACC(1, t_sc);
-            BD_WAIT(2, named_bar(1, 256));  // the step's sums are complete
-            const int e = k & 1;
-            if (k >= 2) BD_WAIT(3, bar_wait(&a_empty[e], ((k >> 1) - 1) & 1));
+            __syncwarp();
+            if (lane == 0) bar_arrive(&slot_empty[sl]);
+            BD_WAIT(2, named_bar(1 + g, 256));  // the step's sums are complete
+            if (j >= 1) BD_WAIT(3, bar_wait(&a_empty[g], (j - 1) & 1));
             tcg::fence_after();
             BD_T0(t_cv);
-            const bool bad = slow && ((s_rowbad[k & 1][q] >> lane) & 1u);
+            // this thread's row, 32 atoms: fixed point -> f16 hi/lo pairs into
+            // TMEM A stage g, zeroing the cells behind
             uint32_t hv[16], lv[16];
+            const float inv15 = 1.f / 32768.f;
+            if (!slow) {
 #pragma unroll
-            for (int i4 = 0; i4 < 8; ++i4) {
-                const float4 x = lds_f4(rowaddr + 16u * i4);
-                const int cur[4] = {__float_as_int(x.x), __float_as_int(x.y), __float_as_int(x.z), __float_as_int(x.w)};
-                float f[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int dlt = (int)((uint32_t)cur[t] - (uint32_t)prev[4 * i4 + t]);
-                    prev[4 * i4 + t] = cur[t];
-                    f[t] = bad ? __int_as_float(0x7fc00000) : (float)dlt * (1.f / 32768.f);
+                for (int i4 = 0; i4 < 8; ++i4) {
+                    const float4 x = lds_f4(rowaddr + 16u * i4);
+                    sts_f4(rowaddr + 16u * i4, make_float4(0.f, 0.f, 0.f, 0.f));
+                    split2((float)__float_as_int(x.x) * inv15, (float)__float_as_int(x.y) * inv15, hv[2 * i4], lv[2 * i4]);
+                    split2((float)__float_as_int(x.z) * inv15, (float)__float_as_int(x.w) * inv15, hv[2 * i4 + 1],
+                           lv[2 * i4 + 1]);
                 }
-                split2(f[0], f[1], hv[2 * i4], lv[2 * i4]);
-                split2(f[2], f[3], hv[2 * i4 + 1], lv[2 * i4 + 1]);
+            } else {
+                const bool bad = (s_rowbad[g][q] >> lane) & 1u;
+                const float nan = __int_as_float(0x7fc00000);
+#pragma unroll
+                for (int i4 = 0; i4 < 8; ++i4) {
+                    const float4 x = lds_f4(rowaddr + 16u * i4);
+                    sts_f4(rowaddr + 16u * i4, make_float4(0.f, 0.f, 0.f, 0.f));
+                    split2(bad ? nan : (float)__float_as_int(x.x) * inv15, bad ? nan : (float)__float_as_int(x.y) * inv15,
+                           hv[2 * i4], lv[2 * i4]);
+                    split2(bad ? nan : (float)__float_as_int(x.z) * inv15, bad ? nan : (float)__float_as_int(x.w) * inv15,
+                           hv[2 * i4 + 1], lv[2 * i4 + 1]);
+                }
             }
-            const uint32_t ta = tmem + lane_base + (uint32_t)(e * 64 + hh * 16);
+            const uint32_t ta = tmem + lane_base + (uint32_t)(g * 64 + hh * 16);
             tm_st16(ta, hv);
             tm_st16(ta + 32u, lv);
             tcg::wait_st();
             tcg::fence_before();
             __syncwarp();
             BD_ACC(4, t_cv);
-            if (lane == 0) bar_arrive(&a_full[e]);
-            BD_WAIT(5, named_bar(1, 256));  // every cell read before the next step's adds
+            if (lane == 0) bar_arrive(&a_full[g]);
+            BD_WAIT(5, named_bar(1 + g, 256));  // C tile zeroed (and the row flags read) before the next step
+            if (slow) {  // clear the row flags before the group's next adds
+                if (tid < 4) s_rowbad[g][tid] = 0u;
+                named_bar(1 + g, 256);
+            }
         }
     } else if (warp < C::kEpi) {
-#ifndef LIFE_BIN_NOREGSPLIT
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::kRegLow));
-#endif
       if (warp == C::kProdD) {
         // ===== dictionary chunks =====
         if (lane == 0) {
@@ -1494,39 +1647,100 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
                 bar_arrive_tx(&d_full[e], (unsigned)C::DB);
                 bulk_g2s(Dbuf + (size_t)e * C::DB, reinterpret_cast<const unsigned char *>(A.D) + (size_t)c * C::DB,
                          (unsigned)C::DB, &d_full[e], pol);
-                if (k + 3 < total) {  // the builders' entries, three steps ahead
-                    const size_t g3 = it3.gs;
-                    const uint32_t p3 = __ldg(A.step + g3), n3 = __ldg(A.step + g3 + 1) - p3;
-                    if (n3) {
-                        prefetch_l2(A.cellr + p3, n3 * 2u);
-                        prefetch_l2(scr + p3, n3 * 4u);
-                    }
+            }
+        }
+      } else if (warp == C::kProdS) {
+        // ===== step entries into the groups' slots (bulk copies), L2 prefetch
+        // ahead; lane g serves builder group g (independent waits) =====
+        if (lane < 2) {
+            const int g = lane;
+            const uint64_t pol = pol_first();
+            constexpr int PF = 4;  // own steps: pointers loaded PF ahead, L2 prefetch PF - 1 ahead
+            StepIter it(g, A.nch), itp(g + 2 * PF, A.nch);
+            uint32_t pq[PF], nq[PF];
+            {
+                StepIter ip(g, A.nch);
+#pragma unroll
+                for (int i = 0; i < PF; ++i) {
+                    const bool in = g + 2 * i < total;
+                    pq[i] = in ? __ldg(A.step + ip.gs) : 0u;
+                    nq[i] = in ? __ldg(A.step + ip.gs + 1) : 0u;
+                    ip.next();
+                    ip.next();
                 }
+            }
+            for (int k = g, j = 0; k < total; k += 2, ++j) {
+                const int sl = 2 * g + (j & 1);
+                const uint32_t p0 = pq[0], n = nq[0] - pq[0];
+                uint32_t pn = 0, en = 0;
+                if (k + 2 * PF < total) {
+                    pn = __ldg(A.step + itp.gs);
+                    en = __ldg(A.step + itp.gs + 1);
+                }
+                itp.next();
+                itp.next();
+#pragma unroll
+                for (int i = 0; i < PF - 1; ++i) {
+                    pq[i] = pq[i + 1];
+                    nq[i] = nq[i + 1];
+                }
+                pq[PF - 1] = pn;
+                nq[PF - 1] = en;
+                if (j >= 2) BD_WAIT(9, bar_wait(&slot_empty[sl], ((j >> 1) - 1) & 1));
+                const uint32_t nst = min(n, (uint32_t)cap);
+                s_hdr[sl][0] = p0;
+                s_hdr[sl][1] = n;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bar_arrive_tx(&slot_full[sl], nst * 6u);
+                unsigned char *dst = slots + (size_t)sl * cap * 6;
+                if (nst) {
+                    bulk_g2s(dst, A.cellr + p0, nst * 2u, &slot_full[sl], pol);
+                    bulk_g2s(dst + (size_t)cap * 2, scr + p0, nst * 4u, &slot_full[sl], pol);
+                }
+                if (nq[PF - 2] > pq[PF - 2]) {
+                    prefetch_l2(A.cellr + pq[PF - 2], (nq[PF - 2] - pq[PF - 2]) * 2u);
+                    prefetch_l2(scr + pq[PF - 2], (nq[PF - 2] - pq[PF - 2]) * 4u);
+                }
+                it.next();
+                it.next();
             }
         }
       } else if (warp < C::kMma + 2) {
         // ===== MMA issuers: warp kMma + e takes the steps k = e (mod 2) =====
+        // Within a tile, an issuer accumulates pairs of its steps (128
+        // atoms) in one TMEM buffer before the epilogue folds it.
         const int e = warp - C::kMma;
         if (lane == 0) {
             const uint32_t id = (uint32_t)idesc_f16(kTV, N);
             const uint32_t db = sa(Dbuf + (size_t)e * C::DB);
             const uint64_t bh = tcg::sdesc(db), bl = tcg::sdesc(db + (uint32_t)(N * 128));
-            const uint32_t d = tmem + (uint32_t)(C::TACC + e * N), ah = tmem + (uint32_t)(e * 64), al = ah + 32u;
-            for (int k = e, j = 0; k < total; k += 2, ++j) {
-                if (j >= 1) BD_WAIT(6, bar_wait(&acc_empty[e], (j - 1) & 1));
-                BD_WAIT(7, bar_wait(&a_full[e], j & 1));
-                BD_WAIT(8, bar_wait(&d_full[e], j & 1));
-                tcg::fence_after();
+            const uint32_t ah = tmem + (uint32_t)(e * 64), al = ah + 32u;
+            int j = 0, f = 0;
+            for (int i = 0; i < my_tiles; ++i) {
+                const int c0 = (e + i * A.nch) & 1, nown = (A.nch - c0 + 1) >> 1;
+                for (int oi = 0; oi < nown; ++oi, ++j) {
+                    const int b = e * C::NACC + (C::NACC == 2 ? (f & 1) : 0);
+                    const int fpar = C::NACC == 2 ? ((f >> 1) - 1) & 1 : (f - 1) & 1;
+                    const bool start = (oi & 1) == 0, fold = (oi & 1) == 1 || oi == nown - 1;
+                    if (start && f >= C::NACC) BD_WAIT(6, bar_wait(&acc_empty[b], fpar));
+                    BD_WAIT(7, bar_wait(&a_full[e], j & 1));
+                    BD_WAIT(8, bar_wait(&d_full[e], j & 1));
+                    tcg::fence_after();
+                    const uint32_t d = tmem + (uint32_t)(C::TACC + b * N);
 #pragma unroll
-                for (int kk = 0; kk < kKA / 16; ++kk) {
-                    const uint64_t o = (uint64_t)((kk * 32) >> 4);
-                    mma_f16(d, ah + 8u * kk, bh + o, id, kk ? 1u : 0u);
-                    mma_f16(d, al + 8u * kk, bh + o, id, 1u);
-                    mma_f16(d, ah + 8u * kk, bl + o, id, 1u);
+                    for (int kk = 0; kk < kKA / 16; ++kk) {
+                        const uint64_t o = (uint64_t)((kk * 32) >> 4);
+                        mma_f16(d, ah + 8u * kk, bh + o, id, (start && kk == 0) ? 0u : 1u);
+                        mma_f16(d, al + 8u * kk, bh + o, id, 1u);
+                        mma_f16(d, ah + 8u * kk, bl + o, id, 1u);
+                    }
+                    tcg::commit(&a_empty[e]);
+                    tcg::commit(&d_empty[e]);
+                    if (fold) {
+                        tcg::commit(&acc_full[b]);
+                        ++f;
+                    }
                 }
-                tcg::commit(&a_empty[e]);
-                tcg::commit(&d_empty[e]);
-                tcg::commit(&acc_full[e]);
             }
         }
         __syncwarp();
@@ -1540,22 +1754,27 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
         const bool accumulate = flags & LIFE_ACCUMULATE;
         const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
         const float oscale = s_scale[1];
-        int k = 0;
+        int fcount[2] = {0, 0};  // folds seen per issuer
         for (int i = 0; i < my_tiles; ++i) {
             const int t = (int)blockIdx.x + i * (int)gridDim.x;
             float acc[C::MB * 16];
 #pragma unroll
             for (int x = 0; x < C::MB * 16; ++x) acc[x] = 0.f;
-            for (int c = 0; c < A.nch; ++c, ++k) {
-                const int e = k & 1;
-                BD_WAIT(11, bar_wait(&acc_full[e], (k >> 1) & 1));
+            for (int c = 0; c < A.nch; ++c) {
+                const int e = (i * A.nch + c) & 1, c0 = (e + i * A.nch) & 1;
+                const int nown = (A.nch - c0 + 1) >> 1, oi = (c - c0) >> 1;
+                if (!((oi & 1) == 1 || oi == nown - 1)) continue;  // not a fold step
+                const int f = fcount[e]++;
+                const int b = e * C::NACC + (C::NACC == 2 ? (f & 1) : 0);
+                const int par = C::NACC == 2 ? (f >> 1) & 1 : f & 1;
+                BD_WAIT(11, bar_wait(&acc_full[b], par));
                 tcg::fence_after();
                 BD_T0(t_fd);
 #pragma unroll
                 for (int bb = 0; bb < C::MB; ++bb) {
                     if (b0 + bb < b1) {
                         uint32_t r[16];
-                        tm_ld16(tmem + lane_base + (uint32_t)(C::TACC + e * N + 16 * (b0 + bb)), r);
+                        tm_ld16(tmem + lane_base + (uint32_t)(C::TACC + b * N + 16 * (b0 + bb)), r);
                         tm_wait_ld();
 #pragma unroll
                         for (int x = 0; x < 16; ++x) acc[16 * bb + x] += __uint_as_float(r[x]);
@@ -1564,7 +1783,7 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
                 BD_ACC(12, t_fd);
                 tcg::fence_before();
                 __syncwarp();
-                if (lane == 0) bar_arrive(&acc_empty[e]);
+                if (lane == 0) bar_arrive(&acc_empty[b]);
             }
             const int rv = __ldg(A.rowvox + (size_t)t * kTV + row);
             const int rp = __ldg(A.rowpart + (size_t)t * kTV + row);
@@ -1984,8 +2203,12 @@ constexpr int kSmemMax = 232448 - 2048;  // opt-in dynamic limit minus static + 
 
 SideArgs side_args(const life_phi *phi)
 {
-    return SideArgs{phi->b_vid, phi->b_val, phi->b_segsrc, phi->b_segdst, phi->b_binptr, phi->b_ctaseg,
+    return SideArgs{phi->b_vid, phi->b_val, phi->b_segsrc, phi->b_segdst, phi->b_binptr,
                     phi->b_vf2f, phi->b_nvf, phi->b_nbins};
+}
+ChunkArgs chunk_args(const life_phi *phi)
+{
+    return ChunkArgs{reinterpret_cast<const uint4 *>(phi->b_chunks), phi->b_ctachunk};
 }
 
 template <int N>
@@ -1993,12 +2216,16 @@ int prep_t(life_phi *phi)
 {
     using CD = DscCfg<N>;
     using CW = WcCfg<N>;
-    phi->b_dsc_smem = 1024 + 2 * (size_t)CD::DB + CD::CBytes;
+    {
+        const long avail = (long)kSmemMax - 1024L - 2L * CD::DB - 2L * CD::CBytes;
+        phi->b_dsc_cap = (int)std::min(16384L, std::max(0L, avail / (4L * 6L) / 32 * 32));
+    }
+    phi->b_dsc_smem = 1024 + 2 * (size_t)CD::DB + 2 * (size_t)CD::CBytes + (size_t)4 * 6 * phi->b_dsc_cap;
     phi->b_wc_smem = 1024 + 2 * (size_t)CW::DB + 2 * (size_t)CW::ZBytes;
     if (phi->b_dsc_smem > (size_t)kSmemMax || phi->b_wc_smem > (size_t)kSmemMax)
         return fail(LIFE_ERR_CONFIG_INVALID, "bin layout: shared memory does not fit");
-    phi->b_side_smem = (size_t)kSB * 4;
-    phi->b_wcs_smem = (size_t)kSB * 8;
+    phi->b_side_smem = (size_t)kSB * 4 + (size_t)kNsDsc * kSlotBytes;
+    phi->b_wcs_smem = (size_t)kSB * 8 + (size_t)kNsWc * kSlotBytes;
     LIFE_TRY(ensure_smem(k_tile_dsc<N>, phi->b_dsc_smem));
     LIFE_TRY(ensure_smem(k_tile_wc<N>, phi->b_wc_smem));
     LIFE_TRY(ensure_smem(k_side_dsc, phi->b_side_smem));
@@ -2011,15 +2238,15 @@ int dsc_t(life_phi *phi, const float *w, float *y, const float *b, uint32_t flag
           const CallHooks &h, cudaStream_t st)
 {
     using CD = DscCfg<N>;
-    k_side_dsc<<<phi->b_side_grid, kSideWarps * 32, phi->b_side_smem, st>>>(
-        side_args(phi), w, phi->b_scr, (flags & LIFE_SKIP_ZERO) ? 1 : 0, phi->b_skip, phi->b_smax, phi->b_nonfin, h);
+    k_side_dsc<<<phi->b_side_grid, kSideThreads, phi->b_side_smem, st>>>(
+        side_args(phi), chunk_args(phi), w, phi->b_scr, (flags & LIFE_SKIP_ZERO) ? 1 : 0, phi->b_skip, phi->b_smax, phi->b_nonfin, h);
     LIFE_CHECK_LAUNCH();
     const TileArgs A{phi->b_cellr, phi->b_step, phi->b_Ddsc, phi->b_rowvox, phi->b_rowpart, phi->b_ypart,
                      phi->b_ntiles, phi->b_nch, phi->nt};
     const int fin = phi->b_nfix == 0 ? 1 : 0;
     k_tile_dsc<N><<<phi->b_tile_grid, CD::kThreads, phi->b_dsc_smem, st>>>(
         A, phi->b_scr, y, b, flags, phi->red, o, h, phi->b_skip, phi->b_side_grid, phi->b_smax, phi->b_side_grid,
-        phi->b_nonfin, fin);
+        phi->b_nonfin, fin, phi->b_dsc_cap);
     LIFE_CHECK_LAUNCH();
     if (!fin) {
         const int blocks = std::max(1, std::min(phi->sms, (phi->b_nfix + 7) / 8));
@@ -2081,7 +2308,7 @@ int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, c
                   double *sumsq, const CallHooks &h, const life_comm *comm, cudaStream_t st)
 {
     LIFE_TRY(wc_tile(phi, y, fx, h, st));
-    k_side_wc<<<phi->b_side_grid, kSideWarps * 32, phi->b_wcs_smem, st>>>(side_args(phi), phi->b_scr, fx, phi->nt,
+    k_side_wc<<<phi->b_side_grid, kSideThreads, phi->b_wcs_smem, st>>>(side_args(phi), chunk_args(phi), phi->b_scr, fx, phi->nt,
                                                                           phi->b_wfix, phi->b_nanf, h);
     LIFE_CHECK_LAUNCH();
     const int blocks = std::max(1, std::min(phi->sms * 4, (phi->nf + 255) / 256));

@@ -148,7 +148,8 @@ struct life_phi {
     uint32_t *b_segsrc = nullptr;  // [nseg + 1] bin-major start of each (bin, tile, chunk), 4-entry units
     uint32_t *b_segdst = nullptr;  // [nseg] its tile-major start, 4-entry units
     uint32_t *b_binptr = nullptr;  // [nbins + 1] first segment of each bin
-    uint32_t *b_ctaseg = nullptr;  // [side grid + 1] first segment of each bin-side CTA
+    uint32_t *b_chunks = nullptr;  // bin-side chunk descriptors (uint4: first unit, units | piece start, first segment, segments | bin)
+    uint32_t *b_ctachunk = nullptr;  // [side grid + 1] first chunk of each bin-side CTA
     uint32_t *b_vf2f = nullptr;    // [nvf] fascicle of each virtual slot
     uint32_t *b_f2vf = nullptr;    // [nf + 1] first virtual slot of each fascicle
     int *b_rowvox = nullptr;       // [ntiles*128] voxel of each tile row, -1 = empty
@@ -165,7 +166,7 @@ struct life_phi {
     unsigned long long *b_skip = nullptr;  // [side grid] skip-count partials of the bin side
     float *b_smax = nullptr;               // [side grid] max |s| partials (DSC fixed-point scale)
     unsigned *b_nonfin = nullptr;          // non-finite s seen by the DSC bin side (this call)
-    int b_tile_grid = 0, b_side_grid = 0;
+    int b_tile_grid = 0, b_side_grid = 0, b_dsc_cap = 0;
     size_t b_dsc_smem = 0, b_wc_smem = 0, b_side_smem = 0, b_wcs_smem = 0;
 
     // fixed-point WC accumulator and its scale inputs

@@ -31,7 +31,9 @@ names = {0: ("build", 8, "wait slot_full"), 1: ("build", 8, "scatter pass"), 2: 
          3: ("build", 8, "wait a_empty"), 4: ("build", 8, "convert"), 5: ("build", 8, "bar zeroed"),
          6: ("mma", 1, "wait acc_empty"), 7: ("mma", 1, "wait a_full"), 8: ("mma", 1, "wait d_full"),
          9: ("prodS", 1, "wait slot_empty"), 10: ("prodD", 1, "wait d_empty"), 11: ("epi", 8, "wait acc_full"),
-         12: ("epi", 8, "fold"),
+         12: ("epi", 8, "fold"), 13: ("sideC", 31, "wait full"), 14: ("sideC", 31, "process"),
+         15: ("sideP", 1, "wait empty"), 9: ("sideC", 31, "process"), 30: ("sideC", 31, "wait full (z)"),
+         31: ("sideP", 1, "wait empty"),
          16: ("gath", 8, "wait slot_full"), 17: ("gath", 8, "wait z_full"), 18: ("gath", 8, "gather pass"),
          19: ("mma", 1, "wait y_ready"), 20: ("mma", 1, "wait d_full"), 21: ("mma", 1, "wait acc_empty"),
          22: ("prodS", 1, "wait slot_empty"), 23: ("prodD", 1, "wait d_empty"), 24: ("yz", 8, "wait y_free"),
