@@ -738,6 +738,7 @@ static int prepare_sparse(life_phi *phi) { LIFE_NT_DISPATCH(prepare_t, phi); }
 
 int prepare_spmv(life_phi *phi)
 {
+    if (phi->has_bin) return LIFE_OK;  // prepared at build (prepare_bin)
     if (phi->has_tc) LIFE_TRY(prepare_tc(phi));
     if (phi->has_dense) return prepare_dense(phi);
     return prepare_sparse(phi);

@@ -138,7 +138,7 @@ def test_c2_fp32_products(scale, c2):
     recs, arrays = scale
     rec = recs["c2"]
     op = L.DeviceOperator(c2.tensor, c2.dictionary)
-    assert op.kind == "tensor" and set(op.tensor_ops) == {"dsc", "wc"}
+    assert op.kind == "bin" and set(op.tensor_ops) == {"dsc", "wc"}
     op.close()
     y64 = L.zeros_signal(c2.dims)
     L.dsc_sequential(c2.tensor, c2.dictionary, c2.w_true, y64, precision="fp64")
