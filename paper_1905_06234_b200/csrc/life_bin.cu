@@ -816,6 +816,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
         LIFE_CUDA(cudaMemcpyAsync(hcta.data(), dcs, hcta.size() * 4, cudaMemcpyDeviceToHost, st));
         LIFE_CUDA(cudaStreamSynchronize(st));
         std::vector<uint32_t> chunks, ctachunk(1, 0);
+        std::vector<uint16_t> cgrp;
         int b = 0;
         for (int c = 0; c < side_grid; ++c) {
             const uint32_t S0 = hcta[c], S1 = hcta[c + 1];
@@ -834,6 +835,13 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
                     uint32_t sh = sl;  // segment containing u1 - 1
                     while (hsrc[sh + 1] < u1) ++sh;
                     const uint32_t ns = sh - sl + 1;
+                    // per 32-unit group of the chunk: its first segment
+                    for (uint32_t g = 0, k = sl; g < 32; ++g) {
+                        const uint32_t ug = u0 + 32u * g;
+                        if (ug < u1)
+                            while (hsrc[k + 1] <= ug) ++k;
+                        cgrp.push_back((uint16_t)(ug < u1 ? k - sl : 0u));
+                    }
                     chunks.push_back(u0);
                     chunks.push_back((u1 - u0) | (first ? 0x80000000u : 0u));
                     chunks.push_back(sl);
@@ -844,8 +852,13 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
             }
             ctachunk.push_back((uint32_t)(chunks.size() / 4));
         }
-        if (chunks.empty()) chunks.assign(4, 0u);
+        if (chunks.empty()) {
+            chunks.assign(4, 0u);
+            cgrp.assign(32, 0);
+        }
         LIFE_TRY(dalloc(phi, &phi->b_chunks, chunks.size()));
+        LIFE_TRY(dalloc(phi, &phi->b_cgrp, cgrp.size()));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_cgrp, cgrp.data(), cgrp.size() * 2, cudaMemcpyHostToDevice, st));
         LIFE_TRY(dalloc(phi, &phi->b_ctachunk, ctachunk.size()));
         LIFE_CUDA(cudaMemcpyAsync(phi->b_chunks, chunks.data(), chunks.size() * 4, cudaMemcpyHostToDevice, st));
         LIFE_CUDA(cudaMemcpyAsync(phi->b_ctachunk, ctachunk.data(), ctachunk.size() * 4, cudaMemcpyHostToDevice, st));
@@ -995,19 +1008,21 @@ constexpr int kCons = kSideThreads - 32;
 // plus the alignment slack of an unaligned global start)
 constexpr uint32_t kSlotVid = 0, kSlotVal = (kCH * 8 + 16 + 15) / 16 * 16, kSlotSrc = kSlotVal + kCH * 16,
                    kSlotDst = kSlotSrc + ((kCH + 2) * 4 + 16 + 15) / 16 * 16,
-                   kSlotBytes = (kSlotDst + (kCH + 1) * 4 + 16 + 127) / 128 * 128;
+                   kSlotGrp = kSlotDst + ((kCH + 1) * 4 + 16 + 15) / 16 * 16,
+                   kSlotBytes = (kSlotGrp + 64 + 127) / 128 * 128;
 constexpr int kNsDsc = 4, kNsWc = 3;
 
 struct ChunkArgs {
     const uint4 *chunks;      // chunk descriptors
     const uint32_t *ctachunk; // [grid + 1]
+    const uint16_t *grp;      // [chunks][32] first segment (chunk-relative) of each 32-unit group
 };
 
 // producer: stage chunk j of the CTA into slot j % NS (header: byte offsets of
 // the unaligned starts)
 template <int NS, int CAT>
-__device__ __forceinline__ void side_produce(const SideArgs &A, const uint4 *tab, int nch, unsigned char *ring,
-                                             uint4 (*hdr)[2], uint64_t *full, uint64_t *empty)
+__device__ __forceinline__ void side_produce(const SideArgs &A, const uint4 *tab, const uint16_t *grp, int nch,
+                                             unsigned char *ring, uint4 (*hdr)[2], uint64_t *full, uint64_t *empty)
 {
     BD_DECL;
     const uint64_t pol = pol_first();
@@ -1028,31 +1043,37 @@ __device__ __forceinline__ void side_produce(const SideArgs &A, const uint4 *tab
         const uint64_t dz = (db1 + 15) & ~15ull;
         hdr[sl][0] = c;  // the descriptor and the byte offsets of the unaligned starts
         hdr[sl][1] = make_uint4((uint32_t)(vb0 - va), (uint32_t)(sb0 - sa0), 0u, 0u);
-        const unsigned bytes = (unsigned)((vz - va) + 16ull * nu + (sz - sa0) + (dz - sa0));
+        const unsigned bytes = (unsigned)((vz - va) + 16ull * nu + (sz - sa0) + (dz - sa0) + 64ull);
         bar_arrive_tx(&full[sl], bytes);
         bulk_g2s(slot + kSlotVid, reinterpret_cast<const unsigned char *>(A.vid) + va, (unsigned)(vz - va), &full[sl], pol);
         bulk_g2s(slot + kSlotVal, reinterpret_cast<const unsigned char *>(A.val) + 16ull * u0, 16u * nu, &full[sl], pol);
         bulk_g2s(slot + kSlotSrc, reinterpret_cast<const unsigned char *>(A.src4) + sa0, (unsigned)(sz - sa0), &full[sl], pol);
         bulk_g2s(slot + kSlotDst, reinterpret_cast<const unsigned char *>(A.dst4) + sa0, (unsigned)(dz - sa0), &full[sl], pol);
+        bulk_g2s(slot + kSlotGrp, reinterpret_cast<const unsigned char *>(grp + 32ull * j), 64u, &full[sl], pol);
     }
     BD_FLUSH;
 }
 
-// consumer: tile-major unit of chunk unit u (staged segment records)
+// consumer: tile-major unit of chunk unit u (staged segment records): start
+// at the first segment of u's 32-unit group, walk forward (segments average
+// tens of units, so mostly zero or one step)
 __device__ __forceinline__ uint32_t side_dst(uint32_t slot_sa, uint32_t hs, uint32_t u0, uint32_t ns, uint32_t u)
 {
     const uint32_t U = u0 + u;
     const uint32_t src = slot_sa + kSlotSrc + hs, dst = slot_sa + kSlotDst + hs;
-    uint32_t lo = 0, hi = ns;  // largest i < ns with src4[i] <= U
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        uint32_t v;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(src + 4u * mid));
-        if (v <= U) lo = mid; else hi = mid;
+    uint32_t k;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(k) : "r"(slot_sa + kSlotGrp + 2u * (u >> 5)));
+    uint32_t s0, s1;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s0) : "r"(src + 4u * k));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s1) : "r"(src + 4u * k + 4u));
+    while (s1 <= U) {
+        ++k;
+        s0 = s1;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s1) : "r"(src + 4u * k + 4u));
     }
-    uint32_t s0, d0;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s0) : "r"(src + 4u * lo));
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d0) : "r"(dst + 4u * lo));
+    (void)ns;
+    uint32_t d0;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d0) : "r"(dst + 4u * k));
     return d0 + (U - s0);
 }
 
@@ -1085,7 +1106,7 @@ __global__ void __launch_bounds__(kSideThreads, 1)
     float smax = 0.f;
     bool nonfin = false;
     if (warp == 0) {
-        if (lane == 0) side_produce<kNsDsc, 15>(A, tab, nch, ring, hdr, full, empty);
+        if (lane == 0) side_produce<kNsDsc, 15>(A, tab, CA.grp + 32ull * c0, nch, ring, hdr, full, empty);
     } else {
         const uint32_t ct = threadIdx.x - 32;
         BD_DECL;
@@ -1182,7 +1203,7 @@ __global__ void __launch_bounds__(kSideThreads, 1)
     }
     __syncthreads();
     if (warp == 0) {
-        if (lane == 0) side_produce<kNsWc, 31>(A, tab, nch, ring, hdr, full, empty);
+        if (lane == 0) side_produce<kNsWc, 31>(A, tab, CA.grp + 32ull * c0, nch, ring, hdr, full, empty);
         return;
     }
     const uint32_t ct = threadIdx.x - 32;
@@ -1282,25 +1303,55 @@ __global__ void __launch_bounds__(BT)
     const bool accumulate = flags & LIFE_ACCUMULATE;
     const bool project = (flags & LIFE_PROJECT_GRAD) && w_ref != nullptr;
     double sq = 0.0;
-    for (int f = blockIdx.x * BT + threadIdx.x; f < nf; f += gridDim.x * BT) {
+    const int lane = threadIdx.x & 31;
+    // warp-uniform walk over 32-fascicle groups; a fascicle split into many
+    // virtual slots (a Zipf-heavy one) is folded by the whole warp
+    for (int base = (blockIdx.x * BT + threadIdx.x) & ~31; base < nf; base += gridDim.x * BT) {
+        const int f = base + lane;
+        const bool valid = f < nf;
         long long q = 0;
         bool bad = false;
         if (mode == 2) {
-            q = (long long)wsum[f];
+            if (valid) q = (long long)wsum[f];
         } else {
-            for (uint32_t s = __ldg(f2vf + f); s < __ldg(f2vf + f + 1); ++s) {
-                q += (long long)wfix[s];
-                wfix[s] = 0ull;
-                if (nanf[s]) {
-                    bad = true;
-                    nanf[s] = 0;
+            const uint32_t s0 = valid ? __ldg(f2vf + f) : 0u, s1 = valid ? __ldg(f2vf + f + 1) : 0u;
+            const bool longf = s1 - s0 > 8u;
+            if (!longf)
+                for (uint32_t s = s0; s < s1; ++s) {
+                    q += (long long)wfix[s];
+                    wfix[s] = 0ull;
+                    if (nanf[s]) {
+                        bad = true;
+                        nanf[s] = 0;
+                    }
+                }
+            for (unsigned m = __ballot_sync(0xffffffffu, longf); m; m &= m - 1) {
+                const int l = __ffs(m) - 1;
+                const uint32_t a = __shfl_sync(0xffffffffu, s0, l), b = __shfl_sync(0xffffffffu, s1, l);
+                long long qq = 0;
+                bool bb = false;
+                for (uint32_t s = a + lane; s < b; s += 32) {
+                    qq += (long long)wfix[s];
+                    wfix[s] = 0ull;
+                    if (nanf[s]) {
+                        bb = true;
+                        nanf[s] = 0;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
+                bb = __any_sync(0xffffffffu, bb);
+                if (lane == l) {
+                    q = qq;
+                    bad = bb;
                 }
             }
             if (mode == 1) {
-                wsum[f] = (unsigned long long)q;
+                if (valid) wsum[f] = (unsigned long long)q;
                 continue;
             }
         }
+        if (!valid) continue;
         float o = bad ? __int_as_float(0x7fc00000) : (float)((double)q * inv);
         if (accumulate) o = w_out[f] + o;
         if (project && w_ref[f] == 0.f && o > 0.f) o = 0.f;
@@ -2208,7 +2259,7 @@ SideArgs side_args(const life_phi *phi)
 }
 ChunkArgs chunk_args(const life_phi *phi)
 {
-    return ChunkArgs{reinterpret_cast<const uint4 *>(phi->b_chunks), phi->b_ctachunk};
+    return ChunkArgs{reinterpret_cast<const uint4 *>(phi->b_chunks), phi->b_ctachunk, phi->b_cgrp};
 }
 
 template <int N>

@@ -149,6 +149,7 @@ struct life_phi {
     uint32_t *b_segdst = nullptr;  // [nseg] its tile-major start, 4-entry units
     uint32_t *b_binptr = nullptr;  // [nbins + 1] first segment of each bin
     uint32_t *b_chunks = nullptr;  // bin-side chunk descriptors (uint4: first unit, units | piece start, first segment, segments | bin)
+    uint16_t *b_cgrp = nullptr;      // [chunks][32] first segment of each 32-unit group of a chunk
     uint32_t *b_ctachunk = nullptr;  // [side grid + 1] first chunk of each bin-side CTA
     uint32_t *b_vf2f = nullptr;    // [nvf] fascicle of each virtual slot
     uint32_t *b_f2vf = nullptr;    // [nf + 1] first virtual slot of each fascicle

@@ -556,6 +556,8 @@ __global__ void k_max_u32(const unsigned *x, int64_t n, unsigned *mx, unsigned *
     atomicAdd(nz, c);
 }
 
+static void destroy_impl(life_phi *phi);
+
 static int create_impl(const life_dims *dims, const uint32_t *atoms,
                        const uint32_t *voxels, const uint32_t *fibers,
                        const double *values, const double *dict, uint32_t flags,
@@ -611,7 +613,7 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         ~Guard()
         {
             for (void *q : tmp) cudaFree(q);
-            if (p) life_phi_destroy(p);
+            if (p) destroy_impl(p);  // keeps the error message of the failed build
         }
     } guard{out, phi, {}, st};
 
@@ -791,12 +793,16 @@ int life_phi_create(const life_dims *dims, const uint32_t *atoms,
                        static_cast<cudaStream_t>(stream), out, bad_position);
 }
 
-int life_phi_destroy(life_phi *phi)
+static void destroy_impl(life_phi *phi)
 {
-    if (!phi) return ok();
     cudaDeviceSynchronize();
     for (void *p : phi->allocs) cudaFree(p);
     delete phi;
+}
+
+int life_phi_destroy(life_phi *phi)
+{
+    if (phi) destroy_impl(phi);
     return ok();
 }
 

@@ -99,6 +99,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", action="store_true")
     ap.add_argument("--layouts", default="bin")
+    ap.add_argument("--skew", action="store_true", help="16M/100M uniform vs Zipf fascicles vs one 5%% voxel")
     args = ap.parse_args()
     cases = [
         ("tiny", custom(64, 500, 800, 96, 40_000, 3)),
@@ -117,6 +118,14 @@ def main():
         c2 = L.generate(L.GenConfig(dims=L.Dims(1057, 200_000, 500_000, 96, 100_000_000),
                                     mean_run_length=520.0, weight_density=0.5, noise_sigma=0.1, seed=0))
         cases.append(("C2", (c2.tensor, c2.dictionary)))
+    if args.skew:
+        cases = [
+            ("16M-uniform", custom(1057, 40_000, 100_000, 96, 16_000_000, 11)),
+            ("16M-zipf1.3", custom(1057, 40_000, 100_000, 96, 16_000_000, 11, zipf=1.3)),
+            ("16M-hot-voxel-5%", custom(1057, 40_000, 100_000, 96, 16_000_000, 11, hot_voxel=0.05)),
+            ("100M-uniform", custom(1057, 200_000, 500_000, 96, 100_000_000, 12)),
+            ("100M-zipf1.3", custom(1057, 200_000, 500_000, 96, 100_000_000, 12, zipf=1.3)),
+        ]
     bad = 0
     for name, (t, dic) in cases:
         for lay in args.layouts.split(","):
