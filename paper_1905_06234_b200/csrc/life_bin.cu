@@ -47,6 +47,7 @@ namespace bin {
 constexpr int kTV = 128;            // tile rows (tcgen05 M)
 constexpr int kRanks = 7;           // duplicate ranks per tile row (rank field value 7 = pad)
 constexpr uint16_t kPad = 0xFFFFu;  // tile-major pad entry
+constexpr int kFixRows = 32;        // partial rows per fixup piece (one warp)
 constexpr int kSlotCap = 256;       // coefficients per virtual fascicle slot (2-limb fixed point)
 constexpr int kSB = 16384;          // virtual slots per bin: 64 KB (DSC w) / 128 KB (WC limbs)
 constexpr int kBuild = 8;           // builder / gatherer warps of the tile kernels
@@ -454,14 +455,19 @@ __global__ void k_bin_seg(const unsigned long long *segkey, int64_t nseg, int nb
     }
 }
 // bin-side CTA c takes the segments whose start lies in units [c*U/g, (c+1)*U/g)
+// bin-side CTA ranges balanced by cost = units + kSegCost per segment (a
+// segment start is a scattered scratch access and a search; sparse bins of
+// one-unit segments would otherwise make stragglers)
+constexpr unsigned long long kSegCost = 4;
 __global__ void k_cta_seg(const uint32_t *src4, int64_t nseg, int grid, uint32_t *ctaseg)
 {
     for (int64_t c = gtid(); c <= grid; c += gstride()) {
-        const unsigned long long target = (unsigned long long)src4[nseg] * (unsigned long long)c / (unsigned long long)grid;
+        const unsigned long long total = (unsigned long long)src4[nseg] + kSegCost * (unsigned long long)nseg;
+        const unsigned long long target = total * (unsigned long long)c / (unsigned long long)grid;
         int64_t lo = 0, hi = nseg;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
-            if ((unsigned long long)src4[mid] < target) lo = mid + 1; else hi = mid;
+            if ((unsigned long long)src4[mid] + kSegCost * (unsigned long long)mid < target) lo = mid + 1; else hi = mid;
         }
         ctaseg[c] = (uint32_t)(c == grid ? nseg : lo);
     }
@@ -662,11 +668,38 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     phi->b_nfix = (int)fixvox.size();
     phi->b_nprow = nprow;
     if (phi->b_nfix) {
-        LIFE_TRY(dalloc(phi, &phi->b_fixptr, fixptr.size()));
-        LIFE_TRY(dalloc(phi, &phi->b_fixvox, fixvox.size()));
+        // fold work: pieces of at most kFixRows partial rows (one warp each);
+        // a voxel of several pieces stores piece sums and is folded by a
+        // whole CTA afterwards (fixed order: deterministic)
+        std::vector<uint32_t> pcs, big, bpp(1, 0);
+        uint32_t nsum = 0;
+        for (int m = 0; m < phi->b_nfix; ++m) {
+            const uint32_t r0 = fixptr[m], r1 = fixptr[m + 1];
+            const bool multi = r1 - r0 > (uint32_t)kFixRows;
+            for (uint32_t r = r0; r < r1; r += kFixRows) {
+                pcs.push_back((uint32_t)fixvox[m]);
+                pcs.push_back(r);
+                pcs.push_back(std::min(r1, r + (uint32_t)kFixRows));
+                pcs.push_back(multi ? nsum++ : 0xFFFFFFFFu);
+            }
+            if (multi) {
+                big.push_back((uint32_t)fixvox[m]);
+                bpp.push_back(nsum);
+            }
+        }
+        phi->b_npc = (int)(pcs.size() / 4);
+        phi->b_nbig = (int)big.size();
+        LIFE_TRY(dalloc(phi, &phi->b_fixpc, pcs.size()));
         LIFE_TRY(dalloc(phi, &phi->b_ypart, (size_t)nprow * N));
-        LIFE_CUDA(cudaMemcpyAsync(phi->b_fixptr, fixptr.data(), fixptr.size() * 4, cudaMemcpyHostToDevice, st));
-        LIFE_CUDA(cudaMemcpyAsync(phi->b_fixvox, fixvox.data(), fixvox.size() * 4, cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaMemcpyAsync(phi->b_fixpc, pcs.data(), pcs.size() * 4, cudaMemcpyHostToDevice, st));
+        if (phi->b_nbig) {
+            LIFE_TRY(dalloc(phi, &phi->b_fixbig, big.size()));
+            LIFE_TRY(dalloc(phi, &phi->b_fixbpp, bpp.size()));
+            LIFE_TRY(dalloc(phi, &phi->b_fixsum, (size_t)nsum * N));
+            LIFE_CUDA(cudaMemcpyAsync(phi->b_fixbig, big.data(), big.size() * 4, cudaMemcpyHostToDevice, st));
+            LIFE_CUDA(cudaMemcpyAsync(phi->b_fixbpp, bpp.data(), bpp.size() * 4, cudaMemcpyHostToDevice, st));
+        }
+        LIFE_CUDA(cudaStreamSynchronize(st));
     }
 
     // 4. virtual fascicle slots (at most kSlotCap coefficients each) and bins
@@ -840,7 +873,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
                         const uint32_t ug = u0 + 32u * g;
                         if (ug < u1)
                             while (hsrc[k + 1] <= ug) ++k;
-                        cgrp.push_back((uint16_t)(ug < u1 ? k - sl : 0u));
+                        cgrp.push_back((uint16_t)(ug < u1 ? k - sl : ns - 1));
                     }
                     chunks.push_back(u0);
                     chunks.push_back((u1 - u0) | (first ? 0x80000000u : 0u));
@@ -895,10 +928,13 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
         LIFE_CUDA(cudaStreamSynchronize(st));
     }
 
-    LIFE_TRY(dalloc(phi, &phi->b_wfix, (size_t)nvf));
-    LIFE_TRY(dalloc(phi, &phi->b_nanf, (size_t)nvf));
-    LIFE_CUDA(cudaMemsetAsync(phi->b_wfix, 0, (size_t)nvf * 8, st));
-    LIFE_CUDA(cudaMemsetAsync(phi->b_nanf, 0, (size_t)nvf, st));
+    {   // per-fascicle int64 sums, then the non-finite flags (bytes) in the
+        // same buffer so one all-reduce carries both
+        const size_t words = (size_t)nf + ((size_t)nf + 7) / 8;
+        LIFE_TRY(dalloc(phi, &phi->b_wfix, words));
+        phi->b_nanf = reinterpret_cast<unsigned char *>(phi->b_wfix + nf);
+        LIFE_CUDA(cudaMemsetAsync(phi->b_wfix, 0, words * 8, st));
+    }
     phi->b_ka = ka;
     phi->b_n = N;
     phi->b_nch = nch;
@@ -1054,26 +1090,28 @@ __device__ __forceinline__ void side_produce(const SideArgs &A, const uint4 *tab
     BD_FLUSH;
 }
 
-// consumer: tile-major unit of chunk unit u (staged segment records): start
-// at the first segment of u's 32-unit group, walk forward (segments average
-// tens of units, so mostly zero or one step)
+// consumer: tile-major unit of chunk unit u (staged segment records): the
+// segment lies between the first segments of u's 32-unit group and of the
+// next group (build-time table); usually one or two candidates, at most 32
+// when a sparse bin has one-unit segments (binary search)
 __device__ __forceinline__ uint32_t side_dst(uint32_t slot_sa, uint32_t hs, uint32_t u0, uint32_t ns, uint32_t u)
 {
     const uint32_t U = u0 + u;
     const uint32_t src = slot_sa + kSlotSrc + hs, dst = slot_sa + kSlotDst + hs;
-    uint32_t k;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(k) : "r"(slot_sa + kSlotGrp + 2u * (u >> 5)));
-    uint32_t s0, s1;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s0) : "r"(src + 4u * k));
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s1) : "r"(src + 4u * k + 4u));
-    while (s1 <= U) {
-        ++k;
-        s0 = s1;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s1) : "r"(src + 4u * k + 4u));
+    const uint32_t g = u >> 5;
+    uint32_t lo, hi;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(lo) : "r"(slot_sa + kSlotGrp + 2u * g));
+    if (g < 31) asm volatile("ld.shared.u16 %0, [%1];" : "=r"(hi) : "r"(slot_sa + kSlotGrp + 2u * g + 2u));
+    else hi = ns - 1;
+    while (hi > lo) {  // largest k in [lo, hi] with src4[k] <= U
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(src + 4u * mid));
+        if (v <= U) lo = mid; else hi = mid - 1;
     }
-    (void)ns;
-    uint32_t d0;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d0) : "r"(dst + 4u * k));
+    uint32_t s0, d0;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s0) : "r"(src + 4u * lo));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d0) : "r"(dst + 4u * lo));
     return d0 + (U - s0);
 }
 
@@ -1225,12 +1263,28 @@ __global__ void __launch_bounds__(kSideThreads, 1)
         }
     };
     int cur_bin = -1;
+    // flush a bin piece into the per-fascicle sums: the virtual slots of a
+    // fascicle are consecutive, so a warp first sums its runs (segmented
+    // suffix scan) and only run heads issue the int64 atomic
     auto flush = [&]() {
         const int64_t s0 = (int64_t)cur_bin * kSB;
         const int nsl = (int)min((int64_t)kSB, A.nvf - s0);
-        for (int i = ct; i < nsl; i += kCons) {
-            const long long v = (long long)(int32_t)hi[i] * 16777216ll + (long long)lo[i];
-            if (v) atomicAdd(wfix + s0 + i, (unsigned long long)v);
+        for (int ib = (int)ct - lane; ib < nsl; ib += kCons) {
+            const int i = ib + lane;
+            long long v = 0;
+            uint32_t fid = 0xFFFFFFFFu;
+            if (i < nsl) {
+                v = (long long)(int32_t)hi[i] * 16777216ll + (long long)lo[i];
+                fid = __ldg(A.vf2f + s0 + i);
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long ov = __shfl_down_sync(0xffffffffu, v, o);
+                const uint32_t of = __shfl_down_sync(0xffffffffu, fid, o);
+                if (lane + o < 32 && of == fid) v += ov;
+            }
+            const uint32_t pf = __shfl_up_sync(0xffffffffu, fid, 1);
+            if (i < nsl && (lane == 0 || pf != fid) && v) atomicAdd(wfix + fid, (unsigned long long)v);
         }
     };
     if (nch > 0) load_z(0, zn);
@@ -1271,7 +1325,7 @@ __global__ void __launch_bounds__(kSideThreads, 1)
                 if (ids[e] == kPad) continue;
                 const float t = __fmul_rn(zs[e], vs[e]);  // acc * value (_kernels.py:67)
                 if (!isfinite(t)) {
-                    nanf[s0 + ids[e]] = 1;
+                    nanf[__ldg(A.vf2f + s0 + ids[e])] = 1;
                     continue;
                 }
                 const long long q = __double2ll_rn((double)t * scale);
@@ -1288,77 +1342,31 @@ __global__ void __launch_bounds__(kSideThreads, 1)
     BD_FLUSH;
 }
 
-// WC finish: mode 0 = single GPU (fold virtual slots, convert, flags, sum of
-// squares); mode 1 = fold into per-fascicle int64 sums (multi-GPU, before the
-// all-reduce); mode 2 = convert all-reduced sums.
+// WC finish: per-fascicle int64 sums (all-reduced first on multi-GPU runs)
+// to fp32, the non-finite flags, accumulate / project, sum of squares; clears
+// the sums and flags for the next call.
 template <int BT>
 __global__ void __launch_bounds__(BT)
-    k_wc_fin(unsigned long long *__restrict__ wfix, unsigned char *__restrict__ nanf, const uint32_t *__restrict__ f2vf,
-             unsigned long long *__restrict__ wsum, int nf, float *__restrict__ w_out, const float *__restrict__ w_ref,
-             uint32_t flags, const FixParams fx, int nt, int mode, double *part, unsigned *counter, double *sumsq_out,
-             const CallHooks hooks)
+    k_wc_fin(unsigned long long *__restrict__ wfix, unsigned char *__restrict__ nanf, int nf, float *__restrict__ w_out,
+             const float *__restrict__ w_ref, uint32_t flags, const FixParams fx, int nt, double *part, unsigned *counter,
+             double *sumsq_out, const CallHooks hooks)
 {
     if (hooks.done && *hooks.done) return;
     const double inv = ldexp(1.0, -bin_exponent_dev(fx, nt));
     const bool accumulate = flags & LIFE_ACCUMULATE;
     const bool project = (flags & LIFE_PROJECT_GRAD) && w_ref != nullptr;
     double sq = 0.0;
-    const int lane = threadIdx.x & 31;
-    // warp-uniform walk over 32-fascicle groups; a fascicle split into many
-    // virtual slots (a Zipf-heavy one) is folded by the whole warp
-    for (int base = (blockIdx.x * BT + threadIdx.x) & ~31; base < nf; base += gridDim.x * BT) {
-        const int f = base + lane;
-        const bool valid = f < nf;
-        long long q = 0;
-        bool bad = false;
-        if (mode == 2) {
-            if (valid) q = (long long)wsum[f];
-        } else {
-            const uint32_t s0 = valid ? __ldg(f2vf + f) : 0u, s1 = valid ? __ldg(f2vf + f + 1) : 0u;
-            const bool longf = s1 - s0 > 8u;
-            if (!longf)
-                for (uint32_t s = s0; s < s1; ++s) {
-                    q += (long long)wfix[s];
-                    wfix[s] = 0ull;
-                    if (nanf[s]) {
-                        bad = true;
-                        nanf[s] = 0;
-                    }
-                }
-            for (unsigned m = __ballot_sync(0xffffffffu, longf); m; m &= m - 1) {
-                const int l = __ffs(m) - 1;
-                const uint32_t a = __shfl_sync(0xffffffffu, s0, l), b = __shfl_sync(0xffffffffu, s1, l);
-                long long qq = 0;
-                bool bb = false;
-                for (uint32_t s = a + lane; s < b; s += 32) {
-                    qq += (long long)wfix[s];
-                    wfix[s] = 0ull;
-                    if (nanf[s]) {
-                        bb = true;
-                        nanf[s] = 0;
-                    }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
-                bb = __any_sync(0xffffffffu, bb);
-                if (lane == l) {
-                    q = qq;
-                    bad = bb;
-                }
-            }
-            if (mode == 1) {
-                if (valid) wsum[f] = (unsigned long long)q;
-                continue;
-            }
-        }
-        if (!valid) continue;
+    for (int f = blockIdx.x * BT + threadIdx.x; f < nf; f += gridDim.x * BT) {
+        const long long q = (long long)wfix[f];
+        wfix[f] = 0ull;
+        const bool bad = nanf[f] != 0;
+        if (bad) nanf[f] = 0;
         float o = bad ? __int_as_float(0x7fc00000) : (float)((double)q * inv);
         if (accumulate) o = w_out[f] + o;
         if (project && w_ref[f] == 0.f && o > 0.f) o = 0.f;
         w_out[f] = o;
         sq += (double)o * (double)o;
     }
-    if (mode == 1) return;
     __shared__ double s[BT];
     s[threadIdx.x] = sq;
     __syncthreads();
@@ -1921,11 +1929,53 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
 
 // voxels split over several tile rows: sum their partial rows in row order
 // and apply the epilogue; then the DSC outputs over all partials
+// final value of y[vx, col] from its folded sum
+__device__ __forceinline__ void fix_store(float r, size_t o, float *__restrict__ y, const float *__restrict__ b,
+                                          bool accumulate, bool subtract, double &sq, float &amax)
+{
+    if (accumulate) r += y[o];
+    if (subtract) r -= b[o];
+    y[o] = r;
+    sq += (double)r * (double)r;
+    amax = fmaxf(amax, fabsf(r));
+}
+
+// per-CTA (sum of squares, max) into the reduction slot part
+__device__ __forceinline__ void fix_partial(double sq, float amax, const ReduceSlots &red, int part)
+{
+    __shared__ double s_sq[32];
+    __shared__ float s_mx[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    if (lane == 0) {
+        s_sq[warp] = sq;
+        s_mx[warp] = amax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        float m = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            t += s_sq[i];
+            m = fmaxf(m, s_mx[i]);
+        }
+        red.part_d[part] = t;
+        red.part_f[part] = m;
+    }
+}
+
+// DSC fixup of split voxels, step 1: one warp per piece (at most kFixRows
+// partial rows, lanes over directions); single-piece voxels are final here,
+// the others store their piece sums for k_tile_dsc_fold
 template <int N>
-__global__ void __launch_bounds__(256)
-    k_tile_dsc_fix(const uint32_t *__restrict__ fixptr, const int *__restrict__ fixvox, int nfix,
-                   const float *__restrict__ ypart, int nt, float *__restrict__ y, const float *__restrict__ b,
-                   uint32_t flags, const ReduceSlots red, int part0, const DscOut out, const CallHooks hooks,
+__global__ void __launch_bounds__(512)
+    k_tile_dsc_fix(const uint4 *__restrict__ pcs, int npc, const float *__restrict__ ypart, int nt,
+                   float *__restrict__ fixsum, float *__restrict__ y, const float *__restrict__ b, uint32_t flags,
+                   const ReduceSlots red, int part0, int finish, const DscOut out, const CallHooks hooks,
                    const unsigned long long *__restrict__ skip_part, int nskip, unsigned *__restrict__ nonfinite)
 {
     if (hooks.done && *hooks.done) return;
@@ -1934,31 +1984,53 @@ __global__ void __launch_bounds__(256)
     const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
     double sq = 0.0;
     float amax = 0.f;
-    for (int m = blockIdx.x * 8 + warp; m < nfix; m += gridDim.x * 8) {
-        const int vx = fixvox[m];
-        const uint32_t r0 = fixptr[m], r1 = fixptr[m + 1];
+    for (int p = blockIdx.x * 16 + warp; p < npc; p += gridDim.x * 16) {
+        const uint4 d = __ldg(pcs + p);  // voxel, first row, end row, piece-sum slot (or ~0: final)
         for (int col = lane; col < nt; col += 32) {
             float r = 0.f;
-            for (uint32_t p = r0; p < r1; ++p) r += ypart[(size_t)p * N + col];
-            const size_t o = (size_t)vx * nt + col;
-            if (accumulate) r += y[o];
-            if (subtract) r -= b[o];
-            y[o] = r;
-            sq += (double)r * (double)r;
-            amax = fmaxf(amax, fabsf(r));
+            for (uint32_t q = d.y; q < d.z; ++q) r += ypart[(size_t)q * N + col];
+            if (d.w != 0xFFFFFFFFu) fixsum[(size_t)d.w * N + col] = r;
+            else fix_store(r, (size_t)d.x * nt + col, y, b, accumulate, subtract, sq, amax);
         }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    fix_partial(sq, amax, red, part0 + blockIdx.x);
+    if (finish && last_cta(red.counter))
+        dsc_finish(red, part0 + (int)gridDim.x, skip_part, nskip, out, red.counter, hooks, 512, nonfinite);
+}
+
+// step 2: one CTA per voxel of several pieces; thread (group g, direction c)
+// sums pieces g, g + G, ..., then the groups are added in order
+template <int N>
+__global__ void __launch_bounds__(1024)
+    k_tile_dsc_fold(const uint32_t *__restrict__ big, const uint32_t *__restrict__ bpp, int nbig,
+                    const float *__restrict__ fixsum, int nt, float *__restrict__ y, const float *__restrict__ b,
+                    uint32_t flags, const ReduceSlots red, int part0, const DscOut out, const CallHooks hooks,
+                    const unsigned long long *__restrict__ skip_part, int nskip, unsigned *__restrict__ nonfinite)
+{
+    if (hooks.done && *hooks.done) return;
+    __shared__ float buf[1024];
+    const bool accumulate = flags & LIFE_ACCUMULATE;
+    const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
+    const int G = 1024 / nt, t = threadIdx.x, c = t % nt, g = t / nt;
+    double sq = 0.0;
+    float amax = 0.f;
+    for (int i = blockIdx.x; i < nbig; i += gridDim.x) {
+        const uint32_t s0 = __ldg(bpp + i), s1 = __ldg(bpp + i + 1);
+        float r = 0.f;
+        if (g < G)
+            for (uint32_t q = s0 + g; q < s1; q += G) r += fixsum[(size_t)q * N + c];
+        buf[t] = r;
+        __syncthreads();
+        if (t < nt) {
+            float tot = 0.f;
+            for (int k = 0; k < G; ++k) tot += buf[k * nt + t];
+            fix_store(tot, (size_t)__ldg(big + i) * nt + t, y, b, accumulate, subtract, sq, amax);
+        }
+        __syncthreads();
     }
-    if (lane == 0) {
-        red.part_d[part0 + blockIdx.x * 8 + warp] = sq;
-        red.part_f[part0 + blockIdx.x * 8 + warp] = amax;
-    }
+    fix_partial(sq, amax, red, part0 + blockIdx.x);
     if (last_cta(red.counter))
-        dsc_finish(red, part0 + (int)gridDim.x * 8, skip_part, nskip, out, red.counter, hooks, 256, nonfinite);
+        dsc_finish(red, part0 + (int)gridDim.x, skip_part, nskip, out, red.counter, hooks, 1024, nonfinite);
 }
 
 // WC tile side.  Roles (warps):
@@ -2300,11 +2372,20 @@ int dsc_t(life_phi *phi, const float *w, float *y, const float *b, uint32_t flag
         phi->b_nonfin, fin, phi->b_dsc_cap);
     LIFE_CHECK_LAUNCH();
     if (!fin) {
-        const int blocks = std::max(1, std::min(phi->sms, (phi->b_nfix + 7) / 8));
-        k_tile_dsc_fix<N><<<blocks, 256, 0, st>>>(phi->b_fixptr, phi->b_fixvox, phi->b_nfix, phi->b_ypart, phi->nt,
-                                                  y, b, flags, phi->red, phi->b_tile_grid * CD::kWarps, o, h,
-                                                  phi->b_skip, phi->b_side_grid, phi->b_nonfin);
+        const int part0 = phi->b_tile_grid * CD::kWarps;
+        const int ga = std::max(1, std::min(phi->sms * 4, (phi->b_npc + 15) / 16));
+        k_tile_dsc_fix<N><<<ga, 512, 0, st>>>(reinterpret_cast<const uint4 *>(phi->b_fixpc), phi->b_npc, phi->b_ypart,
+                                              phi->nt, phi->b_fixsum, y, b, flags, phi->red, part0,
+                                              phi->b_nbig == 0 ? 1 : 0, o, h, phi->b_skip, phi->b_side_grid,
+                                              phi->b_nonfin);
         LIFE_CHECK_LAUNCH();
+        if (phi->b_nbig) {
+            const int gf = std::min(phi->sms, phi->b_nbig);
+            k_tile_dsc_fold<N><<<gf, 1024, 0, st>>>(phi->b_fixbig, phi->b_fixbpp, phi->b_nbig, phi->b_fixsum, phi->nt,
+                                                    y, b, flags, phi->red, part0 + ga, o, h, phi->b_skip,
+                                                    phi->b_side_grid, phi->b_nonfin);
+            LIFE_CHECK_LAUNCH();
+        }
     }
     return LIFE_OK;
 }
@@ -2362,22 +2443,19 @@ int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, c
     k_side_wc<<<phi->b_side_grid, kSideThreads, phi->b_wcs_smem, st>>>(side_args(phi), chunk_args(phi), phi->b_scr, fx, phi->nt,
                                                                           phi->b_wfix, phi->b_nanf, h);
     LIFE_CHECK_LAUNCH();
-    const int blocks = std::max(1, std::min(phi->sms * 4, (phi->nf + 255) / 256));
     if (comm && comm->nranks > 1) {
-        if (!phi->b_wsum) LIFE_TRY(dalloc(phi, &phi->b_wsum, (size_t)phi->nf));
-        k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->b_f2vf, phi->b_wsum, phi->nf, w, w_ref,
-                                              flags, fx, phi->nt, 1, phi->part_d2, phi->counter2, sumsq, h);
-        LIFE_CHECK_LAUNCH();
-        if (comm->allreduce(phi->b_wsum, phi->nf, LIFE_DT_I64, LIFE_OP_SUM, st, comm->ctx) != 0)
-            return fail(LIFE_ERR_NCCL, "allreduce(wsum) failed");
-        k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->b_f2vf, phi->b_wsum, phi->nf, w, w_ref,
-                                              flags, fx, phi->nt, 2, phi->part_d2, phi->counter2, sumsq, h);
-        LIFE_CHECK_LAUNCH();
-    } else {
-        k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->b_f2vf, nullptr, phi->nf, w, w_ref,
-                                              flags, fx, phi->nt, 0, phi->part_d2, phi->counter2, sumsq, h);
-        LIFE_CHECK_LAUNCH();
+        // one integer all-reduce: the fascicle sums and, in the tail, the
+        // non-finite flags as 8-bit counters (8 fascicles per word, no carry
+        // for fewer than 256 ranks); sums are exact, so every rank gets
+        // bit-identical totals whatever the reduction order
+        const int64_t cnt = (int64_t)phi->nf + (phi->nf + 7) / 8;
+        if (comm->allreduce(phi->b_wfix, cnt, LIFE_DT_I64, LIFE_OP_SUM, st, comm->ctx) != 0)
+            return fail(LIFE_ERR_NCCL, "allreduce(wfix) failed");
     }
+    const int blocks = std::max(1, std::min(phi->sms * 4, (phi->nf + 255) / 256));
+    k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->nf, w, w_ref, flags, fx, phi->nt,
+                                          phi->part_d2, phi->counter2, sumsq, h);
+    LIFE_CHECK_LAUNCH();
     return LIFE_OK;
 }
 

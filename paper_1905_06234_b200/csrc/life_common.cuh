@@ -158,12 +158,13 @@ struct life_phi {
     uint16_t *b_Ddsc = nullptr;    // per chunk: f16 [hi|lo][N][64 atoms] swizzled D^T * 256 (DSC B operand)
     uint16_t *b_Dwc = nullptr;     // per chunk: f16 [hi|lo][N/64][64 atoms][64] swizzled D * 256 (WC B operand)
     float *b_ypart = nullptr;      // [nprow * N] rows of voxels split over several rows
-    uint32_t *b_fixptr = nullptr;  // [nfix + 1] partial rows of each split voxel
-    int *b_fixvox = nullptr;       // [nfix]
-    int b_nfix = 0, b_nprow = 0;
-    unsigned long long *b_wfix = nullptr;  // [nvf] int64 fixed-point sums (zero between calls)
-    unsigned char *b_nanf = nullptr;       // [nvf] non-finite term seen
-    unsigned long long *b_wsum = nullptr;  // [nf] per-fascicle sums for multi-GPU reduction
+    uint32_t *b_fixpc = nullptr;   // [npc] uint4 fixup pieces: voxel, first row, end row, piece-sum slot (~0: final)
+    uint32_t *b_fixbig = nullptr;  // [nbig] voxels folded from several pieces
+    uint32_t *b_fixbpp = nullptr;  // [nbig + 1] their piece-sum slots
+    float *b_fixsum = nullptr;     // [piece-sum slots][N]
+    int b_nfix = 0, b_nprow = 0, b_npc = 0, b_nbig = 0;
+    unsigned long long *b_wfix = nullptr;  // [nf + ceil(nf/8)] int64 fixed-point fascicle sums, then the flags (zero between calls)
+    unsigned char *b_nanf = nullptr;       // [nf] non-finite term seen (bytes in the tail of b_wfix)
     unsigned long long *b_skip = nullptr;  // [side grid] skip-count partials of the bin side
     float *b_smax = nullptr;               // [side grid] max |s| partials (DSC fixed-point scale)
     unsigned *b_nonfin = nullptr;          // non-finite s seen by the DSC bin side (this call)
