@@ -365,9 +365,14 @@ def run_ours(args, dims):
             tt = torch.tensor([e2e_s], device="cuda")
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             e2e_s = float(tt.item())
-        h2d = nc * (4 * 3 + 8) + na * nt * 8 + nv * nt * 8
+        # bytes crossing PCIe (life_phi_create with LIFE_PHI_HOST_INPUT): atoms as
+        # u16 when na <= 65536, voxels and fibers u32, values f32 (fp32-only
+        # operator); the dictionary and b as f64
+        h2d = nc * ((2 if na <= 65536 else 4) + 4 + 4 + 4) + na * nt * 8 + nv * nt * 8
+        cached = fresh.__dict__.get("_device_cache", {}).get("op")
         e2e = {"value": args.steps / e2e_s, "unit": UNIT,
                "setup_s": round(tr.setup_seconds, 3), "loop_s": round(tr.loop_seconds, 4),
+               "create_ms": round(cached[0].info.sort_ms, 1) if cached else None,
                "other_s": round(e2e_s - tr.setup_seconds - tr.loop_seconds, 3),
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": nf * 8 // args.steps,
                "seconds": round(e2e_s, 3),

@@ -91,6 +91,7 @@ LIFE_API uint64_t life_launch_count(void);
 #define LIFE_PHI_NO_TENSOR    0x20u /* fp32: no tcgen05 products (CUDA cores only) */
 #define LIFE_PHI_TENSOR       0x40u /* fp32: single-pass tcgen05 tile products (with LIFE_PHI_NO_BIN) */
 #define LIFE_PHI_NO_BIN       0x80u /* fp32: not the binned two-phase products (life_bin.cu)   */
+#define LIFE_PHI_VALUES_F32   0x100u /* with HOST_INPUT: values may cross PCIe as f32 (fp32-only operator; ignored with EXACT_F64) */
 
 /* Build the device operator from COO arrays (PhiTensor + Dictionary,
  * tensor.py:76-170).  atoms/voxels/fibers: u32[n_coeffs]; values:
@@ -105,6 +106,12 @@ LIFE_API int life_phi_create(const life_dims *dims, const uint32_t *atoms,
                     const double *values, const double *dict, uint32_t flags,
                     void *stream, life_phi **out, int64_t *bad_position);
 LIFE_API int life_phi_destroy(life_phi *phi);
+
+/* Copy bytes from pageable host memory to the device through pinned staging
+ * buffers (host memcpy overlapped with the DMA); stream-ordered, returns when
+ * the source may be reused.  Used for the LIFE_PHI_HOST_INPUT arrays and by
+ * the Python layer for b / w0 (sbbnnls.solve's inputs, sbbnnls.py:223). */
+LIFE_API int life_copy_h2d(void *dst_dev, const void *src_host, int64_t bytes, void *stream);
 
 typedef struct life_phi_info {
     life_dims dims;

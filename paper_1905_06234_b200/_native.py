@@ -26,6 +26,7 @@ PHI_FORCE_DENSE = 0x10
 PHI_NO_TENSOR = 0x20
 PHI_TENSOR = 0x40
 PHI_NO_BIN = 0x80
+PHI_VALUES_F32 = 0x100
 ACCUMULATE = 0x01
 SKIP_ZERO = 0x02
 SUBTRACT_B = 0x04
@@ -92,6 +93,7 @@ SIGNATURES = {
                                        c_void_p, c_void_p, c_u32, c_void_p,
                                        ctypes.POINTER(c_void_p), ctypes.POINTER(c_i64)]),
     "life_phi_destroy": (ctypes.c_int, [c_void_p]),
+    "life_copy_h2d": (ctypes.c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "life_phi_get_info": (ctypes.c_int, [c_void_p, ctypes.POINTER(PhiInfo)]),
     "life_stable_argsort_u32": (ctypes.c_int, [c_void_p, c_i64, c_void_p, c_void_p]),
     "life_detect_runs_u32": (ctypes.c_int, [c_void_p, c_i64, c_void_p, c_void_p,

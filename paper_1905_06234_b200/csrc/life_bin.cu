@@ -555,7 +555,7 @@ static inline size_t sw16(uint32_t row, uint32_t k)
 int prepare_bin(life_phi *phi);
 
 int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f, const double *val,
-              const std::vector<double> &hdict, cudaStream_t st)
+              const std::vector<double> &hdict, const std::function<int()> &ready_fv, cudaStream_t st)
 {
     using namespace bin;
     const int64_t n = phi->nc;
@@ -605,6 +605,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     k_rank_va<<<gridn(n), 256, 0, st>>>(skva, perm, rstart, n, na, rank_o, vmaxr);
     LIFE_CHECK_LAUNCH();
 
+    setup_mark(st, "bin phase 1");
     // 2. tile rows: a voxel gets one row per kRanks duplicate ranks
     uint32_t *nr, *rowbase, *row_o;
     unsigned *rcnt;
@@ -626,6 +627,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     LIFE_CUDA(cudaMemcpyAsync(hbase.data(), rowbase, ((size_t)nv + 1) * 4, cudaMemcpyDeviceToHost, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
 
+    setup_mark(st, "bin phase 2");
     // 3. deal rows to tiles: counting sort by coefficient count (descending,
     // stable), snake order over the tiles so every tile carries about the
     // same number of coefficients
@@ -702,6 +704,8 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
         LIFE_CUDA(cudaStreamSynchronize(st));
     }
 
+    setup_mark(st, "bin phase 3");
+    LIFE_TRY(ready_fv());  // phases 1-3 read only atoms and voxels
     // 4. virtual fascicle slots (at most kSlotCap coefficients each) and bins
     unsigned *fcnt;
     uint32_t *nslot, *vf_o;
@@ -737,6 +741,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     }
     const int nbins = (int)((nvf + kSB - 1) / kSB);
 
+    setup_mark(st, "bin phase 4");
     // 5. bin-major order (bin, tile, chunk), stable; its runs are the
     // segments, each padded to 4 entries in both orders
     unsigned long long *kbm = kva, *skbm = skva;
@@ -816,6 +821,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     LIFE_CUDA(cudaMemcpyAsync(&nbm4, phi->b_segsrc + nseg, 4, cudaMemcpyDeviceToHost, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
 
+    setup_mark(st, "bin phase 5");
     // 6. placement (pads: cellr kPad, vid kPad, value 0)
     const int64_t nbm = (int64_t)nbm4 * 4;
     LIFE_TRY(dalloc(phi, &phi->b_cellr, (size_t)npad + 8));
@@ -832,6 +838,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
                                       d_slot, ka, phi->b_vid, phi->b_val, phi->b_cellr);
     LIFE_CHECK_LAUNCH();
 
+    setup_mark(st, "bin phase 6");
     // 7. bin and CTA segment ranges of the bin side
     LIFE_TRY(dalloc(phi, &phi->b_binptr, (size_t)nbins + 1));
     k_bin_seg<<<gridn(nbins + 1), 256, 0, st>>>(segkey, nseg, nbins, per_bin, phi->b_binptr);
@@ -898,6 +905,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
         LIFE_CUDA(cudaStreamSynchronize(st));
     }
 
+    setup_mark(st, "bin phase 7");
     // 8. dictionary chunks as the two B operands: f16 hi | lo of D * kDScale,
     // K-major SWIZZLE_128B (64 f16 per 128-byte row)
     {

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -207,6 +208,13 @@ struct life_phi {
 };
 
 namespace life {
+// pageable host -> device through pinned staging (life_phi.cu)
+int h2d_staged(void *dst, const void *src, size_t bytes, cudaStream_t st);
+int h2d_staged_cvt(void *dst, const void *src, size_t bytes, int mode, cudaStream_t st);  // 1: f64->f32, 2: u32->u16
+// LIFE_B200_SETUP_TRACE=1: synchronize and print the time since the last mark
+// (operator construction phases, stderr)
+void setup_mark(cudaStream_t st, const char *what);
+
 template <typename T>
 int dalloc(life_phi *phi, T **p, size_t n)
 {
@@ -288,7 +296,8 @@ int launch_dsc_tc(life_phi *phi, const float *w, float *y, const float *b, uint3
 int prepare_tc(life_phi *phi);
 // binned two-phase products (life_bin.cu)
 int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
-              const double *val, const std::vector<double> &hdict, cudaStream_t st);
+              const double *val, const std::vector<double> &hdict, const std::function<int()> &ready_fv,
+              cudaStream_t st);  // ready_fv(): fibers/values resident (called before they are read)
 int launch_dsc_bin(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
                    const DscOut &o, const CallHooks &h, cudaStream_t st);
 int bin_tile_warps(const life_phi *phi);

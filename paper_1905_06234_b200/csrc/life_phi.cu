@@ -11,8 +11,13 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
+#include <thread>
+#include <vector>
 #include <unordered_map>
 
 #include "life_common.cuh"
@@ -75,10 +80,21 @@ __global__ void k_check_range(const uint32_t *a, const uint32_t *v,
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        if (a[i] >= na) atomicMin(&first_bad[0], (unsigned long long)i);
-        if (v[i] >= nv) atomicMin(&first_bad[1], (unsigned long long)i);
-        if (f[i] >= nf) atomicMin(&first_bad[2], (unsigned long long)i);
+        if (a && a[i] >= na) atomicMin(&first_bad[0], (unsigned long long)i);
+        if (v && v[i] >= nv) atomicMin(&first_bad[1], (unsigned long long)i);
+        if (f && f[i] >= nf) atomicMin(&first_bad[2], (unsigned long long)i);
     }
+}
+
+__global__ void k_widen_u16(const uint16_t *in, int64_t n, uint32_t *out)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+__global__ void k_widen_f32(const float *in, int64_t n, double *out)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (double)in[i];
 }
 
 // composite key: (atom group) * nv + voxel
@@ -253,6 +269,124 @@ using namespace life;
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Host -> device copies of pageable host arrays through a process-wide ring of
+// pinned staging buffers: the host memcpy of chunk k+1 overlaps the DMA of
+// chunk k (pageable cudaMemcpy runs at ~7 GB/s on the B200 hosts, pinned DMA
+// at ~53 GB/s; tools/h2d_probe.py).
+// ---------------------------------------------------------------------------
+namespace {
+constexpr size_t kStageChunk = 16u << 20;
+constexpr int kStageThreads = 12;  // one host memcpy stream reaches ~10 GB/s
+struct Staging {
+    std::mutex mu;
+    void *buf[kStageThreads][2] = {};
+    cudaEvent_t ev[kStageThreads][2] = {};
+    int dev = -1;
+};
+Staging &staging()
+{
+    static Staging *s = new Staging;  // process lifetime (pinned memory freed at exit)
+    return *s;
+}
+}  // namespace
+
+namespace life {
+// Thread t copies chunks t, t + T, ... through its two pinned slots; the
+// copies of all threads go to the caller's stream (distinct destinations, so
+// their order does not matter); a slot is reused once its event completed.
+void setup_mark(cudaStream_t st, const char *what)
+{
+    static const bool on = [] {
+        const char *e = std::getenv("LIFE_B200_SETUP_TRACE");
+        return e && *e && *e != '0';
+    }();
+    if (!on) return;
+    static auto last = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[life setup] %-28s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
+int h2d_staged(void *dst, const void *src, size_t bytes, cudaStream_t st) { return h2d_staged_cvt(dst, src, bytes, 0, st); }
+
+// mode 0: copy; 1: f64 -> f32; 2: u32 -> u16 (`bytes` counts the DESTINATION)
+int h2d_staged_cvt(void *dst, const void *src, size_t bytes, int mode, cudaStream_t st)
+{
+    if (bytes == 0) return LIFE_OK;
+    const size_t in_per_out = mode == 0 ? 1 : 2;  // source bytes per destination byte
+    auto stage = [mode](void *out, const char *in, size_t m) {  // m destination bytes
+        if (mode == 0) {
+            std::memcpy(out, in, m);
+        } else if (mode == 1) {
+            const double *x = reinterpret_cast<const double *>(in);
+            float *y = static_cast<float *>(out);
+            for (size_t i = 0, k = m / 4; i < k; ++i) y[i] = (float)x[i];
+        } else {
+            const uint32_t *x = reinterpret_cast<const uint32_t *>(in);
+            uint16_t *y = static_cast<uint16_t *>(out);
+            for (size_t i = 0, k = m / 2; i < k; ++i) y[i] = (uint16_t)x[i];
+        }
+    };
+    if (mode == 0 && bytes < (4u << 20)) {  // small: one direct copy
+        LIFE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return LIFE_OK;
+    }
+    Staging &S = staging();
+    std::lock_guard<std::mutex> lk(S.mu);
+    int dev = 0;
+    LIFE_CUDA(cudaGetDevice(&dev));
+    if (S.dev != dev) {  // (re)create on this device's context
+        for (auto &row : S.ev)
+            for (auto &e : row) {
+                if (e) cudaEventDestroy(e);
+                e = nullptr;
+            }
+        for (auto &row : S.buf)
+            for (auto &p : row) {
+                if (p) cudaFreeHost(p);
+                p = nullptr;
+            }
+        for (int t = 0; t < kStageThreads; ++t)
+            for (int j = 0; j < 2; ++j) {
+                LIFE_CUDA(cudaHostAlloc(&S.buf[t][j], kStageChunk, cudaHostAllocDefault));
+                LIFE_CUDA(cudaEventCreateWithFlags(&S.ev[t][j], cudaEventDisableTiming));
+            }
+        S.dev = dev;
+    }
+    const size_t nchunk = (bytes + kStageChunk - 1) / kStageChunk;
+    const int T = (int)std::min<size_t>(kStageThreads, nchunk);
+    std::vector<cudaError_t> err(T, cudaSuccess);
+    auto work = [&](int t) {
+        cudaError_t e = cudaSetDevice(dev);
+        int n = 0;
+        for (size_t k = t; k < nchunk && e == cudaSuccess; k += T, ++n) {
+            const int j = n & 1;
+            const size_t off = k * kStageChunk, m = std::min(kStageChunk, bytes - off);
+            if ((e = cudaEventSynchronize(S.ev[t][j])) != cudaSuccess) break;  // slot's previous DMA done
+            stage(S.buf[t][j], static_cast<const char *>(src) + off * in_per_out, m);
+            if ((e = cudaMemcpyAsync(static_cast<char *>(dst) + off, S.buf[t][j], m, cudaMemcpyHostToDevice, st)) !=
+                cudaSuccess)
+                break;
+            e = cudaEventRecord(S.ev[t][j], st);
+        }
+        err[t] = e;
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto &th : pool) th.join();
+    for (cudaError_t e : err)
+        if (e != cudaSuccess) return fail(LIFE_ERR_CUDA, std::string("staged copy: ") + cudaGetErrorString(e));
+    // the staging slots are reused by the next call: make its waits valid
+    for (int t = 0; t < T; ++t)
+        for (int j = 0; j < 2; ++j) LIFE_CUDA(cudaEventRecord(S.ev[t][j], st));
+    return LIFE_OK;
+}
+}  // namespace life
+
 extern "C" {
 
 int life_abi_version(void) { return LIFE_B200_ABI_VERSION; }
@@ -581,6 +715,7 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
     if (!dict) return fail(LIFE_ERR_INVALID_ARGUMENT, "null dictionary");
 
     auto t0 = std::chrono::steady_clock::now();
+    setup_mark(st, "start");
     {   // keep freed stream-ordered allocations mapped for reuse (restructuring
         // temporaries are GBs at C2; re-mapping them each create costs seconds)
         static bool pool_set = false;
@@ -621,6 +756,22 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
     const uint32_t *a = atoms, *v = voxels, *f = fibers;
     const double *val = values, *D = dict;
     const size_t dlen = (size_t)phi->na * phi->nt;
+    // Host input: atoms, voxels and the dictionary are staged now; fibers and
+    // values follow from a host thread on a side stream while the first
+    // restructuring phases (which read only atoms and voxels) run.
+    struct Deferred {
+        std::thread th;
+        cudaStream_t s2 = nullptr;
+        cudaEvent_t ev = nullptr;
+        int rc = LIFE_OK;
+        std::string msg;
+        ~Deferred()
+        {
+            if (th.joinable()) th.join();
+            if (ev) cudaEventDestroy(ev);
+            if (s2) cudaStreamDestroy(s2);
+        }
+    } dfr;
     if (host) {
         uint32_t *da, *dv, *df;
         double *dval, *dD;
@@ -630,25 +781,69 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         LIFE_CUDA(cudaMalloc(&df, nn * 4)); guard.tmp.push_back(df);
         LIFE_CUDA(cudaMalloc(&dval, nn * 8)); guard.tmp.push_back(dval);
         LIFE_CUDA(cudaMalloc(&dD, dlen * 8)); guard.tmp.push_back(dD);
-        if (n > 0) {
-            LIFE_CUDA(cudaMemcpyAsync(da, atoms, n * 4, cudaMemcpyHostToDevice, st));
-            LIFE_CUDA(cudaMemcpyAsync(dv, voxels, n * 4, cudaMemcpyHostToDevice, st));
-            LIFE_CUDA(cudaMemcpyAsync(df, fibers, n * 4, cudaMemcpyHostToDevice, st));
-            LIFE_CUDA(cudaMemcpyAsync(dval, values, n * 8, cudaMemcpyHostToDevice, st));
+        // fewer bytes over PCIe: atoms as u16 when they fit (widened on the
+        // device, lossless); values as f32 when the caller allows it
+        // (LIFE_PHI_VALUES_F32: fp32-only operator, whose kernels round the
+        // values to f32 anyway)
+        const bool a16 = phi->na <= 65536 && n > 0;
+        const bool v32 = (flags & LIFE_PHI_VALUES_F32) && !(flags & LIFE_PHI_EXACT_F64) && n > 0;
+        void *narrow = nullptr;
+        if (a16 || v32) {
+            LIFE_CUDA(cudaMalloc(&narrow, (size_t)n * 4));
+            guard.tmp.push_back(narrow);
         }
-        LIFE_CUDA(cudaMemcpyAsync(dD, dict, dlen * 8, cudaMemcpyHostToDevice, st));
+        uint16_t *na16 = static_cast<uint16_t *>(narrow);
+        float *nv32 = static_cast<float *>(narrow);  // reused after the atoms are widened
+        if (n > 0) {
+            if (a16) {
+                LIFE_TRY(h2d_staged_cvt(na16, atoms, (size_t)n * 2, 2, st));
+                k_widen_u16<<<grid_for(n), 256, 0, st>>>(na16, n, da);
+                LIFE_CHECK_LAUNCH();
+            } else {
+                LIFE_TRY(h2d_staged(da, atoms, (size_t)n * 4, st));
+            }
+            LIFE_TRY(h2d_staged(dv, voxels, (size_t)n * 4, st));
+        }
+        if (v32 && a16) {  // the side stream must not overwrite the u16 atoms before they are widened
+            LIFE_CUDA(cudaStreamSynchronize(st));
+        }
+        LIFE_TRY(h2d_staged(dD, dict, dlen * 8, st));
+        if (n > 0) {
+            LIFE_CUDA(cudaStreamCreateWithFlags(&dfr.s2, cudaStreamNonBlocking));
+            LIFE_CUDA(cudaEventCreateWithFlags(&dfr.ev, cudaEventDisableTiming));
+            dfr.th = std::thread([&dfr, df, dval, fibers, values, n, v32, nv32, dev = phi->device] {
+                cudaSetDevice(dev);
+                int rc = h2d_staged(df, fibers, (size_t)n * 4, dfr.s2);
+                if (rc == LIFE_OK) {
+                    if (v32) {
+                        rc = h2d_staged_cvt(nv32, values, (size_t)n * 4, 1, dfr.s2);
+                        if (rc == LIFE_OK) {
+                            k_widen_f32<<<grid_for(n), 256, 0, dfr.s2>>>(nv32, n, dval);
+                            if (cudaGetLastError() != cudaSuccess) rc = fail(LIFE_ERR_CUDA, "widen launch");
+                        }
+                    } else {
+                        rc = h2d_staged(dval, values, (size_t)n * 8, dfr.s2);
+                    }
+                }
+                if (rc == LIFE_OK && cudaEventRecord(dfr.ev, dfr.s2) != cudaSuccess) rc = fail(LIFE_ERR_CUDA, "event record");
+                if (rc != LIFE_OK) dfr.msg = life_last_error();
+                dfr.rc = rc;
+            });
+        }
         a = da; v = dv; f = df; val = dval; D = dD;
     }
+    setup_mark(st, "h2d (atoms, voxels)");
 
-    // index range check (validate(), tensor.py:232-286; first bad position)
-    {
-        unsigned long long *bad = nullptr;
-        LIFE_CUDA(cudaMalloc(&bad, 3 * sizeof(unsigned long long)));
-        guard.tmp.push_back(bad);
+    // index range check (validate(), tensor.py:232-286; first bad position):
+    // atoms and voxels now, fibers once they are on the device
+    unsigned long long *bad = nullptr;
+    LIFE_CUDA(cudaMalloc(&bad, 3 * sizeof(unsigned long long)));
+    guard.tmp.push_back(bad);
+    auto range_check = [&](bool av, bool fib) -> int {
         LIFE_CUDA(cudaMemsetAsync(bad, 0xFF, 3 * sizeof(unsigned long long), st));
         if (n > 0) {
-            k_check_range<<<grid_for(n), 256, 0, st>>>(a, v, f, n, phi->na, phi->nv,
-                                                       phi->nf, bad);
+            k_check_range<<<grid_for(n), 256, 0, st>>>(av ? a : nullptr, av ? v : nullptr, fib ? f : nullptr, n,
+                                                       phi->na, phi->nv, phi->nf, bad);
             LIFE_CHECK_LAUNCH();
         }
         unsigned long long hb[3];
@@ -659,23 +854,25 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
             if (hb[i] != ~0ull) {
                 if (bad_position) *bad_position = (int64_t)hb[i];
                 return fail(LIFE_ERR_INDEX_OUT_OF_RANGE,
-                            std::string(names[i]) + " index out of range at position " +
-                                std::to_string(hb[i]));
+                            std::string(names[i]) + " index out of range at position " + std::to_string(hb[i]));
             }
-    }
+        return LIFE_OK;
+    };
+    LIFE_TRY(range_check(true, !host));
 
-    // host copy of the dictionary (small): fp32 slices and row norms
-    std::vector<double> hdict(dlen);
-    LIFE_CUDA(cudaMemcpyAsync(hdict.data(), D, dlen * 8, cudaMemcpyDeviceToHost, st));
-    LIFE_CUDA(cudaStreamSynchronize(st));
-    double dmax = 0.0;
-    for (int64_t at = 0; at < phi->na; ++at) {
-        double s = 0.0;
-        for (int t = 0; t < phi->nt; ++t) s += hdict[at * phi->nt + t] * hdict[at * phi->nt + t];
-        dmax = std::max(dmax, std::sqrt(s));
-    }
-    phi->dmax = dmax * (1.0 + 1e-6);
-    {
+    // fibers and values resident (joins the staging thread), fiber range
+    // check, value bound and fascicle sizes; idempotent
+    bool fv_ready = false;
+    auto ready_fv = [&]() -> int {
+        if (fv_ready) return LIFE_OK;
+        fv_ready = true;
+        if (dfr.th.joinable()) {
+            dfr.th.join();
+            if (dfr.rc != LIFE_OK) return fail(dfr.rc, dfr.msg);
+            LIFE_CUDA(cudaStreamWaitEvent(st, dfr.ev, 0));
+            LIFE_TRY(range_check(false, true));
+        }
+        setup_mark(st, "h2d (fibers, values)");
         unsigned long long *vm = nullptr;
         unsigned *cnt = nullptr, *mx = nullptr;
         LIFE_CUDA(cudaMalloc(&vm, 8)); guard.tmp.push_back(vm);
@@ -703,7 +900,20 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         phi->fmax_nnz = std::max<int64_t>(hmx[0], 1);
         phi->max_fiber_run = hmx[0];
         phi->n_fiber_runs = hmx[1];
+        return LIFE_OK;
+    };
+
+    // host copy of the dictionary (small): fp32 slices and row norms
+    std::vector<double> hdict(dlen);
+    LIFE_CUDA(cudaMemcpyAsync(hdict.data(), D, dlen * 8, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    double dmax = 0.0;
+    for (int64_t at = 0; at < phi->na; ++at) {
+        double s = 0.0;
+        for (int t = 0; t < phi->nt; ++t) s += hdict[at * phi->nt + t] * hdict[at * phi->nt + t];
+        dmax = std::max(dmax, std::sqrt(s));
     }
+    phi->dmax = dmax * (1.0 + 1e-6);
 
     if (!(flags & LIFE_PHI_NO_FAST_F32)) {
         // Layout choice: register-tiled dense kernels when voxels
@@ -738,7 +948,10 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         const char *bin_env = getenv("LIFE_BIN");
         const bool want_bin = dense && !(flags & (LIFE_PHI_NO_TENSOR | LIFE_PHI_NO_BIN)) &&
                               !(bin_env && bin_env[0] == '0');
-        if (want_bin) LIFE_TRY(build_bin(phi, a, v, f, val, hdict, st));
+        setup_mark(st, "checks + dictionary");
+        if (want_bin) LIFE_TRY(build_bin(phi, a, v, f, val, hdict, ready_fv, st));
+        setup_mark(st, "build_bin");
+        LIFE_TRY(ready_fv());
         if (phi->has_bin) dense = false;
         if (dense) LIFE_TRY(build_dense(phi, a, v, f, val, hdict, st));
         // tcgen05 DSC over its own tile layout (life_tc.cu) next to the dense
@@ -755,6 +968,7 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
             LIFE_TRY(build_tc(phi, a, v, f, val, hdict, st));
         if (!phi->has_dense && !phi->has_bin) LIFE_TRY(build_fast(phi, a, v, f, val, hdict, st));
     }
+    LIFE_TRY(ready_fv());
     std::vector<int64_t> fiber_start;
     if (flags & LIFE_PHI_EXACT_F64)
         LIFE_TRY(build_exact(phi, a, v, f, val, D, st, fiber_start));
@@ -777,6 +991,7 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
     LIFE_CUDA(cudaMemsetAsync(phi->red.counter, 0, 16, st));
     LIFE_CUDA(cudaMemsetAsync(phi->counter2, 0, 16, st));
     LIFE_CUDA(cudaStreamSynchronize(st));
+    setup_mark(st, "finish");
     phi->sort_ms = std::chrono::duration<double, std::milli>(
                        std::chrono::steady_clock::now() - t0).count();
     guard.p = nullptr;
@@ -798,6 +1013,14 @@ static void destroy_impl(life_phi *phi)
     cudaDeviceSynchronize();
     for (void *p : phi->allocs) cudaFree(p);
     delete phi;
+}
+
+int life_copy_h2d(void *dst_dev, const void *src_host, int64_t bytes, void *stream)
+{
+    if ((!dst_dev || !src_host) && bytes > 0) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
+    if (bytes < 0) return fail(LIFE_ERR_INVALID_ARGUMENT, "negative size");
+    LIFE_TRY(h2d_staged(dst_dev, src_host, (size_t)bytes, static_cast<cudaStream_t>(stream)));
+    return ok();
 }
 
 int life_phi_destroy(life_phi *phi)

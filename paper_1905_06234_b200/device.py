@@ -65,9 +65,19 @@ def _phi(tensor):
     return tensor.tensor if isinstance(tensor, OffsetPhiTensor) else tensor
 
 
-def _u32_cuda(torch, arr):
-    a = np.ascontiguousarray(arr, dtype=np.uint32)
-    return torch.from_numpy(a.view(np.int32)).to("cuda")
+def upload(arr, dtype=None, stream=None):
+    """Host numpy array -> new CUDA tensor through the library's pinned
+    staging copy (life_copy_h2d: ~50 GB/s against ~7 GB/s for a pageable
+    torch .to("cuda")); `dtype` converts on the device afterwards."""
+    torch = N.require_cuda()
+    a = np.ascontiguousarray(arr)
+    tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+           np.dtype(np.uint32): torch.int32, np.dtype(np.int32): torch.int32,
+           np.dtype(np.int64): torch.int64}[a.dtype]
+    t = torch.empty(a.shape, dtype=tdt, device="cuda")
+    N.check(N.lib().life_copy_h2d(ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(a.ctypes.data),
+                                  a.nbytes, N.stream_ptr(stream)))
+    return t if dtype is None or dtype == tdt else t.to(dtype)
 
 
 class DeviceOperator:
@@ -83,12 +93,13 @@ class DeviceOperator:
         self.exact = bool(exact)
         self.fast = bool(fast)
         nc = d.n_coeffs
-        a = _u32_cuda(torch, phi.atoms) if nc else None
-        v = _u32_cuda(torch, phi.voxels) if nc else None
-        f = _u32_cuda(torch, phi.fibers) if nc else None
-        val = torch.from_numpy(np.ascontiguousarray(phi.values)).to("cuda") if nc else None
-        dic = torch.from_numpy(np.ascontiguousarray(dictionary.data)).to("cuda")
-        self._create(d, a, v, f, val, dic, stream)
+        # host arrays straight into life_phi_create (LIFE_PHI_HOST_INPUT):
+        # the library stages them through pinned buffers
+        u32 = (lambda x: np.ascontiguousarray(x, dtype=np.uint32) if nc else None)
+        a, v, f = u32(phi.atoms), u32(phi.voxels), u32(phi.fibers)
+        val = np.ascontiguousarray(phi.values, dtype=np.float64) if nc else None
+        dic = np.ascontiguousarray(dictionary.data, dtype=np.float64)
+        self._create(d, a, v, f, val, dic, stream, host=True)
 
     @classmethod
     def from_device(cls, dims, atoms, voxels, fibers, values, dictionary,
@@ -100,8 +111,10 @@ class DeviceOperator:
         self._create(dims, atoms, voxels, fibers, values, dictionary, stream)
         return self
 
-    def _create(self, d, a, v, f, val, dic, stream):
+    def _create(self, d, a, v, f, val, dic, stream, host=False):
         flags = (N.PHI_EXACT_F64 if self.exact else 0) | (0 if self.fast else N.PHI_NO_FAST_F32)
+        # host input: the fp32-only operator lets values cross PCIe as f32
+        flags |= (N.PHI_HOST_INPUT | (0 if self.exact else N.PHI_VALUES_F32)) if host else 0
         flags |= {"auto": 0, "sparse": N.PHI_FORCE_SPARSE, "dense": N.PHI_FORCE_DENSE,
                   "bin": N.PHI_FORCE_DENSE,
                   "fma": N.PHI_FORCE_DENSE | N.PHI_NO_TENSOR | N.PHI_NO_BIN,
@@ -109,7 +122,8 @@ class DeviceOperator:
         dims = N.Dims(d.n_atoms, d.n_voxels, d.n_fibers, d.n_dirs, d.n_coeffs)
         handle = ctypes.c_void_p()
         bad = ctypes.c_int64(-1)
-        ptr = (lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None)
+        ptr = (lambda t: None if t is None else ctypes.c_void_p(
+            t.ctypes.data if isinstance(t, np.ndarray) else t.data_ptr()))
         st = N.stream_ptr(stream)
         rc = N.lib().life_phi_create(ctypes.byref(dims), ptr(a), ptr(v), ptr(f), ptr(val),
                                      ptr(dic), flags, st, ctypes.byref(handle),

@@ -262,13 +262,11 @@ def solve(problem, w0=None, config=None):
     exact = config.precision == "fp64"
     dtype = torch.float64 if exact else torch.float32
     op = device.operator_for(problem.tensor, problem.dictionary, exact=exact)
-    b = torch.from_numpy(np.ascontiguousarray(problem.y, dtype=np.float64)).to(
-        device="cuda", dtype=dtype)
+    b = device.upload(np.asarray(problem.y, dtype=np.float64), dtype)
     if w0 is None:
         w = torch.empty(problem.dims.n_fibers, dtype=dtype, device="cuda")
     else:
-        w = torch.from_numpy(np.ascontiguousarray(w0, dtype=np.float64)).to(
-            device="cuda", dtype=dtype)
+        w = device.upload(np.asarray(w0, dtype=np.float64), dtype)
     config._has_w0 = w0 is not None
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
