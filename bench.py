@@ -253,7 +253,7 @@ def run_ours(args, dims):
     comm = None
     if world > 1:
         from paper_1905_06234_b200 import distributed as D
-        comm = D.TorchComm()
+        comm = D.NcclComm()  # the library's own NCCL communicator (graphs on)
         counts = np.bincount(problem.tensor.voxels, minlength=nv)
         v0, v1 = D.shard_voxel_ranges(counts, world)[rank]
         t_loc, dic_loc, b_loc = D.shard_problem(problem.tensor, problem.dictionary,

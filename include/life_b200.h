@@ -200,12 +200,16 @@ LIFE_API int life_wc_f64(life_phi *phi, const double *y, double *w, void *stream
 
 /* ---- multi-GPU ------------------------------------------
  * Phi is sharded by contiguous voxel ranges, one process per GPU.  DSC is
- * local; each WC ends with one all-reduce of the length-Nf fixed-point
- * fascicle sums (int64, so the result is bit-identical on every rank), and
- * each DSC with one all-reduce of two doubles (sum of squares, skip count).
- * The library does not link a communication library: the caller supplies an
- * all-reduce that enqueues on `stream` (the Python layer binds it to
- * torch.distributed / NCCL over NVLink). */
+ * local.  Each WC ends with ONE all-reduce: the length-Nf fixed-point
+ * fascicle sums (int64, so every rank gets bit-identical totals), the
+ * non-finite flags, and the DSC scalars of the same iteration (sum of
+ * squares, skip count; rank slots, added in rank order).  The WC scale comes
+ * from a bound every rank computes alike (max|w| times a per-voxel constant),
+ * so no collective precedes the WC.  Odd iterations add one scalar all-reduce
+ * (||M g||^2 for the step size).  The communicator is either the library's
+ * own NCCL one (life_comm_init_nccl: ncclAllReduce on the solver stream,
+ * capturable, so iterations run as CUDA graphs) or a caller-supplied
+ * all-reduce that enqueues on `stream` (capturable = 0: no graphs). */
 typedef enum life_dtype { LIFE_DT_F64 = 0, LIFE_DT_F32 = 1, LIFE_DT_I64 = 2 } life_dtype;
 typedef enum life_redop { LIFE_OP_SUM = 0, LIFE_OP_MAX = 1 } life_redop;
 typedef int (*life_allreduce_fn)(void *buf, int64_t count, int dtype, int op, void *stream,
@@ -215,7 +219,18 @@ typedef struct life_comm {
     void *ctx;
     int32_t rank;
     int32_t nranks;
+    int32_t capturable;     /* allreduce may be captured in a CUDA graph   */
+    int32_t reserved;
 } life_comm;
+
+/* NCCL communicator (libnccl.so.2 resolved at run time; the process's
+ * already-loaded copy when there is one).  unique_id: 128 bytes
+ * (ncclUniqueId) made by rank 0 with life_nccl_unique_id and shared by the
+ * caller (e.g. torch.distributed broadcast).  life_comm_init_nccl fills
+ * *comm (caller-owned struct); life_comm_destroy_nccl releases it. */
+LIFE_API int life_nccl_unique_id(void *unique_id_out);
+LIFE_API int life_comm_init_nccl(const void *unique_id, int rank, int nranks, life_comm *comm);
+LIFE_API int life_comm_destroy_nccl(life_comm *comm);
 
 /* Global bounds for the WC fixed-point scale (every rank must use the same
  * exponent): max |value| and the longest fascicle over the WHOLE problem,

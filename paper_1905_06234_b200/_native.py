@@ -60,7 +60,7 @@ OP_SUM, OP_MAX = 0, 1
 
 class CommC(ctypes.Structure):
     _fields_ = [("allreduce", ALLREDUCE_FN), ("ctx", c_void_p), ("rank", c_i32),
-                ("nranks", c_i32)]
+                ("nranks", c_i32), ("capturable", c_i32), ("reserved", c_i32)]
 
 
 class SolverConfigC(ctypes.Structure):
@@ -121,6 +121,9 @@ SIGNATURES = {
                                        ctypes.POINTER(SolverResultC), c_void_p]),
     "life_sbb_destroy": (ctypes.c_int, [c_void_p]),
     "life_phi_set_fix_bounds": (ctypes.c_int, [c_void_p, c_double, c_double, c_i64]),
+    "life_nccl_unique_id": (ctypes.c_int, [c_void_p]),
+    "life_comm_init_nccl": (ctypes.c_int, [c_void_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(CommC)]),
+    "life_comm_destroy_nccl": (ctypes.c_int, [ctypes.POINTER(CommC)]),
     "life_phi_get_fix_bounds": (ctypes.c_int, [c_void_p, ctypes.POINTER(c_double),
                                                ctypes.POINTER(c_double),
                                                ctypes.POINTER(c_i64)]),

@@ -218,7 +218,8 @@ __host__ __device__ inline int bin_exponent(double vmax, double dmax, double yno
 }
 __device__ inline int bin_exponent_dev(const FixParams &fx, int nt)
 {
-    const double yn = fx.ysumsq ? sqrt(*fx.ysumsq) : sqrt((double)nt) * (double)*fx.ymax;
+    const double yn = fx.yvbound ? (double)*fx.yvbound
+                      : fx.ysumsq ? sqrt(*fx.ysumsq) : sqrt((double)nt) * (double)*fx.ymax;
     return bin_exponent(fx.vmax, fx.dmax, yn, fx.fmax_nnz);
 }
 
@@ -938,7 +939,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
 
     {   // per-fascicle int64 sums, then the non-finite flags (bytes) in the
         // same buffer so one all-reduce carries both
-        const size_t words = (size_t)nf + ((size_t)nf + 7) / 8;
+        const size_t words = (size_t)nf + ((size_t)nf + 7) / 8 + 3 * (size_t)kTailRanks;
         LIFE_TRY(dalloc(phi, &phi->b_wfix, words));
         phi->b_nanf = reinterpret_cast<unsigned char *>(phi->b_wfix + nf);
         LIFE_CUDA(cudaMemsetAsync(phi->b_wfix, 0, words * 8, st));
@@ -2444,21 +2445,55 @@ static int wc_tile(life_phi *phi, const float *y, const FixParams &fx, const Cal
     LIFE_BIN_DISPATCH(wc_tile_t, phi, y, fx, h, st);
 }
 
+// scalar tail of the WC buffer: value k of rank r at k * nranks + r, zeros
+// elsewhere, so the integer SUM all-reduce delivers every rank's double
+// untouched and all ranks add them in rank order (deterministic)
+__global__ void k_tail_pack(const WcScalars sc, unsigned long long *tail, int rank, int nranks)
+{
+    for (int i = threadIdx.x; i < sc.n * nranks; i += blockDim.x) {
+        const int k = i / nranks, r = i % nranks;
+        tail[i] = r == rank ? (unsigned long long)__double_as_longlong(*sc.v[k]) : 0ull;
+    }
+}
+__global__ void k_tail_unpack(const WcScalars sc, const unsigned long long *tail, int nranks)
+{
+    if (threadIdx.x < sc.n) {
+        double t = 0.0;
+        for (int r = 0; r < nranks; ++r) t += __longlong_as_double((long long)tail[threadIdx.x * nranks + r]);
+        *sc.v[threadIdx.x] = t;
+    }
+}
+
 int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, const FixParams &fx, uint32_t flags,
-                  double *sumsq, const CallHooks &h, const life_comm *comm, cudaStream_t st)
+                  double *sumsq, const CallHooks &h, const life_comm *comm, cudaStream_t st, const WcScalars *sc)
 {
     LIFE_TRY(wc_tile(phi, y, fx, h, st));
     k_side_wc<<<phi->b_side_grid, kSideThreads, phi->b_wcs_smem, st>>>(side_args(phi), chunk_args(phi), phi->b_scr, fx, phi->nt,
                                                                           phi->b_wfix, phi->b_nanf, h);
     LIFE_CHECK_LAUNCH();
-    if (comm && comm->nranks > 1) {
-        // one integer all-reduce: the fascicle sums and, in the tail, the
-        // non-finite flags as 8-bit counters (8 fascicles per word, no carry
-        // for fewer than 256 ranks); sums are exact, so every rank gets
-        // bit-identical totals whatever the reduction order
-        const int64_t cnt = (int64_t)phi->nf + (phi->nf + 7) / 8;
+    if (comm) {
+        // one integer all-reduce: the fascicle sums, the non-finite flags as
+        // 8-bit counters (8 fascicles per word, no carry below 256 ranks) and
+        // the DSC scalars of this iteration (rank slots); sums are exact, so
+        // every rank gets bit-identical totals whatever the reduction order
+        const int64_t nflag = (phi->nf + 7) / 8;
+        unsigned long long *tail = phi->b_wfix + phi->nf + nflag;
+        const int ns = (sc && comm->nranks <= kTailRanks) ? sc->n : 0;
+        if (sc && !ns)  // more ranks than tail slots: scalars on their own
+            for (int k = 0; k < sc->n; ++k)
+                if (comm->allreduce(sc->v[k], 1, LIFE_DT_F64, LIFE_OP_SUM, st, comm->ctx) != 0)
+                    return fail(LIFE_ERR_NCCL, "allreduce(scalar) failed");
+        if (ns) {
+            k_tail_pack<<<1, 256, 0, st>>>(*sc, tail, comm->rank, comm->nranks);
+            LIFE_CHECK_LAUNCH();
+        }
+        const int64_t cnt = (int64_t)phi->nf + nflag + (int64_t)ns * comm->nranks;
         if (comm->allreduce(phi->b_wfix, cnt, LIFE_DT_I64, LIFE_OP_SUM, st, comm->ctx) != 0)
             return fail(LIFE_ERR_NCCL, "allreduce(wfix) failed");
+        if (ns) {
+            k_tail_unpack<<<1, 32, 0, st>>>(*sc, tail, comm->nranks);
+            LIFE_CHECK_LAUNCH();
+        }
     }
     const int blocks = std::max(1, std::min(phi->sms * 4, (phi->nf + 255) / 256));
     k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->nf, w, w_ref, flags, fx, phi->nt,

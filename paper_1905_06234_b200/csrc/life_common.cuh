@@ -176,6 +176,7 @@ struct life_phi {
     unsigned long long *wfix = nullptr;  // [nf] two's-complement int64
     double vmax = 0.0;                   // max |value|
     double dmax = 0.0;                   // max ||D_a||_2
+    double vsmax = 0.0;                  // max_v sum_{c in v} ||D_a(c)||_2 |value_c| (||(M w)_v|| <= vsmax max|w|)
     int64_t fmax_nnz = 0;                // longest fascicle segment
 
     // fp64 bit-exact layouts (stable voxel sort, stable fiber sort)
@@ -240,7 +241,19 @@ struct FixParams {
     const float *ymax;         // device max|y|, or null
     const double *ysumsq;      // device sum of y^2, or null (takes precedence)
     double vmax, dmax, fmax_nnz;
+    // bin layout, voxel-sharded runs: device bound on max_v ||y_v||_2 that
+    // every rank computes identically before any collective (takes
+    // precedence; life_solver.cu k_vbound)
+    const float *yvbound = nullptr;
 };
+
+// DSC scalars (this rank's partial sums) carried in the tail of the WC
+// all-reduce of a voxel-sharded run; replaced by the global sums
+struct WcScalars {
+    double *v[3];
+    int n;
+};
+constexpr int kTailRanks = 64;  // scalar slots per value in the WC buffer tail (ranks)
 
 __host__ __device__ inline int fix_exponent_from(double vmax, double dmax, double ynorm,
                                                  double fmax_nnz)
@@ -284,7 +297,8 @@ int launch_dsc(life_phi *phi, const float *w, float *y, const float *b,
                uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st);
 int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
               const float *ymax_dev, const double *ysumsq_dev, uint32_t flags, double *sumsq,
-              const CallHooks &h, const life_comm *comm, cudaStream_t st);
+              const CallHooks &h, const life_comm *comm, cudaStream_t st,
+              const float *yvbound_dev = nullptr, const WcScalars *sc = nullptr);
 int prepare_spmv(life_phi *phi);
 int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
                 const double *val, const std::vector<double> &hdict, cudaStream_t st);
@@ -303,7 +317,7 @@ int launch_dsc_bin(life_phi *phi, const float *w, float *y, const float *b, uint
 int bin_tile_warps(const life_phi *phi);
 int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, const FixParams &fx,
                   uint32_t flags, double *sumsq, const CallHooks &h, const life_comm *comm,
-                  cudaStream_t st);
+                  cudaStream_t st, const WcScalars *sc);
 // tcgen05 path geometry (life_tc.cu)
 constexpr int kTcTV = 128;       // voxels per CTA tile (MMA M)
 constexpr int kTcCA = 32;        // atoms per chunk (one 128-byte swizzle row of fp32)

@@ -86,6 +86,12 @@ __global__ void k_check_range(const uint32_t *a, const uint32_t *v,
     }
 }
 
+__global__ void k_voxel_l1(const uint32_t *a, const uint32_t *v, const double *val, const double *dn, int64_t n,
+                           double *acc)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&acc[v[i]], fabs(val[i]) * dn[a[i]]);
+}
 __global__ void k_widen_u16(const uint16_t *in, int64_t n, uint32_t *out)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -860,6 +866,18 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
     };
     LIFE_TRY(range_check(true, !host));
 
+    // host copy of the dictionary (small): fp32 slices and row norms
+    std::vector<double> hdict(dlen);
+    LIFE_CUDA(cudaMemcpyAsync(hdict.data(), D, dlen * 8, cudaMemcpyDeviceToHost, st));
+    LIFE_CUDA(cudaStreamSynchronize(st));
+    double dmax = 0.0;
+    for (int64_t at = 0; at < phi->na; ++at) {
+        double s = 0.0;
+        for (int t = 0; t < phi->nt; ++t) s += hdict[at * phi->nt + t] * hdict[at * phi->nt + t];
+        dmax = std::max(dmax, std::sqrt(s));
+    }
+    phi->dmax = dmax * (1.0 + 1e-6);
+
     // fibers and values resident (joins the staging thread), fiber range
     // check, value bound and fascicle sizes; idempotent
     bool fv_ready = false;
@@ -897,23 +915,43 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         double dv;
         std::memcpy(&dv, &hvm, 8);
         phi->vmax = dv * (1.0 + 1e-6);
+        // max_v sum_{c in v} ||D_a||_2 |value|: bounds ||(M w)_v|| by max|w|
+        // without a collective (voxel-sharded WC scale, life_solver.cu)
+        if (n > 0) {
+            double *dn = nullptr, *acc = nullptr;
+            unsigned long long *mxv = nullptr;
+            std::vector<double> hdn(phi->na);
+            for (int64_t at = 0; at < phi->na; ++at) {
+                double q = 0.0;
+                for (int t = 0; t < phi->nt; ++t) q += hdict[at * phi->nt + t] * hdict[at * phi->nt + t];
+                hdn[at] = std::sqrt(q);
+            }
+            LIFE_CUDA(cudaMalloc(&dn, (size_t)phi->na * 8)); guard.tmp.push_back(dn);
+            LIFE_CUDA(cudaMalloc(&acc, (size_t)phi->nv * 8)); guard.tmp.push_back(acc);
+            LIFE_CUDA(cudaMalloc(&mxv, 8)); guard.tmp.push_back(mxv);
+            LIFE_CUDA(cudaMemcpyAsync(dn, hdn.data(), (size_t)phi->na * 8, cudaMemcpyHostToDevice, st));
+            LIFE_CUDA(cudaMemsetAsync(acc, 0, (size_t)phi->nv * 8, st));
+            LIFE_CUDA(cudaMemsetAsync(mxv, 0, 8, st));
+            k_voxel_l1<<<std::min(grid_for(n), phi->sms * 8), 256, 0, st>>>(a, v, val, dn, n, acc);
+            LIFE_CHECK_LAUNCH();
+            k_absmax_f64<<<std::min(grid_for(phi->nv), phi->sms * 8), 256, 0, st>>>(acc, phi->nv, mxv);
+            LIFE_CHECK_LAUNCH();
+            unsigned long long hm;
+            LIFE_CUDA(cudaMemcpyAsync(&hm, mxv, 8, cudaMemcpyDeviceToHost, st));
+            LIFE_CUDA(cudaStreamSynchronize(st));
+            double vs;
+            std::memcpy(&vs, &hm, 8);
+            // rounded up to a power of two: the atomic sums' last bits vary
+            // run to run, the bound (and so the WC scale) must not
+            int e = 0;
+            std::frexp(vs * (1.0 + 1e-6), &e);
+            phi->vsmax = vs > 0.0 ? std::ldexp(1.0, e) : 0.0;
+        }
         phi->fmax_nnz = std::max<int64_t>(hmx[0], 1);
         phi->max_fiber_run = hmx[0];
         phi->n_fiber_runs = hmx[1];
         return LIFE_OK;
     };
-
-    // host copy of the dictionary (small): fp32 slices and row norms
-    std::vector<double> hdict(dlen);
-    LIFE_CUDA(cudaMemcpyAsync(hdict.data(), D, dlen * 8, cudaMemcpyDeviceToHost, st));
-    LIFE_CUDA(cudaStreamSynchronize(st));
-    double dmax = 0.0;
-    for (int64_t at = 0; at < phi->na; ++at) {
-        double s = 0.0;
-        for (int t = 0; t < phi->nt; ++t) s += hdict[at * phi->nt + t] * hdict[at * phi->nt + t];
-        dmax = std::max(dmax, std::sqrt(s));
-    }
-    phi->dmax = dmax * (1.0 + 1e-6);
 
     if (!(flags & LIFE_PHI_NO_FAST_F32)) {
         // Layout choice: register-tiled dense kernels when voxels

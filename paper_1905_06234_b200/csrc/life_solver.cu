@@ -26,6 +26,9 @@ struct Scal {
     double rr, skipped_d, mgmg, mg_pad;
     double gg, mtmg2, alpha, obj, init_obj, final_obj;
     double bb, m1;            // ||b||^2, ||M 1||^2 for the default w0
+    double vS, vB;            // voxel-sharded runs: max_v sum ||D_a|| |val| and max_v ||b_v|| (all ranks)
+    float ybound, yb_pad;     // bound on max_v ||y_v|| of the next WC input
+    unsigned vmax_bits, vcount;
     unsigned long long t_begin, dsc_ns, wc_ns;
     int done, term, iter, max_iters;
     double grad_tol;
@@ -81,6 +84,48 @@ __global__ void k_project_nonneg(T *w, int n)
 {
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x)
         w[f] = (w[f] >= T(0) || w[f] != w[f]) ? w[f] : T(0);  // np.maximum(v, 0): NaN propagates
+}
+
+// Bound on max_v ||y_v||_2 of the next WC input, identical on every rank
+// before any collective (w and g~ are replicated):
+//   y = M x - b:  ||y_v|| <= vS max|x| + vB;   y = M x:  ||y_v|| <= vS max|x|.
+// Sets the WC fixed-point scale of voxel-sharded runs (FixParams::yvbound).
+__global__ void __launch_bounds__(256) k_vbound(const float *__restrict__ x, int nf, Scal *s, int with_b)
+{
+    if (s->done) return;
+    float m = 0.f;
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x)
+        m = fmaxf(m, fabsf(x[f]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&s->vmax_bits, __float_as_uint(m));
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&s->vcount, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        const double xm = (double)__uint_as_float(atomicAdd(&s->vmax_bits, 0u));
+        const double b = s->vS * xm + (with_b ? s->vB : 0.0);
+        s->ybound = (float)(b * (1.0 + 1e-5));
+        s->vmax_bits = 0u;
+        s->vcount = 0u;
+    }
+}
+
+// max_v ||b_v||_2 into s->vB (before the MAX all-reduce of (vS, vB))
+__global__ void __launch_bounds__(256) k_bnorm_max(const float *__restrict__ b, int nv, int nt, Scal *s)
+{
+    double m = 0.0;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+        double q = 0.0;
+        for (int t = 0; t < nt; ++t) q += (double)b[(size_t)v * nt + t] * (double)b[(size_t)v * nt + t];
+        m = fmax(m, sqrt(q));
+    }
+    atomicMax(reinterpret_cast<unsigned long long *>(&s->vB), (unsigned long long)__double_as_longlong(m));
 }
 
 template <int BT>
@@ -258,7 +303,7 @@ struct Solver {
 // Enqueue an all-reduce through the caller's communicator (multi-GPU only).
 static int comm_reduce(const Solver &S, void *buf, int64_t count, int dtype, int op)
 {
-    if (!S.comm || S.comm->nranks <= 1) return LIFE_OK;
+    if (!S.comm) return LIFE_OK;
     if (S.comm->allreduce(buf, count, dtype, op, S.st, S.comm->ctx) != 0)
         return fail(LIFE_ERR_NCCL, "solver all-reduce failed");
     return LIFE_OK;
@@ -278,17 +323,33 @@ static int iter_fast(Solver &S, const float *b, float *w, int even)
     // scalar that multi-GPU runs reduce together with the skip count
     LIFE_TRY(launch_dsc(phi, w, r, b, LIFE_SUBTRACT_B | skip,
                         DscOut{nullptr, &s->rr, nullptr, &s->skipped_d}, hd, S.st));
-    LIFE_TRY(comm_reduce(S, &s->rr, 2, LIFE_DT_F64, LIFE_OP_SUM));
+    // voxel-sharded runs: the WC scale comes from a bound every rank computes
+    // alike, so this iteration's DSC scalars ride in the tail of the WC
+    // all-reduce (one collective per WC)
+    const float *yb = nullptr;
+    if (S.comm) {
+        k_vbound<<<S.nblk_f, 256, 0, S.st>>>(w, phi->nf, s, 1);
+        LIFE_CHECK_LAUNCH();
+        yb = &s->ybound;
+    }
+    const WcScalars sc_r{{&s->rr, &s->skipped_d, nullptr}, 2};
     LIFE_TRY(launch_wc(phi, r, gt, w, nullptr, &s->rr, LIFE_PROJECT_GRAD, &s->gg, hw, S.comm,
-                       S.st));
+                       S.st, yb, S.comm ? &sc_r : nullptr));
     k_check_grad<<<1, 1, 0, S.st>>>(s);
     LIFE_CHECK_LAUNCH();
     LIFE_TRY(launch_dsc(phi, gt, mg, nullptr, skip, DscOut{nullptr, &s->mgmg, nullptr, nullptr},
                         hd, S.st));
-    LIFE_TRY(comm_reduce(S, &s->mgmg, 1, LIFE_DT_F64, LIFE_OP_SUM));
-    if (even)
+    if (even) {
+        if (S.comm) {
+            k_vbound<<<S.nblk_f, 256, 0, S.st>>>(gt, phi->nf, s, 0);
+            LIFE_CHECK_LAUNCH();
+        }
+        const WcScalars sc_m{{&s->mgmg, nullptr, nullptr}, 1};
         LIFE_TRY(launch_wc(phi, mg, mtmg, nullptr, nullptr, &s->mgmg, 0u, &s->mtmg2, hw, S.comm,
-                           S.st));
+                           S.st, yb, S.comm ? &sc_m : nullptr));
+    } else {
+        LIFE_TRY(comm_reduce(S, &s->mgmg, 1, LIFE_DT_F64, LIFE_OP_SUM));  // ||M g~||^2 for alpha
+    }
     k_alpha<<<1, 1, 0, S.st>>>(s, even);
     LIFE_CHECK_LAUNCH();
     k_update<float, 256><<<S.nblk_f, 256, 0, S.st>>>(w, gt, phi->nf, s, S.rec, S.part,
@@ -403,7 +464,7 @@ extern "C" int life_sbb_create(life_phi *phi, const void *b_dev, void *w_dev,
     S.skip = cfg->skip_zero;
     S.nblk_f = blocks_for<float>(phi, phi->nf);
     S.comm = cfg->comm;
-    if (S.comm && S.comm->nranks > 1 && exact)
+    if (S.comm && exact)
         return fail(LIFE_ERR_CONFIG_INVALID, "voxel-sharded runs use the fp32 path");
     LIFE_CUDA(cudaMalloc(&S.s, sizeof(Scal)));
     LIFE_CUDA(cudaMalloc(&S.rec, sizeof(life_trace_record) * cfg->max_iters));
@@ -462,9 +523,18 @@ extern "C" int life_sbb_create(life_phi *phi, const void *b_dev, void *w_dev,
         else k_project_nonneg<float><<<bf, 256, 0, st>>>((float *)w_dev, phi->nf);
         LIFE_CHECK_LAUNCH();
     }
+    if (!exact && S.comm) {
+        // WC scale bounds of voxel-sharded runs (k_vbound): local maxima, then
+        // one MAX all-reduce at setup
+        LIFE_CUDA(cudaMemcpyAsync(&S.s->vS, &phi->vsmax, sizeof(double), cudaMemcpyHostToDevice, st));
+        LIFE_CUDA(cudaMemsetAsync(&S.s->vB, 0, sizeof(double), st));
+        k_bnorm_max<<<blocks_for<float>(phi, phi->nv), 256, 0, st>>>((const float *)b_dev, phi->nv, phi->nt, S.s);
+        LIFE_CHECK_LAUNCH();
+        LIFE_TRY(comm_reduce(S, &S.s->vS, 2, LIFE_DT_F64, LIFE_OP_MAX));
+    }
     if (!exact) {
         LIFE_TRY(prepare_spmv(phi));
-        if (cfg->use_graph && !(S.comm && S.comm->nranks > 1)) {
+        if (cfg->use_graph && !(S.comm && !S.comm->capturable)) {
             // capture one odd+even iteration pair; replays are parity-correct
             // because pairs always start at an odd iteration index
             // (captured on a private stream: the legacy default stream cannot

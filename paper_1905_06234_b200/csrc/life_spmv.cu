@@ -746,16 +746,28 @@ int prepare_spmv(life_phi *phi)
 
 int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
               const float *ymax_dev, const double *ysumsq_dev, uint32_t flags, double *sumsq,
-              const CallHooks &h, const life_comm *comm, cudaStream_t st)
+              const CallHooks &h, const life_comm *comm, cudaStream_t st,
+              const float *yvbound_dev, const WcScalars *sc)
 {
+    if (phi->has_bin) {
+        if (!ymax_dev && !ysumsq_dev && !yvbound_dev) {
+            LIFE_TRY(launch_absmax(phi, y, (int64_t)phi->nv * phi->nt, phi->ybound, st));
+            ymax_dev = phi->ybound;
+        }
+        FixParams fb{phi->wfix, ymax_dev, ysumsq_dev, phi->vmax, phi->dmax, (double)phi->fmax_nnz, yvbound_dev};
+        return launch_wc_bin(phi, y, w, w_ref, fb, flags, sumsq, h, comm, st, sc);
+    }
+    if (comm && sc)  // other layouts: the scalars first (the scale needs the global sum of squares)
+        for (int k = 0; k < sc->n; ++k)
+            if (comm->allreduce(sc->v[k], 1, LIFE_DT_F64, LIFE_OP_SUM, st, comm->ctx) != 0)
+                return fail(LIFE_ERR_NCCL, "allreduce(scalar) failed");
     if (!ymax_dev && !ysumsq_dev) {
         LIFE_TRY(launch_absmax(phi, y, (int64_t)phi->nv * phi->nt, phi->ybound, st));
         ymax_dev = phi->ybound;
     }
     WcFix fx{phi->wfix, ymax_dev, ysumsq_dev, phi->vmax, phi->dmax, (double)phi->fmax_nnz};
-    if (phi->has_bin) return launch_wc_bin(phi, y, w, w_ref, fx, flags, sumsq, h, comm, st);
     LIFE_TRY(launch_wc_main(phi, y, fx, h, st));
-    if (comm && comm->nranks > 1) {
+    if (comm) {
         // fascicle partial sums of all voxel shards: integer sum, so every
         // rank gets bit-identical totals whatever the reduction order
         const int rc = comm->allreduce(phi->wfix, phi->nf, LIFE_DT_I64, LIFE_OP_SUM, st,

@@ -144,6 +144,49 @@ class TorchComm:
         self.c = N.CommC(allreduce=self._fn, ctx=None, rank=self.rank, nranks=self.nranks)
 
 
+class NcclComm:
+    """life_comm over the library's own NCCL communicator (life_comm_init_nccl):
+    ncclAllReduce enqueued by the C side on the solver stream, capturable, so
+    sharded iterations run as CUDA graphs.  The 128-byte ncclUniqueId is made
+    on rank 0 and broadcast over the torch.distributed group (any backend)."""
+
+    def __init__(self, group=None, rank=None, nranks=None):
+        import torch
+        if rank is None or nranks is None:
+            import torch.distributed as dist
+            rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                buf = ctypes.create_string_buffer(128)
+                N.check(N.lib().life_nccl_unique_id(buf))
+                uid = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                uid = uid.cuda()
+                dist.broadcast(uid, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+                uid = uid.cpu()
+            else:
+                dist.broadcast(uid, src=0, group=group)
+            raw = bytes(uid.numpy().tobytes())
+        else:  # single process (world 1): a local id
+            buf = ctypes.create_string_buffer(128)
+            N.check(N.lib().life_nccl_unique_id(buf))
+            raw = buf.raw
+        self.rank, self.nranks, self.error = int(rank), int(nranks), None
+        self.c = N.CommC()
+        idbuf = ctypes.create_string_buffer(raw, 128)
+        N.check(N.lib().life_comm_init_nccl(idbuf, self.rank, self.nranks, ctypes.byref(self.c)))
+
+    def close(self):
+        if self.c is not None and self.c.ctx:
+            N.lib().life_comm_destroy_nccl(ctypes.byref(self.c))
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def solve_sharded(problem, config=None, group=None, w0=None, ranges=None):
     """SBBNNLS with Phi voxel-sharded over the ranks of a torch.distributed
     group (every rank calls it with the same problem).  Returns (w, trace);
@@ -156,7 +199,10 @@ def solve_sharded(problem, config=None, group=None, w0=None, ranges=None):
     config = config or SolverConfig()
     if config.precision != "fp32":
         raise ConfigInvalid("voxel-sharded solves run the fp32 path")
-    comm = TorchComm(group)
+    import torch.distributed as dist
+    # NCCL process groups: the library's own capturable NCCL communicator
+    # (graphs on); other backends (gloo in tests): the torch callback
+    comm = NcclComm(group) if dist.get_backend(group) == "nccl" else TorchComm(group)
     counts = np.bincount(problem.tensor.voxels, minlength=problem.dims.n_voxels)
     ranges = ranges or shard_voxel_ranges(counts, comm.nranks)
     v0, v1 = ranges[comm.rank]
@@ -182,5 +228,5 @@ def solve_sharded(problem, config=None, group=None, w0=None, ranges=None):
     return w.double().cpu().numpy(), trace_from(res, recs)
 
 
-__all__ = ["TorchComm", "global_fix_bounds", "shard_problem", "shard_voxel_ranges",
+__all__ = ["NcclComm", "TorchComm", "global_fix_bounds", "shard_problem", "shard_voxel_ranges",
            "solve_sharded"]

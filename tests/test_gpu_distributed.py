@@ -1,6 +1,7 @@
-"""Voxel-sharded SBBNNLS through the C-ABI comm hook: two ranks on one GPU
-(gloo process group, host-staged all-reduce) against the single-GPU solve.
-The NCCL path differs only in the transport of the same all-reduce calls."""
+"""Voxel-sharded SBBNNLS: two and three ranks on one GPU through the C-ABI
+comm hook (gloo process group, host-staged all-reduce), and the library's
+own NCCL communicator at world 1 through the graph path, against the
+single-GPU solve."""
 
 import os
 import socket
@@ -67,3 +68,46 @@ def test_sharded_solve_matches_single_gpu(world):
     assert abs(fo - tr1.final_objective) <= 1e-5 * tr1.final_objective
     assert outs[0][4] == [r.dsc_skipped for r in tr1.records]  # global skip counts
     assert outs[0][5] == tr1.termination
+
+
+def test_nccl_comm_world1_through_graphs():
+    """The library's own NCCL communicator (life_comm_init_nccl) at world 1,
+    the only shape one GPU allows: the sharded iteration (bound-scaled WC,
+    DSC scalars in the tail of the WC all-reduce, odd-iteration scalar
+    all-reduce) runs as CUDA graphs and matches the single-GPU solve."""
+    import torch
+
+    import paper_1905_06234_b200 as L
+    from paper_1905_06234_b200 import _native as N
+    from paper_1905_06234_b200 import device
+    from paper_1905_06234_b200 import distributed as D
+    from paper_1905_06234_b200.sbbnnls import SolverSession, trace_from
+
+    p = _problem()
+    cfg = L.SolverConfig(max_iters=12, grad_tol=0.0)
+    w1, tr1 = L.solve(p, config=cfg)
+    comm = D.NcclComm(rank=0, nranks=1)
+    assert comm.c.capturable == 1 and comm.c.nranks == 1
+    op = device.DeviceOperator(p.tensor, p.dictionary)
+    b = device.upload(np.asarray(p.y, dtype=np.float64), torch.float32)
+    w = torch.empty(p.dims.n_fibers, dtype=torch.float32, device="cuda")
+    launches0 = N.launch_count()
+    sess = SolverSession(op, b, w, cfg, comm=comm)
+    sess.iterate(cfg.max_iters)
+    res, recs = sess.finish()
+    sess.close()
+    assert N.launch_count() > launches0
+    tr = trace_from(res, recs)
+    wn = w.double().cpu().numpy()
+    rel = np.linalg.norm(wn - w1) / np.linalg.norm(w1)
+    assert rel <= 1e-5, rel
+    assert abs(tr.final_objective - tr1.final_objective) <= 1e-5 * tr1.final_objective
+    assert [r.dsc_skipped for r in tr.records] == [r.dsc_skipped for r in tr1.records]
+    # bitwise repeatable through the communicator
+    w2 = torch.empty_like(w)
+    sess = SolverSession(op, b, w2, cfg, comm=comm)
+    sess.iterate(cfg.max_iters)
+    sess.finish()
+    sess.close()
+    assert torch.equal(w, w2)
+    comm.close()
