@@ -302,7 +302,13 @@ def run_ours(args, dims):
     # ---- kernel-level timing (DSC / WC) for the roofline -------------------
     # (this rank's shard when N > 1: local bytes over local kernel time)
     dsc_b, wc_b = spmv_bytes(local_dims)
-    if "dsc" in op.tensor_ops:
+    if op.kind == "bin":
+        # binned layout: per coefficient a 2-byte tile cell, a 2-byte bin slot
+        # and a 4-byte value, for both products (SURVEY 8(d) counts the
+        # actual sizes under compression); the tile<->bin exchange through
+        # the scratch is design overhead and shows up in `traffic`
+        dsc_b, wc_b = spmv_bytes(local_dims, idx_bytes=2)
+    elif "dsc" in op.tensor_ops:
         # the tensor-core DSC streams 8-byte packed entries (fascicle << 12 |
         # cell, value): SURVEY 8(d) counts the actual sizes under compression
         dsc_b, _ = spmv_bytes(local_dims, idx_bytes=2)

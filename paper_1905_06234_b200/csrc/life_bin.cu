@@ -792,7 +792,8 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     k_seg_info<<<gridn(nseg), 256, 0, st>>>(skbm, first, nseg, n, per_bin, (uint32_t)nbins, len4, segkey, tmkey, sstep);
     LIFE_CHECK_LAUNCH();
     // bin-major unit starts
-    LIFE_TRY(dalloc(phi, &phi->b_segsrc, (size_t)nseg + 1));
+    // +4: the bin side bulk-copies segment records rounded up to 16 bytes
+    LIFE_TRY(dalloc(phi, &phi->b_segsrc, (size_t)nseg + 1 + 4));
     LIFE_TRY(scan_excl(len4, phi->b_segsrc, nseg, st));
     // tile-major: steps padded to 8 entries, segments in bin order inside
     LIFE_CUDA(cudaMemsetAsync(units, 0, nsteps * 4, st));
@@ -811,7 +812,7 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
         LIFE_CHECK_LAUNCH();
         LIFE_TRY(scan_excl(len_tm, tm_excl, nseg, st));
     }
-    LIFE_TRY(dalloc(phi, &phi->b_segdst, (size_t)nseg + 1));
+    LIFE_TRY(dalloc(phi, &phi->b_segdst, (size_t)nseg + 1 + 4));
     uint32_t *stepx = (uint32_t *)spad;  // reuse: padded sizes are scanned already
     k_step_first<<<gridn(nseg), 256, 0, st>>>(perm_seg, tm_excl, sstep, nseg, stepx);
     LIFE_CHECK_LAUNCH();
