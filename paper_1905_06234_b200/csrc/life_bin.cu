@@ -18,12 +18,14 @@
 // bin-major arrays and reads/writes the scratch in runs.  Random accesses per
 // coefficient are shared-memory only; global memory is streamed.
 //
-// Determinism without ordering constraints: DSC repeats of a (row, atom) cell
-// are added in rank order (rank-level passes); WC fascicle sums are exact
-// integers (64-bit fixed point, accumulated as two 32-bit limbs with native
-// shared-memory atomics; a virtual fascicle slot holds at most kSlotCap
-// coefficients so the limbs cannot overflow), so any summation order gives
-// the same bits, across CTAs, slots, and ranks.
+// Determinism without ordering constraints: the DSC C tile is int32 fixed
+// point (per-call scale from max |s|, so the <= kRanks repeats of a (row,
+// atom) cell add exactly with shared-memory atomics); WC fascicle sums are
+// exact integers (64-bit fixed point, accumulated as two 32-bit limbs with
+// native shared-memory atomics; a virtual fascicle slot holds at most
+// kSlotCap coefficients so the limbs cannot overflow; flushed per fascicle
+// run into int64 sums), so any summation order gives the same bits, across
+// CTAs, slots, and ranks.
 //
 // Reference: _kernels.dsc_range / wc_range (/root/reference/pkg/src/
 // lifespmv/_kernels.py:14-33, 57-68) under the owned regimes of
