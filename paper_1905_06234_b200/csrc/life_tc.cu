@@ -4,7 +4,8 @@
 // chunks of 32:  Y(128 x N) += C(128 x 32) . D_c(32 x N), N = directions
 // padded to 32, with C[v, a] = sum_k w[f_k] value_k built on the fly in
 // shared memory from the sorted coefficient stream (life_dense.cu
-// build_tc).  Roles inside one persistent CTA per SM (13 warps):
+// build_tc).  Roles inside one persistent CTA per SM (16 warps: 8 builders,
+// 3 gatherers, producer, MMA issuer, 4 epilogue; see DscTc in the code):
 //
 //   warps 0-7   builders.  Warp p owns voxel rows 16p..16p+15 of the A tile:
 //               it zeroes them, stores C[cell] = s from the staged step
