@@ -1170,7 +1170,21 @@ __global__ void __launch_bounds__(kSideThreads, 1)
                 const int64_t s0 = (int64_t)(c.w >> 16) * kSB;
                 const int nsl = (int)min((int64_t)kSB, A.nvf - s0);
                 named_bar(1, kCons);
-                for (int i = ct; i < nsl; i += kCons) ws[i] = __ldg(w + __ldg(A.vf2f + s0 + i));
+                // the bin's w slice: 8 independent gathers in flight per thread
+                for (int i0 = ct; i0 < nsl; i0 += 8 * kCons) {
+                    uint32_t fi[8];
+                    float wv[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int i = i0 + k * kCons;
+                        fi[k] = i < nsl ? __ldg(A.vf2f + s0 + i) : 0u;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) wv[k] = i0 + k * kCons < nsl ? __ldg(w + fi[k]) : 0.f;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (i0 + k * kCons < nsl) ws[i0 + k * kCons] = wv[k];
+                }
                 named_bar(1, kCons);
             }
             const uint32_t slot_sa = sa(ring) + (uint32_t)sl * kSlotBytes;
@@ -1281,14 +1295,22 @@ __global__ void __launch_bounds__(kSideThreads, 1)
     auto flush = [&]() {
         const int64_t s0 = (int64_t)cur_bin * kSB;
         const int nsl = (int)min((int64_t)kSB, A.nvf - s0);
-        for (int ib = (int)ct - lane; ib < nsl; ib += kCons) {
+        constexpr int kFU = 4;  // flush rounds with their fascicle ids loaded together
+        for (int ib0 = (int)ct - lane; ib0 < nsl; ib0 += kFU * kCons) {
+          uint32_t fids[kFU];
+#pragma unroll
+          for (int r = 0; r < kFU; ++r) {
+              const int i = ib0 + r * kCons + lane;
+              fids[r] = i < nsl ? __ldg(A.vf2f + s0 + i) : 0xFFFFFFFFu;
+          }
+#pragma unroll
+          for (int r = 0; r < kFU; ++r) {
+            const int ib = ib0 + r * kCons;
+            if (ib >= nsl) break;  // warp-uniform
             const int i = ib + lane;
             long long v = 0;
-            uint32_t fid = 0xFFFFFFFFu;
-            if (i < nsl) {
-                v = (long long)(int32_t)hi[i] * 16777216ll + (long long)lo[i];
-                fid = __ldg(A.vf2f + s0 + i);
-            }
+            const uint32_t fid = fids[r];
+            if (i < nsl) v = (long long)(int32_t)hi[i] * 16777216ll + (long long)lo[i];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const long long ov = __shfl_down_sync(0xffffffffu, v, o);
@@ -1297,6 +1319,7 @@ __global__ void __launch_bounds__(kSideThreads, 1)
             }
             const uint32_t pf = __shfl_up_sync(0xffffffffu, fid, 1);
             if (i < nsl && (lane == 0 || pf != fid) && v) atomicAdd(wfix + fid, (unsigned long long)v);
+          }
         }
     };
     if (nch > 0) load_z(0, zn);
