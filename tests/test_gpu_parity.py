@@ -333,6 +333,30 @@ def test_odd_direction_counts(oracle, n_dirs, layout):
     assert np.array_equal(wc(t, dic, d, q["y"], "fp64"), wo)
 
 
+@pytest.mark.parametrize("n_dirs", [96, 150])
+def test_fascicles_beyond_2_20(oracle, n_dirs, layout):
+    """Nf > 2^20 (C4: 1M fascicles, C5 at 256M+): the binned products take it
+    on the tensor path (round 1's packed 20-bit fascicle field fell back to
+    CUDA cores)."""
+    from paper_1905_06234_b200 import device
+    dims = (1057, 1500, 1_200_000, n_dirs, 450_000)
+    q = oracle.generate(dims, 300.0, 0.5, 0.1, 17)
+    d = L.Dims(*dims)
+    t = L.PhiTensor(atoms=q["atoms"], voxels=q["voxels"], fibers=q["fibers"],
+                    values=q["values"], dims=d)
+    dic = L.Dictionary(data=q["dict"], dims=d)
+    if layout == "bin":
+        op = device.operator_for(t, dic)
+        assert op.kind == "bin" and op.tensor_ops == ("dsc", "wc")
+    w = np.random.default_rng(2).random(d.n_fibers)
+    yo = np.zeros(d.signal_len)
+    oracle.dsc(q, w, yo)
+    assert rel_l2(dsc(t, dic, d, w, "fp32")[0], yo) <= TOL32
+    wo = np.zeros(d.n_fibers)
+    oracle.wc(q, q["y"], wo)
+    assert rel_l2(wc(t, dic, d, q["y"], "fp32"), wo) <= TOL32
+
+
 def test_single_giant_run_and_long_fascicle(oracle, layout):
     # every coefficient in voxel 0 and fascicle 0 (maximal segments)
     n = 20000
