@@ -308,10 +308,7 @@ def run_ours(args, dims):
         # actual sizes under compression); the tile<->bin exchange through
         # the scratch is design overhead and shows up in `traffic`
         dsc_b, wc_b = spmv_bytes(local_dims, idx_bytes=2)
-    elif "dsc" in op.tensor_ops:
-        # the tensor-core DSC streams 8-byte packed entries (fascicle << 12 |
-        # cell, value): SURVEY 8(d) counts the actual sizes under compression
-        dsc_b, _ = spmv_bytes(local_dims, idx_bytes=2)
+
     y = torch.empty(local_dims[1] * nt, dtype=torch.float32, device="cuda")
     g = torch.empty(nf, dtype=torch.float32, device="cuda")
     ymax = torch.zeros(1, dtype=torch.float32, device="cuda")
@@ -419,7 +416,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--layout", default="auto", choices=["auto", "sparse", "dense", "fma", "tensor"])
+    ap.add_argument("--layout", default="auto", choices=["auto", "sparse", "bin"])
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -87,10 +87,10 @@ LIFE_API uint64_t life_launch_count(void);
 #define LIFE_PHI_EXACT_F64    0x2u  /* also build the fp64 bit-exact layout */
 #define LIFE_PHI_NO_FAST_F32  0x4u  /* skip the fp32 fast layout           */
 #define LIFE_PHI_FORCE_SPARSE 0x8u  /* fp32: voxel-segment kernels only    */
-#define LIFE_PHI_FORCE_DENSE  0x10u /* fp32: register-tiled dense kernels  */
-#define LIFE_PHI_NO_TENSOR    0x20u /* fp32: no tcgen05 products (CUDA cores only) */
-#define LIFE_PHI_TENSOR       0x40u /* fp32: single-pass tcgen05 tile products (with LIFE_PHI_NO_BIN) */
-#define LIFE_PHI_NO_BIN       0x80u /* fp32: not the binned two-phase products (life_bin.cu)   */
+#define LIFE_PHI_FORCE_DENSE  0x10u /* fp32: the tile layout (binned products) even for sparse operators */
+#define LIFE_PHI_NO_TENSOR    0x20u /* fp32: no tcgen05 products (voxel-segment kernels) */
+#define LIFE_PHI_TENSOR       0x40u /* retired in round 2 (the single-pass tcgen05 tile family); ignored */
+#define LIFE_PHI_NO_BIN       0x80u /* fp32: not the binned products (voxel-segment kernels) */
 #define LIFE_PHI_VALUES_F32   0x100u /* with HOST_INPUT: values may cross PCIe as f32 (fp32-only operator; ignored with EXACT_F64) */
 
 /* Build the device operator from COO arrays (PhiTensor + Dictionary,
@@ -115,7 +115,7 @@ LIFE_API int life_copy_h2d(void *dst_dev, const void *src_host, int64_t bytes, v
 
 typedef struct life_phi_info {
     life_dims dims;
-    int32_t atom_groups;        /* sparse kernels: passes over Phi (D slices); 0 = dense, -1 = dense + tcgen05 DSC, -2 = binned two-phase (tcgen05) */
+    int32_t atom_groups;        /* sparse kernels: passes over Phi (D slices); -2 = binned two-phase (tcgen05) */
     int32_t atoms_per_group;
     int32_t n_warps;            /* persistent warps of the SpMV kernels   */
     int32_t has_exact;          /* fp64 bit-exact layout present          */

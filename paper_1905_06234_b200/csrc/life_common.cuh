@@ -97,42 +97,6 @@ struct life_phi {
     int nblocks = 0, W = 0;
     size_t smem = 0;
 
-    // dense tile layout (register-tiled kernels, life_dense.cu): coefficients
-    // sorted by (voxel tile of 16, atom chunk of 64, duplicate rank, cell)
-    bool has_dense = false;
-    uint32_t *d_cr = nullptr;     // rank << 10 | (atom%64)*16 + voxel%16
-    uint32_t *d_fiber = nullptr;
-    float *d_val = nullptr;
-    uint32_t *d_tptr = nullptr;   // [n_tiles*n_chunks + 1]
-    float *d_D = nullptr;         // [n_chunks][64][nt_pad] zero padded
-    float *d_Bwc = nullptr;       // ws WC on tcgen05: [n_chunks][hi|lo][nt_pad/32][32][32] swizzled
-    int n_tiles = 0, n_chunks = 0, nt_pad = 0, d_blocks = 0, d_W = 0;
-    int d_kind = 0;       // 1: register-tiled v1 (life_dense.cu), 2: warp-specialized (life_ws.cu)
-    int d_tv = 0;         // voxels per tile
-    uint32_t *d_t1 = nullptr;  // ws layout: start of each segment's rank>=1 region
-    int64_t d_npad = 0;        // ws layout: padded coefficient count
-    int d_ca = 0;              // atoms per chunk (ws layout: 32, v1: 64)
-    int64_t d_maxpw = 0;       // ws layout: largest per-producer-warp step range
-    bool d_staged = false;     // ws layout: producer ranges staged by TMA bulk copies
-    uint32_t *d_vslot = nullptr;  // ws layout: tile slot of each voxel (load-balanced order)
-    int *d_slotv = nullptr;       // ws layout: voxel of each tile slot, -1 = padding
-    size_t d_smem = 0;
-
-    // tensor-core tile layout (life_tc.cu): coefficients sorted by (CTA tile of
-    // 128 voxels, atom chunk of 32, producer warp = 16-voxel row block, rank,
-    // cell); cell = fp32 index of (row, atom) in the K-major SWIZZLE_128B
-    // A tile the tcgen05 MMA reads.
-    bool has_tc = false;
-    uint32_t *t_q = nullptr;      // 32-byte quads {pk[4], value[4]}, pk = fascicle << 12 | cell
-    uint32_t *t_tptr = nullptr;   // [n_ct*nch*8 + 1] padded segment starts
-    uint32_t *t_t1 = nullptr;     // start of each segment's rank>=1 region
-    uint32_t *t_vslot = nullptr;  // tile slot of each voxel
-    int *t_slotv = nullptr;       // voxel of each tile slot, -1 = padding
-    float *t_D = nullptr;         // [nch][hi|lo][N rows][32] swizzled tf32 split of D^T
-    int t_nct = 0, t_nch = 0, t_n = 0, t_blocks = 0, t_W = 0;
-    int64_t t_npad = 0, t_maxseg = 0, t_maxstep = 0;
-    size_t t_smem = 0;
-
     // binned two-phase layout (life_bin.cu, the default fp32 products):
     // "tile side" = 128-row voxel tiles x atom chunks on tcgen05, "bin
     // side" = fascicle bins held in shared memory; the two meet in a
@@ -300,14 +264,6 @@ int launch_wc(life_phi *phi, const float *y, float *w, const float *w_ref,
               const CallHooks &h, const life_comm *comm, cudaStream_t st,
               const float *yvbound_dev = nullptr, const WcScalars *sc = nullptr);
 int prepare_spmv(life_phi *phi);
-int build_dense(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
-                const double *val, const std::vector<double> &hdict, cudaStream_t st);
-int build_wc_tc(life_phi *phi, const std::vector<double> &hdict, cudaStream_t st);
-int build_tc(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
-             const double *val, const std::vector<double> &hdict, cudaStream_t st);
-int launch_dsc_tc(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
-                  const DscOut &o, const CallHooks &h, cudaStream_t st);
-int prepare_tc(life_phi *phi);
 // binned two-phase products (life_bin.cu)
 int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_t *f,
               const double *val, const std::vector<double> &hdict, const std::function<int()> &ready_fv,
@@ -318,9 +274,4 @@ int bin_tile_warps(const life_phi *phi);
 int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, const FixParams &fx,
                   uint32_t flags, double *sumsq, const CallHooks &h, const life_comm *comm,
                   cudaStream_t st, const WcScalars *sc);
-// tcgen05 path geometry (life_tc.cu)
-constexpr int kTcTV = 128;       // voxels per CTA tile (MMA M)
-constexpr int kTcCA = 32;        // atoms per chunk (one 128-byte swizzle row of fp32)
-constexpr int kTcProd = 8;       // producer warps, 16 voxel rows each
-constexpr int kTcCellBits = 12;  // cell = fp32 index in the 128 x 32 A tile
 }  // namespace life

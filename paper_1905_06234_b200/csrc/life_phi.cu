@@ -977,34 +977,20 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
             phi->n_voxel_runs = hm[1];
             phi->max_voxel_run = hm[0];
         }
-        bool dense = (n * 8 >= occupied * (int64_t)phi->na) && n > 0;
-        if (flags & LIFE_PHI_FORCE_SPARSE) dense = false;
-        if (flags & LIFE_PHI_FORCE_DENSE) dense = n > 0;
-        // binned two-phase products (life_bin.cu): the default for tile
-        // operators; LIFE_PHI_NO_BIN, LIFE_PHI_NO_TENSOR or LIFE_BIN=0 keep
-        // the single-pass tile families below
+        // Layout choice: the binned tile products when
+        // voxels carry >= 1/8 of all atoms on average (and n_dirs <= 192),
+        // the voxel-segment kernels otherwise; flags can force either.
+        bool tile = (n * 8 >= occupied * (int64_t)phi->na) && n > 0;
+        if (flags & LIFE_PHI_FORCE_SPARSE) tile = false;
+        if (flags & LIFE_PHI_FORCE_DENSE) tile = n > 0;
         const char *bin_env = getenv("LIFE_BIN");
-        const bool want_bin = dense && !(flags & (LIFE_PHI_NO_TENSOR | LIFE_PHI_NO_BIN)) &&
+        const bool want_bin = tile && !(flags & (LIFE_PHI_NO_TENSOR | LIFE_PHI_NO_BIN)) &&
                               !(bin_env && bin_env[0] == '0');
         setup_mark(st, "checks + dictionary");
         if (want_bin) LIFE_TRY(build_bin(phi, a, v, f, val, hdict, ready_fv, st));
         setup_mark(st, "build_bin");
         LIFE_TRY(ready_fv());
-        if (phi->has_bin) dense = false;
-        if (dense) LIFE_TRY(build_dense(phi, a, v, f, val, hdict, st));
-        // tcgen05 DSC over its own tile layout (life_tc.cu) next to the dense
-        // one: default since it beats the CUDA-core tile DSC (1.08 vs 1.19 ms
-        // at C2); LIFE_PHI_NO_TENSOR or LIFE_TC=0 opt out
-        const char *tc_env = getenv("LIFE_TC");
-        const bool want_tc = (flags & LIFE_PHI_TENSOR) || !(tc_env && tc_env[0] == '0');
-        // WC on tcgen05 over the same tile layout (k_wc_tc): default, it is
-        // faster than the CUDA-core WC (0.97 vs 1.19 ms at C2)
-        const char *wc_env = getenv("LIFE_WC_TC");
-        if (phi->has_dense && !(flags & LIFE_PHI_NO_TENSOR) && !(wc_env && wc_env[0] == '0'))
-            LIFE_TRY(build_wc_tc(phi, hdict, st));
-        if (dense && phi->has_dense && want_tc && !(flags & LIFE_PHI_NO_TENSOR))
-            LIFE_TRY(build_tc(phi, a, v, f, val, hdict, st));
-        if (!phi->has_dense && !phi->has_bin) LIFE_TRY(build_fast(phi, a, v, f, val, hdict, st));
+        if (!phi->has_bin) LIFE_TRY(build_fast(phi, a, v, f, val, hdict, st));
     }
     LIFE_TRY(ready_fv());
     std::vector<int64_t> fiber_start;
@@ -1015,7 +1001,7 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
     // fixed-point WC accumulator (both fp32 kernel families)
     LIFE_TRY(dalloc(phi, &phi->wfix, phi->nf));
     LIFE_CUDA(cudaMemsetAsync(phi->wfix, 0, (size_t)phi->nf * sizeof(unsigned long long), st));
-    phi->red_cap = std::max(std::max(std::max(std::max(phi->W, phi->xW), phi->d_W), phi->t_W), phi->sms * 16) + 1;
+    phi->red_cap = std::max(std::max(phi->W, phi->xW), phi->sms * 16) + 1;
     if (phi->has_bin)
         phi->red_cap = std::max(phi->red_cap, phi->b_tile_grid * bin_tile_warps(phi) + phi->sms * 8 + 1);
     LIFE_TRY(dalloc(phi, &phi->red.part_d, phi->red_cap));
@@ -1092,7 +1078,7 @@ int life_phi_get_info(const life_phi *phi, life_phi_info *info)
 {
     if (!phi || !info) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
     info->dims = phi->dims;
-    info->atom_groups = phi->has_bin ? -2 : phi->has_tc ? -1 : phi->has_dense ? 0 : phi->G;
+    info->atom_groups = phi->has_bin ? -2 : phi->G;
     info->atoms_per_group = phi->ag;
     info->n_warps = phi->W;
     info->has_exact = phi->has_exact ? 1 : 0;
@@ -1102,7 +1088,7 @@ int life_phi_get_info(const life_phi *phi, life_phi_info *info)
     info->max_voxel_run = phi->max_voxel_run;
     info->device_bytes = phi->device_bytes;
     info->sort_ms = phi->sort_ms;
-    info->tensor_ops = phi->has_bin ? 3 : (phi->has_tc ? 1 : 0) | (phi->d_Bwc ? 2 : 0);
+    info->tensor_ops = phi->has_bin ? 3 : 0;
     info->reserved = 0;
     return ok();
 }

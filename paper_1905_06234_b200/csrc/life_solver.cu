@@ -443,7 +443,7 @@ extern "C" int life_sbb_create(life_phi *phi, const void *b_dev, void *w_dev,
     const bool exact = cfg->exact_f64 != 0;
     if (exact && !phi->has_exact)
         return fail(LIFE_ERR_CONFIG_INVALID, "exact_f64 needs an operator built with LIFE_PHI_EXACT_F64");
-    if (!exact && !phi->has_fast && !phi->has_dense && !phi->has_bin)
+    if (!exact && !phi->has_fast && !phi->has_bin)
         return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t ny = (int64_t)phi->nv * phi->nt;

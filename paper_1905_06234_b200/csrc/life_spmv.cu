@@ -661,12 +661,6 @@ static int launch_wc_t(life_phi *phi, const float *y, const WcFix &fx,
     default: return fail(LIFE_ERR_CONFIG_INVALID, "unsupported n_dirs");     \
     }
 
-int launch_dsc_dense(life_phi *phi, const float *w, float *y, const float *b, uint32_t flags,
-                     const DscOut &o, const CallHooks &h, cudaStream_t st);
-int launch_wc_dense(life_phi *phi, const FixParams &fx, const float *y, const CallHooks &h,
-                    cudaStream_t st);
-int prepare_dense(life_phi *phi);
-
 static int launch_dsc_sparse(life_phi *phi, const float *w, float *y, const float *b,
                              uint32_t flags, const DscOut &o, const CallHooks &h,
                              cudaStream_t st)
@@ -678,8 +672,6 @@ static int launch_dsc_kernel(life_phi *phi, const float *w, float *y, const floa
                              uint32_t flags, const DscOut &o, const CallHooks &h, cudaStream_t st)
 {
     if (phi->has_bin) return launch_dsc_bin(phi, w, y, b, flags, o, h, st);
-    if (phi->has_tc) return launch_dsc_tc(phi, w, y, b, flags, o, h, st);
-    if (phi->has_dense) return launch_dsc_dense(phi, w, y, b, flags, o, h, st);
     return launch_dsc_sparse(phi, w, y, b, flags, o, h, st);
 }
 
@@ -712,7 +704,6 @@ static int launch_wc_sparse(life_phi *phi, const float *y, const WcFix &fx,
 int launch_wc_main(life_phi *phi, const float *y, const WcFix &fx,
                    const CallHooks &h, cudaStream_t st)
 {
-    if (phi->has_dense) return launch_wc_dense(phi, fx, y, h, st);
     return launch_wc_sparse(phi, y, fx, h, st);
 }
 
@@ -739,8 +730,6 @@ static int prepare_sparse(life_phi *phi) { LIFE_NT_DISPATCH(prepare_t, phi); }
 int prepare_spmv(life_phi *phi)
 {
     if (phi->has_bin) return LIFE_OK;  // prepared at build (prepare_bin)
-    if (phi->has_tc) LIFE_TRY(prepare_tc(phi));
-    if (phi->has_dense) return prepare_dense(phi);
     return prepare_sparse(phi);
 }
 
@@ -792,7 +781,7 @@ int life_dsc_f32(life_phi *phi, const float *w, float *y, const float *b,
                  uint32_t flags, const life_spmv_out *out, void *stream)
 {
     if (!phi || !w || !y) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
-    if (!phi->has_fast && !phi->has_dense && !phi->has_bin)
+    if (!phi->has_fast && !phi->has_bin)
         return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     if ((flags & LIFE_SUBTRACT_B) && !b) return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_SUBTRACT_B needs b");
     if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(y) |
@@ -810,7 +799,7 @@ int life_wc_f32(life_phi *phi, const float *y, float *w, const float *w_ref,
                 const life_spmv_out *out, void *stream)
 {
     if (!phi || !w || !y) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
-    if (!phi->has_fast && !phi->has_dense && !phi->has_bin)
+    if (!phi->has_fast && !phi->has_bin)
         return fail(LIFE_ERR_CONFIG_INVALID, "operator has no fp32 layout");
     if ((flags & LIFE_PROJECT_GRAD) && !w_ref)
         return fail(LIFE_ERR_INVALID_ARGUMENT, "LIFE_PROJECT_GRAD needs w_ref");

@@ -5,10 +5,10 @@
 C ABI on either host arrays (numpy: copied in and out) or CUDA tensors
 (used in place).  Two precisions:
 
-* ``"fp32"`` -- the fast path (fp32 values, fixed-point WC accumulation);
-  tile operators run both products on the tcgen05 tensor cores (3xTF32,
-  ~1e-6 relative of the reference), ``set_layout("fma")`` keeps them on CUDA
-  cores (~3e-7), sparse operators use voxel-segment kernels.
+* ``"fp32"`` -- the fast path: tile-shaped operators run the binned
+  two-phase products (tcgen05 tile contraction + shared-memory fascicle
+  bins, exact integer reductions; ~5e-7 relative L2 of the reference),
+  operators whose voxels carry few atoms the voxel-segment kernels.
 * ``"fp64"`` -- the bit-exact path: same rounding and per-output order as
   the reference loops (_kernels.py:14-68), equal to
   ``dsc_sequential``/``wc_sequential`` bit for bit.
@@ -32,16 +32,16 @@ warnings.filterwarnings("ignore", message="The given NumPy array is not writable
 _LAYOUT = ["auto"]
 
 
-_LAYOUTS = ("auto", "sparse", "dense", "bin", "fma", "tensor")
+_LAYOUTS = ("auto", "sparse", "dense", "bin")
 
 
 def set_layout(name):
     """fp32 kernel family for operators built from now on: "auto" (density
     heuristic: "bin" for tile-shaped operators, else "sparse"), "sparse"
-    (voxel-segment kernels), "bin" or "dense" (binned two-phase products:
-    tcgen05 tile side + shared-memory fascicle bins, n_dirs <= 192), "tensor"
-    (single-pass tcgen05 tile kernels) or "fma" (single-pass tile kernels on
-    CUDA cores)."""
+    (voxel-segment kernels) or "bin" / "dense" (binned two-phase products:
+    tcgen05 tile side + shared-memory fascicle bins, n_dirs <= 192; larger
+    direction counts take the voxel-segment kernels).  The round-1
+    single-pass tile families ("fma", "tensor") were retired in round 2."""
     if name not in _LAYOUTS:
         raise ConfigInvalid(f"layout must be one of {'/'.join(_LAYOUTS)}, got {name!r}")
     _LAYOUT[0] = name
@@ -116,9 +116,7 @@ class DeviceOperator:
         # host input: the fp32-only operator lets values cross PCIe as f32
         flags |= (N.PHI_HOST_INPUT | (0 if self.exact else N.PHI_VALUES_F32)) if host else 0
         flags |= {"auto": 0, "sparse": N.PHI_FORCE_SPARSE, "dense": N.PHI_FORCE_DENSE,
-                  "bin": N.PHI_FORCE_DENSE,
-                  "fma": N.PHI_FORCE_DENSE | N.PHI_NO_TENSOR | N.PHI_NO_BIN,
-                  "tensor": N.PHI_FORCE_DENSE | N.PHI_TENSOR | N.PHI_NO_BIN}[_LAYOUT[0]]
+                  "bin": N.PHI_FORCE_DENSE}[_LAYOUT[0]]
         dims = N.Dims(d.n_atoms, d.n_voxels, d.n_fibers, d.n_dirs, d.n_coeffs)
         handle = ctypes.c_void_p()
         bad = ctypes.c_int64(-1)
@@ -137,11 +135,9 @@ class DeviceOperator:
 
     @property
     def kind(self):
-        """"bin" (binned two-phase products), "tensor" (single-pass tcgen05
-        tile kernels), "dense" (single-pass CUDA-core tile kernels) or
-        "sparse": the fp32 kernel family this operator uses."""
-        g = self.info.atom_groups
-        return "sparse" if g > 0 else "bin" if g == -2 else "tensor" if g < 0 else "dense"
+        """"bin" (binned two-phase products) or "sparse" (voxel-segment
+        kernels): the fp32 kernel family this operator uses."""
+        return "bin" if self.info.atom_groups == -2 else "sparse"
 
     @property
     def tensor_ops(self):
@@ -311,7 +307,7 @@ def wc_accumulate(tensor, dictionary, y, w_out, precision=None):
     return start.elapsed_time(stop) * 1e-3
 
 
-def autotune_layout(problem, trials=3, candidates=("sparse", "dense", "fma")):
+def autotune_layout(problem, trials=3, candidates=("sparse", "bin")):
     """Pick the fp32 kernel family for a problem by timing one DSC + one WC
     per candidate on the device (the paper's runtime selection between
     kernel variants, restructure.py:107-144 for

@@ -22,15 +22,14 @@ TOL32 = 1e-5
 
 
 # set_layout name -> DeviceOperator.kind it yields (at n_dirs <= 128)
-KIND = {"sparse": "sparse", "dense": "bin", "bin": "bin", "fma": "dense", "tensor": "tensor"}
-TENSOR_OPS = {"sparse": (), "dense": ("dsc", "wc"), "bin": ("dsc", "wc"), "fma": (), "tensor": ("dsc", "wc")}
+KIND = {"sparse": "sparse", "dense": "bin", "bin": "bin"}
+TENSOR_OPS = {"sparse": (), "dense": ("dsc", "wc"), "bin": ("dsc", "wc")}
 
 
-@pytest.fixture(params=["sparse", "bin", "fma", "tensor"])
+@pytest.fixture(params=["sparse", "bin"])
 def layout(request):
-    """Run a test against every fp32 kernel family: voxel-segment (sparse),
-    binned two-phase products on tcgen05 (bin, the default), single-pass tile
-    kernels on tcgen05 (tensor) or on CUDA cores only (fma)."""
+    """Run a test against every fp32 kernel family: voxel-segment (sparse)
+    and the binned two-phase products on tcgen05 (bin, the default)."""
     from paper_1905_06234_b200 import device
     device.set_layout(request.param)
     yield request.param

@@ -2,7 +2,7 @@
 kernels and timing (CUDA events) on a set of shapes, incl. duplicate-heavy
 voxels (split rows), long fascicles (split virtual slots) and C1/C2.
 
-    python tools/bin_check.py [--c2] [--layouts bin,tensor]
+    python tools/bin_check.py [--c2] [--skew] [--layouts bin,sparse]
 """
 import argparse
 import os
