@@ -1271,7 +1271,14 @@ __global__ void __launch_bounds__(kSideThreads, 1)
         return;
     }
     const uint32_t ct = threadIdx.x - 32;
-    const double scale = ldexp(1.0, bin_exponent_dev(fx, nt));
+    // fixed point in fp32 arithmetic (no 64-bit conversions): x = rint(t 2^e)
+    // is exact (|x| < 2^45, power-of-two scaling split so neither factor
+    // overflows), hi = floor(x / 2^24) and lo = x - hi 2^24 in [0, 2^24) are
+    // exact integers in float; identical to __double2ll_rn((double)t * 2^e)
+    // (ex > 252 only when every finite term is 0 in fp32: clamped, sc2 stays finite)
+    const int ex = min(bin_exponent_dev(fx, nt), 252);
+    const int ex1 = ex > 126 ? 126 : ex < -126 ? -126 : ex;
+    const float sc1 = ldexpf(1.f, ex1), sc2 = ldexpf(1.f, ex - ex1);
     constexpr int UPT = (kCH + kCons - 1) / kCons;  // units per consumer thread per chunk
     float4 zc[UPT], zn[UPT];
     // z of chunk j (its records are staged) into z[]
@@ -1363,9 +1370,11 @@ __global__ void __launch_bounds__(kSideThreads, 1)
                     nanf[__ldg(A.vf2f + s0 + ids[e])] = 1;
                     continue;
                 }
-                const long long q = __double2ll_rn((double)t * scale);
-                atomicAdd(lo + ids[e], (uint32_t)q & 0xFFFFFFu);
-                atomicAdd(hi + ids[e], (uint32_t)(int32_t)(q >> 24));
+                const float x = rintf(__fmul_rn(__fmul_rn(t, sc1), sc2));
+                const float hf = floorf(__fmul_rn(x, 0x1p-24f));
+                const float lf = __fsub_rn(x, __fmul_rn(hf, 0x1p24f));
+                atomicAdd(lo + ids[e], (uint32_t)lf);
+                atomicAdd(hi + ids[e], (uint32_t)(int32_t)hf);
             }
         }
         BD_ACC(9, t_p);

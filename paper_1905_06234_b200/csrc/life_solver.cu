@@ -178,13 +178,27 @@ __global__ void __launch_bounds__(BT)
         part_z[blockIdx.x] = sz[0];
     }
     if (last_arrive<BT>(counter)) {
-        if (threadIdx.x == 0) {
-            double m = INFINITY;
-            unsigned long long zz = 0;
-            for (int b = 0; b < (int)gridDim.x; ++b) {
-                m = fmin(m, __ldcg(part_min + b));
-                zz += __ldcg(part_z + b);
+        // the block's threads fold the per-block partials (fixed order:
+        // strided, then the shared-memory tree)
+        double m = INFINITY;
+        unsigned long long zz = 0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += BT) {
+            m = fmin(m, __ldcg(part_min + b));
+            zz += __ldcg(part_z + b);
+        }
+        smn[threadIdx.x] = m;
+        sz[threadIdx.x] = zz;
+        __syncthreads();
+        for (int o = BT / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) {
+                smn[threadIdx.x] = fmin(smn[threadIdx.x], smn[threadIdx.x + o]);
+                sz[threadIdx.x] += sz[threadIdx.x + o];
             }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            m = smn[0];
+            zz = sz[0];
             const int it = s->iter;
             life_trace_record r;
             r.iteration = it;
