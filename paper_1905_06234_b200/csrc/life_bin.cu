@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstring>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 #include "life_common.cuh"
@@ -859,42 +860,66 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
         LIFE_CUDA(cudaMemcpyAsync(hbin.data(), phi->b_binptr, hbin.size() * 4, cudaMemcpyDeviceToHost, st));
         LIFE_CUDA(cudaMemcpyAsync(hcta.data(), dcs, hcta.size() * 4, cudaMemcpyDeviceToHost, st));
         LIFE_CUDA(cudaStreamSynchronize(st));
+        // CTAs are independent: host threads build their chunk lists, which
+        // are concatenated in CTA order
+        const int nthr = std::max(1, std::min(8, side_grid));
+        std::vector<std::vector<uint32_t>> tch(nthr);
+        std::vector<std::vector<uint16_t>> tgr(nthr);
+        std::vector<std::vector<uint32_t>> tcnt(nthr);  // chunks per CTA
+        auto build = [&](int t) {
+            const int c0 = side_grid * t / nthr, c1 = side_grid * (t + 1) / nthr;
+            auto &chunks = tch[t];
+            auto &cgrp = tgr[t];
+            int b = (int)(std::upper_bound(hbin.begin(), hbin.end(), hcta[c0]) - hbin.begin()) - 1;
+            b = std::max(0, std::min(b, nbins));
+            for (int c = c0; c < c1; ++c) {
+                const size_t before = chunks.size();
+                const uint32_t S0 = hcta[c], S1 = hcta[c + 1];
+                uint32_t s = S0;
+                while (b < nbins && hbin[b + 1] <= S0) ++b;
+                int bb = b;
+                while (s < S1) {
+                    while (bb < nbins && hbin[bb + 1] <= s) ++bb;
+                    const uint32_t pe = std::min(S1, hbin[bb + 1]);
+                    const uint32_t pu0 = hsrc[s], pu1 = hsrc[pe];
+                    uint32_t sl = s;  // segment containing the chunk start
+                    bool first = true;
+                    for (uint32_t u0 = pu0; u0 < pu1; u0 += (uint32_t)kCH) {
+                        const uint32_t u1 = std::min(pu1, u0 + (uint32_t)kCH);
+                        while (hsrc[sl + 1] <= u0) ++sl;
+                        uint32_t sh = sl;  // segment containing u1 - 1
+                        while (hsrc[sh + 1] < u1) ++sh;
+                        const uint32_t ns = sh - sl + 1;
+                        // per 32-unit group of the chunk: its first segment
+                        for (uint32_t g = 0, k = sl; g < 32; ++g) {
+                            const uint32_t ug = u0 + 32u * g;
+                            if (ug < u1)
+                                while (hsrc[k + 1] <= ug) ++k;
+                            cgrp.push_back((uint16_t)(ug < u1 ? k - sl : ns - 1));
+                        }
+                        chunks.push_back(u0);
+                        chunks.push_back((u1 - u0) | (first ? 0x80000000u : 0u));
+                        chunks.push_back(sl);
+                        chunks.push_back(ns | ((uint32_t)bb << 16));
+                        first = false;
+                    }
+                    s = pe;
+                }
+                tcnt[t].push_back((uint32_t)((chunks.size() - before) / 4));
+            }
+        };
+        {
+            std::vector<std::thread> pool;
+            for (int t = 1; t < nthr; ++t) pool.emplace_back(build, t);
+            build(0);
+            for (auto &th : pool) th.join();
+        }
         std::vector<uint32_t> chunks, ctachunk(1, 0);
         std::vector<uint16_t> cgrp;
-        int b = 0;
-        for (int c = 0; c < side_grid; ++c) {
-            const uint32_t S0 = hcta[c], S1 = hcta[c + 1];
-            uint32_t s = S0;
-            while (b < nbins && hbin[b + 1] <= S0) ++b;
-            int bb = b;
-            while (s < S1) {
-                while (bb < nbins && hbin[bb + 1] <= s) ++bb;
-                const uint32_t pe = std::min(S1, hbin[bb + 1]);
-                const uint32_t pu0 = hsrc[s], pu1 = hsrc[pe];
-                uint32_t sl = s;  // segment containing the chunk start
-                bool first = true;
-                for (uint32_t u0 = pu0; u0 < pu1; u0 += (uint32_t)kCH) {
-                    const uint32_t u1 = std::min(pu1, u0 + (uint32_t)kCH);
-                    while (hsrc[sl + 1] <= u0) ++sl;
-                    uint32_t sh = sl;  // segment containing u1 - 1
-                    while (hsrc[sh + 1] < u1) ++sh;
-                    const uint32_t ns = sh - sl + 1;
-                    // per 32-unit group of the chunk: its first segment
-                    for (uint32_t g = 0, k = sl; g < 32; ++g) {
-                        const uint32_t ug = u0 + 32u * g;
-                        if (ug < u1)
-                            while (hsrc[k + 1] <= ug) ++k;
-                        cgrp.push_back((uint16_t)(ug < u1 ? k - sl : ns - 1));
-                    }
-                    chunks.push_back(u0);
-                    chunks.push_back((u1 - u0) | (first ? 0x80000000u : 0u));
-                    chunks.push_back(sl);
-                    chunks.push_back(ns | ((uint32_t)bb << 16));
-                    first = false;
-                }
-                s = pe;
-            }
-            ctachunk.push_back((uint32_t)(chunks.size() / 4));
+        for (int t = 0; t < nthr; ++t) {
+            chunks.insert(chunks.end(), tch[t].begin(), tch[t].end());
+            cgrp.insert(cgrp.end(), tgr[t].begin(), tgr[t].end());
+            for (uint32_t k : tcnt[t]) ctachunk.push_back(ctachunk.back() + k);
         }
         if (chunks.empty()) {
             chunks.assign(4, 0u);
