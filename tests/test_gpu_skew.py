@@ -137,3 +137,32 @@ def test_host_input_reports_first_bad_fiber():
     with pytest.raises(IndexOutOfRange) as ei:
         device.DeviceOperator(bad, dic)
     assert ei.value.dimension == "fiber" and ei.value.position == 123_457, str(ei.value)
+
+
+@pytest.mark.parametrize("skew", ["lognormal", "zipf"])
+def test_device_generator_c5(skew):
+    """The C5 device generator (datagen.draw_skewed_device): deterministic per
+    seed, skewed as asked, and the default products within tolerance of the
+    fp64 ones on what it draws (tools/sweep_c5.py checks up to 16M)."""
+    from paper_1905_06234_b200 import datagen
+    d1 = datagen.draw_skewed_device(2_000_000, skew, seed=5)
+    d2 = datagen.draw_skewed_device(2_000_000, skew, seed=5)
+    for x, y in zip(d1[1:6], d2[1:6]):
+        assert torch.equal(x, y)
+    dims, a, v, f, val, dic, fmax = d1
+    assert dims.n_coeffs == 2_000_000 and int(torch.bincount(f).max()) == fmax
+    assert fmax > 20 * dims.n_coeffs // dims.n_fibers  # long fascicles present
+    op = device.DeviceOperator.from_device(dims, a, v, f, val, dic, exact=True)
+    assert op.kind == "bin"
+    w = torch.rand(dims.n_fibers, device="cuda")
+    y = torch.empty(dims.signal_len, device="cuda")
+    g = torch.empty(dims.n_fibers, device="cuda")
+    op.dsc_f32(w, y)
+    op.wc_f32(y, g)
+    y64 = torch.zeros(dims.signal_len, dtype=torch.float64, device="cuda")
+    op.dsc_f64(w.double(), y64)
+    g64 = torch.zeros(dims.n_fibers, dtype=torch.float64, device="cuda")
+    op.wc_f64(y.double(), g64)
+    assert float((y.double() - y64).norm() / y64.norm()) <= TOL32
+    assert float((g.double() - g64).norm() / g64.norm()) <= TOL32
+    op.close()

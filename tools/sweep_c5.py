@@ -27,32 +27,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402  (spmv_bytes, peaks)
 import paper_1905_06234_b200 as L  # noqa: E402
-from paper_1905_06234_b200 import _native, device  # noqa: E402
+from paper_1905_06234_b200 import _native, datagen, device  # noqa: E402
 
 
 def draw(nc, skew, seed):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    na, nt = 1057, 96
-    nv, nf = max(1, nc // 500), max(1, nc // 200)
-    if skew == "zipf":
-        ranks = torch.arange(1, nf + 1, device="cuda", dtype=torch.float64)
-        w = 1.0 / ranks ** 0.8
-    else:
-        w = torch.exp(torch.randn(nf, generator=g, device="cuda", dtype=torch.float64))
-    w = w[torch.randperm(nf, generator=g, device="cuda")]
-    counts = torch.floor(w / w.sum() * nc).to(torch.int64)
-    short = nc - int(counts.sum())
-    if short > 0:
-        counts[torch.randperm(nf, generator=g, device="cuda")[:short]] += 1
-    fibers = torch.repeat_interleave(torch.arange(nf, device="cuda", dtype=torch.int32), counts)
-    fibers = fibers[torch.randperm(nc, generator=g, device="cuda")]
-    voxels = torch.randint(0, nv, (nc,), generator=g, device="cuda", dtype=torch.int32)
-    atoms = torch.randint(0, na, (nc,), generator=g, device="cuda", dtype=torch.int32)
-    values = 1.0 - torch.rand(nc, generator=g, device="cuda", dtype=torch.float64)
-    rows = torch.randn(na, nt, generator=g, device="cuda", dtype=torch.float64)
-    rows /= rows.norm(dim=1, keepdim=True)
-    dims = L.Dims(na, nv, nf, nt, nc)
-    return dims, atoms, voxels, fibers, values, rows.reshape(-1), int(counts.max())
+    return datagen.draw_skewed_device(nc, skew, seed)
 
 
 def timed(fn, reps):
@@ -95,9 +74,10 @@ def main():
         ymax = torch.empty(1, device="cuda")
         dsc_ms = timed(lambda: op.dsc_f32(w, y, flags=_native.SKIP_ZERO, absmax=ymax), args.reps)
         wc_ms = timed(lambda: op.wc_f32(y, g, y_absmax=ymax), args.reps)
-        bd, bw = bench.spmv_bytes((dims.n_atoms, dims.n_voxels, dims.n_fibers, dims.n_dirs, nc))
-        if "dsc" in op.tensor_ops:  # 8-byte packed entries (actual sizes)
-            bd, _ = bench.spmv_bytes((dims.n_atoms, dims.n_voxels, dims.n_fibers, dims.n_dirs, nc), idx_bytes=2)
+        # binned layout: 2-byte cell + 2-byte slot + 4-byte value per coefficient
+        # for both products (SURVEY 8(d) under compression, as bench.py)
+        ib = 2 if op.kind == "bin" else 4
+        bd, bw = bench.spmv_bytes((dims.n_atoms, dims.n_voxels, dims.n_fibers, dims.n_dirs, nc), idx_bytes=ib)
         parity = None
         if exact:
             y64 = torch.zeros(dims.signal_len, dtype=torch.float64, device="cuda")
