@@ -299,12 +299,14 @@ __global__ void k_iota(uint32_t *o, int64_t n)
 {
     for (int64_t i = gtid(); i < n; i += gstride()) o[i] = (uint32_t)i;
 }
-__global__ void k_key_va(const uint32_t *a, const uint32_t *v, int64_t n, uint32_t na, unsigned long long *key)
+template <typename K>
+__global__ void k_key_va(const uint32_t *a, const uint32_t *v, int64_t n, uint32_t na, K *key)
 {
-    for (int64_t i = gtid(); i < n; i += gstride()) key[i] = (unsigned long long)v[i] * na + a[i];
+    for (int64_t i = gtid(); i < n; i += gstride()) key[i] = (K)((unsigned long long)v[i] * na + a[i]);
 }
 // run heads of a sorted u64 key: head[p] = p at a run start, else 0
-__global__ void k_heads64(const unsigned long long *k, int64_t n, uint32_t *head)
+template <typename K>
+__global__ void k_heads64(const K *k, int64_t n, uint32_t *head)
 {
     for (int64_t p = gtid(); p < n; p += gstride()) head[p] = (p == 0 || k[p] != k[p - 1]) ? (uint32_t)p : 0u;
 }
@@ -314,7 +316,8 @@ __global__ void k_heads32(const uint32_t *k, int64_t n, uint32_t *head)
 }
 // rank of each coefficient among the equal (voxel, atom) pairs in stable
 // order, and the largest rank per voxel
-__global__ void k_rank_va(const unsigned long long *sk, const uint32_t *perm, const uint32_t *rstart, int64_t n,
+template <typename K>
+__global__ void k_rank_va(const K *sk, const uint32_t *perm, const uint32_t *rstart, int64_t n,
                           uint32_t na, uint32_t *rank_o, uint32_t *vmaxr)
 {
     for (int64_t p = gtid(); p < n; p += gstride()) {
@@ -361,16 +364,19 @@ __global__ void k_vf_identity(const uint32_t *f, const uint32_t *f2vf, int64_t n
 {
     for (int64_t i = gtid(); i < n; i += gstride()) vf_o[i] = f2vf[f[i]];
 }
-// bin-major key (bin, tile, chunk) of each coefficient
+// bin-major key (bin, tile, chunk) of each coefficient and the payload the
+// placement needs, sorted along with it (no gathers afterwards): fp32 value
+// bits << 32 | bin slot << 16 | tile cell
 __global__ void k_key_bm(const uint32_t *a, const uint32_t *row_o, const uint32_t *vf_o, const uint32_t *slot_of_row,
-                         const uint32_t *rank_o, int64_t n, int ka_shift, uint32_t nch, uint32_t ntiles,
-                         unsigned long long *kbm)
+                         const double *val, int64_t n, int ka_shift, int ka, uint32_t nch, uint32_t ntiles,
+                         unsigned long long *kbm, unsigned long long *pay)
 {
     for (int64_t i = gtid(); i < n; i += gstride()) {
-        const uint32_t t = slot_of_row[row_o[i]] / kTV;
-        const uint32_t c = a[i] >> ka_shift;
-        const uint32_t b = vf_o[i] / kSB;
+        const uint32_t sr = slot_of_row[row_o[i]], ai = a[i], vf = vf_o[i];
+        const uint32_t t = sr / kTV, c = ai >> ka_shift, b = vf / kSB;
         kbm[i] = ((unsigned long long)b * ntiles + t) * nch + c;
+        const uint32_t cell = (sr % kTV) * (uint32_t)(ka + 4) + (ai & (uint32_t)(ka - 1));
+        pay[i] = ((unsigned long long)__float_as_uint((float)val[i]) << 32) | ((vf % kSB) << 16) | cell;
     }
 }
 __global__ void k_head_flags(const unsigned long long *k, int64_t n, uint8_t *head, uint32_t *head32)
@@ -429,19 +435,18 @@ __global__ void k_seg_tm(const uint32_t *perm_seg, const uint32_t *tm_excl, cons
     }
 }
 // place every coefficient in both orders
-__global__ void k_place(const uint32_t *perm_bm, const uint32_t *segid, const uint32_t *first, const uint32_t *src4,
-                        const uint32_t *dst4, int64_t n, const uint32_t *vf_o, const double *val, const uint32_t *a,
-                        const uint32_t *row_o, const uint32_t *slot_of_row, int ka, uint16_t *vid, float *val32,
+__global__ void k_place(const unsigned long long *pay, const uint32_t *segid, const uint32_t *first,
+                        const uint32_t *src4, const uint32_t *dst4, int64_t n, uint16_t *vid, float *val32,
                         uint16_t *cellr)
 {
     for (int64_t p = gtid(); p < n; p += gstride()) {
-        const uint32_t i = perm_bm[p], s = segid[p] - 1u;
+        const uint32_t s = segid[p] - 1u;
         const uint32_t idx = (uint32_t)p - first[s];
         const uint32_t bp = 4u * src4[s] + idx, tp = 4u * dst4[s] + idx;
-        vid[bp] = (uint16_t)(vf_o[i] % kSB);
-        val32[bp] = (float)val[i];
-        const uint32_t lane = slot_of_row[row_o[i]] % kTV;
-        cellr[tp] = (uint16_t)(lane * (uint32_t)(ka + 4) + (a[i] & (uint32_t)(ka - 1)));
+        const unsigned long long q = pay[p];
+        vid[bp] = (uint16_t)((uint32_t)q >> 16);
+        val32[bp] = __uint_as_float((uint32_t)(q >> 32));
+        cellr[tp] = (uint16_t)(q & 0xFFFFu);
     }
 }
 // lower bound of key b * per_bin over the bin-major segment keys
@@ -497,8 +502,8 @@ static int bits64(unsigned long long x)
     return std::max(b, 1);
 }
 
-template <typename K>
-static int sort_pairs(const K *kin, K *kout, const uint32_t *vin, uint32_t *vout, int64_t n, int bits,
+template <typename K, typename V = uint32_t>
+static int sort_pairs(const K *kin, K *kout, const V *vin, V *vout, int64_t n, int bits,
                       cudaStream_t st)
 {
     size_t tb = 0;
@@ -599,15 +604,28 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     LIFE_TRY(talloc((void **)&vmaxr, (size_t)nv * 4));
     k_iota<<<gridn(n), 256, 0, st>>>(iota, n);
     LIFE_CHECK_LAUNCH();
-    k_key_va<<<gridn(n), 256, 0, st>>>(a, v, n, na, kva);
-    LIFE_CHECK_LAUNCH();
-    LIFE_TRY(sort_pairs<unsigned long long>(kva, skva, iota, perm, n, bits64((unsigned long long)nv * na), st));
-    k_heads64<<<gridn(n), 256, 0, st>>>(skva, n, head);
-    LIFE_CHECK_LAUNCH();
-    LIFE_TRY(scan_max(head, rstart, n, st));
+    const unsigned long long vamax = (unsigned long long)nv * na;
     LIFE_CUDA(cudaMemsetAsync(vmaxr, 0, (size_t)nv * 4, st));
-    k_rank_va<<<gridn(n), 256, 0, st>>>(skva, perm, rstart, n, na, rank_o, vmaxr);
-    LIFE_CHECK_LAUNCH();
+    if (vamax <= 0xFFFFFFFFull) {  // 32-bit (voxel, atom) keys: a third less sort traffic
+        uint32_t *k32 = reinterpret_cast<uint32_t *>(kva), *sk32 = reinterpret_cast<uint32_t *>(skva);
+        k_key_va<uint32_t><<<gridn(n), 256, 0, st>>>(a, v, n, na, k32);
+        LIFE_CHECK_LAUNCH();
+        LIFE_TRY(sort_pairs<uint32_t>(k32, sk32, iota, perm, n, bits64(vamax), st));
+        k_heads64<uint32_t><<<gridn(n), 256, 0, st>>>(sk32, n, head);
+        LIFE_CHECK_LAUNCH();
+        LIFE_TRY(scan_max(head, rstart, n, st));
+        k_rank_va<uint32_t><<<gridn(n), 256, 0, st>>>(sk32, perm, rstart, n, na, rank_o, vmaxr);
+        LIFE_CHECK_LAUNCH();
+    } else {
+        k_key_va<unsigned long long><<<gridn(n), 256, 0, st>>>(a, v, n, na, kva);
+        LIFE_CHECK_LAUNCH();
+        LIFE_TRY(sort_pairs<unsigned long long>(kva, skva, iota, perm, n, bits64(vamax), st));
+        k_heads64<unsigned long long><<<gridn(n), 256, 0, st>>>(skva, n, head);
+        LIFE_CHECK_LAUNCH();
+        LIFE_TRY(scan_max(head, rstart, n, st));
+        k_rank_va<unsigned long long><<<gridn(n), 256, 0, st>>>(skva, perm, rstart, n, na, rank_o, vmaxr);
+        LIFE_CHECK_LAUNCH();
+    }
 
     setup_mark(st, "bin phase 1");
     // 2. tile rows: a voxel gets one row per kRanks duplicate ranks
@@ -748,14 +766,15 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     setup_mark(st, "bin phase 4");
     // 5. bin-major order (bin, tile, chunk), stable; its runs are the
     // segments, each padded to 4 entries in both orders
-    unsigned long long *kbm = kva, *skbm = skva;
-    uint32_t *perm_bm = perm;
-    k_key_bm<<<gridn(n), 256, 0, st>>>(a, row_o, vf_o, d_slot, rank_o, n, ka_shift, (uint32_t)nch, (uint32_t)ntiles,
-                                       kbm);
+    unsigned long long *kbm = kva, *skbm = skva, *pay, *spay;
+    LIFE_TRY(talloc((void **)&pay, n * 8));
+    LIFE_TRY(talloc((void **)&spay, n * 8));
+    k_key_bm<<<gridn(n), 256, 0, st>>>(a, row_o, vf_o, d_slot, val, n, ka_shift, ka, (uint32_t)nch, (uint32_t)ntiles,
+                                       kbm, pay);
     LIFE_CHECK_LAUNCH();
     const int64_t nsteps = ntiles * nch;
     const unsigned long long per_bin = (unsigned long long)ntiles * nch;
-    LIFE_TRY(sort_pairs<unsigned long long>(kbm, skbm, iota, perm_bm, n, bits64(per_bin * nbins), st));
+    LIFE_TRY((sort_pairs<unsigned long long, unsigned long long>(kbm, skbm, pay, spay, n, bits64(per_bin * nbins), st)));
     uint8_t *seghead;
     uint32_t *head32 = head, *segid = rstart, *first;
     int64_t *nsel;
@@ -839,8 +858,8 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     LIFE_CHECK_LAUNCH();
     LIFE_CUDA(cudaMemsetAsync(phi->b_val, 0, ((size_t)nbm + 8) * 4, st));
     LIFE_CUDA(cudaMemsetAsync(phi->b_scr, 0, ((size_t)npad + 8) * 4, st));
-    k_place<<<gridn(n), 256, 0, st>>>(perm_bm, segid, first, phi->b_segsrc, phi->b_segdst, n, vf_o, val, a, row_o,
-                                      d_slot, ka, phi->b_vid, phi->b_val, phi->b_cellr);
+    k_place<<<gridn(n), 256, 0, st>>>(spay, segid, first, phi->b_segsrc, phi->b_segdst, n, phi->b_vid, phi->b_val,
+                                      phi->b_cellr);
     LIFE_CHECK_LAUNCH();
 
     setup_mark(st, "bin phase 6");
