@@ -187,10 +187,11 @@ class NcclComm:
             pass
 
 
-def solve_sharded(problem, config=None, group=None, w0=None, ranges=None):
+def solve_sharded(problem, config=None, group=None, w0=None, ranges=None, comm=None):
     """SBBNNLS with Phi voxel-sharded over the ranks of a torch.distributed
     group (every rank calls it with the same problem).  Returns (w, trace);
-    both are identical on all ranks."""
+    both are identical on all ranks.  `comm` reuses a communicator
+    (NcclComm / TorchComm) across calls; by default one is made per call."""
     import torch
 
     from . import device
@@ -202,7 +203,8 @@ def solve_sharded(problem, config=None, group=None, w0=None, ranges=None):
     import torch.distributed as dist
     # NCCL process groups: the library's own capturable NCCL communicator
     # (graphs on); other backends (gloo in tests): the torch callback
-    comm = NcclComm(group) if dist.get_backend(group) == "nccl" else TorchComm(group)
+    if comm is None:
+        comm = NcclComm(group) if dist.get_backend(group) == "nccl" else TorchComm(group)
     counts = np.bincount(problem.tensor.voxels, minlength=problem.dims.n_voxels)
     ranges = ranges or shard_voxel_ranges(counts, comm.nranks)
     v0, v1 = ranges[comm.rank]
