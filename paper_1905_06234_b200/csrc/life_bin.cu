@@ -1444,25 +1444,44 @@ __global__ void __launch_bounds__(BT)
     const bool accumulate = flags & LIFE_ACCUMULATE;
     const bool project = (flags & LIFE_PROJECT_GRAD) && w_ref != nullptr;
     double sq = 0.0;
-    for (int f = blockIdx.x * BT + threadIdx.x; f < nf; f += gridDim.x * BT) {
-        const long long q = (long long)wfix[f];
-        wfix[f] = 0ull;
-        const bool bad = nanf[f] != 0;
-        if (bad) nanf[f] = 0;
-        float o = bad ? __int_as_float(0x7fc00000) : (float)((double)q * inv);
-        if (accumulate) o = w_out[f] + o;
-        if (project && w_ref[f] == 0.f && o > 0.f) o = 0.f;
-        w_out[f] = o;
-        sq += (double)o * (double)o;
+    constexpr int U = 4;  // fascicles in flight per thread
+    const int stride = gridDim.x * BT;
+    for (int f0 = blockIdx.x * BT + threadIdx.x; f0 < nf; f0 += U * stride) {
+        long long q[U];
+        bool bad[U];
+        float acc[U], ref[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int f = f0 + k * stride;
+            q[k] = f < nf ? (long long)wfix[f] : 0ll;
+            bad[k] = f < nf && nanf[f] != 0;
+            acc[k] = (accumulate && f < nf) ? w_out[f] : 0.f;
+            ref[k] = (project && f < nf) ? w_ref[f] : 1.f;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int f = f0 + k * stride;
+            if (f >= nf) break;
+            wfix[f] = 0ull;
+            if (bad[k]) nanf[f] = 0;
+            float o = bad[k] ? __int_as_float(0x7fc00000) : (float)((double)q[k] * inv);
+            if (accumulate) o = acc[k] + o;
+            if (project && ref[k] == 0.f && o > 0.f) o = 0.f;
+            w_out[f] = o;
+            sq += (double)o * (double)o;
+        }
     }
-    __shared__ double s[BT];
-    s[threadIdx.x] = sq;
+    // block partial: warp shuffles, then the warps in order
+    __shared__ double s[BT / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = sq;
     __syncthreads();
-    for (int h = BT / 2; h > 0; h >>= 1) {
-        if (threadIdx.x < h) s[threadIdx.x] += s[threadIdx.x + h];
-        __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < BT / 32; ++i) t += s[i];
+        part[blockIdx.x] = t;
     }
-    if (threadIdx.x == 0) part[blockIdx.x] = s[0];
     if (last_cta(counter)) {
         const double tot = block_reduce<double>(part, gridDim.x, 0.0, OpSum{}, BT);
         if (threadIdx.x == 0) {
@@ -2574,7 +2593,7 @@ int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, c
             LIFE_CHECK_LAUNCH();
         }
     }
-    const int blocks = std::max(1, std::min(phi->sms * 4, (phi->nf + 255) / 256));
+    const int blocks = std::max(1, std::min(phi->sms, (phi->nf + 255) / 256));
     k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->nf, w, w_ref, flags, fx, phi->nt,
                                           phi->part_d2, phi->counter2, sumsq, h);
     LIFE_CHECK_LAUNCH();
