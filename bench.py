@@ -373,8 +373,8 @@ def run_ours(args, dims):
             e2e_s = float(tt.item())
         # bytes crossing PCIe (life_phi_create with LIFE_PHI_HOST_INPUT): atoms as
         # u16 when na <= 65536, voxels and fibers u32, values f32 (fp32-only
-        # operator); the dictionary and b as f64
-        h2d = nc * ((2 if na <= 65536 else 4) + 4 + 4 + 4) + na * nt * 8 + nv * nt * 8
+        # operator); the dictionary as f64, b as f32 (rounded while staging)
+        h2d = nc * ((2 if na <= 65536 else 4) + 4 + 4 + 4) + na * nt * 8 + nv * nt * 4
         cached = fresh.__dict__.get("_device_cache", {}).get("op")
         e2e = {"value": args.steps / e2e_s, "unit": UNIT,
                "setup_s": round(tr.setup_seconds, 3), "loop_s": round(tr.loop_seconds, 4),

@@ -112,6 +112,10 @@ LIFE_API int life_phi_destroy(life_phi *phi);
  * the source may be reused.  Used for the LIFE_PHI_HOST_INPUT arrays and by
  * the Python layer for b / w0 (sbbnnls.solve's inputs, sbbnnls.py:223). */
 LIFE_API int life_copy_h2d(void *dst_dev, const void *src_host, int64_t bytes, void *stream);
+/* The same for an f64 host vector into an f32 device vector (rounded to
+ * nearest on the host while staging: half the bytes cross PCIe); the fp32
+ * solver's b (sbbnnls.py:223 problem.y). */
+LIFE_API int life_copy_h2d_f32(float *dst_dev, const double *src_host, int64_t count, void *stream);
 
 typedef struct life_phi_info {
     life_dims dims;

@@ -94,6 +94,7 @@ SIGNATURES = {
                                        ctypes.POINTER(c_void_p), ctypes.POINTER(c_i64)]),
     "life_phi_destroy": (ctypes.c_int, [c_void_p]),
     "life_copy_h2d": (ctypes.c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
+    "life_copy_h2d_f32": (ctypes.c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "life_phi_get_info": (ctypes.c_int, [c_void_p, ctypes.POINTER(PhiInfo)]),
     "life_stable_argsort_u32": (ctypes.c_int, [c_void_p, c_i64, c_void_p, c_void_p]),
     "life_detect_runs_u32": (ctypes.c_int, [c_void_p, c_i64, c_void_p, c_void_p,

@@ -1047,6 +1047,22 @@ int life_copy_h2d(void *dst_dev, const void *src_host, int64_t bytes, void *stre
     return ok();
 }
 
+int life_copy_h2d_f32(float *dst_dev, const double *src_host, int64_t count, void *stream)
+{
+    if ((!dst_dev || !src_host) && count > 0) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
+    if (count < 0) return fail(LIFE_ERR_INVALID_ARGUMENT, "negative size");
+    if (count > 0 && count * 4 < (4 << 20)) {  // small: round on the host, one copy
+        std::vector<float> tmp((size_t)count);
+        for (int64_t i = 0; i < count; ++i) tmp[i] = (float)src_host[i];
+        LIFE_CUDA(cudaMemcpyAsync(dst_dev, tmp.data(), (size_t)count * 4, cudaMemcpyHostToDevice,
+                                  static_cast<cudaStream_t>(stream)));
+        LIFE_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+        return ok();
+    }
+    LIFE_TRY(h2d_staged_cvt(dst_dev, src_host, (size_t)count * 4, 1, static_cast<cudaStream_t>(stream)));
+    return ok();
+}
+
 int life_phi_destroy(life_phi *phi)
 {
     if (phi) destroy_impl(phi);

@@ -71,6 +71,11 @@ def upload(arr, dtype=None, stream=None):
     torch .to("cuda")); `dtype` converts on the device afterwards."""
     torch = N.require_cuda()
     a = np.ascontiguousarray(arr)
+    if a.dtype == np.float64 and dtype == torch.float32:  # rounded while staging
+        t = torch.empty(a.shape, dtype=torch.float32, device="cuda")
+        N.check(N.lib().life_copy_h2d_f32(ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(a.ctypes.data),
+                                          a.size, N.stream_ptr(stream)))
+        return t
     tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
            np.dtype(np.uint32): torch.int32, np.dtype(np.int32): torch.int32,
            np.dtype(np.int64): torch.int64}[a.dtype]
