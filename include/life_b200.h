@@ -107,6 +107,15 @@ LIFE_API int life_phi_create(const life_dims *dims, const uint32_t *atoms,
                     void *stream, life_phi **out, int64_t *bad_position);
 LIFE_API int life_phi_destroy(life_phi *phi);
 
+/* Device blocks of destroyed operators and solver sessions stay mapped in a
+ * per-process cache (up to LIFE_B200_BLOCK_CACHE_MB, default 24 GiB) and are
+ * reused by the next operator; cudaMalloc/cudaFree of the GBs an operator
+ * holds cost 0.1-0.3 s on some hosts.  The reference has no counterpart (it
+ * allocates numpy arrays per call, engine.py:218-244).  Release hands every
+ * cached block back to the driver; bytes reports the cached total. */
+LIFE_API int life_release_cached_memory(void);
+LIFE_API int life_cached_memory_bytes(int64_t *bytes);
+
 /* Copy bytes from pageable host memory to the device through pinned staging
  * buffers (host memcpy overlapped with the DMA); stream-ordered, returns when
  * the source may be reused.  Used for the LIFE_PHI_HOST_INPUT arrays and by

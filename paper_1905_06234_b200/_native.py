@@ -93,6 +93,8 @@ SIGNATURES = {
                                        c_void_p, c_void_p, c_u32, c_void_p,
                                        ctypes.POINTER(c_void_p), ctypes.POINTER(c_i64)]),
     "life_phi_destroy": (ctypes.c_int, [c_void_p]),
+    "life_release_cached_memory": (ctypes.c_int, []),
+    "life_cached_memory_bytes": (ctypes.c_int, [ctypes.POINTER(c_i64)]),
     "life_copy_h2d": (ctypes.c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "life_copy_h2d_f32": (ctypes.c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "life_phi_get_info": (ctypes.c_int, [c_void_p, ctypes.POINTER(PhiInfo)]),
@@ -167,6 +169,18 @@ def check(status, position=None):
 
 def launch_count():
     return int(lib().life_launch_count())
+
+
+def cached_memory_bytes():
+    """Device bytes of destroyed operators / sessions kept for reuse."""
+    n = c_i64(0)
+    check(lib().life_cached_memory_bytes(ctypes.byref(n)))
+    return int(n.value)
+
+
+def release_cached_memory():
+    """Hand the library's cached device blocks back to the driver."""
+    check(lib().life_release_cached_memory())
 
 
 def require_cuda():

@@ -180,16 +180,23 @@ int h2d_staged_cvt(void *dst, const void *src, size_t bytes, int mode, cudaStrea
 // (operator construction phases, stderr)
 void setup_mark(cudaStream_t st, const char *what);
 
+// Device block cache (life_phi.cu).  Operators and solver sessions allocate
+// GBs at C2; cudaMalloc / cudaFree of them costs 0.1-0.3 s per operator on
+// some hosts (page mapping, implicit device syncs), so freed blocks are kept
+// mapped per (device, size class) and handed to the next operator.
+// dev_free's caller guarantees the device no longer uses the block.
+int dev_alloc(void **p, size_t bytes);
+void dev_free(void *p);
+int pinned_alloc(void **p, size_t bytes);  // small page-locked host words (same idea)
+void pinned_free(void *p);
+
 template <typename T>
 int dalloc(life_phi *phi, T **p, size_t n)
 {
     *p = nullptr;
     if (n == 0) n = 1;
-    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T));
-    if (e != cudaSuccess)
-        return fail(e == cudaErrorMemoryAllocation ? LIFE_ERR_OUT_OF_MEMORY
-                                                    : LIFE_ERR_CUDA,
-                    std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    const int rc = dev_alloc(reinterpret_cast<void **>(p), n * sizeof(T));
+    if (rc != LIFE_OK) return rc;
     phi->allocs.push_back(*p);
     phi->device_bytes += static_cast<int64_t>(n * sizeof(T));
     return LIFE_OK;

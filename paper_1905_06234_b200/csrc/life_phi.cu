@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -52,6 +53,144 @@ int ensure_smem_ptr(const void *func, size_t bytes)
         return fail(LIFE_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     cur = bytes;
     return LIFE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device block cache (see life_common.cuh)
+// ---------------------------------------------------------------------------
+
+namespace {
+struct BlockCache {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void *> free_;      // (device, size class) -> block
+    std::unordered_map<void *, std::pair<int, size_t>> owned;  // every block handed out
+    size_t cached = 0, cap = 0;
+};
+BlockCache &bcache()
+{
+    static BlockCache *c = [] {
+        auto *b = new BlockCache;  // process lifetime
+        const char *e = std::getenv("LIFE_B200_BLOCK_CACHE_MB");
+        b->cap = e ? (size_t)std::strtoull(e, nullptr, 10) << 20 : (size_t)24 << 30;
+        return b;
+    }();
+    return *c;
+}
+size_t size_class(size_t b)
+{
+    if (b >= ((size_t)1 << 20)) return (b + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1);
+    return (std::max<size_t>(b, 256) + 255) & ~(size_t)255;
+}
+// free cached blocks until `need` more bytes fit under the cap (largest first)
+void trim_locked(BlockCache &c, size_t need)
+{
+    while (!c.free_.empty() && c.cached + need > c.cap) {
+        auto it = std::prev(c.free_.end());
+        c.cached -= it->first.second;
+        c.owned.erase(it->second);
+        cudaFree(it->second);
+        c.free_.erase(it);
+    }
+}
+}  // namespace
+
+int dev_alloc(void **p, size_t bytes)
+{
+    *p = nullptr;
+    const size_t r = size_class(bytes);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    BlockCache &c = bcache();
+    {
+        std::lock_guard<std::mutex> lock(c.mu);
+        // smallest cached block of this device that fits, at most 1/8 larger
+        auto it = c.free_.lower_bound({dev, r});
+        if (it != c.free_.end() && it->first.first == dev && it->first.second <= r + r / 8) {
+            *p = it->second;
+            c.cached -= it->first.second;
+            c.free_.erase(it);
+            return LIFE_OK;
+        }
+    }
+    cudaError_t e = cudaMalloc(p, r);
+    if (e == cudaErrorMemoryAllocation) {  // give the cache back and retry once
+        cudaGetLastError();
+        {
+            std::lock_guard<std::mutex> lock(c.mu);
+            cudaDeviceSynchronize();
+            const size_t keep = c.cap;
+            c.cap = 0;
+            trim_locked(c, 0);
+            c.cap = keep;
+        }
+        e = cudaMalloc(p, r);
+    }
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return fail(e == cudaErrorMemoryAllocation ? LIFE_ERR_OUT_OF_MEMORY : LIFE_ERR_CUDA,
+                    std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    std::lock_guard<std::mutex> lock(c.mu);
+    c.owned[*p] = {dev, r};
+    return LIFE_OK;
+}
+
+void dev_free(void *p)
+{
+    if (!p) return;
+    BlockCache &c = bcache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    auto it = c.owned.find(p);
+    if (it == c.owned.end()) {
+        cudaFree(p);
+        return;
+    }
+    const auto key = it->second;
+    if (key.second > c.cap) {
+        c.owned.erase(it);
+        cudaFree(p);
+        return;
+    }
+    trim_locked(c, key.second);
+    c.free_.emplace(key, p);
+    c.cached += key.second;
+}
+
+namespace {
+std::mutex g_pin_mu;
+std::multimap<size_t, void *> g_pin_free;
+std::unordered_map<void *, size_t> g_pin_size;
+}  // namespace
+
+int pinned_alloc(void **p, size_t bytes)
+{
+    const size_t r = size_class(bytes);
+    {
+        std::lock_guard<std::mutex> lock(g_pin_mu);
+        auto it = g_pin_free.find(r);
+        if (it != g_pin_free.end()) {
+            *p = it->second;
+            g_pin_free.erase(it);
+            return LIFE_OK;
+        }
+    }
+    cudaError_t e = cudaMallocHost(p, r);
+    if (e != cudaSuccess) return fail(LIFE_ERR_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    g_pin_size[*p] = r;
+    return LIFE_OK;
+}
+
+void pinned_free(void *p)
+{
+    if (!p) return;
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    auto it = g_pin_size.find(p);
+    if (it == g_pin_size.end()) {
+        cudaFreeHost(p);
+        return;
+    }
+    g_pin_free.emplace(it->second, p);
 }
 
 // ---------------------------------------------------------------------------
@@ -753,7 +892,8 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         cudaStream_t st;
         ~Guard()
         {
-            for (void *q : tmp) cudaFree(q);
+            if (!tmp.empty()) cudaDeviceSynchronize();  // as cudaFree would
+            for (void *q : tmp) dev_free(q);
             if (p) destroy_impl(p);  // keeps the error message of the failed build
         }
     } guard{out, phi, {}, st};
@@ -782,11 +922,11 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         uint32_t *da, *dv, *df;
         double *dval, *dD;
         const size_t nn = std::max<int64_t>(n, 1);
-        LIFE_CUDA(cudaMalloc(&da, nn * 4)); guard.tmp.push_back(da);
-        LIFE_CUDA(cudaMalloc(&dv, nn * 4)); guard.tmp.push_back(dv);
-        LIFE_CUDA(cudaMalloc(&df, nn * 4)); guard.tmp.push_back(df);
-        LIFE_CUDA(cudaMalloc(&dval, nn * 8)); guard.tmp.push_back(dval);
-        LIFE_CUDA(cudaMalloc(&dD, dlen * 8)); guard.tmp.push_back(dD);
+        LIFE_TRY(dev_alloc((void **)&da, nn * 4)); guard.tmp.push_back(da);
+        LIFE_TRY(dev_alloc((void **)&dv, nn * 4)); guard.tmp.push_back(dv);
+        LIFE_TRY(dev_alloc((void **)&df, nn * 4)); guard.tmp.push_back(df);
+        LIFE_TRY(dev_alloc((void **)&dval, nn * 8)); guard.tmp.push_back(dval);
+        LIFE_TRY(dev_alloc((void **)&dD, dlen * 8)); guard.tmp.push_back(dD);
         // fewer bytes over PCIe: atoms as u16 when they fit (widened on the
         // device, lossless); values as f32 when the caller allows it
         // (LIFE_PHI_VALUES_F32: fp32-only operator, whose kernels round the
@@ -795,7 +935,7 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         const bool v32 = (flags & LIFE_PHI_VALUES_F32) && !(flags & LIFE_PHI_EXACT_F64) && n > 0;
         void *narrow = nullptr;
         if (a16 || v32) {
-            LIFE_CUDA(cudaMalloc(&narrow, (size_t)n * 4));
+            LIFE_TRY(dev_alloc((void **)&narrow, (size_t)n * 4));
             guard.tmp.push_back(narrow);
         }
         uint16_t *na16 = static_cast<uint16_t *>(narrow);
@@ -843,7 +983,7 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
     // index range check (validate(), tensor.py:232-286; first bad position):
     // atoms and voxels now, fibers once they are on the device
     unsigned long long *bad = nullptr;
-    LIFE_CUDA(cudaMalloc(&bad, 3 * sizeof(unsigned long long)));
+    LIFE_TRY(dev_alloc((void **)&bad, 3 * sizeof(unsigned long long)));
     guard.tmp.push_back(bad);
     auto range_check = [&](bool av, bool fib) -> int {
         LIFE_CUDA(cudaMemsetAsync(bad, 0xFF, 3 * sizeof(unsigned long long), st));
@@ -893,9 +1033,9 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         setup_mark(st, "h2d (fibers, values)");
         unsigned long long *vm = nullptr;
         unsigned *cnt = nullptr, *mx = nullptr;
-        LIFE_CUDA(cudaMalloc(&vm, 8)); guard.tmp.push_back(vm);
-        LIFE_CUDA(cudaMalloc(&cnt, (size_t)phi->nf * 4)); guard.tmp.push_back(cnt);
-        LIFE_CUDA(cudaMalloc(&mx, 8)); guard.tmp.push_back(mx);
+        LIFE_TRY(dev_alloc((void **)&vm, 8)); guard.tmp.push_back(vm);
+        LIFE_TRY(dev_alloc((void **)&cnt, (size_t)phi->nf * 4)); guard.tmp.push_back(cnt);
+        LIFE_TRY(dev_alloc((void **)&mx, 8)); guard.tmp.push_back(mx);
         LIFE_CUDA(cudaMemsetAsync(vm, 0, 8, st));
         LIFE_CUDA(cudaMemsetAsync(cnt, 0, (size_t)phi->nf * 4, st));
         LIFE_CUDA(cudaMemsetAsync(mx, 0, 8, st));
@@ -926,9 +1066,9 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
                 for (int t = 0; t < phi->nt; ++t) q += hdict[at * phi->nt + t] * hdict[at * phi->nt + t];
                 hdn[at] = std::sqrt(q);
             }
-            LIFE_CUDA(cudaMalloc(&dn, (size_t)phi->na * 8)); guard.tmp.push_back(dn);
-            LIFE_CUDA(cudaMalloc(&acc, (size_t)phi->nv * 8)); guard.tmp.push_back(acc);
-            LIFE_CUDA(cudaMalloc(&mxv, 8)); guard.tmp.push_back(mxv);
+            LIFE_TRY(dev_alloc((void **)&dn, (size_t)phi->na * 8)); guard.tmp.push_back(dn);
+            LIFE_TRY(dev_alloc((void **)&acc, (size_t)phi->nv * 8)); guard.tmp.push_back(acc);
+            LIFE_TRY(dev_alloc((void **)&mxv, 8)); guard.tmp.push_back(mxv);
             LIFE_CUDA(cudaMemcpyAsync(dn, hdn.data(), (size_t)phi->na * 8, cudaMemcpyHostToDevice, st));
             LIFE_CUDA(cudaMemsetAsync(acc, 0, (size_t)phi->nv * 8, st));
             LIFE_CUDA(cudaMemsetAsync(mxv, 0, 8, st));
@@ -960,8 +1100,8 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         int64_t occupied = 0;
         {
             unsigned *cnt = nullptr, *mx = nullptr;
-            LIFE_CUDA(cudaMalloc(&cnt, (size_t)phi->nv * 4)); guard.tmp.push_back(cnt);
-            LIFE_CUDA(cudaMalloc(&mx, 8)); guard.tmp.push_back(mx);
+            LIFE_TRY(dev_alloc((void **)&cnt, (size_t)phi->nv * 4)); guard.tmp.push_back(cnt);
+            LIFE_TRY(dev_alloc((void **)&mx, 8)); guard.tmp.push_back(mx);
             LIFE_CUDA(cudaMemsetAsync(cnt, 0, (size_t)phi->nv * 4, st));
             LIFE_CUDA(cudaMemsetAsync(mx, 0, 8, st));
             if (n > 0) {
@@ -1035,7 +1175,7 @@ int life_phi_create(const life_dims *dims, const uint32_t *atoms,
 static void destroy_impl(life_phi *phi)
 {
     cudaDeviceSynchronize();
-    for (void *p : phi->allocs) cudaFree(p);
+    for (void *p : phi->allocs) dev_free(p);
     delete phi;
 }
 
@@ -1066,6 +1206,27 @@ int life_copy_h2d_f32(float *dst_dev, const double *src_host, int64_t count, voi
 int life_phi_destroy(life_phi *phi)
 {
     if (phi) destroy_impl(phi);
+    return ok();
+}
+
+int life_release_cached_memory(void)
+{
+    cudaDeviceSynchronize();
+    BlockCache &c = bcache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    const size_t keep = c.cap;
+    c.cap = 0;
+    trim_locked(c, 0);
+    c.cap = keep;
+    return ok();
+}
+
+int life_cached_memory_bytes(int64_t *bytes)
+{
+    if (!bytes) return fail(LIFE_ERR_INVALID_ARGUMENT, "null argument");
+    BlockCache &c = bcache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    *bytes = (int64_t)c.cached;
     return ok();
 }
 

@@ -435,14 +435,14 @@ static void free_session(life_sbb *x)
 {
     if (!x) return;
     Solver &S = x->S;
-    cudaStreamSynchronize(S.st);
+    cudaDeviceSynchronize();  // as cudaFree would: the blocks go back to the cache
     if (x->gexec) cudaGraphExecDestroy(x->gexec);
     if (x->graph) cudaGraphDestroy(x->graph);
-    if (x->pinned) cudaFreeHost(x->pinned);
+    pinned_free(x->pinned);
     void *bufs[] = {S.s, S.rec, S.r, S.mg, S.gt, S.mtmg, S.part, S.partz, S.counter,
                     S.skipped_dev};
     for (void *p : bufs)
-        if (p) cudaFree(p);
+        dev_free(p);
     delete x;
 }
 
@@ -480,17 +480,17 @@ extern "C" int life_sbb_create(life_phi *phi, const void *b_dev, void *w_dev,
     S.comm = cfg->comm;
     if (S.comm && exact)
         return fail(LIFE_ERR_CONFIG_INVALID, "voxel-sharded runs use the fp32 path");
-    LIFE_CUDA(cudaMalloc(&S.s, sizeof(Scal)));
-    LIFE_CUDA(cudaMalloc(&S.rec, sizeof(life_trace_record) * cfg->max_iters));
-    LIFE_CUDA(cudaMalloc(&S.r, std::max<int64_t>(ny, 1) * es));
-    LIFE_CUDA(cudaMalloc(&S.mg, std::max<int64_t>(ny, 1) * es));
-    LIFE_CUDA(cudaMalloc(&S.gt, std::max(phi->nf, 1) * es));
-    LIFE_CUDA(cudaMalloc(&S.mtmg, std::max(phi->nf, 1) * es));
-    LIFE_CUDA(cudaMalloc(&S.part, phi->sms * 8 * sizeof(double)));
-    LIFE_CUDA(cudaMalloc(&S.partz, phi->sms * 8 * sizeof(unsigned long long)));
-    LIFE_CUDA(cudaMalloc(&S.counter, 16));
-    LIFE_CUDA(cudaMalloc(&S.skipped_dev, 16));
-    LIFE_CUDA(cudaMallocHost(&x->pinned, sizeof(int)));
+    LIFE_TRY(dev_alloc((void **)&S.s, sizeof(Scal)));
+    LIFE_TRY(dev_alloc((void **)&S.rec, sizeof(life_trace_record) * cfg->max_iters));
+    LIFE_TRY(dev_alloc((void **)&S.r, std::max<int64_t>(ny, 1) * es));
+    LIFE_TRY(dev_alloc((void **)&S.mg, std::max<int64_t>(ny, 1) * es));
+    LIFE_TRY(dev_alloc((void **)&S.gt, std::max(phi->nf, 1) * es));
+    LIFE_TRY(dev_alloc((void **)&S.mtmg, std::max(phi->nf, 1) * es));
+    LIFE_TRY(dev_alloc((void **)&S.part, phi->sms * 8 * sizeof(double)));
+    LIFE_TRY(dev_alloc((void **)&S.partz, phi->sms * 8 * sizeof(unsigned long long)));
+    LIFE_TRY(dev_alloc((void **)&S.counter, 16));
+    LIFE_TRY(dev_alloc((void **)&S.skipped_dev, 16));
+    LIFE_TRY(pinned_alloc((void **)&x->pinned, sizeof(int)));
     LIFE_CUDA(cudaMemsetAsync(S.counter, 0, 16, st));
     Scal h{};
     h.iter = 1;

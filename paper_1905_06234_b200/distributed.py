@@ -227,7 +227,7 @@ def solve_sharded(problem, config=None, group=None, w0=None, ranges=None, comm=N
         raise comm.error
     res, recs = sess.finish()
     sess.close()
-    return w.double().cpu().numpy(), trace_from(res, recs)
+    return w.cpu().numpy().astype(np.float64), trace_from(res, recs)
 
 
 __all__ = ["NcclComm", "TorchComm", "global_fix_bounds", "shard_problem", "shard_voxel_ranges",

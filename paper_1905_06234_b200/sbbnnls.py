@@ -271,4 +271,5 @@ def solve(problem, w0=None, config=None):
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     res, recs = solve_device(op, b, w, config)
-    return w.double().cpu().numpy(), trace_from(res, recs, t_setup)
+    # D2H in the solve's own dtype, widened on the host (exact)
+    return w.cpu().numpy().astype(np.float64), trace_from(res, recs, t_setup)
