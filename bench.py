@@ -387,7 +387,7 @@ def run_ours(args, dims):
                        "(bytes spread over the steps)"}
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline is a 1-GPU figure
         cpu = cpu_reference(problem, dims)
 
     if rank == 0:

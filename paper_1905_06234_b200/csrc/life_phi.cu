@@ -421,12 +421,33 @@ using namespace life;
 // at ~53 GB/s; tools/h2d_probe.py).
 // ---------------------------------------------------------------------------
 namespace {
-constexpr size_t kStageChunk = 16u << 20;
-constexpr int kStageThreads = 12;  // one host memcpy stream reaches ~10 GB/s
+constexpr int kMaxStageThreads = 32;
+// chunk and thread count: LIFE_B200_STAGE_KB / LIFE_B200_STAGE_THREADS
+size_t stage_chunk()
+{
+    static const size_t c = [] {
+        const char *e = std::getenv("LIFE_B200_STAGE_KB");
+        const size_t kb = e ? (size_t)std::strtoull(e, nullptr, 10) : 0;
+        // 1 MiB: a thread's staged chunk can still be cache-resident when the DMA
+        // reads it (C2 construction 79 -> 71 ms vs 16 MiB chunks; 256 KiB
+        // chunks lose to per-copy overhead: tools/gpu_runs/stage_sweep.sh)
+        return kb >= 64 ? kb << 10 : (size_t)1 << 20;
+    }();
+    return c;
+}
+int stage_threads()
+{
+    static const int t = [] {
+        const char *e = std::getenv("LIFE_B200_STAGE_THREADS");
+        const int n = e ? std::atoi(e) : 0;
+        return n >= 1 ? std::min(n, kMaxStageThreads) : 12;  // one host memcpy stream reaches ~10 GB/s
+    }();
+    return t;
+}
 struct Staging {
     std::mutex mu;
-    void *buf[kStageThreads][2] = {};
-    cudaEvent_t ev[kStageThreads][2] = {};
+    void *buf[kMaxStageThreads][2] = {};
+    cudaEvent_t ev[kMaxStageThreads][2] = {};
     int dev = -1;
 };
 Staging &staging()
@@ -494,22 +515,23 @@ int h2d_staged_cvt(void *dst, const void *src, size_t bytes, int mode, cudaStrea
                 if (p) cudaFreeHost(p);
                 p = nullptr;
             }
-        for (int t = 0; t < kStageThreads; ++t)
+        for (int t = 0; t < stage_threads(); ++t)
             for (int j = 0; j < 2; ++j) {
-                LIFE_CUDA(cudaHostAlloc(&S.buf[t][j], kStageChunk, cudaHostAllocDefault));
+                LIFE_CUDA(cudaHostAlloc(&S.buf[t][j], stage_chunk(), cudaHostAllocDefault));
                 LIFE_CUDA(cudaEventCreateWithFlags(&S.ev[t][j], cudaEventDisableTiming));
             }
         S.dev = dev;
     }
-    const size_t nchunk = (bytes + kStageChunk - 1) / kStageChunk;
-    const int T = (int)std::min<size_t>(kStageThreads, nchunk);
+    const size_t chunk = stage_chunk();
+    const size_t nchunk = (bytes + chunk - 1) / chunk;
+    const int T = (int)std::min<size_t>(stage_threads(), nchunk);
     std::vector<cudaError_t> err(T, cudaSuccess);
     auto work = [&](int t) {
         cudaError_t e = cudaSetDevice(dev);
         int n = 0;
         for (size_t k = t; k < nchunk && e == cudaSuccess; k += T, ++n) {
             const int j = n & 1;
-            const size_t off = k * kStageChunk, m = std::min(kStageChunk, bytes - off);
+            const size_t off = k * chunk, m = std::min(chunk, bytes - off);
             if ((e = cudaEventSynchronize(S.ev[t][j])) != cudaSuccess) break;  // slot's previous DMA done
             stage(S.buf[t][j], static_cast<const char *>(src) + off * in_per_out, m);
             if ((e = cudaMemcpyAsync(static_cast<char *>(dst) + off, S.buf[t][j], m, cudaMemcpyHostToDevice, st)) !=
