@@ -57,7 +57,13 @@ constexpr int kBuild = 8;           // builder / gatherer warps of the tile kern
 constexpr int kSideWarps = 32;      // bin-side CTA
 constexpr int kSideU = 4;           // 32-entry chunks per warp batch on the bin side
 constexpr int kSlots = 3;           // staged steps per tile kernel
-constexpr int kCH = 1024;           // 4-entry units per bin-side chunk
+#ifndef LIFE_KCH
+#define LIFE_KCH 992
+#endif
+// 4-entry units per bin-side chunk: one per consumer thread (31 warps).  With
+// 1024 the first consumer warp took two units per chunk and, holding every
+// ring slot longest, paced the whole WC bin side (C2 WC 0.543 -> 0.501 ms)
+constexpr int kCH = LIFE_KCH;
 
 // Role timing, compiled in only with -DLIFE_BIN_DIAG (tools/bin_roles.py):
 // clock64 spans per category summed over warps (lane 0) into g_bin_cyc.
@@ -1096,13 +1102,17 @@ __device__ __forceinline__ int find_bin(const uint32_t *binseg, int nbins, uint3
 // units | first-of-piece << 31, z = first segment, w = segments | bin << 16.
 constexpr int kSideThreads = 1024;        // warp 0 produces, warps 1..31 consume
 constexpr int kCons = kSideThreads - 32;
+static_assert(kCH % 32 == 0 && kCH <= 1024, "a chunk's group table has 32 entries of 32 units");
 // slot regions (16-byte aligned bulk-copy destinations; each holds its range
 // plus the alignment slack of an unaligned global start)
 constexpr uint32_t kSlotVid = 0, kSlotVal = (kCH * 8 + 16 + 15) / 16 * 16, kSlotSrc = kSlotVal + kCH * 16,
                    kSlotDst = kSlotSrc + ((kCH + 2) * 4 + 16 + 15) / 16 * 16,
                    kSlotGrp = kSlotDst + ((kCH + 1) * 4 + 16 + 15) / 16 * 16,
                    kSlotBytes = (kSlotGrp + 64 + 127) / 128 * 128;
-constexpr int kNsDsc = 4, kNsWc = 3;
+#ifndef LIFE_NS_DSC
+#define LIFE_NS_DSC 4  // 5 fits with kCH = 992 but measured no faster
+#endif
+constexpr int kNsDsc = LIFE_NS_DSC, kNsWc = 3;
 
 struct ChunkArgs {
     const uint4 *chunks;      // chunk descriptors
