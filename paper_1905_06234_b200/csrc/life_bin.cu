@@ -1566,6 +1566,14 @@ struct DscCfg {
     static_assert(TACC + 2 * NACC * N <= 512, "TMEM budget");
 };
 
+// WC tile: Z tiles in a ring of 3 (2 when shared memory is short), and the
+// accumulator released as soon as Z is in registers (C2 WC 0.499 -> 0.490 ms)
+#ifndef LIFE_WC_NZ
+#define LIFE_WC_NZ 3
+#endif
+#ifndef LIFE_WC_EARLY
+#define LIFE_WC_EARLY 1
+#endif
 template <int N>
 struct WcCfg {
     static constexpr int NKB = (N + 63) / 64;  // 64-direction K blocks of the B operand
@@ -1576,6 +1584,8 @@ struct WcCfg {
     static constexpr int kThreads = kWarps * 32;
     static constexpr int DB = 2 * NKB * kKA * 128;
     static constexpr int ZBytes = kTV * kCS * 4;
+    // shared-memory Z tiles between the YZ warps and the gatherers (ring of NZ)
+    static constexpr int NZ = 1024 + 2 * DB + LIFE_WC_NZ * ZBytes <= 232448 - 2048 ? LIFE_WC_NZ : 2;
     static constexpr int TZ = N;               // TMEM: Y hi at 0 (N/2 cols), lo at N/2, Z buffer e at TZ + e kKA
     static_assert(N + 2 * kKA <= 512, "TMEM budget");
 };
@@ -2167,8 +2177,8 @@ __global__ void __launch_bounds__(WcCfg<N>::kThreads, 1)
 {
     using C = WcCfg<N>;
     extern __shared__ __align__(1024) unsigned char smraw[];
-    __shared__ __align__(8) uint64_t d_full[2], d_empty[2], acc_full[2], acc_empty[2], z_full[2], z_empty[2],
-        y_ready, y_free;
+    __shared__ __align__(8) uint64_t d_full[2], d_empty[2], acc_full[2], acc_empty[2], z_full[WcCfg<N>::NZ],
+        z_empty[WcCfg<N>::NZ], y_ready, y_free;
     __shared__ uint32_t tmem_base;
     if (hooks.done && *hooks.done) return;
     if (hooks.t_begin && blockIdx.x == 0 && threadIdx.x == 0) *hooks.t_begin = globaltimer();
@@ -2185,6 +2195,8 @@ __global__ void __launch_bounds__(WcCfg<N>::kThreads, 1)
             bar_init(&d_empty[e], 1);
             bar_init(&acc_full[e], 1);
             bar_init(&acc_empty[e], 8);
+        }
+        for (int e = 0; e < C::NZ; ++e) {
             bar_init(&z_full[e], 8);
             bar_init(&z_empty[e], kBuild);
         }
@@ -2237,9 +2249,10 @@ __global__ void __launch_bounds__(WcCfg<N>::kThreads, 1)
             nn = n2;
             fetch(np0, nn, nc);  // next step, in flight during this one
             ptrs(k + 2, p2, n2);
-            BD_WAIT(17, bar_wait(&z_full[e], (k >> 1) & 1));
+            const int zb = k % C::NZ;
+            BD_WAIT(17, bar_wait(&z_full[zb], (k / C::NZ) & 1));
             BD_T0(t_g);
-            const uint32_t Z = Zs + (uint32_t)(e * C::ZBytes);
+            const uint32_t Z = Zs + (uint32_t)(zb * C::ZBytes);
             float4 *dst = reinterpret_cast<float4 *>(scr + cp0);
             auto gat = [&](uint2 c, uint32_t u) {
                 const uint32_t o[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
@@ -2255,7 +2268,7 @@ __global__ void __launch_bounds__(WcCfg<N>::kThreads, 1)
                 gat(__ldg(reinterpret_cast<const uint2 *>(A.cellr + cp0) + u), u);
             BD_ACC(18, t_g);
             __syncwarp();
-            if (lane == 0) bar_arrive(&z_empty[e]);
+            if (lane == 0) bar_arrive(&z_empty[zb]);
         }
     } else if (warp == C::kProdD) {
         if (lane == 0) {
@@ -2404,9 +2417,14 @@ __global__ void __launch_bounds__(WcCfg<N>::kThreads, 1)
                 }
                 BD_ACC(27, t_z);
                 tcg::fence_before();
-                if (k >= 2) BD_WAIT(28, bar_wait(&z_empty[e], ((k >> 1) - 1) & 1));
+                if (LIFE_WC_EARLY) {  // Z is in registers: the accumulator is free for the MMA of step k + 2
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(&acc_empty[e]);
+                }
+                const int zb = k % C::NZ;
+                if (k >= C::NZ) BD_WAIT(28, bar_wait(&z_empty[zb], ((k / C::NZ) - 1) & 1));
                 BD_T0(t_zs);
-                const uint32_t za = Zs + (uint32_t)(e * C::ZBytes) + 4u * (uint32_t)(row * kCS + cs * 32);
+                const uint32_t za = Zs + (uint32_t)(zb * C::ZBytes) + 4u * (uint32_t)(row * kCS + cs * 32);
 #pragma unroll
                 for (int i4 = 0; i4 < 8; ++i4)
                     sts_f4(za + 16u * i4, make_float4(__uint_as_float(zr[4 * i4]) * zinv,
@@ -2416,8 +2434,8 @@ __global__ void __launch_bounds__(WcCfg<N>::kThreads, 1)
                 BD_ACC(29, t_zs);
                 __syncwarp();
                 if (lane == 0) {
-                    bar_arrive(&acc_empty[e]);
-                    bar_arrive(&z_full[e]);
+                    if (!LIFE_WC_EARLY) bar_arrive(&acc_empty[e]);
+                    bar_arrive(&z_full[zb]);
                 }
             }
         }
@@ -2461,7 +2479,7 @@ int prep_t(life_phi *phi)
         phi->b_dsc_cap = (int)std::min(16384L, std::max(0L, avail / (4L * 6L) / 32 * 32));
     }
     phi->b_dsc_smem = 1024 + 2 * (size_t)CD::DB + 2 * (size_t)CD::CBytes + (size_t)4 * 6 * phi->b_dsc_cap;
-    phi->b_wc_smem = 1024 + 2 * (size_t)CW::DB + 2 * (size_t)CW::ZBytes;
+    phi->b_wc_smem = 1024 + 2 * (size_t)CW::DB + (size_t)CW::NZ * CW::ZBytes;
     if (phi->b_dsc_smem > (size_t)kSmemMax || phi->b_wc_smem > (size_t)kSmemMax)
         return fail(LIFE_ERR_CONFIG_INVALID, "bin layout: shared memory does not fit");
     phi->b_side_smem = (size_t)kSB * 4 + (size_t)kNsDsc * kSlotBytes;
