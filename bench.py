@@ -67,34 +67,77 @@ def spmv_bytes(dims, val_bytes=4, idx_bytes=4, vec_bytes=4):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    polled every 2 ms from a thread (the timed region of K=20 iterations is
+    ~35 ms, shorter than nvidia-smi's 100 ms period); nvidia-smi when NVML
+    is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("sw_power_cap", 0x4))
 
     def __init__(self, device_index):
         self.dev = device_index
+        self.samples = []   # (sm_mhz, reasons bitmask)
+        self.max_mhz = None
         self.proc = None
-        self.lines = []
+        self._stop = threading.Event()
+        self._nvml = None
 
     def __enter__(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.dev]) if vis and vis.split(",")[0].isdigit() else self.dev
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._nvml = (pynvml, h)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+        except Exception:
+            self._nvml = None
+            self._start_smi()
+        time.sleep(0.01)  # the first samples precede the timed region's start
+        return self
+
+    def _poll(self):
+        pynvml, h = self._nvml
+        reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        while True:
+            try:
+                self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                     reasons(h)))
+            except Exception:
+                pass
+            if self._stop.wait(0.002):
+                break
+
+    def _start_smi(self):
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", str(self.dev),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t = threading.Thread(target=self._read_smi, daemon=True)
             self.t.start()
         except FileNotFoundError:
             self.proc = None
-        return self
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                self.max_mhz = float(parts[1])
+                self.samples.append((float(parts[0]), int(parts[2], 16)))
+            except (ValueError, IndexError):
+                continue
 
     def __exit__(self, *exc):
+        self._stop.set()
+        if self._nvml is not None:
+            self.t.join(timeout=1)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -103,24 +146,16 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for name, flag in zip(names, parts[4:8]):
-                if flag.lower() == "active":
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        mask = 0
+        for _, r in self.samples:
+            mask |= int(r)
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples),
+                "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(n for n, bit in self.REASONS if mask & bit),
+                "samples": len(self.samples),
+                "source": "nvml 2 ms" if self._nvml is not None else "nvidia-smi 100 ms"}
 
 
 def dist_env():
@@ -254,16 +289,11 @@ def run_ours(args, dims):
     if world > 1:
         from paper_1905_06234_b200 import distributed as D
         comm = D.NcclComm()  # the library's own NCCL communicator (graphs on)
-        counts = np.bincount(problem.tensor.voxels, minlength=nv)
-        v0, v1 = D.shard_voxel_ranges(counts, world)[rank]
-        t_loc, dic_loc, b_loc = D.shard_problem(problem.tensor, problem.dictionary,
-                                                problem.y, v0, v1)
-        op = L.DeviceOperator(t_loc, dic_loc)
-        vmax, fmax = D.global_fix_bounds(problem.tensor)
-        _native.check(_native.lib().life_phi_set_fix_bounds(op.handle, vmax, 0.0, fmax))
-        b = torch.from_numpy(b_loc).to(device="cuda", dtype=torch.float32)
-        local_dims = (na, t_loc.dims.n_voxels, nf, nt, t_loc.dims.n_coeffs)
-        info["shard"] = {"voxels": [int(v0), int(v1)], "n_coeffs": int(t_loc.dims.n_coeffs)}
+        # each rank uploads 1/N of the coefficient list; shards are routed
+        # to their owners over NVLink (all_to_all), see shard_from_slices
+        op, b, (v0, v1), _ = D.shard_from_slices(problem)
+        local_dims = (na, op.dims.n_voxels, nf, nt, op.dims.n_coeffs)
+        info["shard"] = {"voxels": [int(v0), int(v1)], "n_coeffs": int(op.dims.n_coeffs)}
     else:
         op = L.DeviceOperator(problem.tensor, problem.dictionary)
         b = torch.from_numpy(problem.y).to(device="cuda", dtype=torch.float32)
@@ -375,6 +405,8 @@ def run_ours(args, dims):
         # u16 when na <= 65536, voxels and fibers u32, values f32 (fp32-only
         # operator); the dictionary as f64, b as f32 (rounded while staging)
         h2d = nc * ((2 if na <= 65536 else 4) + 4 + 4 + 4) + na * nt * 8 + nv * nt * 4
+        if world > 1:  # whole job: each rank's 1/N slice (u32 indices, f64 values), D per rank
+            h2d = nc * (4 + 4 + 4 + 8) + world * na * nt * 8 + nv * nt * 4
         cached = fresh.__dict__.get("_device_cache", {}).get("op")
         e2e = {"value": args.steps / e2e_s, "unit": UNIT,
                "setup_s": round(tr.setup_seconds, 3), "loop_s": round(tr.loop_seconds, 4),

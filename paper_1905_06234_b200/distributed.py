@@ -99,6 +99,96 @@ def global_fix_bounds(tensor):
     return vmax * (1.0 + 1e-6), max(fmax, 1)
 
 
+def slice_bounds(n, rank, nranks):
+    """The contiguous 1/nranks slice of the coefficient list a rank uploads."""
+    return rank * n // nranks, (rank + 1) * n // nranks
+
+
+def reduce_shard_stats(voxels, fibers, values, dims, group, xdev):
+    """Whole-problem statistics from every rank's coefficient slice (torch
+    tensors): per-voxel coefficient counts (the shard rule's input), and the
+    fixed-point bounds of ``global_fix_bounds`` -- computed as slice-local
+    bincounts / max|value| followed by one SUM and one MAX all-reduce, equal
+    to the host computation bit for bit."""
+    import torch
+    import torch.distributed as dist
+    cnt = torch.bincount(voxels.long(), minlength=dims.n_voxels)
+    fcnt = torch.bincount(fibers.long(), minlength=dims.n_fibers)
+    vm = values.abs().max().reshape(1) if values.numel() else \
+        torch.zeros(1, dtype=torch.float64, device=values.device)
+    both = torch.cat((cnt, fcnt)).to(xdev)
+    vm = vm.to(xdev)
+    dist.all_reduce(both, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(vm, op=dist.ReduceOp.MAX, group=group)
+    counts = both[:dims.n_voxels].cpu().numpy()
+    nc = int(counts.sum())
+    vmax = float(vm.item()) if nc else 0.0
+    fmax = int(both[dims.n_voxels:].max().item()) if nc else 1
+    return counts, vmax * (1.0 + 1e-6), max(fmax, 1)
+
+
+def route_to_shards(arrays, voxels, ranges, group, xdev):
+    """Send every coefficient of this rank's slice to the rank owning its
+    voxel (one all_to_all per array over the group: NVLink with NCCL).  A
+    rank receives its voxel range's coefficients in their original relative
+    order (senders' slices are in rank order and each sender's partition is
+    stable), i.e. exactly what ``shard_problem`` selects on the host."""
+    import torch
+    import torch.distributed as dist
+    world = len(ranges)
+    dev = voxels.device
+    ends = torch.tensor([r[1] for r in ranges], dtype=torch.int64, device=dev)
+    dest = torch.searchsorted(ends, voxels.long(), right=True)
+    order = torch.argsort(dest, stable=True)
+    send = torch.bincount(dest, minlength=world).to(xdev)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    sl, rl = send.cpu().tolist(), recv.cpu().tolist()
+    out = []
+    for a in arrays:
+        src = a[order].to(xdev)
+        dst = torch.empty(int(sum(rl)), dtype=a.dtype, device=xdev)
+        dist.all_to_all_single(dst, src, output_split_sizes=rl, input_split_sizes=sl, group=group)
+        out.append(dst)
+    return out
+
+
+def shard_from_slices(problem, group=None):
+    """Each rank's voxel shard built on the GPUs: the rank uploads only its
+    1/N slice of the coefficient list (staged H2D), the statistics and the
+    shard ranges come from two all-reduces, and the coefficients are routed
+    to their owners by all_to_all.  Host work per rank is O(Nc/N), against
+    three full passes over the host arrays for ``shard_problem`` +
+    ``global_fix_bounds`` (2.5 s at C2).  Returns (DeviceOperator, b as a
+    CUDA f32 tensor, (v0, v1), (vmax, fmax)); the operator equals the one
+    built from ``shard_problem`` (same coefficients in the same order)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import device
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    xdev = torch.device("cuda") if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = problem.tensor
+    d = t.dims
+    c0, c1 = slice_bounds(d.n_coeffs, rank, world)
+    a, v, f = (device.upload(x[c0:c1]) for x in (t.atoms, t.voxels, t.fibers))
+    val = device.upload(np.asarray(t.values[c0:c1], dtype=np.float64))
+    counts, vmax, fmax = reduce_shard_stats(v, f, val, d, group, xdev)
+    ranges = shard_voxel_ranges(counts, world)
+    v0, v1 = ranges[rank]
+    a, v, f, val = (x.to("cuda") for x in route_to_shards((a, v, f, val), v, ranges, group, xdev))
+    v -= v0
+    local = Dims(n_atoms=d.n_atoms, n_voxels=max(1, v1 - v0), n_fibers=d.n_fibers,
+                 n_dirs=d.n_dirs, n_coeffs=int(v.numel()))
+    dic = device.upload(np.asarray(problem.dictionary.data, dtype=np.float64))
+    op = device.DeviceOperator.from_device(local, a, v, f, val, dic)
+    N.check(N.lib().life_phi_set_fix_bounds(op.handle, vmax, 0.0, fmax))
+    y = np.asarray(problem.y, dtype=np.float64)
+    b = device.upload(y[v0 * d.n_dirs:v1 * d.n_dirs], torch.float32) if v1 > v0 else \
+        torch.zeros(local.signal_len, dtype=torch.float32, device="cuda")
+    return op, b, (v0, v1), (vmax, fmax)
+
+
 class _CudaArray:
     """Zero-copy torch view of a raw device pointer (__cuda_array_interface__)."""
 
@@ -205,14 +295,16 @@ def solve_sharded(problem, config=None, group=None, w0=None, ranges=None, comm=N
     # (graphs on); other backends (gloo in tests): the torch callback
     if comm is None:
         comm = NcclComm(group) if dist.get_backend(group) == "nccl" else TorchComm(group)
-    counts = np.bincount(problem.tensor.voxels, minlength=problem.dims.n_voxels)
-    ranges = ranges or shard_voxel_ranges(counts, comm.nranks)
-    v0, v1 = ranges[comm.rank]
-    t, dic, b_host = shard_problem(problem.tensor, problem.dictionary, problem.y, v0, v1)
-    op = device.DeviceOperator(t, dic)
-    vmax, fmax = global_fix_bounds(problem.tensor)
-    N.check(N.lib().life_phi_set_fix_bounds(op.handle, vmax, 0.0, fmax))
-    b = torch.from_numpy(b_host).to(device="cuda", dtype=torch.float32)
+    if ranges is None:
+        # shards built on the GPUs from 1/N host slices (shard_from_slices)
+        op, b, _, _ = shard_from_slices(problem, group)
+    else:  # caller-chosen ranges: host selection
+        v0, v1 = ranges[comm.rank]
+        t, dic, b_host = shard_problem(problem.tensor, problem.dictionary, problem.y, v0, v1)
+        op = device.DeviceOperator(t, dic)
+        vmax, fmax = global_fix_bounds(problem.tensor)
+        N.check(N.lib().life_phi_set_fix_bounds(op.handle, vmax, 0.0, fmax))
+        b = torch.from_numpy(b_host).to(device="cuda", dtype=torch.float32)
     if w0 is None:
         w = torch.empty(problem.dims.n_fibers, dtype=torch.float32, device="cuda")
     else:

@@ -114,3 +114,55 @@ def test_global_fix_bounds():
                     fibers=[4, 4, 4, 1, 0, 4], values=[0.5, -2.0, 1.0, 1.0, 0.1, 0.3], dims=d)
     vmax, fmax = D.global_fix_bounds(t)
     assert fmax == 4 and abs(vmax - 2.0) < 1e-5
+
+
+def _route_worker(rank, world, port, q, dims):
+    """shard_from_slices' routing on CPU tensors: each rank takes its 1/N
+    slice of the coefficient list, the statistics come from all-reduces and
+    the coefficients reach their owners by all_to_all."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    p = O.generate(dims, 30.0, 0.5, 0.1, 11)
+    d = L.Dims(*dims)
+    c0, c1 = D.slice_bounds(d.n_coeffs, rank, world)
+    sl = [torch.from_numpy(np.ascontiguousarray(p[k][c0:c1]).view(np.int32))
+          for k in ("atoms", "voxels", "fibers")]
+    val = torch.from_numpy(np.ascontiguousarray(p["values"][c0:c1]))
+    counts, vmax, fmax = D.reduce_shard_stats(sl[1], sl[2], val, d, None, torch.device("cpu"))
+    ranges = D.shard_voxel_ranges(counts, world)
+    a, v, f, vv = D.route_to_shards((*sl, val), sl[1], ranges, None, torch.device("cpu"))
+    q.put((rank, counts, vmax, fmax, ranges, a.numpy().view(np.uint32), v.numpy().view(np.uint32),
+           f.numpy().view(np.uint32), vv.numpy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slices_routed_to_shards_equal_host_selection(world, oracle):
+    dims = (20, 60, 50, 16, 4000)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_route_worker, args=(r, world, port, q, dims)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = sorted((q.get(timeout=120) for _ in range(world)), key=lambda x: x[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = oracle.generate(dims, 30.0, 0.5, 0.1, 11)
+    d = L.Dims(*dims)
+    t = L.PhiTensor(atoms=p["atoms"], voxels=p["voxels"], fibers=p["fibers"], values=p["values"], dims=d)
+    counts = np.bincount(t.voxels, minlength=d.n_voxels)
+    ranges = D.shard_voxel_ranges(counts, world)
+    vmax, fmax = D.global_fix_bounds(t)
+    dic = L.Dictionary(data=p["dict"], dims=d)
+    for rank, c, vm, fm, rg, a, v, f, vv in got:
+        assert np.array_equal(c, counts) and rg == ranges
+        assert vm == vmax and fm == fmax  # bit for bit
+        v0, v1 = ranges[rank]
+        tl, _, _ = D.shard_problem(t, dic, np.zeros(d.signal_len), v0, v1)
+        assert np.array_equal(a, tl.atoms) and np.array_equal(v, tl.voxels + np.uint32(v0))
+        assert np.array_equal(f, tl.fibers) and np.array_equal(vv, tl.values)

@@ -111,3 +111,56 @@ def test_nccl_comm_world1_through_graphs():
     sess.close()
     assert torch.equal(w, w2)
     comm.close()
+
+
+def _nccl_world1_worker(port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    import paper_1905_06234_b200 as L
+    from paper_1905_06234_b200 import _native as N
+    from paper_1905_06234_b200 import distributed as D
+    p = _problem()
+    cfg = L.SolverConfig(max_iters=12, grad_tol=0.0)
+    # shards from 1/N host slices, routed with NCCL all_to_all on the device
+    op, b, rng, bounds = D.shard_from_slices(p)
+    # against the host selection of the same voxel range
+    t, dic, b_host = D.shard_problem(p.tensor, p.dictionary, p.y, *rng)
+    ref = L.DeviceOperator(t, dic)
+    vmax, fmax = D.global_fix_bounds(p.tensor)
+    N.check(N.lib().life_phi_set_fix_bounds(ref.handle, vmax, 0.0, fmax))
+    w = torch.from_numpy(p.w_true).to("cuda", torch.float32)
+    ys = []
+    gs = []
+    for o in (op, ref):
+        y = torch.zeros(o.dims.signal_len, dtype=torch.float32, device="cuda")
+        g = torch.zeros(p.dims.n_fibers, dtype=torch.float32, device="cuda")
+        o.dsc_f32(w, y, flags=N.SKIP_ZERO)
+        o.wc_f32(y, g)
+        ys.append(y.cpu().numpy())
+        gs.append(g.cpu().numpy())
+    same_ops = bool(np.array_equal(ys[0], ys[1]) and np.array_equal(gs[0], gs[1]))
+    same_b = bool(np.array_equal(b.cpu().numpy(), b_host.astype(np.float32)))
+    w_dev, tr_dev = D.solve_sharded(p, cfg)                         # device routing
+    w_host, tr_host = D.solve_sharded(p, cfg, ranges=[(0, p.dims.n_voxels)])  # host selection
+    q.put((rng, bounds, D.global_fix_bounds(p.tensor), same_ops, same_b,
+           bool(np.array_equal(w_dev, w_host)), tr_dev.final_objective, tr_host.final_objective))
+    dist.destroy_process_group()
+
+
+def test_shards_from_slices_over_nccl_world1():
+    """shard_from_slices through an NCCL process group (world 1: the
+    statistics all-reduces and the all_to_all run on the device): the
+    operator, b and the sharded solve equal the host-selected shard's."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_nccl_world1_worker, args=(_free_port(), q))
+    pr.start()
+    rng, bounds, host_bounds, same_ops, same_b, same_w, fo_dev, fo_host = q.get(timeout=300)
+    pr.join(timeout=60)
+    assert pr.exitcode == 0
+    assert rng == (0, 2000) and bounds == host_bounds
+    assert same_ops and same_b and same_w and fo_dev == fo_host
