@@ -84,11 +84,15 @@ size_t size_class(size_t b)
 // free cached blocks until `need` more bytes fit under the cap (largest first)
 void trim_locked(BlockCache &c, size_t need)
 {
+    int cur = 0;
+    cudaGetDevice(&cur);
     while (!c.free_.empty() && c.cached + need > c.cap) {
         auto it = std::prev(c.free_.end());
         c.cached -= it->first.second;
         c.owned.erase(it->second);
+        if (it->first.first != cur) cudaSetDevice(it->first.first);  // the block's own device
         cudaFree(it->second);
+        if (it->first.first != cur) cudaSetDevice(cur);
         c.free_.erase(it);
     }
 }
