@@ -326,10 +326,21 @@ template <typename K>
 __global__ void k_rank_va(const K *sk, const uint32_t *perm, const uint32_t *rstart, int64_t n,
                           uint32_t na, uint32_t *rank_o, uint32_t *vmaxr)
 {
-    for (int64_t p = gtid(); p < n; p += gstride()) {
-        const uint32_t r = (uint32_t)p - rstart[p];
-        rank_o[perm[p]] = r;
-        if (p == n - 1 || sk[p + 1] != sk[p]) atomicMax(&vmaxr[(uint32_t)(sk[p] / na)], r);
+    // p0 is warp-uniform (the grid stride is a multiple of 32); run ends of
+    // one voxel are adjacent in key order, so their lanes combine before one
+    // atomicMax per voxel per warp (was ~60M contended atomics at C2)
+    for (int64_t p0 = gtid() - (threadIdx.x & 31); p0 < n; p0 += gstride()) {
+        const int64_t p = p0 + (threadIdx.x & 31);
+        const bool in = p < n;
+        uint32_t r = 0, vox = 0xFFFFFFFFu;
+        if (in) {
+            r = (uint32_t)p - rstart[p];
+            rank_o[perm[p]] = r;
+            if (p == n - 1 || sk[p + 1] != sk[p]) vox = (uint32_t)(sk[p] / na);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, vox);
+        const uint32_t m = __reduce_max_sync(peers, r);
+        if (vox != 0xFFFFFFFFu && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicMax(&vmaxr[vox], m);
     }
 }
 __global__ void k_rows_per_voxel(const uint32_t *vmaxr, int nv, uint32_t *nr)
