@@ -377,6 +377,10 @@ __global__ void k_vf_split(const uint32_t *perm, const uint32_t *sf, const uint3
     for (int64_t p = gtid(); p < n; p += gstride())
         vf_o[perm[p]] = f2vf[sf[p]] + ((uint32_t)p - rstart[p]) / kSlotCap;
 }
+__global__ void k_big_flags(const uint32_t *f, const unsigned *cnt, int64_t n, uint8_t *big)
+{
+    for (int64_t i = gtid(); i < n; i += gstride()) big[i] = cnt[f[i]] > (unsigned)kSlotCap ? 1 : 0;
+}
 __global__ void k_vf_identity(const uint32_t *f, const uint32_t *f2vf, int64_t n, uint32_t *vf_o)
 {
     for (int64_t i = gtid(); i < n; i += gstride()) vf_o[i] = f2vf[f[i]];
@@ -768,15 +772,45 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
         k_vf_identity<<<gridn(n), 256, 0, st>>>(f, phi->b_f2vf, n, vf_o);
         LIFE_CHECK_LAUNCH();
     } else {
-        // occurrence index within each fascicle (stable order)
-        uint32_t *sf;
-        LIFE_TRY(talloc((void **)&sf, n * 4));
-        LIFE_TRY(sort_pairs<uint32_t>(f, sf, iota, perm, n, bits64((unsigned long long)nf), st));
-        k_heads32<<<gridn(n), 256, 0, st>>>(sf, n, head);
+        // one slot for fascicles of <= kSlotCap coefficients; the others
+        // need each coefficient's occurrence index within its fascicle
+        // (stable order): only their coefficients are selected and sorted
+        // (at C2 a few percent of Phi instead of all 100M)
+        k_vf_identity<<<gridn(n), 256, 0, st>>>(f, phi->b_f2vf, n, vf_o);
         LIFE_CHECK_LAUNCH();
-        LIFE_TRY(scan_max(head, rstart, n, st));
-        k_vf_split<<<gridn(n), 256, 0, st>>>(perm, sf, rstart, phi->b_f2vf, n, vf_o);
+        uint8_t *big;
+        uint32_t *bidx, *bf, *sf, *bperm;
+        int64_t *nbig;
+        LIFE_TRY(talloc((void **)&big, n));
+        LIFE_TRY(talloc((void **)&bidx, n * 4));
+        LIFE_TRY(talloc((void **)&nbig, 8));
+        k_big_flags<<<gridn(n), 256, 0, st>>>(f, fcnt, n, big);
         LIFE_CHECK_LAUNCH();
+        {
+            cub::CountingInputIterator<uint32_t> pos(0);
+            size_t tb = 0;
+            LIFE_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, pos, big, bidx, nbig, n, st));
+            void *temp = nullptr;
+            LIFE_CUDA(cudaMallocAsync(&temp, std::max<size_t>(tb, 16), st));
+            LIFE_CUDA(cub::DeviceSelect::Flagged(temp, tb, pos, big, bidx, nbig, n, st));
+            LIFE_CUDA(cudaFreeAsync(temp, st));
+        }
+        int64_t m = 0;
+        LIFE_CUDA(cudaMemcpyAsync(&m, nbig, 8, cudaMemcpyDeviceToHost, st));
+        LIFE_CUDA(cudaStreamSynchronize(st));
+        if (m > 0) {
+            LIFE_TRY(talloc((void **)&bf, m * 4));
+            LIFE_TRY(talloc((void **)&sf, m * 4));
+            LIFE_TRY(talloc((void **)&bperm, m * 4));
+            k_gather_u32<<<gridn(m), 256, 0, st>>>(bidx, f, m, bf);
+            LIFE_CHECK_LAUNCH();
+            LIFE_TRY(sort_pairs<uint32_t>(bf, sf, bidx, bperm, m, bits64((unsigned long long)nf), st));
+            k_heads32<<<gridn(m), 256, 0, st>>>(sf, m, head);
+            LIFE_CHECK_LAUNCH();
+            LIFE_TRY(scan_max(head, rstart, m, st));
+            k_vf_split<<<gridn(m), 256, 0, st>>>(bperm, sf, rstart, phi->b_f2vf, m, vf_o);
+            LIFE_CHECK_LAUNCH();
+        }
     }
     const int nbins = (int)((nvf + kSB - 1) / kSB);
 
