@@ -403,10 +403,13 @@ def run_ours(args, dims):
             tt = torch.tensor([e2e_s], device="cuda")
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             e2e_s = float(tt.item())
-        # bytes crossing PCIe (life_phi_create with LIFE_PHI_HOST_INPUT): atoms as
-        # u16 when na <= 65536, voxels and fibers u32, values f32 (fp32-only
-        # operator); the dictionary as f64, b as f32 (rounded while staging)
-        h2d = nc * ((2 if na <= 65536 else 4) + 4 + 4 + 4) + na * nt * 8 + nv * nt * 4
+        # bytes crossing PCIe (life_phi_create with LIFE_PHI_HOST_INPUT): atom and
+        # voxel packed into one u32 when both fields fit (else atoms u16 / u32 +
+        # voxels u32), fibers u32, values f32 (fp32-only operator); the
+        # dictionary as f64, b as f32 (rounded while staging)
+        bits = lambda x: max(1, int(x).bit_length())  # field width with an all-ones spare
+        av = 4 if bits(na) + bits(nv) <= 32 else (2 if na < 65535 else 4) + 4
+        h2d = nc * (av + 4 + 4) + na * nt * 8 + nv * nt * 4
         if sharded:  # whole job: each rank's 1/N slice (u32 indices, f64 values), D per rank
             h2d = nc * (4 + 4 + 4 + 8) + world * na * nt * 8 + nv * nt * 4
         cached = fresh.__dict__.get("_device_cache", {}).get("op")

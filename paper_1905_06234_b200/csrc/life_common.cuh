@@ -176,6 +176,8 @@ namespace life {
 // pageable host -> device through pinned staging (life_phi.cu)
 int h2d_staged(void *dst, const void *src, size_t bytes, cudaStream_t st);
 int h2d_staged_cvt(void *dst, const void *src, size_t bytes, int mode, cudaStream_t st);  // 1: f64->f32, 2: u32->u16
+int h2d_staged_pack_av(uint32_t *dst, const uint32_t *atoms, const uint32_t *voxels, int64_t n, int abits, int vbits,
+                       cudaStream_t st);  // (voxel << abits) | atom, saturated fields
 // LIFE_B200_SETUP_TRACE=1: synchronize and print the time since the last mark
 // (operator construction phases, stderr)
 void setup_mark(cudaStream_t st, const char *what);

@@ -235,6 +235,15 @@ __global__ void k_voxel_l1(const uint32_t *a, const uint32_t *v, const double *v
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(&acc[v[i]], fabs(val[i]) * dn[a[i]]);
 }
+__global__ void k_unpack_av(const uint32_t *in, int64_t n, int abits, uint32_t vmax_field, uint32_t *a, uint32_t *v)
+{
+    const uint32_t am = (1u << abits) - 1u;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t w = in[i], vv = w >> abits;
+        a[i] = (w & am) == am ? 0xFFFFFFFFu : (w & am);   // saturated field: out of range
+        v[i] = vv == vmax_field ? 0xFFFFFFFFu : vv;
+    }
+}
 __global__ void k_widen_u16(const uint16_t *in, int64_t n, uint32_t *out)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -482,28 +491,56 @@ void setup_mark(cudaStream_t st, const char *what)
 
 int h2d_staged(void *dst, const void *src, size_t bytes, cudaStream_t st) { return h2d_staged_cvt(dst, src, bytes, 0, st); }
 
-// mode 0: copy; 1: f64 -> f32; 2: u32 -> u16 (`bytes` counts the DESTINATION)
+// Staged copy of `bytes` destination bytes; stage(out, off, m) fills a
+// pinned chunk with destination bytes [off, off + m)
+static int h2d_staged_gen(void *dst, size_t bytes, const std::function<void(void *, size_t, size_t)> &stage,
+                          cudaStream_t st);
+
+// mode 0: copy; 1: f64 -> f32; 2: u32 -> u16, saturated (`bytes` counts the DESTINATION)
 int h2d_staged_cvt(void *dst, const void *src, size_t bytes, int mode, cudaStream_t st)
 {
     if (bytes == 0) return LIFE_OK;
+    if (mode == 0 && bytes < (4u << 20)) {  // small: one direct copy
+        LIFE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return LIFE_OK;
+    }
     const size_t in_per_out = mode == 0 ? 1 : 2;  // source bytes per destination byte
-    auto stage = [mode](void *out, const char *in, size_t m) {  // m destination bytes
+    const char *in0 = static_cast<const char *>(src);
+    return h2d_staged_gen(dst, bytes, [mode, in0, in_per_out](void *out, size_t off, size_t m) {
+        const char *in = in0 + off * in_per_out;
         if (mode == 0) {
             std::memcpy(out, in, m);
         } else if (mode == 1) {
             const double *x = reinterpret_cast<const double *>(in);
             float *y = static_cast<float *>(out);
             for (size_t i = 0, k = m / 4; i < k; ++i) y[i] = (float)x[i];
-        } else {
+        } else {  // an out-of-range atom stays out of range (0xFFFF >= n_atoms)
             const uint32_t *x = reinterpret_cast<const uint32_t *>(in);
             uint16_t *y = static_cast<uint16_t *>(out);
-            for (size_t i = 0, k = m / 2; i < k; ++i) y[i] = (uint16_t)x[i];
+            for (size_t i = 0, k = m / 2; i < k; ++i) y[i] = (uint16_t)std::min<uint32_t>(x[i], 0xFFFFu);
         }
-    };
-    if (mode == 0 && bytes < (4u << 20)) {  // small: one direct copy
-        LIFE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
-        return LIFE_OK;
-    }
+    }, st);
+}
+
+// atoms and voxels packed into one u32 per coefficient (atom in the low
+// `abits` bits), fields saturated so an out-of-range index stays out of
+// range for the device check: 4 bytes across PCIe instead of 2 + 4
+int h2d_staged_pack_av(uint32_t *dst, const uint32_t *atoms, const uint32_t *voxels, int64_t n, int abits, int vbits,
+                       cudaStream_t st)
+{
+    if (n <= 0) return LIFE_OK;
+    const uint32_t am = (1u << abits) - 1u, vm = vbits >= 32 ? ~0u : (1u << vbits) - 1u;
+    return h2d_staged_gen(dst, (size_t)n * 4, [=](void *out, size_t off, size_t m) {
+        const size_t i0 = off / 4;
+        uint32_t *y = static_cast<uint32_t *>(out);
+        for (size_t i = 0, k = m / 4; i < k; ++i)
+            y[i] = std::min(atoms[i0 + i], am) | (std::min(voxels[i0 + i], vm) << abits);
+    }, st);
+}
+
+static int h2d_staged_gen(void *dst, size_t bytes, const std::function<void(void *, size_t, size_t)> &stage,
+                          cudaStream_t st)
+{
     Staging &S = staging();
     std::lock_guard<std::mutex> lk(S.mu);
     int dev = 0;
@@ -537,7 +574,7 @@ int h2d_staged_cvt(void *dst, const void *src, size_t bytes, int mode, cudaStrea
             const int j = n & 1;
             const size_t off = k * chunk, m = std::min(chunk, bytes - off);
             if ((e = cudaEventSynchronize(S.ev[t][j])) != cudaSuccess) break;  // slot's previous DMA done
-            stage(S.buf[t][j], static_cast<const char *>(src) + off * in_per_out, m);
+            stage(S.buf[t][j], off, m);
             if ((e = cudaMemcpyAsync(static_cast<char *>(dst) + off, S.buf[t][j], m, cudaMemcpyHostToDevice, st)) !=
                 cudaSuccess)
                 break;
@@ -957,16 +994,27 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
         // device, lossless); values as f32 when the caller allows it
         // (LIFE_PHI_VALUES_F32: fp32-only operator, whose kernels round the
         // values to f32 anyway)
-        const bool a16 = phi->na <= 65536 && n > 0;
+        // atoms and voxels packed into one u32 when both fields fit with an
+        // all-ones value left over (>= the dimension: out of range)
+        auto field_bits = [](int64_t dim) { int b = 1; while (b < 32 && ((1ll << b) - 1) < dim) ++b; return b; };
+        const int abits = field_bits(phi->na), vbits = field_bits(phi->nv);
+        static const bool no_pack = [] { const char *e = std::getenv("LIFE_B200_NO_PACK"); return e && *e == '1'; }();
+        const bool pack = n > 0 && abits + vbits <= 32 && !no_pack;
+        const bool a16 = !pack && phi->na < 65535 && n > 0;
         const bool v32 = (flags & LIFE_PHI_VALUES_F32) && !(flags & LIFE_PHI_EXACT_F64) && n > 0;
         void *narrow = nullptr;
-        if (a16 || v32) {
+        if (a16 || v32 || pack) {
             LIFE_TRY(dev_alloc((void **)&narrow, (size_t)n * 4));
             guard.tmp.push_back(narrow);
         }
         uint16_t *na16 = static_cast<uint16_t *>(narrow);
         float *nv32 = static_cast<float *>(narrow);  // reused after the atoms are widened
-        if (n > 0) {
+        if (pack) {
+            uint32_t *pk = static_cast<uint32_t *>(narrow);
+            LIFE_TRY(h2d_staged_pack_av(pk, atoms, voxels, n, abits, vbits, st));
+            k_unpack_av<<<grid_for(n), 256, 0, st>>>(pk, n, abits, vbits >= 32 ? ~0u : (1u << vbits) - 1u, da, dv);
+            LIFE_CHECK_LAUNCH();
+        } else if (n > 0) {
             if (a16) {
                 LIFE_TRY(h2d_staged_cvt(na16, atoms, (size_t)n * 2, 2, st));
                 k_widen_u16<<<grid_for(n), 256, 0, st>>>(na16, n, da);
@@ -976,7 +1024,7 @@ static int create_impl(const life_dims *dims, const uint32_t *atoms,
             }
             LIFE_TRY(h2d_staged(dv, voxels, (size_t)n * 4, st));
         }
-        if (v32 && a16) {  // the side stream must not overwrite the u16 atoms before they are widened
+        if (v32 && (a16 || pack)) {  // the side stream must not overwrite the narrow atoms before they are widened
             LIFE_CUDA(cudaStreamSynchronize(st));
         }
         LIFE_TRY(h2d_staged(dD, dict, dlen * 8, st));

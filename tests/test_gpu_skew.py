@@ -139,6 +139,24 @@ def test_host_input_reports_first_bad_fiber():
     assert ei.value.dimension == "fiber" and ei.value.position == 123_457, str(ei.value)
 
 
+@pytest.mark.parametrize("dim,big", [("atom", 1_000_000), ("atom", 2**31 + 7), ("atom", None),
+                                     ("voxel", 2**20), ("voxel", 2**32 - 1), ("voxel", None)])
+def test_host_input_reports_first_bad_atom_voxel(dim, big):
+    """Atoms and voxels cross PCIe packed into one word (saturated fields):
+    an index just past the dimension, or far beyond the packed field, still
+    fails with its dimension and the first bad position."""
+    t, dic = _custom(200_000, 4, nv=2000, nf=3000)
+    arrs = {"atom": t.atoms.copy(), "voxel": t.voxels.copy()}
+    n_dim = t.dims.n_atoms if dim == "atom" else t.dims.n_voxels
+    arrs[dim][98_765] = n_dim if big is None else big
+    arrs[dim][150_000] = n_dim + 1
+    bad = L.PhiTensor(atoms=arrs["atom"], voxels=arrs["voxel"], fibers=t.fibers, values=t.values,
+                      dims=t.dims)
+    with pytest.raises(IndexOutOfRange) as ei:
+        device.DeviceOperator(bad, dic)
+    assert ei.value.dimension == dim and ei.value.position == 98_765, str(ei.value)
+
+
 @pytest.mark.parametrize("skew", ["lognormal", "zipf"])
 def test_device_generator_c5(skew):
     """The C5 device generator (datagen.draw_skewed_device): deterministic per
