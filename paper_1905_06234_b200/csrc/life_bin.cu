@@ -388,19 +388,21 @@ __global__ void k_vf_identity(const uint32_t *f, const uint32_t *f2vf, int64_t n
 // bin-major key (bin, tile, chunk) of each coefficient and the payload the
 // placement needs, sorted along with it (no gathers afterwards): fp32 value
 // bits << 32 | bin slot << 16 | tile cell
+template <typename K>
 __global__ void k_key_bm(const uint32_t *a, const uint32_t *row_o, const uint32_t *vf_o, const uint32_t *slot_of_row,
                          const double *val, int64_t n, int ka_shift, int ka, uint32_t nch, uint32_t ntiles,
-                         unsigned long long *kbm, unsigned long long *pay)
+                         K *kbm, unsigned long long *pay)
 {
     for (int64_t i = gtid(); i < n; i += gstride()) {
         const uint32_t sr = slot_of_row[row_o[i]], ai = a[i], vf = vf_o[i];
         const uint32_t t = sr / kTV, c = ai >> ka_shift, b = vf / kSB;
-        kbm[i] = ((unsigned long long)b * ntiles + t) * nch + c;
+        kbm[i] = (K)(((unsigned long long)b * ntiles + t) * nch + c);
         const uint32_t cell = (sr % kTV) * (uint32_t)(ka + 4) + (ai & (uint32_t)(ka - 1));
         pay[i] = ((unsigned long long)__float_as_uint((float)val[i]) << 32) | ((vf % kSB) << 16) | cell;
     }
 }
-__global__ void k_head_flags(const unsigned long long *k, int64_t n, uint8_t *head, uint32_t *head32)
+template <typename K>
+__global__ void k_head_flags(const K *k, int64_t n, uint8_t *head, uint32_t *head32)
 {
     for (int64_t p = gtid(); p < n; p += gstride()) {
         const bool h = p == 0 || k[p] != k[p - 1];
@@ -410,13 +412,14 @@ __global__ void k_head_flags(const unsigned long long *k, int64_t n, uint8_t *he
 }
 // per segment (bin-major order): key, length in 4-entry units, and the
 // tile-major sort key (tile, chunk, bin)
-__global__ void k_seg_info(const unsigned long long *kbm_sorted, const uint32_t *first, int64_t nseg, int64_t n,
+template <typename K>
+__global__ void k_seg_info(const K *kbm_sorted, const uint32_t *first, int64_t nseg, int64_t n,
                            unsigned long long per_bin, uint32_t nbins, uint32_t *len4, unsigned long long *segkey,
                            unsigned long long *tmkey, uint32_t *step)
 {
     for (int64_t s = gtid(); s < nseg; s += gstride()) {
         const uint32_t f0 = first[s], f1 = s + 1 < nseg ? first[s + 1] : (uint32_t)n;
-        const unsigned long long k = kbm_sorted[f0];
+        const unsigned long long k = (unsigned long long)kbm_sorted[f0];
         len4[s] = (f1 - f0 + 3u) / 4u;
         segkey[s] = k;
         const unsigned long long b = k / per_bin, tc = k % per_bin;
@@ -820,19 +823,31 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     unsigned long long *kbm = kva, *skbm = skva, *pay, *spay;
     LIFE_TRY(talloc((void **)&pay, n * 8));
     LIFE_TRY(talloc((void **)&spay, n * 8));
-    k_key_bm<<<gridn(n), 256, 0, st>>>(a, row_o, vf_o, d_slot, val, n, ka_shift, ka, (uint32_t)nch, (uint32_t)ntiles,
-                                       kbm, pay);
-    LIFE_CHECK_LAUNCH();
     const int64_t nsteps = ntiles * nch;
     const unsigned long long per_bin = (unsigned long long)ntiles * nch;
-    LIFE_TRY((sort_pairs<unsigned long long, unsigned long long>(kbm, skbm, pay, spay, n, bits64(per_bin * nbins), st)));
+    // 32-bit (bin, tile, chunk) keys when they fit: a quarter less sort traffic
+    const bool k32 = per_bin * (unsigned long long)nbins <= 0xFFFFFFFFull;
+    uint32_t *kbm32 = reinterpret_cast<uint32_t *>(kbm), *skbm32 = reinterpret_cast<uint32_t *>(skbm);
+    if (k32) {
+        k_key_bm<uint32_t><<<gridn(n), 256, 0, st>>>(a, row_o, vf_o, d_slot, val, n, ka_shift, ka, (uint32_t)nch,
+                                                     (uint32_t)ntiles, kbm32, pay);
+        LIFE_CHECK_LAUNCH();
+        LIFE_TRY((sort_pairs<uint32_t, unsigned long long>(kbm32, skbm32, pay, spay, n, bits64(per_bin * nbins), st)));
+    } else {
+        k_key_bm<unsigned long long><<<gridn(n), 256, 0, st>>>(a, row_o, vf_o, d_slot, val, n, ka_shift, ka,
+                                                               (uint32_t)nch, (uint32_t)ntiles, kbm, pay);
+        LIFE_CHECK_LAUNCH();
+        LIFE_TRY((sort_pairs<unsigned long long, unsigned long long>(kbm, skbm, pay, spay, n, bits64(per_bin * nbins),
+                                                                     st)));
+    }
     uint8_t *seghead;
     uint32_t *head32 = head, *segid = rstart, *first;
     int64_t *nsel;
     LIFE_TRY(talloc((void **)&seghead, n));
     LIFE_TRY(talloc((void **)&nsel, 8));
     LIFE_TRY(talloc((void **)&first, n * 4));
-    k_head_flags<<<gridn(n), 256, 0, st>>>(skbm, n, seghead, head32);
+    if (k32) k_head_flags<uint32_t><<<gridn(n), 256, 0, st>>>(skbm32, n, seghead, head32);
+    else k_head_flags<unsigned long long><<<gridn(n), 256, 0, st>>>(skbm, n, seghead, head32);
     LIFE_CHECK_LAUNCH();
     {
         cub::CountingInputIterator<uint32_t> pos(0);
@@ -862,7 +877,12 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     LIFE_TRY(talloc((void **)&stmkey, nseg * 8));
     LIFE_TRY(talloc((void **)&units, nsteps * 4));
     LIFE_TRY(talloc((void **)&spad, nsteps * 4));
-    k_seg_info<<<gridn(nseg), 256, 0, st>>>(skbm, first, nseg, n, per_bin, (uint32_t)nbins, len4, segkey, tmkey, sstep);
+    if (k32)
+        k_seg_info<uint32_t><<<gridn(nseg), 256, 0, st>>>(skbm32, first, nseg, n, per_bin, (uint32_t)nbins, len4, segkey,
+                                                          tmkey, sstep);
+    else
+        k_seg_info<unsigned long long><<<gridn(nseg), 256, 0, st>>>(skbm, first, nseg, n, per_bin, (uint32_t)nbins, len4,
+                                                                    segkey, tmkey, sstep);
     LIFE_CHECK_LAUNCH();
     // bin-major unit starts
     // +4: the bin side bulk-copies segment records rounded up to 16 bytes
