@@ -33,6 +33,8 @@ CONFIGS = {
     "c2": (1057, 200_000, 500_000, 96, 100_000_000),
     "c1": (1057, 10_000, 20_000, 96, 5_000_000),
     "c2s": (1057, 50_000, 125_000, 96, 25_000_000),
+    # one rank's share of C3 at 8 GPUs (an eighth of C2's voxels, all fascicles)
+    "c2x8": (1057, 25_000, 500_000, 96, 12_500_000),
     # BASELINE.json configs[3] (quoted on 8 GPUs; Nv assumed):
     # N_theta = 150 takes the 160-wide register-tiled kernels
     "c4": (1057, 250_000, 1_000_000, 150, 400_000_000),
@@ -41,6 +43,7 @@ WORKLOADS = {
     "c2": "C2 STN96-shaped synthetic LiFE problem (BASELINE.json configs[1])",
     "c1": "C1 synthetic STD LiFE problem (BASELINE.json configs[0])",
     "c2s": "C2 at quarter scale",
+    "c2x8": "one rank's share of C3 at 8 GPUs (C2 voxels / 8, all fascicles) on 1 GPU",
     "c4": "C4 probabilistic-tractography scale, N_theta=150 (BASELINE.json configs[3])",
 }
 METRIC = "SBBNNLS iters/sec"

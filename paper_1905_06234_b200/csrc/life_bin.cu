@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <thread>
@@ -677,7 +678,15 @@ int build_bin(life_phi *phi, const uint32_t *a, const uint32_t *v, const uint32_
     // 3. deal rows to tiles: counting sort by coefficient count (descending,
     // stable), snake order over the tiles so every tile carries about the
     // same number of coefficients
-    const int64_t ntiles = ((int64_t)R + kTV - 1) / kTV;
+    // tile count rounded up to a multiple of the tile grid (one CTA per SM):
+    // rows are dealt by coefficient count, so every CTA then gets the same
+    // number of equally loaded tiles, instead of the last round leaving
+    // CTAs idle (196 full tiles on 148 SMs: half the CTAs did 2 tiles).
+    // Each row's products do not depend on its tile: results are unchanged.
+    static const bool no_round = [] { const char *e = std::getenv("LIFE_B200_NO_TILE_ROUND"); return e && *e == '1'; }();
+    const int64_t tiles_full = ((int64_t)R + kTV - 1) / kTV;
+    const int64_t ntiles = no_round || tiles_full == 0 ? tiles_full
+                                                       : (tiles_full + phi->sms - 1) / phi->sms * phi->sms;
     std::vector<uint32_t> slot_of_row(R);
     std::vector<int> rowvox((size_t)ntiles * kTV, -1), rowpart((size_t)ntiles * kTV, -1);
     {
