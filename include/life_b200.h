@@ -97,10 +97,14 @@ LIFE_API uint64_t life_launch_count(void);
  * tensor.py:76-170).  atoms/voxels/fibers: u32[n_coeffs]; values:
  * f64[n_coeffs]; dict: f64[n_atoms*n_dirs] atom-major.  Indices are
  * range-checked on the device (LIFE_ERR_INDEX_OUT_OF_RANGE, the first bad
- * position in *bad_position when non-NULL).  The fast layout is the
- * restructuring of restructure.sort_by(tensor, "voxel") (restructure.py:54)
- * refined by atom group; the exact layout is the plain stable
- * voxel sort plus the stable fiber sort.  Synchronizes the stream. */
+ * position in *bad_position when non-NULL).  The default fp32 layout is the
+ * binned two-phase layout (tile-major and fascicle-bin-major orders, DESIGN.md
+ * section 3) built from stable device sorts; the sparse layout refines
+ * restructure.sort_by(tensor, "voxel") (restructure.py:54) by atom group; the
+ * exact layout is the plain stable voxel sort plus the stable fiber sort.
+ * With LIFE_PHI_HOST_INPUT the arrays are staged through pinned buffers:
+ * atom and voxel packed into one u32 when both fit (saturated fields, so the
+ * range check still sees out-of-range indices).  Synchronizes the stream. */
 LIFE_API int life_phi_create(const life_dims *dims, const uint32_t *atoms,
                     const uint32_t *voxels, const uint32_t *fibers,
                     const double *values, const double *dict, uint32_t flags,
