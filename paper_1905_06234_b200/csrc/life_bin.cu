@@ -235,11 +235,32 @@ __device__ inline int bin_exponent_dev(const FixParams &fx, int nt)
 
 // fixed-order reductions of per-warp partials (last CTA)
 template <typename T, typename Op>
+__device__ T block_finish(T acc, T init, Op op, int nthreads);
+template <typename T, typename Op>
 __device__ T block_reduce(const T *part, int n, T init, Op op, int nthreads)
 {
-    __shared__ T s[32];
     T acc = init;
-    for (int i = threadIdx.x; i < n; i += nthreads) acc = op(acc, __ldcg(part + i));
+    // loads batched 8 deep (one L2 round trip per batch instead of per
+    // element), combined in the same ascending order: same bits as a plain loop
+    for (int b = threadIdx.x; b < n; b += 8 * nthreads) {
+        T v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = b + k * nthreads;
+            v[k] = i < n ? __ldcg(part + i) : init;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (b + k * nthreads < n) acc = op(acc, v[k]);
+    }
+    return block_finish<T>(acc, init, op, nthreads);
+}
+// the block's per-thread values combined: warp shuffles, then warp 0 over
+// the warps' results (fixed order)
+template <typename T, typename Op>
+__device__ T block_finish(T acc, T init, Op op, int nthreads)
+{
+    __shared__ T s[32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc = op(acc, __shfl_xor_sync(0xffffffffu, acc, o));
     if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
@@ -282,9 +303,36 @@ __device__ void dsc_finish(const ReduceSlots &red, int nparts, const unsigned lo
                            const DscOut &out, unsigned *counter, const CallHooks &hooks, int nthreads,
                            unsigned *nonfinite)
 {
-    const double tsq = block_reduce<double>(red.part_d, nparts, 0.0, OpSum{}, nthreads);
-    const float tmax = block_reduce<float>(red.part_f, nparts, 0.f, OpMaxF{}, nthreads);
-    const unsigned long long tsk = block_reduce<unsigned long long>(skip, nskip, 0ull, OpSum{}, nthreads);
+    // the three reductions in one pass (each in block_reduce's order: the
+    // same bits), so the last CTA waits on one round of loads, not three
+    double a = 0.0;
+    float m = 0.f;
+    unsigned long long k = 0ull;
+    const int nmax = max(nparts, nskip);
+    for (int b = threadIdx.x; b < nmax; b += 8 * nthreads) {
+        double va[8];
+        float vm[8];
+        unsigned long long vk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int i = b + j * nthreads;
+            va[j] = i < nparts ? __ldcg(red.part_d + i) : 0.0;
+            vm[j] = i < nparts ? __ldcg(red.part_f + i) : 0.f;
+            vk[j] = i < nskip ? __ldcg(skip + i) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int i = b + j * nthreads;
+            if (i < nparts) {
+                a += va[j];
+                m = fmaxf(m, vm[j]);
+            }
+            if (i < nskip) k += vk[j];
+        }
+    }
+    const double tsq = block_finish<double>(a, 0.0, OpSum{}, nthreads);
+    const float tmax = block_finish<float>(m, 0.f, OpMaxF{}, nthreads);
+    const unsigned long long tsk = block_finish<unsigned long long>(k, 0ull, OpSum{}, nthreads);
     if (threadIdx.x == 0) {
         if (out.sumsq) *out.sumsq = tsq;
         if (out.absmax) *out.absmax = tmax;
@@ -2187,11 +2235,33 @@ __global__ void __launch_bounds__(512)
     float amax = 0.f;
     for (int p = blockIdx.x * 16 + warp; p < npc; p += gridDim.x * 16) {
         const uint4 d = __ldg(pcs + p);  // voxel, first row, end row, piece-sum slot (or ~0: final)
-        for (int col = lane; col < nt; col += 32) {
-            float r = 0.f;
-            for (uint32_t q = d.y; q < d.z; ++q) r += ypart[(size_t)q * N + col];
-            if (d.w != 0xFFFFFFFFu) fixsum[(size_t)d.w * N + col] = r;
-            else fix_store(r, (size_t)d.x * nt + col, y, b, accumulate, subtract, sq, amax);
+        // all of the lane's columns and 4 partial rows in flight per round
+        // (the sums still run in row order: same bits as a plain loop)
+        constexpr int CPL = (N + 31) / 32;
+        float r[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) r[c] = 0.f;
+        for (uint32_t q0 = d.y; q0 < d.z; q0 += 4) {
+            float v[4][CPL];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int col = lane + 32 * c;
+                    v[k][c] = (q0 + k < d.z && col < nt) ? __ldcg(ypart + (size_t)(q0 + k) * N + col) : 0.f;
+                }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (q0 + k < d.z)
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) r[c] += v[k][c];
+        }
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int col = lane + 32 * c;
+            if (col >= nt) continue;
+            if (d.w != 0xFFFFFFFFu) fixsum[(size_t)d.w * N + col] = r[c];
+            else fix_store(r[c], (size_t)d.x * nt + col, y, b, accumulate, subtract, sq, amax);
         }
     }
     fix_partial(sq, amax, red, part0 + blockIdx.x);
