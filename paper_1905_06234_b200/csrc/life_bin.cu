@@ -2765,7 +2765,9 @@ int launch_wc_bin(life_phi *phi, const float *y, float *w, const float *w_ref, c
             LIFE_CHECK_LAUNCH();
         }
     }
-    const int blocks = std::max(1, std::min(phi->sms, (phi->nf + 255) / 256));
+    // enough CTAs for one round of 4 fascicles per thread (a latency-bound
+    // pass: 3-4 dependent rounds with one CTA per SM cost ~9 us at C2)
+    const int blocks = std::max(1, std::min(4 * phi->sms, (phi->nf + 1023) / 1024));
     k_wc_fin<256><<<blocks, 256, 0, st>>>(phi->b_wfix, phi->b_nanf, phi->nf, w, w_ref, flags, fx, phi->nt,
                                           phi->part_d2, phi->counter2, sumsq, h);
     LIFE_CHECK_LAUNCH();
