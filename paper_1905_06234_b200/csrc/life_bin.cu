@@ -1745,6 +1745,87 @@ struct StepRegs {
     float4 s[kUBld];
 };
 
+// voxels split over several tile rows: sum their partial rows in row order
+// and apply the epilogue; then the DSC outputs over all partials
+// final value of y[vx, col] from its folded sum
+__device__ __forceinline__ void fix_store(float r, size_t o, float *__restrict__ y, const float *__restrict__ b,
+                                          bool accumulate, bool subtract, double &sq, float &amax)
+{
+    if (accumulate) r += y[o];
+    if (subtract) r -= b[o];
+    y[o] = r;
+    sq += (double)r * (double)r;
+    amax = fmaxf(amax, fabsf(r));
+}
+
+// per-CTA (sum of squares, max) into the reduction slot part
+__device__ __forceinline__ void fix_partial(double sq, float amax, const ReduceSlots &red, int part)
+{
+    __shared__ double s_sq[32];
+    __shared__ float s_mx[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    if (lane == 0) {
+        s_sq[warp] = sq;
+        s_mx[warp] = amax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        float m = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            t += s_sq[i];
+            m = fmaxf(m, s_mx[i]);
+        }
+        red.part_d[part] = t;
+        red.part_f[part] = m;
+    }
+}
+
+// pieces p0, p0 + pstride, ... of the split voxels (one warp each)
+template <int N>
+__device__ __forceinline__ void fix_pieces(const uint4 *__restrict__ pcs, int npc, const float *__restrict__ ypart,
+                                           int nt, float *__restrict__ fixsum, float *__restrict__ y,
+                                           const float *__restrict__ b, bool accumulate, bool subtract, int p0,
+                                           int pstride, int lane, double &sq, float &amax)
+{
+    for (int p = p0; p < npc; p += pstride) {
+        const uint4 d = __ldg(pcs + p);  // voxel, first row, end row, piece-sum slot (or ~0: final)
+        // all of the lane's columns and 4 partial rows in flight per round
+        // (the sums still run in row order: same bits as a plain loop)
+        constexpr int CPL = (N + 31) / 32;
+        float r[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) r[c] = 0.f;
+        for (uint32_t q0 = d.y; q0 < d.z; q0 += 4) {
+            float v[4][CPL];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    const int col = lane + 32 * c;
+                    v[k][c] = (q0 + k < d.z && col < nt) ? __ldcg(ypart + (size_t)(q0 + k) * N + col) : 0.f;
+                }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (q0 + k < d.z)
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) r[c] += v[k][c];
+        }
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int col = lane + 32 * c;
+            if (col >= nt) continue;
+            if (d.w != 0xFFFFFFFFu) fixsum[(size_t)d.w * N + col] = r[c];
+            else fix_store(r[c], (size_t)d.x * nt + col, y, b, accumulate, subtract, sq, amax);
+        }
+    }
+}
+
 // DSC tile side.  Roles (warps):
 //   0-7   builders: per step, C[row, atom] = sum of s as 32-bit fixed point
 //         (red.shared.add.u32: order independent, deterministic) from entries
@@ -1764,7 +1845,7 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
     k_tile_dsc(const TileArgs A, const float *__restrict__ scr, float *__restrict__ y, const float *__restrict__ b,
                const uint32_t flags, const ReduceSlots red, const DscOut out, const CallHooks hooks,
                const unsigned long long *__restrict__ skip_part, int nskip, const float *__restrict__ smax, int nsmax,
-               unsigned *__restrict__ nonfinite, int finalize, int cap)
+               unsigned *__restrict__ nonfinite, int finalize, int cap, const uint4 *__restrict__ fix_pcs, int fix_npc)
 {
     using C = DscCfg<N>;
     extern __shared__ __align__(1024) unsigned char smraw[];
@@ -2171,49 +2252,23 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
         red.part_d[gw] = sq;
         red.part_f[gw] = amax;
     }
-    if (finalize && last_cta(red.counter))
-        dsc_finish(red, (int)gridDim.x * C::kWarps, skip_part, nskip, out, red.counter, hooks, C::kThreads,
-                   nonfinite);
-}
-
-// voxels split over several tile rows: sum their partial rows in row order
-// and apply the epilogue; then the DSC outputs over all partials
-// final value of y[vx, col] from its folded sum
-__device__ __forceinline__ void fix_store(float r, size_t o, float *__restrict__ y, const float *__restrict__ b,
-                                          bool accumulate, bool subtract, double &sq, float &amax)
-{
-    if (accumulate) r += y[o];
-    if (subtract) r -= b[o];
-    y[o] = r;
-    sq += (double)r * (double)r;
-    amax = fmaxf(amax, fabsf(r));
-}
-
-// per-CTA (sum of squares, max) into the reduction slot part
-__device__ __forceinline__ void fix_partial(double sq, float amax, const ReduceSlots &red, int part)
-{
-    __shared__ double s_sq[32];
-    __shared__ float s_mx[32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    }
-    if (lane == 0) {
-        s_sq[warp] = sq;
-        s_mx[warp] = amax;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        float m = 0.f;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
-            t += s_sq[i];
-            m = fmaxf(m, s_mx[i]);
+    if (finalize && last_cta(red.counter)) {
+        int nparts = (int)gridDim.x * C::kWarps;
+        if (fix_npc > 0) {
+            // few voxels split over several rows (single pieces): every CTA
+            // has written its partial rows, so the last CTA folds them here
+            // instead of a fixup launch
+            const bool accumulate = flags & LIFE_ACCUMULATE;
+            const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
+            double fsq = 0.0;
+            float famax = 0.f;
+            fix_pieces<N>(fix_pcs, fix_npc, A.ypart, A.nt, nullptr, y, b, accumulate, subtract, warp, C::kWarps, lane,
+                          fsq, famax);
+            fix_partial(fsq, famax, red, nparts);
+            __syncthreads();
+            nparts += 1;
         }
-        red.part_d[part] = t;
-        red.part_f[part] = m;
+        dsc_finish(red, nparts, skip_part, nskip, out, red.counter, hooks, C::kThreads, nonfinite);
     }
 }
 
@@ -2233,37 +2288,8 @@ __global__ void __launch_bounds__(512)
     const bool subtract = (flags & LIFE_SUBTRACT_B) && b != nullptr;
     double sq = 0.0;
     float amax = 0.f;
-    for (int p = blockIdx.x * 16 + warp; p < npc; p += gridDim.x * 16) {
-        const uint4 d = __ldg(pcs + p);  // voxel, first row, end row, piece-sum slot (or ~0: final)
-        // all of the lane's columns and 4 partial rows in flight per round
-        // (the sums still run in row order: same bits as a plain loop)
-        constexpr int CPL = (N + 31) / 32;
-        float r[CPL];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) r[c] = 0.f;
-        for (uint32_t q0 = d.y; q0 < d.z; q0 += 4) {
-            float v[4][CPL];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    const int col = lane + 32 * c;
-                    v[k][c] = (q0 + k < d.z && col < nt) ? __ldcg(ypart + (size_t)(q0 + k) * N + col) : 0.f;
-                }
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (q0 + k < d.z)
-#pragma unroll
-                    for (int c = 0; c < CPL; ++c) r[c] += v[k][c];
-        }
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-            const int col = lane + 32 * c;
-            if (col >= nt) continue;
-            if (d.w != 0xFFFFFFFFu) fixsum[(size_t)d.w * N + col] = r[c];
-            else fix_store(r[c], (size_t)d.x * nt + col, y, b, accumulate, subtract, sq, amax);
-        }
-    }
+    fix_pieces<N>(pcs, npc, ypart, nt, fixsum, y, b, accumulate, subtract, blockIdx.x * 16 + warp, gridDim.x * 16,
+                  lane, sq, amax);
     fix_partial(sq, amax, red, part0 + blockIdx.x);
     if (finish && last_cta(red.counter))
         dsc_finish(red, part0 + (int)gridDim.x, skip_part, nskip, out, red.counter, hooks, 512, nonfinite);
@@ -2645,10 +2671,14 @@ int dsc_t(life_phi *phi, const float *w, float *y, const float *b, uint32_t flag
     LIFE_CHECK_LAUNCH();
     const TileArgs A{phi->b_cellr, phi->b_step, phi->b_Ddsc, phi->b_rowvox, phi->b_rowpart, phi->b_ypart,
                      phi->b_ntiles, phi->b_nch, phi->nt};
-    const int fin = phi->b_nfix == 0 ? 1 : 0;
+    // split voxels: a handful of single-piece ones are folded by the tile
+    // kernel's last CTA; many, or multi-piece ones, by the fixup kernels
+    const bool inline_fix = phi->b_nfix > 0 && phi->b_nbig == 0 && phi->b_npc <= 4 * CD::kWarps;
+    const int fin = (phi->b_nfix == 0 || inline_fix) ? 1 : 0;
     k_tile_dsc<N><<<phi->b_tile_grid, CD::kThreads, phi->b_dsc_smem, st>>>(
         A, phi->b_scr, y, b, flags, phi->red, o, h, phi->b_skip, phi->b_side_grid, phi->b_smax, phi->b_side_grid,
-        phi->b_nonfin, fin, phi->b_dsc_cap);
+        phi->b_nonfin, fin, phi->b_dsc_cap, inline_fix ? reinterpret_cast<const uint4 *>(phi->b_fixpc) : nullptr,
+        inline_fix ? phi->b_npc : 0);
     LIFE_CHECK_LAUNCH();
     if (!fin) {
         const int part0 = phi->b_tile_grid * CD::kWarps;
