@@ -1668,6 +1668,9 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t &hi, uint32_
     lo = *reinterpret_cast<const uint32_t *>(&l);
 }
 
+#ifndef LIFE_DSC_FOLD1
+#define LIFE_DSC_FOLD1 2
+#endif
 template <int N>
 struct DscCfg {
     static constexpr int EQ = (N + 63) / 64;   // epilogue warps per TMEM lane quarter
@@ -1684,6 +1687,10 @@ struct DscCfg {
     static constexpr int MB = (NBLK + EQ - 1) / EQ;
     static constexpr int TACC = 128;           // TMEM: A stage e at 64 e (hi 32 cols | lo 32), accumulators from TACC
     static constexpr int NACC = TACC + 4 * N <= 512 ? 2 : 1;  // accumulator buffers per issuer
+    // an issuer's own steps accumulated in TMEM per epilogue fold: 2 (128
+    // atoms); with a single accumulator buffer (N > 128) the issuer waits
+    // for every fold (LIFE_DSC_FOLD1)
+    static constexpr int FOLD = NACC == 2 ? 2 : LIFE_DSC_FOLD1;
     static constexpr int kSlotsG = 2;          // staged steps per builder group
     static_assert(TACC + 2 * NACC * N <= 512, "TMEM budget");
 };
@@ -2110,7 +2117,7 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
                 for (int oi = 0; oi < nown; ++oi, ++j) {
                     const int b = e * C::NACC + (C::NACC == 2 ? (f & 1) : 0);
                     const int fpar = C::NACC == 2 ? ((f >> 1) - 1) & 1 : (f - 1) & 1;
-                    const bool start = (oi & 1) == 0, fold = (oi & 1) == 1 || oi == nown - 1;
+                    const bool start = (oi % C::FOLD) == 0, fold = (oi % C::FOLD) == C::FOLD - 1 || oi == nown - 1;
                     if (start && f >= C::NACC) BD_WAIT(6, bar_wait(&acc_empty[b], fpar));
                     BD_WAIT(7, bar_wait(&a_full[e], j & 1));
                     BD_WAIT(8, bar_wait(&d_full[e], j & 1));
@@ -2152,7 +2159,7 @@ __global__ void __launch_bounds__(DscCfg<N>::kThreads, 1)
             for (int c = 0; c < A.nch; ++c) {
                 const int e = (i * A.nch + c) & 1, c0 = (e + i * A.nch) & 1;
                 const int nown = (A.nch - c0 + 1) >> 1, oi = (c - c0) >> 1;
-                if (!((oi & 1) == 1 || oi == nown - 1)) continue;  // not a fold step
+                if (!((oi % C::FOLD) == C::FOLD - 1 || oi == nown - 1)) continue;  // not a fold step
                 const int f = fcount[e]++;
                 const int b = e * C::NACC + (C::NACC == 2 ? (f & 1) : 0);
                 const int par = C::NACC == 2 ? (f >> 1) & 1 : f & 1;
